@@ -1,0 +1,150 @@
+"""Generate golden vectors by running the UNMODIFIED reference (turbobench).
+
+Run here (the reference exists only in this container):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Outputs tests/golden/*.npz.  Inputs are regenerated from seeds by
+tests/golden/gen.py at test time, so only outputs (or sha256 digests of the
+large ones) are stored.  Nothing on the GPU box reads /root/reference.
+"""
+from __future__ import annotations
+
+import hashlib
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+import gen  # noqa: E402
+
+from turbobench import attention as A  # noqa: E402
+from turbobench import blockquant as Q  # noqa: E402
+from turbobench import sampler as S  # noqa: E402
+
+SMALL = 1 << 18   # arrays up to 256 KiB are stored verbatim
+
+
+def sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def put(store: dict, name: str, a: np.ndarray, force: bool = False):
+    a = np.ascontiguousarray(a)
+    store[name + ".sha"] = np.array(sha(a))
+    store[name + ".shape"] = np.array(a.shape, dtype=np.int64)
+    if force or a.nbytes <= SMALL:
+        store[name] = a
+
+
+def attention_cases():
+    for (name, g, seed, h, s, d, qb, kvb, ratio) in gen.ATTN_CASES:
+        q, k, v = gen.make_inputs(g, seed, h, s, d)
+        cfg = A.SLAConfig(q_block=qb, kv_block=kvb, topk_ratio=ratio)
+        st: dict = {}
+        qp = A.pool_block_means(q, qb)
+        kp = A.pool_block_means(k, kvb)
+        put(st, "qp", qp)
+        put(st, "kp", kp)
+        mask = A.select_topk_blocks(qp, kp, cfg)
+        put(st, "idx", mask.indices, force=True)
+        put(st, "comp_idx", mask.complement().indices)
+        kc, km = A.smooth_keys(k)
+        put(st, "k_mean", km, force=True)
+        qq, sq = A._quantize_token_blocks(q, qb)
+        kq, sk = A._quantize_token_blocks(kc, kvb)
+        put(st, "q_codes", qq)
+        put(st, "q_scales", sq, force=True)
+        put(st, "k_codes", kq)
+        put(st, "k_scales", sk, force=True)
+        scores = np.matmul(qp, kp.transpose(0, 2, 1))
+        put(st, "scores", scores)
+        if s <= 4096:
+            inputs = A.AttnInputs(q, k, v)
+            for mix in (1.0, 0.0):
+                c2 = A.SLAConfig(q_block=qb, kv_block=kvb, topk_ratio=ratio, linear_mix=mix)
+                out = A.sla_attention(inputs, c2)
+                tag = f"sla_mix{mix:g}"
+                put(st, tag, out)
+                # row subsample kept verbatim for tolerance checks at any size
+                st[tag + ".rows"] = np.ascontiguousarray(out[:, ::7, :])
+            num_s, den_s, rmax = A._sparse_branch(inputs, mask, cfg)
+            st["sparse_rowmax.rows"] = np.ascontiguousarray(rmax[:, ::7])
+            st["sparse_den.rows"] = np.ascontiguousarray(den_s[:, ::7])
+            num_l, den_l = A.linear_attention(inputs, mask.complement())
+            st["lin_num.rows"] = np.ascontiguousarray(num_l[:, ::7, :])
+            st["lin_den.rows"] = np.ascontiguousarray(den_l[:, ::7])
+            ref = A.reference_attention(inputs)
+            st["dense.rows"] = np.ascontiguousarray(ref[:, ::7, :])
+        np.savez_compressed(os.path.join(HERE, f"attn_{name}.npz"), **st)
+        print("attn", name, "done", flush=True)
+
+
+def quant_cases():
+    st: dict = {}
+    for (name, seed, r, c, scale, block) in gen.QUANT_CASES:
+        m = gen.gaussian_matrix(seed, r, c, scale)
+        bq = Q.quantize_blockwise(m, Q.BlockQuantConfig(block=block))
+        put(st, name + ".q", bq.q)
+        put(st, name + ".scales", bq.scales, force=True)
+        put(st, name + ".deq", Q.dequantize_blockwise(bq))
+    for (name, seed, M, K, N, block, with_bias) in gen.W8A8_CASES:
+        x = gen.gaussian_matrix(seed, M, K)
+        w = gen.gaussian_matrix(seed + 1, K, N, 1.0 / np.sqrt(K))
+        bias = gen.gaussian_matrix(seed + 2, 1, N)[0] if with_bias else None
+        cfg = Q.BlockQuantConfig(block=block)
+        wq = Q.quantize_blockwise(w, cfg)
+        xq = Q.quantize_blockwise(x, cfg)
+        put(st, name + ".w8a8", Q.w8a8_matmul(xq, wq))
+        put(st, name + ".linear", Q.quantized_linear_forward(x, wq, bias))
+    np.savez_compressed(os.path.join(HERE, "quant.npz"), **st)
+    print("quant done", flush=True)
+
+
+def sampler_cases():
+    st: dict = {}
+    for step in range(4):
+        st[f"noise_7_{step}"] = S.step_noise(7, step, (64, 32))
+    st["sched4"] = S.make_schedule(4).sigmas
+    st["sched3"] = S.make_schedule(3).sigmas
+    # small random-init DiT, SLA + INT8 branch + W8A8 (test_acceptance.py:185-187 scale-down)
+    layers = S.make_random_weights(128, 2, seed=3)
+    qlayers = S.quantize_weights(layers)
+    cfg = A.SLAConfig(q_block=64, kv_block=64, topk_ratio=0.25)
+    model = S.ToyModel(layers=qlayers, heads=2, attn_mode="sla", sla_cfg=cfg)
+    st["dit_sample"] = S.consistency_sample(model, S.make_schedule(3), (256, 128), seed=5)
+    dense_model = S.ToyModel(layers=layers, heads=2, attn_mode="dense")
+    st["dit_dense_sample"] = S.consistency_sample(dense_model, S.make_schedule(3), (256, 128), seed=5)
+    x = S.step_noise(11, 0, (256, 128))
+    st["block_out"] = S.toy_block_forward(x, 2.0, qlayers[0], 2, "sla", cfg)
+    st["block_out_quantized"] = S.toy_block_forward(x, 2.0, qlayers[0], 2, "quantized")
+    np.savez_compressed(os.path.join(HERE, "sampler.npz"), **st)
+    print("sampler done", flush=True)
+
+
+def score_probes():
+    """Block scores around OpenBLAS's small-matrix TN threshold."""
+    st: dict = {}
+    for (nq, nkv, d) in gen.SCORE_PROBES:
+        rng = np.random.default_rng(nq * 1000 + nkv * 10 + d)
+        qp = rng.standard_normal((2, nq, d), dtype=np.float32)
+        kp = rng.standard_normal((2, nkv, d), dtype=np.float32)
+        tag = f"{nq}x{nkv}x{d}"
+        st[tag + ".scores"] = np.matmul(qp, kp.transpose(0, 2, 1))
+        st[tag + ".idx"] = A.select_topk_blocks(qp, kp, A.SLAConfig(topk_ratio=0.3)).indices
+    np.savez_compressed(os.path.join(HERE, "scores.npz"), **st)
+    print("scores done", flush=True)
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["attn", "quant", "sampler", "scores"]
+    if "scores" in which:
+        score_probes()
+    if "quant" in which:
+        quant_cases()
+    if "sampler" in which:
+        sampler_cases()
+    if "attn" in which:
+        attention_cases()
