@@ -1,0 +1,327 @@
+"""Benchmark of the TurboDiffusion hot path on B200 (contract: one JSON line on rank 0).
+
+Default workload (N=1): SLA + Sage attention at the Wan2.1-14B-720P shape
+(BASELINE.json configs[3]: 40 heads, 75600 tokens, d=128, top-k 10% ->
+119/1182 kv blocks, q_block 128 / kv_block 64) -- one step = one full
+``sla_attention`` call (pool/quant Q, k_mean, pool/quant K, top-k, V^T,
+linear branch, fused tcgen05 sparse attention + combine) on inputs resident
+in HBM.  metric = executed sparse-softmax work (attention_flop_report,
+attention.py:441-448) / step time, in TOPS.  Inputs (3 x 774 MB bf16) exceed
+the 126 MB L2, so no flush is needed between steps.
+
+Secondary line items in the same JSON: the W8A8 GEMM sweep at the
+Wan2.1-1.3B shapes (configs[1]) and the fused-kernel roofline.
+
+N>1 (torchrun): Ulysses -- each rank holds a token shard [L/P, H, d] of
+q/k/v, all-to-all to a head shard, attention on H/P heads, all-to-all back
+(strong scaling: the global problem is fixed).
+
+--impl reference: the CPU oracle port (oracle/oracle.py, numpy + the C
+restatement) on the host cores, one head of the same workload per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+H_, L_, D_ = 40, 75600, 128
+QB, KVB, RATIO = 128, 64, 0.1
+METRIC = "SLA-Sage attn TOPS & W8A8 GEMM TOPS at Wan2.1-14B-720P shapes, 1/2/4/8 B200"
+UNIT = "TOPS"
+
+
+def sparse_ops(H=H_, L=L_, d=D_, qb=QB, kvb=KVB, ratio=RATIO) -> int:
+    """attention.py:441-448 sparse_softmax_flops (QK^T + PV over selected blocks)."""
+    nkv = -(-L // kvb)
+    count = math.ceil(ratio * nkv)
+    return 4 * H * L * min(count * kvb, L) * d
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        reasons = set()
+        for r in self.rows:
+            if len(r) >= 7:
+                for name, val in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                                      "sw_power_cap"), r[3:7]):
+                    if val.lower() == "active":
+                        reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------- reference arm
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+    import numpy as np
+
+    import gen
+    from oracle import oracle as O
+    cores = os.cpu_count() or 1
+    q, k, v = gen.gaussian_qkv(2, 1, L_, D_, bf16=True)
+    ops_head = sparse_ops(H=1)
+    for _ in range(args.warmup if args.warmup <= 1 else 1):
+        O.sla_attention(q[:, :8192], k[:, :8192], v[:, :8192], QB, KVB, RATIO, 1.0)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.sla_attention(q, k, v, QB, KVB, RATIO, 1.0)
+        times.append(time.perf_counter() - t0)
+    t = statistics.median(times)
+    val = ops_head / t / 1e12
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "cfg4 SLA attention, 1 of 40 heads per step (CPU oracle port)",
+                       "heads": 1, "seq_len": L_, "head_dim": D_, "q_block": QB, "kv_block": KVB,
+                       "topk_ratio": RATIO},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": "1 head x 75600 tokens of cfg4 per step (numpy/OpenBLAS oracle)"},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- our arm
+
+def cpu_baseline_sample():
+    """Oracle port on a bounded sample (one cfg4 head, ~10-20 s), rank 0 only."""
+    sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+    import gen
+    from oracle import oracle as O
+    q, k, v = gen.gaussian_qkv(2, 1, L_, D_, bf16=True)
+    t0 = time.perf_counter()
+    O.sla_attention(q, k, v, QB, KVB, RATIO, 1.0)
+    t = time.perf_counter() - t0
+    return {"value": sparse_ops(H=1) / t / 1e12, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port",
+            "sample": f"1 of 40 heads of cfg4 (75600 tokens), {t:.1f} s, numpy/OpenBLAS oracle port"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-w8a8", action="store_true")
+    ap.add_argument("--heads", type=int, default=H_)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2512_16093_b200 import _lib, ops, ulysses
+    from paper_2512_16093_b200.attention import attention_flop_report, SLAConfig
+    _lib.load(require_device=True)
+
+    H = args.heads
+    total_ops = sparse_ops(H=H)
+    assert total_ops == attention_flop_report(L_, D_, H, SLAConfig(QB, KVB, RATIO)).sparse_softmax_flops
+    hp = H // world
+    g = torch.Generator(device="cuda").manual_seed(1234 + rank)
+    lo, hi = ulysses.token_bounds(L_, world, rank)
+    # token shard [L_p, H, d] of q/k/v (bf16), resident in HBM
+    shard = [torch.randn((hi - lo, H, D_), generator=g, device="cuda", dtype=torch.float32).to(torch.bfloat16)
+             for _ in range(3)]
+
+    def attn(qh, kh, vh):
+        return ops.sla_attention(qh, kh, vh, QB, KVB, RATIO, 1.0, out_dtype=torch.bfloat16)
+
+    def step():
+        if world == 1:
+            return attn(*head_major)                               # head-major copies resident in HBM
+        return ulysses.ulysses_sla_attention(shard[0], shard[1], shard[2], L_, attn)
+
+    head_major = [t.permute(1, 0, 2).contiguous() for t in shard] if world == 1 else None
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ev0.record()
+        for _ in range(args.steps):
+            step()
+        ev1.record()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = total_ops / (ms * 1e-3) / 1e12
+
+    # ---- dominant kernel (fused tcgen05 attention) timed alone on its stream
+    hbm, bf16_peak, peak_kind = peaks()
+    mixed_peak = bf16_peak * 4.0 / 3.0   # QK^T at INT8 (2x bf16) + PV at bf16, equal op counts
+    roof = None
+    if world == 1:
+        qh, kh, vh = head_major
+        _, parts = ops.sla_attention(qh, kh, vh, QB, KVB, RATIO, 1.0, out_dtype=torch.bfloat16, return_parts=True)
+        vt = ops.transpose_v(vh, (-(-L_ // 64)) * 64)
+        out = torch.empty((H, L_, D_), dtype=torch.bfloat16, device="cuda")
+        a = ops.sla_args(q=ops.ptr(qh), k=ops.ptr(kh), v=ops.ptr(vh), dtype=1, H=H, L=L_, d=D_, q_block=QB,
+                         kv_block=KVB, count=parts["count"], scale=1.0 / math.sqrt(D_), linear_mix=1.0, quantized=1,
+                         q_codes=ops.ptr(parts["q_codes"]), k_codes=ops.ptr(parts["k_codes"]),
+                         q_scales=ops.ptr(parts["q_scales"]), k_scales=ops.ptr(parts["k_scales"]),
+                         k_mean=ops.ptr(parts["k_mean"]), idx=ops.ptr(parts["idx"]), vt=ops.ptr(vt),
+                         l_pad=(-(-L_ // 64)) * 64, num_l=ops.ptr(parts["num_l"]), den_l=ops.ptr(parts["den_l"]),
+                         out=ops.ptr(out), out_dtype=1, row_max=None, den=None)
+        import ctypes
+        lib = _lib.load()
+        for _ in range(3):
+            lib.tb_sla_attention(ctypes.byref(a), ops.stream_ptr())
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 10
+        e0.record()
+        for _ in range(reps):
+            lib.tb_sla_attention(ctypes.byref(a), ops.stream_ptr())
+        e1.record()
+        torch.cuda.synchronize()
+        kms = e0.elapsed_time(e1) / reps
+        ach = total_ops / (kms * 1e-3) / 1e12
+        roof = {"bound": "tensor", "achieved": ach, "peak": mixed_peak, "unit": "TFLOP/s",
+                "frac": ach / mixed_peak, "traffic": None, "kernel": "sla_tc_kernel",
+                "kernel_ms": kms, "share_of_step": kms / ms,
+                "peak_note": f"INT8 QK^T (2x) + BF16 PV at {peak_kind} bf16 burst {bf16_peak} TFLOP/s x 4/3; "
+                             "INT8 dense peak not in MEASURED_PEAKS.json"}
+
+    # ---- W8A8 GEMM sweep (configs[1]), tensor-core exact + fast promotion
+    w8 = None
+    if world == 1 and not args.no_w8a8:
+        w8 = {}
+        M = 32760
+        for (K, N) in ((1536, 1536), (1536, 4608), (1536, 8960), (8960, 1536)):
+            xq = torch.randint(-127, 128, (M, K), dtype=torch.int8, device="cuda")
+            xs = torch.rand((-(-M // 128), K // 128), device="cuda") * 0.01
+            bt = torch.randint(-127, 128, (N, K), dtype=torch.int8, device="cuda")
+            bs = torch.rand((K // 128, N // 128), device="cuda") * 0.01
+            res = {}
+            for mode in ("exact", "fast"):
+                fn = lambda: ops.w8a8_gemm(xq, xs, bt, bs, 128, exact=(mode == "exact"))
+                for _ in range(3):
+                    fn()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(10):
+                    fn()
+                e1.record()
+                torch.cuda.synchronize()
+                gms = e0.elapsed_time(e1) / 10
+                res[mode] = {"ms": gms, "TOPS": 2 * M * K * N / (gms * 1e-3) / 1e12}
+            w8[f"{K}x{N}"] = res
+
+    # ---- e2e through the public API with pinned host buffers
+    e2e = None
+    if world == 1:
+        hq = [t.cpu().pin_memory() for t in head_major]
+        hout = torch.empty((H, L_, D_), dtype=torch.bfloat16).pin_memory()
+        def e2e_step():
+            dq = [t.to("cuda", non_blocking=True) for t in hq]
+            o = ops.sla_attention(dq[0], dq[1], dq[2], QB, KVB, RATIO, 1.0, out_dtype=torch.bfloat16)
+            hout.copy_(o, non_blocking=True)
+        e2e_step()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n_e2e = max(2, min(args.steps, 5))
+        e0.record()
+        for _ in range(n_e2e):
+            e2e_step()
+        e1.record()
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1) / n_e2e
+        e2e = {"value": total_ops / (ems * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": ems,
+               "h2d_bytes_per_step": sum(t.numel() * 2 for t in hq), "d2h_bytes_per_step": hout.numel() * 2}
+
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline_sample()
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "int8/bf16", "data": "synthetic",
+                "config": {"workload": "cfg4: SLA+Sage attention, Wan2.1-14B-720P shape (configs[3])",
+                           "heads": H, "seq_len": L_, "head_dim": D_, "q_block": QB, "kv_block": KVB,
+                           "topk_ratio": RATIO, "parallelism": f"ulysses{world}",
+                           "l2": "inputs 3 x 774 MB bf16 > 126 MB L2 (no flush needed)"},
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "w8a8": w8,
+                "gpu_launches": 8 * args.steps, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

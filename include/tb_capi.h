@@ -1,0 +1,167 @@
+/*
+ * tb_capi.h -- C ABI of the B200 (sm_100a) TurboDiffusion hot path.
+ *
+ * Every entry point is extern "C", takes plain device pointers, int64 sizes
+ * and a cudaStream_t passed as void*, is stream-ordered and asynchronous,
+ * allocates nothing (callers own every output and workspace), and returns
+ * 0 on success or a negative TB_E* code; tb_last_error() returns the
+ * thread-local message of the last failure.
+ *
+ * Each function names the reference operator it replaces
+ * (/root/reference/pkg/src/turbobench/<file>:<line>).  The Python drop-in
+ * modules (paper_2512_16093_b200/{attention,blockquant,sampler}.py) are the
+ * reference-facing binding; INTEGRATION.md shows the ctypes binding a
+ * turbobench maintainer would add.
+ */
+#ifndef TB_CAPI_H
+#define TB_CAPI_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum tb_status {
+    TB_OK = 0,
+    TB_EINVAL = -1,      /* bad shape / argument (Python: ValueError) */
+    TB_ECUDA = -2,       /* CUDA runtime / launch failure (RuntimeError) */
+    TB_EUNSUPPORTED = -3 /* shape outside the kernel's envelope */
+};
+
+enum tb_dtype { TB_F32 = 0, TB_BF16 = 1, TB_I8 = 2 };
+
+const char *tb_last_error(void);
+/* 1 when the library was built for sm_100a and a capable device is visible. */
+int tb_device_ok(void);
+const char *tb_build_info(void);
+
+/* ---------------------------------------------------------------- quant */
+
+/* blockquant.quantize_blockwise (blockquant.py:91-110): symmetric absmax
+ * INT8 codes per block x block tile, scale = absmax/127 (IEEE RN), code =
+ * clip(rint(x/scale)) with zero tiles -> scale 0, codes 0.  x is [rows,cols]
+ * row-major f32 or bf16; q int8 [rows,cols]; scales f32 [ceil(r/b),ceil(c/b)].
+ * *nonfinite (device int, may be NULL) is set to 1 if any input is inf/nan
+ * (the reference raises ValueError, blockquant.py:103-104). */
+int tb_quantize_blockwise(const void *x, int dtype, int64_t rows, int64_t cols, int64_t block,
+                          int8_t *q, float *scales, int32_t *nonfinite, void *stream);
+
+/* blockquant.dequantize_blockwise (blockquant.py:113-116). */
+int tb_dequantize_blockwise(const int8_t *q, const float *scales, int64_t rows, int64_t cols,
+                            int64_t block, float *out, void *stream);
+
+/* Transposes weight codes [K,N] -> [N,K] (the K-major B operand layout of
+ * the tensor-core GEMM).  Done once per weight at load time. */
+int tb_transpose_codes(const int8_t *src, int64_t rows, int64_t cols, int8_t *dst, void *stream);
+
+/* blockquant.w8a8_matmul + quantized_linear_forward bias add
+ * (blockquant.py:132-161, 164-182).  a: codes [M,K] + scales [ceil(M/b),ceil(K/b)];
+ * b: TRANSPOSED weight codes bt [N,K] + scales [ceil(K/b),ceil(N/b)] (the
+ * reference's [K,N] weight, transposed once).  out[M,N] (f32 or bf16) =
+ * sum over k-blocks ascending of (exact_int_segment * sa) * sb, then + bias
+ * (f32 [N], may be NULL).  block==128, K%128==0, N%16==0 runs on tcgen05
+ * (kind::i8, s32 TMEM accumulators); other shapes on a CUDA-core kernel with
+ * the identical arithmetic. */
+int tb_w8a8_gemm(const int8_t *a, const float *sa, const int8_t *bt, const float *sb,
+                 const float *bias, int64_t M, int64_t N, int64_t K, int64_t block,
+                 void *out, int out_dtype, void *stream);
+
+/* Fused activation quantization + W8A8 GEMM (quantized_linear_forward,
+ * blockquant.py:164-182): x [M,K] f32/bf16 is block-quantized into the
+ * caller's workspace (xq [M,K] int8, xs scales) then multiplied. */
+int tb_quantized_linear(const void *x, int x_dtype, const int8_t *bt, const float *sb,
+                        const float *bias, int64_t M, int64_t N, int64_t K, int64_t block,
+                        int8_t *xq_ws, float *xs_ws, void *out, int out_dtype, void *stream);
+
+/* ------------------------------------------------------- SLA importance */
+
+/* attention.pool_block_means (attention.py:256-266), numpy pairwise order:
+ * out[h,b,c] = (x[lo] + pairwise(x[lo+1:lo+e])) / f32(e).  x [H,L,d]. */
+int tb_pool_block_means(const void *x, int dtype, int64_t H, int64_t L, int64_t d, int64_t block,
+                        float *out, void *stream);
+
+/* smooth_keys k_mean (attention.py:179-188): sequential f32 chain over
+ * tokens per (h, channel), / f32(L).  k [H,L,d] -> kmean [H,d]. */
+int tb_kmean(const void *k, int dtype, int64_t H, int64_t L, int64_t d, float *kmean, void *stream);
+
+/* _quantize_token_blocks (attention.py:201-220) of x - center (center
+ * [H,d] may be NULL: Q path; k_mean: K path), optionally fused with the
+ * block pooling of the RAW x (pooled may be NULL).  codes int8 [H,L,d],
+ * scales f32 [H,ceil(L/block)]. */
+int tb_pool_quant_tokens(const void *x, int dtype, const float *center, int64_t H, int64_t L,
+                         int64_t d, int64_t block, int8_t *codes, float *scales, float *pooled,
+                         void *stream);
+
+/* select_topk_blocks + BlockMask.complement (attention.py:269-284,
+ * 122-132): scores = qp.kp^T in the reference's OpenBLAS order, top-count
+ * per row with ties to the lower index, ascending.  idx int32
+ * [H,nq,count]; comp (may be NULL) uint8 [H,nq,nkv] = 1 for blocks NOT
+ * selected; scores_out (may be NULL) f32 [H,nq,nkv]. */
+int tb_topk_blocks(const float *qp, const float *kp, int64_t H, int64_t nq, int64_t nkv,
+                   int64_t d, int64_t count, int32_t *idx, uint8_t *comp, float *scores_out,
+                   void *stream);
+
+/* ------------------------------------------------------- SLA attention */
+
+typedef struct tb_sla_args {
+    /* raw inputs [H,L,d] (dtype f32 or bf16) */
+    const void *q, *k, *v;
+    int dtype;
+    int64_t H, L, d, q_block, kv_block, count;
+    float scale;            /* logit scale (1/sqrt(d) default) */
+    float linear_mix;       /* attention.py:416-421 */
+    int quantized;          /* SLAConfig.quantized_sparse_branch */
+    /* prepared operands (from the prep entry points above) */
+    const int8_t *q_codes, *k_codes;   /* [H,L,d] */
+    const float *q_scales, *k_scales;  /* [H,nq], [H,nkv] */
+    const float *k_mean;               /* [H,d] */
+    const int32_t *idx;                /* [H,nq,count] ascending */
+    const void *vt;                    /* bf16 V^T [H,d,Lpad] (tensor-core path) */
+    int64_t l_pad;                     /* padded token stride of vt */
+    /* linear branch over the complement (may be NULL -> no linear term) */
+    const float *num_l, *den_l;        /* [H,L,d], [H,L] */
+    /* outputs */
+    float *out;                        /* [H,L,d] f32 (or bf16 when out_dtype) */
+    int out_dtype;
+    float *row_max, *den;              /* optional [H,L] sparse-branch stats */
+} tb_sla_args;
+
+/* _sparse_branch + combine (attention.py:347-389, 392-421).  d==128,
+ * q_block==128, kv_block==64, quantized -> tcgen05 kernel (INT8 QK^T with
+ * s32 TMEM accumulators, BF16 PV with f32 TMEM accumulators, TMA/bulk
+ * staged tiles, warp-specialised online softmax); other shapes -> CUDA-core
+ * kernel with the same semantics. */
+int tb_sla_attention(const tb_sla_args *a, void *stream);
+
+/* V [H,L,d] -> bf16 V^T [H,d,l_pad] (zero padded), the K-major B operand
+ * of the PV MMA. */
+int tb_transpose_v(const void *v, int dtype, int64_t H, int64_t L, int64_t d, int64_t l_pad,
+                   void *vt, void *stream);
+
+/* Feature map phi (attention.py:287-290) of x [H,L,d] into a padded GEMM
+ * operand out [H,l_pad,d] (f32 or bf16); rows t >= L are ZERO (not phi(0)),
+ * so padded kv blocks contribute nothing to phi(K)^T V (attention.py:320-325). */
+int tb_feature_map(const void *x, int dtype, int64_t H, int64_t L, int64_t d, int64_t l_pad,
+                   void *out, int out_dtype, void *stream);
+
+/* Fast-mode W8A8: identical operands, the two block scales folded into one
+ * FMA per element (tolerance-level, not bit-exact); used by the DiT step. */
+int tb_w8a8_gemm_fast(const int8_t *a, const float *sa, const int8_t *bt, const float *sb,
+                      const float *bias, int64_t M, int64_t N, int64_t K, int64_t block,
+                      void *out, int out_dtype, void *stream);
+
+/* ----------------------------------------------------------- DiT pieces */
+
+/* sampler.rmsnorm / layernorm (sampler.py:34-52), f32 rows. */
+int tb_rmsnorm(const float *x, const float *gain, int64_t rows, int64_t cols, float eps,
+               float *out, void *stream);
+int tb_layernorm(const float *x, const float *gain, const float *offset, int64_t rows,
+                 int64_t cols, float eps, float *out, void *stream);
+/* sampler._gelu tanh approximation (sampler.py:55-58), in place allowed. */
+int tb_gelu(const float *x, int64_t n, float *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TB_CAPI_H */

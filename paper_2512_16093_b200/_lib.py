@@ -1,0 +1,126 @@
+"""ctypes binding of the C ABI (include/tb_capi.h) -> libtb200.so.
+
+The library is built in-tree (``make -C paper_2512_16093_b200/csrc``) and
+loaded from the package directory.  There is no fallback: if the library or
+a CUDA device is missing, every op raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtb200.so")
+
+TB_OK, TB_EINVAL, TB_ECUDA, TB_EUNSUPPORTED = 0, -1, -2, -3
+TB_F32, TB_BF16, TB_I8 = 0, 1, 2
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int64
+_i = ctypes.c_int
+_f = ctypes.c_float
+
+# exported symbol -> argtypes (restype int unless listed in _RESTYPES)
+SIGNATURES = {
+    "tb_last_error": [],
+    "tb_device_ok": [],
+    "tb_build_info": [],
+    "tb_quantize_blockwise": [_P, _i, _I, _I, _I, _P, _P, _P, _P],
+    "tb_dequantize_blockwise": [_P, _P, _I, _I, _I, _P, _P],
+    "tb_transpose_codes": [_P, _I, _I, _P, _P],
+    "tb_w8a8_gemm": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _i, _P],
+    "tb_w8a8_gemm_fast": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _i, _P],
+    "tb_quantized_linear": [_P, _i, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _i, _P],
+    "tb_pool_block_means": [_P, _i, _I, _I, _I, _I, _P, _P],
+    "tb_kmean": [_P, _i, _I, _I, _I, _P, _P],
+    "tb_pool_quant_tokens": [_P, _i, _P, _I, _I, _I, _I, _P, _P, _P, _P],
+    "tb_topk_blocks": [_P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P],
+    "tb_sla_attention": [_P, _P],
+    "tb_transpose_v": [_P, _i, _I, _I, _I, _I, _P, _P],
+    "tb_feature_map": [_P, _i, _I, _I, _I, _I, _P, _i, _P],
+    "tb_rmsnorm": [_P, _P, _I, _I, _f, _P, _P],
+    "tb_layernorm": [_P, _P, _P, _I, _I, _f, _P, _P],
+    "tb_gelu": [_P, _I, _P, _P],
+}
+_RESTYPES = {"tb_last_error": ctypes.c_char_p, "tb_build_info": ctypes.c_char_p}
+
+
+class SlaArgs(ctypes.Structure):
+    """Mirror of ``tb_sla_args`` (include/tb_capi.h)."""
+    _fields_ = [
+        ("q", _P), ("k", _P), ("v", _P),
+        ("dtype", _i),
+        ("H", _I), ("L", _I), ("d", _I), ("q_block", _I), ("kv_block", _I), ("count", _I),
+        ("scale", _f), ("linear_mix", _f),
+        ("quantized", _i),
+        ("q_codes", _P), ("k_codes", _P),
+        ("q_scales", _P), ("k_scales", _P),
+        ("k_mean", _P),
+        ("idx", _P),
+        ("vt", _P),
+        ("l_pad", _I),
+        ("num_l", _P), ("den_l", _P),
+        ("out", _P),
+        ("out_dtype", _i),
+        ("row_max", _P), ("den", _P),
+    ]
+
+
+_lib = None
+
+
+def load(require_device: bool = False):
+    """Load libtb200.so (raises if absent)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run `make -C {os.path.join(_HERE, 'csrc')}` "
+                              "(or __graft_entry__.build()); there is no CPU fallback")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, args in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = _RESTYPES.get(name, ctypes.c_int)
+        _lib = lib
+    if require_device:
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2512_16093_b200 needs a CUDA device (B200, sm_100a); no CPU fallback")
+        if _lib.tb_device_ok() != 1:
+            raise RuntimeError("libtb200.so is built for sm_100a only; the visible device is not a B200")
+    return _lib
+
+
+def exported_symbols():
+    return list(SIGNATURES)
+
+
+def check(rc: int, what: str):
+    if rc == TB_OK:
+        return
+    msg = load().tb_last_error().decode(errors="replace")
+    if rc == TB_EINVAL:
+        raise ValueError(msg or what)
+    raise RuntimeError(f"{what}: {msg} (status {rc})")
+
+
+def call(name: str, *args):
+    lib = load(require_device=True)
+    check(getattr(lib, name)(*args), name)
+
+
+def ptr(t: torch.Tensor | None):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def stream_ptr():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.float32:
+        return TB_F32
+    if t.dtype == torch.bfloat16:
+        return TB_BF16
+    raise ValueError(f"unsupported dtype {t.dtype} (need float32 or bfloat16)")

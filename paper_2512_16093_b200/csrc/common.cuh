@@ -1,0 +1,65 @@
+// common.cuh -- shared device helpers for the sm_100a hot-path kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include <string>
+
+#include "../../include/tb_capi.h"
+
+namespace tb {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string &msg);
+int fail(int code, const std::string &msg);
+int check_launch(const char *what);
+
+#define TB_REQUIRE(cond, msg) \
+    do { if (!(cond)) return ::tb::fail(TB_EINVAL, (msg)); } while (0)
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ----------------------------------------------------------- load helpers
+template <typename T> __device__ __forceinline__ float to_f32(T v);
+template <> __device__ __forceinline__ float to_f32<float>(float v) { return v; }
+template <> __device__ __forceinline__ float to_f32<__nv_bfloat16>(__nv_bfloat16 v) {
+    return __bfloat162float(v);
+}
+
+// The reference quantization rule (attention.py:215-219, blockquant.py:106-109):
+// scale = f32(f64(am)/127) == __fdiv_rn(am, 127) (double rounding innocuous for
+// division at 53 >= 2*24+2 bits); code = clip(rint(x/safe), -127, 127), IEEE divide.
+__device__ __forceinline__ float quant_scale(float am) { return __fdiv_rn(am, 127.0f); }
+__device__ __forceinline__ int8_t quant_code(float x, float safe) {
+    float r = rintf(__fdiv_rn(x, safe));
+    r = fminf(fmaxf(r, -127.0f), 127.0f);
+    return (int8_t)(int)r;
+}
+
+template <int N>
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Block-wide max of non-negative floats (absmax); `red` needs 32 floats.
+__device__ __forceinline__ float block_max_nonneg(float v, float *red) {
+    v = warp_max<32>(v);
+    int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    int nw = (blockDim.x + 31) >> 5;
+    float r = (l < nw) ? red[l] : 0.0f;
+    r = warp_max<32>(r);
+    return r;
+}
+
+__host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace tb
+
+namespace tb {
+__host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+}  // namespace tb

@@ -1,0 +1,472 @@
+// quant.cu -- bit-exact block quantization, pooling and k_mean kernels (HBM-bound).
+//
+// Replaces (reference /root/reference/pkg/src/turbobench/):
+//   blockquant.quantize_blockwise      blockquant.py:91-110
+//   blockquant.dequantize_blockwise    blockquant.py:113-116
+//   attention.pool_block_means         attention.py:256-266
+//   attention.smooth_keys (k_mean)     attention.py:179-188
+//   attention._quantize_token_blocks   attention.py:201-220
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace tb {
+
+// ---------------------------------------------------- quantize_blockwise
+// One CTA per (block x block) tile.  Pass 1: absmax (order-free) + finite
+// check; pass 2 re-reads the tile (L1/L2 hit) and writes codes.
+template <typename T>
+__global__ void __launch_bounds__(256) quantize_blockwise_kernel(
+    const T *__restrict__ x, int64_t rows, int64_t cols, int64_t block, int64_t nbc,
+    int8_t *__restrict__ q, float *__restrict__ scales, int32_t *__restrict__ nonfinite) {
+    __shared__ float red[32];
+    const int64_t bi = blockIdx.y, bj = blockIdx.x;
+    const int64_t r0 = bi * block, c0 = bj * block;
+    const int64_t nr = min(block, rows - r0), nc = min(block, cols - c0);
+    const int64_t n = nr * nc;
+    float am = 0.0f;
+    bool bad = false;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        int64_t r = i / nc, c = i - r * nc;
+        float v = to_f32(x[(r0 + r) * cols + c0 + c]);
+        bad |= !isfinite(v);
+        am = fmaxf(am, fabsf(v));
+    }
+    if (nonfinite && __syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite, 1);
+    am = block_max_nonneg(am, red);
+    const float s = quant_scale(am);
+    if (threadIdx.x == 0) scales[bi * nbc + bj] = s;
+    const float safe = (s == 0.0f) ? 1.0f : s;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        int64_t r = i / nc, c = i - r * nc;
+        q[(r0 + r) * cols + c0 + c] = quant_code(to_f32(x[(r0 + r) * cols + c0 + c]), safe);
+    }
+}
+
+// Fast path: block == 128, cols % 8 == 0.  Each thread owns 8 consecutive
+// columns of a row (16 B of bf16 / 32 B of f32 loaded as vectors), codes
+// stored as one 8-byte word.
+template <typename T>
+__global__ void __launch_bounds__(256) quantize_blockwise128_kernel(
+    const T *__restrict__ x, int64_t rows, int64_t cols, int64_t nbc,
+    int8_t *__restrict__ q, float *__restrict__ scales, int32_t *__restrict__ nonfinite) {
+    __shared__ float red[32];
+    const int64_t bi = blockIdx.y, bj = blockIdx.x;
+    const int64_t r0 = bi * 128, c0 = bj * 128;
+    const int nr = (int)imin64(128, rows - r0), nc = (int)imin64(128, cols - c0);
+    const int lane16 = threadIdx.x & 15;           // column group (8 cols each)
+    const int rsub = threadIdx.x >> 4;             // 16 rows per pass
+    const bool col_ok = lane16 * 8 < nc;
+    float v[8][8];
+    float am = 0.0f;
+    bool bad = false;
+#pragma unroll
+    for (int p = 0; p < 8; p++) {
+        int r = rsub + p * 16;
+        if (col_ok && r < nr) {
+            const T *src = x + (r0 + r) * cols + c0 + lane16 * 8;
+            if constexpr (sizeof(T) == 2) {
+                uint4 raw = *reinterpret_cast<const uint4 *>(src);
+                const __nv_bfloat16 *b = reinterpret_cast<const __nv_bfloat16 *>(&raw);
+#pragma unroll
+                for (int j = 0; j < 8; j++) v[p][j] = __bfloat162float(b[j]);
+            } else {
+                float4 a = *reinterpret_cast<const float4 *>(src);
+                float4 b = *reinterpret_cast<const float4 *>(src + 4);
+                v[p][0] = a.x; v[p][1] = a.y; v[p][2] = a.z; v[p][3] = a.w;
+                v[p][4] = b.x; v[p][5] = b.y; v[p][6] = b.z; v[p][7] = b.w;
+            }
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+                bad |= !isfinite(v[p][j]);
+                am = fmaxf(am, fabsf(v[p][j]));
+            }
+        }
+    }
+    if (nonfinite && __syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite, 1);
+    am = block_max_nonneg(am, red);
+    const float s = quant_scale(am);
+    if (threadIdx.x == 0) scales[bi * nbc + bj] = s;
+    const float safe = (s == 0.0f) ? 1.0f : s;
+#pragma unroll
+    for (int p = 0; p < 8; p++) {
+        int r = rsub + p * 16;
+        if (col_ok && r < nr) {
+            uint32_t w[2] = {0, 0};
+#pragma unroll
+            for (int j = 0; j < 8; j++)
+                w[j >> 2] |= (uint32_t)(uint8_t)quant_code(v[p][j], safe) << ((j & 3) * 8);
+            *reinterpret_cast<uint2 *>(q + (r0 + r) * cols + c0 + lane16 * 8) = make_uint2(w[0], w[1]);
+        }
+    }
+}
+
+__global__ void dequantize_blockwise_kernel(const int8_t *__restrict__ q, const float *__restrict__ scales,
+                                            int64_t rows, int64_t cols, int64_t block, int64_t nbc,
+                                            float *__restrict__ out) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= rows * cols) return;
+    int64_t r = i / cols, c = i - r * cols;
+    out[i] = (float)q[i] * scales[(r / block) * nbc + c / block];
+}
+
+__global__ void transpose_codes_kernel(const int8_t *__restrict__ src, int64_t rows, int64_t cols,
+                                       int8_t *__restrict__ dst) {
+    __shared__ int8_t tile[32][33];
+    int64_t c = blockIdx.x * 32 + threadIdx.x, r = blockIdx.y * 32 + threadIdx.y;
+    for (int k = 0; k < 32; k += 8)
+        if (r + k < rows && c < cols) tile[threadIdx.y + k][threadIdx.x] = src[(r + k) * cols + c];
+    __syncthreads();
+    int64_t oc = blockIdx.y * 32 + threadIdx.x, orow = blockIdx.x * 32 + threadIdx.y;
+    for (int k = 0; k < 32; k += 8)
+        if (orow + k < cols && oc < rows) dst[(orow + k) * rows + oc] = tile[threadIdx.x][threadIdx.y + k];
+}
+
+// --------------------------------------------------------- pooling order
+// numpy pairwise summation (FLOAT_pairwise_sum, PW_BLOCKSIZE 128) over n
+// elements at `stride`, in f32.
+template <typename T>
+__device__ float pw_sum(const T *a, int64_t n, int64_t stride) {
+    if (n < 8) {
+        float res = -0.0f;
+        for (int64_t i = 0; i < n; i++) res = __fadd_rn(res, to_f32(a[i * stride]));
+        return res;
+    } else if (n <= 128) {
+        float r[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) r[j] = to_f32(a[j * stride]);
+        int64_t i;
+        for (i = 8; i < n - (n % 8); i += 8) {
+#pragma unroll
+            for (int j = 0; j < 8; j++) r[j] = __fadd_rn(r[j], to_f32(a[(i + j) * stride]));
+        }
+        float res = __fadd_rn(__fadd_rn(__fadd_rn(r[0], r[1]), __fadd_rn(r[2], r[3])),
+                              __fadd_rn(__fadd_rn(r[4], r[5]), __fadd_rn(r[6], r[7])));
+        for (; i < n; i++) res = __fadd_rn(res, to_f32(a[i * stride]));
+        return res;
+    } else {
+        int64_t n2 = n / 2;
+        n2 -= n2 % 8;
+        return __fadd_rn(pw_sum(a, n2, stride), pw_sum(a + n2 * stride, n - n2, stride));
+    }
+}
+
+// --------------------------------------------------- token-block pool+quant
+// One CTA per (head, token block).  Thread per channel (strided if d >
+// blockDim): pooled mean of the raw x in numpy reduceat order, absmax of
+// (x - center), then codes of (x - center).
+template <typename T>
+__global__ void __launch_bounds__(128) pool_quant_tokens_kernel(
+    const T *__restrict__ x, const float *__restrict__ center, int64_t L, int64_t d, int64_t block,
+    int64_t nb, int8_t *__restrict__ codes, float *__restrict__ scales, float *__restrict__ pooled) {
+    __shared__ float red[32];
+    const int64_t h = blockIdx.y, b = blockIdx.x;
+    const int64_t lo = b * block, e = min(block, L - lo);
+    const T *xb = x + (h * L + lo) * d;
+    float am = 0.0f;
+    for (int64_t c = threadIdx.x; c < d; c += blockDim.x) {
+        const float ctr = center ? center[h * d + c] : 0.0f;
+        if (pooled) {
+            float acc = to_f32(xb[c]);
+            if (e > 1) acc = __fadd_rn(acc, pw_sum(xb + d + c, e - 1, d));
+            pooled[(h * nb + b) * d + c] = __fdiv_rn(acc, (float)e);
+        }
+        if (codes) {
+            for (int64_t t = 0; t < e; t++) {
+                float v = center ? __fsub_rn(to_f32(xb[t * d + c]), ctr) : to_f32(xb[t * d + c]);
+                am = fmaxf(am, fabsf(v));
+            }
+        }
+    }
+    if (!codes) return;
+    am = block_max_nonneg(am, red);
+    const float s = quant_scale(am);
+    if (threadIdx.x == 0) scales[h * nb + b] = s;
+    const float safe = (s == 0.0f) ? 1.0f : s;
+    int8_t *cb = codes + (h * L + lo) * d;
+    for (int64_t i = threadIdx.x; i < e * d; i += blockDim.x) {
+        int64_t c = i % d;
+        float v = to_f32(xb[i]);
+        if (center) v = __fsub_rn(v, center[h * d + c]);
+        cb[i] = quant_code(v, safe);
+    }
+}
+
+// Fast path for d == 128, block <= 129 (the hot-path shapes): 128 threads,
+// thread c owns channel c; the tile is staged in registers once so the pool,
+// absmax and code passes read HBM a single time.  Codes are written by
+// transposing through shared memory so each warp stores contiguous 128 B rows.
+template <typename T, int BLOCK>
+__global__ void __launch_bounds__(128) pool_quant_tokens_d128_kernel(
+    const T *__restrict__ x, const float *__restrict__ center, int64_t L, int64_t nb,
+    int8_t *__restrict__ codes, float *__restrict__ scales, float *__restrict__ pooled) {
+    __shared__ float red[32];
+    __shared__ __align__(16) int8_t stile[BLOCK][128];
+    const int64_t h = blockIdx.y, b = blockIdx.x;
+    const int64_t lo = b * BLOCK;
+    const int e = (int)imin64(BLOCK, L - lo);
+    const int c = threadIdx.x;
+    const T *xb = x + (h * L + lo) * 128 + c;
+    const float ctr = center ? center[h * 128 + c] : 0.0f;
+    float v[BLOCK];
+#pragma unroll
+    for (int t = 0; t < BLOCK; t++) v[t] = (t < e) ? to_f32(xb[(int64_t)t * 128]) : 0.0f;
+    if (pooled) {
+        // x[lo] + pairwise(x[lo+1 : lo+e]) with n = e-1 <= 128
+        float acc = v[0];
+        const int n = e - 1;
+        if (n > 0) {
+            float res;
+            if (n < 8) {
+                res = -0.0f;
+#pragma unroll
+                for (int i = 0; i < 8; i++) if (i < n) res = __fadd_rn(res, v[1 + i]);
+            } else {
+                float r[8];
+#pragma unroll
+                for (int j = 0; j < 8; j++) r[j] = v[1 + j];
+                const int full = n - (n % 8);
+#pragma unroll
+                for (int i = 8; i + 8 <= BLOCK - 1; i += 8)
+                    if (i < full) {
+#pragma unroll
+                        for (int j = 0; j < 8; j++) r[j] = __fadd_rn(r[j], v[1 + i + j]);
+                    }
+                res = __fadd_rn(__fadd_rn(__fadd_rn(r[0], r[1]), __fadd_rn(r[2], r[3])),
+                                __fadd_rn(__fadd_rn(r[4], r[5]), __fadd_rn(r[6], r[7])));
+#pragma unroll
+                for (int i = 0; i < BLOCK - 1; i++)
+                    if (i >= full && i < n) res = __fadd_rn(res, v[1 + i]);
+            }
+            acc = __fadd_rn(acc, res);
+        }
+        pooled[(h * nb + b) * 128 + c] = __fdiv_rn(acc, (float)e);
+    }
+    float am = 0.0f;
+#pragma unroll
+    for (int t = 0; t < BLOCK; t++) {
+        if (center) v[t] = __fsub_rn(v[t], ctr);
+        if (t < e) am = fmaxf(am, fabsf(v[t]));
+    }
+    am = block_max_nonneg(am, red);
+    const float s = quant_scale(am);
+    if (threadIdx.x == 0) scales[h * nb + b] = s;
+    const float safe = (s == 0.0f) ? 1.0f : s;
+#pragma unroll
+    for (int t = 0; t < BLOCK; t++) stile[t][c] = quant_code(v[t], safe);
+    __syncthreads();
+    int8_t *cb = codes + (h * L + lo) * 128;
+    const uint4 *st = reinterpret_cast<const uint4 *>(&stile[0][0]);
+    for (int i = threadIdx.x; i < e * 8; i += 128) reinterpret_cast<uint4 *>(cb)[i] = st[i];
+}
+
+// ------------------------------------------------------------------ k_mean
+// Sequential f32 chain over all L tokens per (head, channel) -- the numpy
+// strided-reduce order.  The chain is latency-bound
+// (L dependent FADDs), so the kernel streams the head's [L,d] slab through a
+// shared-memory ring with 1-D bulk (TMA) copies: one CTA per head, one thread
+// per channel, the copy engine keeps STAGES chunks in flight.
+template <typename T, int STAGES>
+__global__ void __launch_bounds__(128) kmean_bulk_kernel(const T *__restrict__ k, int64_t L, int d,
+                                                         int chunk_tokens, float *__restrict__ kmean) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+    const int64_t h = blockIdx.x;
+    const T *src = k + h * L * d;
+    const int64_t nchunks = cdiv(L, chunk_tokens);
+    const uint32_t chunk_bytes = (uint32_t)(chunk_tokens * d * sizeof(T));
+    T *ring = reinterpret_cast<T *>(smem);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; s++) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], blockDim.x); }
+        ptx::fence_barrier_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int64_t i = 0; i < imin64(STAGES, nchunks); i++) {
+            int64_t toks = imin64(chunk_tokens, L - i * chunk_tokens);
+            uint32_t bytes = (uint32_t)(toks * d * sizeof(T));
+            ptx::mbar_arrive_expect_tx(&full[i], bytes);
+            ptx::bulk_g2s(ring + (size_t)i * chunk_tokens * d, src + i * chunk_tokens * d, bytes, &full[i]);
+        }
+    }
+    (void)chunk_bytes;
+    const int c = threadIdx.x;
+    float acc = 0.0f;
+    for (int64_t i = 0; i < nchunks; i++) {
+        const int s = (int)(i % STAGES);
+        const uint32_t par = (uint32_t)((i / STAGES) & 1);
+        ptx::mbar_wait(&full[s], par);
+        const int64_t toks = imin64(chunk_tokens, L - i * chunk_tokens);
+        const T *buf = ring + (size_t)s * chunk_tokens * d;
+        if (c < d) {
+            int64_t t = 0;
+            for (; t + 8 <= toks; t += 8) {
+                float w[8];
+#pragma unroll
+                for (int j = 0; j < 8; j++) w[j] = to_f32(buf[(t + j) * d + c]);
+#pragma unroll
+                for (int j = 0; j < 8; j++) acc = __fadd_rn(acc, w[j]);
+            }
+            for (; t < toks; t++) acc = __fadd_rn(acc, to_f32(buf[t * d + c]));
+        }
+        ptx::mbar_arrive(&empty[s]);
+        if (threadIdx.x == 0 && i + STAGES < nchunks) {
+            ptx::mbar_wait(&empty[s], par);
+            const int64_t j = i + STAGES;
+            int64_t tk = imin64(chunk_tokens, L - j * chunk_tokens);
+            uint32_t bytes = (uint32_t)(tk * d * sizeof(T));
+            ptx::mbar_arrive_expect_tx(&full[s], bytes);
+            ptx::bulk_g2s(ring + (size_t)s * chunk_tokens * d, src + j * chunk_tokens * d, bytes, &full[s]);
+        }
+    }
+    if (c < d) kmean[h * d + c] = __fdiv_rn(acc, (float)L);
+}
+
+// Generic fallback (unaligned rows / large d): same order, direct loads.
+template <typename T>
+__global__ void kmean_simple_kernel(const T *__restrict__ k, int64_t H, int64_t L, int64_t d,
+                                    float *__restrict__ kmean) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= H * d) return;
+    int64_t h = i / d, c = i - h * d;
+    const T *p = k + h * L * d + c;
+    float acc = 0.0f;
+    int64_t t = 0;
+    for (; t + 8 <= L; t += 8) {
+        float w[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) w[j] = to_f32(p[(t + j) * d]);
+#pragma unroll
+        for (int j = 0; j < 8; j++) acc = __fadd_rn(acc, w[j]);
+    }
+    for (; t < L; t++) acc = __fadd_rn(acc, to_f32(p[t * d]));
+    kmean[i] = __fdiv_rn(acc, (float)L);
+}
+
+// ---------------------------------------------------------- V transpose
+// V [H,L,d] -> bf16 V^T [H,d,l_pad] with zero padding (K-major B operand of
+// the PV MMA: rows = channels, contiguous tokens).
+template <typename T>
+__global__ void transpose_v_kernel(const T *__restrict__ v, int64_t L, int64_t d, int64_t l_pad,
+                                   __nv_bfloat16 *__restrict__ vt) {
+    __shared__ float tile[32][33];
+    const int64_t h = blockIdx.z;
+    const int64_t t0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+    for (int k = threadIdx.y; k < 32; k += 8) {
+        int64_t t = t0 + k, c = c0 + threadIdx.x;
+        tile[k][threadIdx.x] = (t < L && c < d) ? to_f32(v[(h * L + t) * d + c]) : 0.0f;
+    }
+    __syncthreads();
+    for (int k = threadIdx.y; k < 32; k += 8) {
+        int64_t c = c0 + k, t = t0 + threadIdx.x;
+        if (c < d && t < l_pad) vt[(h * d + c) * l_pad + t] = __float2bfloat16_rn(tile[threadIdx.x][k]);
+    }
+}
+
+}  // namespace tb
+
+using namespace tb;
+
+extern "C" int tb_quantize_blockwise(const void *x, int dtype, int64_t rows, int64_t cols, int64_t block,
+                                     int8_t *q, float *scales, int32_t *nonfinite, void *stream) {
+    TB_REQUIRE(block >= 1, "block must be >= 1");
+    TB_REQUIRE(rows >= 0 && cols >= 0, "negative shape");
+    TB_REQUIRE(dtype == TB_F32 || dtype == TB_BF16, "dtype must be f32 or bf16");
+    if (rows == 0 || cols == 0) return TB_OK;
+    const int64_t nbr = cdiv(rows, block), nbc = cdiv(cols, block);
+    TB_REQUIRE(nbr < 65536, "too many row blocks");
+    dim3 grid((unsigned)nbc, (unsigned)nbr);
+    cudaStream_t st = as_stream(stream);
+    bool fast = block == 128 && cols % 8 == 0 && ((uintptr_t)x % 16) == 0;
+    if (dtype == TB_F32) {
+        if (fast) quantize_blockwise128_kernel<float><<<grid, 256, 0, st>>>((const float *)x, rows, cols, nbc, q, scales, nonfinite);
+        else quantize_blockwise_kernel<float><<<grid, 256, 0, st>>>((const float *)x, rows, cols, block, nbc, q, scales, nonfinite);
+    } else {
+        if (fast) quantize_blockwise128_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>((const __nv_bfloat16 *)x, rows, cols, nbc, q, scales, nonfinite);
+        else quantize_blockwise_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>((const __nv_bfloat16 *)x, rows, cols, block, nbc, q, scales, nonfinite);
+    }
+    return check_launch("quantize_blockwise");
+}
+
+extern "C" int tb_dequantize_blockwise(const int8_t *q, const float *scales, int64_t rows, int64_t cols,
+                                       int64_t block, float *out, void *stream) {
+    TB_REQUIRE(block >= 1, "block must be >= 1");
+    int64_t n = rows * cols;
+    if (n == 0) return TB_OK;
+    dequantize_blockwise_kernel<<<(unsigned)cdiv(n, 256), 256, 0, as_stream(stream)>>>(
+        q, scales, rows, cols, block, cdiv(cols, block), out);
+    return check_launch("dequantize_blockwise");
+}
+
+extern "C" int tb_transpose_codes(const int8_t *src, int64_t rows, int64_t cols, int8_t *dst, void *stream) {
+    if (rows == 0 || cols == 0) return TB_OK;
+    dim3 grid((unsigned)cdiv(cols, 32), (unsigned)cdiv(rows, 32));
+    transpose_codes_kernel<<<grid, dim3(32, 8), 0, as_stream(stream)>>>(src, rows, cols, dst);
+    return check_launch("transpose_codes");
+}
+
+extern "C" int tb_pool_block_means(const void *x, int dtype, int64_t H, int64_t L, int64_t d, int64_t block,
+                                   float *out, void *stream) {
+    return tb_pool_quant_tokens(x, dtype, nullptr, H, L, d, block, nullptr, nullptr, out, stream);
+}
+
+extern "C" int tb_pool_quant_tokens(const void *x, int dtype, const float *center, int64_t H, int64_t L,
+                                    int64_t d, int64_t block, int8_t *codes, float *scales, float *pooled,
+                                    void *stream) {
+    TB_REQUIRE(block >= 1, "block must be >= 1");
+    TB_REQUIRE(dtype == TB_F32 || dtype == TB_BF16, "dtype must be f32 or bf16");
+    TB_REQUIRE((codes == nullptr) == (scales == nullptr), "codes and scales go together");
+    if (H == 0 || L == 0 || d == 0) return TB_OK;
+    const int64_t nb = cdiv(L, block);
+    TB_REQUIRE(H < 65536, "too many heads");
+    dim3 grid((unsigned)nb, (unsigned)H);
+    cudaStream_t st = as_stream(stream);
+    const bool fast = d == 128 && codes != nullptr && (block == 64 || block == 128);
+#define TB_POOLQ(T)                                                                                      \
+    if (fast && block == 64)                                                                             \
+        pool_quant_tokens_d128_kernel<T, 64><<<grid, 128, 0, st>>>((const T *)x, center, L, nb, codes, scales, pooled); \
+    else if (fast)                                                                                       \
+        pool_quant_tokens_d128_kernel<T, 128><<<grid, 128, 0, st>>>((const T *)x, center, L, nb, codes, scales, pooled); \
+    else                                                                                                 \
+        pool_quant_tokens_kernel<T><<<grid, 128, 0, st>>>((const T *)x, center, L, d, block, nb, codes, scales, pooled);
+    if (dtype == TB_F32) { TB_POOLQ(float) } else { TB_POOLQ(__nv_bfloat16) }
+#undef TB_POOLQ
+    return check_launch("pool_quant_tokens");
+}
+
+extern "C" int tb_kmean(const void *k, int dtype, int64_t H, int64_t L, int64_t d, float *kmean, void *stream) {
+    TB_REQUIRE(dtype == TB_F32 || dtype == TB_BF16, "dtype must be f32 or bf16");
+    if (H == 0 || d == 0) return TB_OK;
+    TB_REQUIRE(L >= 1, "seq must be >= 1");
+    cudaStream_t st = as_stream(stream);
+    const size_t es = dtype == TB_F32 ? 4 : 2;
+    const bool aligned = ((uintptr_t)k % 16 == 0) && ((L * d * es) % 16 == 0) && ((d * es) % 16 == 0);
+    if (aligned && d <= 128) {
+        constexpr int STAGES = 6;
+        int chunk = (int)(16384 / (d * es));          // 16 KiB per stage
+        if (chunk < 8) chunk = 8;
+        size_t smem = (size_t)STAGES * chunk * d * es;
+        if (dtype == TB_F32) {
+            cudaFuncSetAttribute(kmean_bulk_kernel<float, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            kmean_bulk_kernel<float, STAGES><<<(unsigned)H, 128, smem, st>>>((const float *)k, L, (int)d, chunk, kmean);
+        } else {
+            cudaFuncSetAttribute(kmean_bulk_kernel<__nv_bfloat16, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            kmean_bulk_kernel<__nv_bfloat16, STAGES><<<(unsigned)H, 128, smem, st>>>((const __nv_bfloat16 *)k, L, (int)d, chunk, kmean);
+        }
+    } else {
+        unsigned grid = (unsigned)cdiv(H * d, 128);
+        if (dtype == TB_F32) kmean_simple_kernel<float><<<grid, 128, 0, st>>>((const float *)k, H, L, d, kmean);
+        else kmean_simple_kernel<__nv_bfloat16><<<grid, 128, 0, st>>>((const __nv_bfloat16 *)k, H, L, d, kmean);
+    }
+    return check_launch("kmean");
+}
+
+extern "C" int tb_transpose_v(const void *v, int dtype, int64_t H, int64_t L, int64_t d, int64_t l_pad,
+                              void *vt, void *stream) {
+    TB_REQUIRE(l_pad >= L, "l_pad < L");
+    if (H == 0 || d == 0 || l_pad == 0) return TB_OK;
+    dim3 grid((unsigned)cdiv(l_pad, 32), (unsigned)cdiv(d, 32), (unsigned)H);
+    cudaStream_t st = as_stream(stream);
+    if (dtype == TB_F32) transpose_v_kernel<float><<<grid, dim3(32, 8), 0, st>>>((const float *)v, L, d, l_pad, (__nv_bfloat16 *)vt);
+    else transpose_v_kernel<__nv_bfloat16><<<grid, dim3(32, 8), 0, st>>>((const __nv_bfloat16 *)v, L, d, l_pad, (__nv_bfloat16 *)vt);
+    return check_launch("transpose_v");
+}

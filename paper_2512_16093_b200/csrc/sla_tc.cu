@@ -1,0 +1,336 @@
+// sla_tc.cu -- fused SLA + Sage block-sparse attention on tcgen05 (sm_100a).
+//
+// Replaces _sparse_branch (attention.py:347-389) and the combine of
+// sla_attention (attention.py:410-421) for the throughput envelope
+// (head_dim 128, q_block 128, kv_block 64, quantized INT8 branch).
+//
+// One CTA per (head, 128-row q-block); two CTAs per SM so one CTA's softmax
+// overlaps the other's tensor-core work.  Warp roles (192 threads):
+//   warps 0-3  softmax/epilogue, thread = query row = TMEM lane
+//   warp 4     TMA producer: Q codes once, then for each selected kv block the
+//              K code tile (64x128 int8) and the V^T tile (128x64 bf16) into a
+//              2-stage ring (128B-swizzled, mbarrier complete_tx)
+//   warp 5     MMA issuer (one elected thread):
+//                S_j  = Qc . Kc_j^T   4 x tcgen05.mma kind::i8  (M128 N64 K32) -> s32 TMEM
+//                O   += P_j . V_j     4 x tcgen05.mma kind::f16 (M128 N128 K16) -> f32 TMEM
+//              issued as QK(j+1) before PV(j) so QK overlaps softmax(j).
+// Softmax per block (log2 domain): logit2 = s32 * (sq*sk*scale*log2e) +
+// corr*scale*log2e with corr = q_row . k_mean; running reference max with
+// lazy O rescaling (only when the block max exceeds it by > 8, i.e. p <=
+// 256); P in bf16 written straight into the 128B-swizzled K-major smem
+// layout the PV MMA reads.  Epilogue: O and l rebased to the true row max,
+// combined with the linear branch exactly as attention.py:416-421.
+#include "common.cuh"
+#include "ptx.cuh"
+#include "tmap.cuh"
+
+namespace tb {
+
+namespace sla {
+constexpr int BM = 128, BN = 64, D = 128, STAGES = 2;
+constexpr int THREADS = 192;
+constexpr uint32_t Q_BYTES = BM * D;          // int8
+constexpr uint32_t K_BYTES = BN * D;          // int8
+constexpr uint32_t V_BYTES = D * BN * 2;      // bf16 V^T tile
+constexpr uint32_t P_BYTES = BM * BN * 2;     // bf16
+struct Smem {
+    uint8_t q[Q_BYTES];
+    uint8_t p[2][P_BYTES];
+    uint8_t v[STAGES][V_BYTES];
+    uint8_t k[STAGES][K_BYTES];
+    uint64_t q_full, o_final;
+    uint64_t kv_full[STAGES], kv_empty[STAGES];
+    uint64_t s_full[2], s_empty[2], p_full[2], p_empty[2];
+    uint32_t tmem_base;
+};
+constexpr size_t SMEM_BYTES = sizeof(Smem) + 1024;
+constexpr float LOG2E = 1.4426950408889634f;
+constexpr float LN2 = 0.6931471805599453f;
+}  // namespace sla
+
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
+    const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+    const __grid_constant__ CUtensorMap tm_v, tb_sla_args a, int nq, int nkv) {
+    using namespace sla;
+    extern __shared__ uint8_t smem_raw[];
+    Smem &S = *reinterpret_cast<Smem *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n = blockIdx.x, h = blockIdx.y;
+    const int count = (int)a.count;
+    const int L = (int)a.L;
+    const int32_t *sel = a.idx + ((int64_t)h * nq + n) * count;
+
+    if (warp == 4 && lane == 0) {
+        ptx::mbar_init(&S.q_full, 1);
+        ptx::mbar_init(&S.o_final, 1);
+        for (int s = 0; s < STAGES; s++) { ptx::mbar_init(&S.kv_full[s], 1); ptx::mbar_init(&S.kv_empty[s], 1); }
+        for (int b = 0; b < 2; b++) {
+            ptx::mbar_init(&S.s_full[b], 1);
+            ptx::mbar_init(&S.s_empty[b], 128);
+            ptx::mbar_init(&S.p_full[b], 128);
+            ptx::mbar_init(&S.p_empty[b], 1);
+        }
+        ptx::fence_barrier_init();
+        ptx::prefetch_tmap(&tm_q);
+        ptx::prefetch_tmap(&tm_k);
+        ptx::prefetch_tmap(&tm_v);
+    }
+    if (warp == 5) ptx::tmem_alloc<256>(&S.tmem_base);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = S.tmem_base;
+    const uint32_t TM_O = tmem + 128;
+
+    if (warp == 4) {
+        // ------------------------------------------------------ TMA producer
+        if (lane == 0) {
+            ptx::mbar_arrive_expect_tx(&S.q_full, Q_BYTES);
+            ptx::tma_load_3d(S.q, &tm_q, 0, n * BM, h, &S.q_full);
+            for (int j = 0; j < count; j++) {
+                const int st = j % STAGES;
+                const uint32_t par = (uint32_t)((j / STAGES) & 1);
+                const int b = __ldg(sel + j);
+                ptx::mbar_wait(&S.kv_empty[st], par ^ 1);
+                ptx::mbar_arrive_expect_tx(&S.kv_full[st], K_BYTES + V_BYTES);
+                ptx::tma_load_3d(S.k[st], &tm_k, 0, b * BN, h, &S.kv_full[st]);
+                ptx::tma_load_3d(S.v[st], &tm_v, b * BN, 0, h, &S.kv_full[st]);
+            }
+        }
+    } else if (warp == 5) {
+        // ------------------------------------------------------- MMA issuer
+        if (lane == 0) {
+            constexpr uint32_t ID_QK = ptx::idesc_i8(BM, BN);
+            constexpr uint32_t ID_PV = ptx::idesc_bf16(BM, D);
+            const uint64_t qd = ptx::sdesc_sw128(ptx::smem_u32(S.q));
+            ptx::mbar_wait(&S.q_full, 0);
+            auto pv = [&](int i) {
+                const int pb = i & 1, st = i % STAGES;
+                ptx::mbar_wait(&S.p_full[pb], (uint32_t)((i >> 1) & 1));
+                ptx::tc_fence_after();
+                const uint64_t pd = ptx::sdesc_sw128(ptx::smem_u32(S.p[pb]));
+                const uint64_t vd = ptx::sdesc_sw128(ptx::smem_u32(S.v[st]));
+#pragma unroll
+                for (int k = 0; k < BN / 16; k++)   // K=16 bf16 = 32 B per MMA
+                    ptx::mma_f16(TM_O, pd + 2 * k, vd + 2 * k, ID_PV, (i > 0 || k > 0) ? 1u : 0u);
+                ptx::mma_commit(&S.p_empty[pb]);
+                ptx::mma_commit(&S.kv_empty[st]);
+            };
+            for (int j = 0; j < count; j++) {
+                const int st = j % STAGES, sb = j & 1;
+                ptx::mbar_wait(&S.kv_full[st], (uint32_t)((j / STAGES) & 1));
+                if (j >= 2) ptx::mbar_wait(&S.s_empty[sb], (uint32_t)(((j >> 1) - 1) & 1));
+                ptx::tc_fence_after();
+                const uint64_t kd = ptx::sdesc_sw128(ptx::smem_u32(S.k[st]));
+#pragma unroll
+                for (int k = 0; k < D / 32; k++)    // K=32 int8 = 32 B per MMA
+                    ptx::mma_i8(tmem + sb * BN, qd + 2 * k, kd + 2 * k, ID_QK, k > 0 ? 1u : 0u);
+                ptx::mma_commit(&S.s_full[sb]);
+                if (j >= 1) pv(j - 1);
+            }
+            pv(count - 1);
+            ptx::mma_commit(&S.o_final);
+        }
+    } else {
+        // ------------------------------------------------ softmax + epilogue
+        const int r = warp * 32 + lane;             // row in tile == TMEM lane
+        const int row = n * BM + r;                 // token index
+        const bool row_ok = row < L;
+        const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+        const float scale2 = a.scale * LOG2E;
+        // corr = q_row . k_mean (unquantized q, f32)
+        float corr = 0.0f;
+        if (row_ok) {
+            const T *qr = reinterpret_cast<const T *>(a.q) + ((int64_t)h * L + row) * D;
+            const float *km = a.k_mean + (int64_t)h * D;
+#pragma unroll 8
+            for (int c = 0; c < D; c++) corr = fmaf(to_f32(qr[c]), __ldg(km + c), corr);
+        }
+        const float c0 = corr * scale2;
+        const float sq = __ldg(a.q_scales + (int64_t)h * nq + n);
+        const int last_blk = nkv - 1;
+        const int last_ext = L - last_blk * BN;
+        float m_ref = -INFINITY, m_true = -INFINITY, l = 0.0f;
+        uint8_t *prow0 = S.p[0] + r * 128;
+        uint8_t *prow1 = S.p[1] + r * 128;
+        for (int j = 0; j < count; j++) {
+            const int sb = j & 1;
+            const int b = __ldg(sel + j);
+            const float c1 = sq * __ldg(a.k_scales + (int64_t)h * nkv + b) * scale2;
+            ptx::mbar_wait(&S.s_full[sb], (uint32_t)((j >> 1) & 1));
+            ptx::tc_fence_after();
+            uint32_t s[4][16];
+#pragma unroll
+            for (int q4 = 0; q4 < 4; q4++) ptx::tmem_ld16(tmem + lane_base + sb * BN + q4 * 16, s[q4]);
+            ptx::tmem_wait_ld();
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&S.s_empty[sb]);
+            float t[64];
+            float mx = -INFINITY;
+            const int lim = (b == last_blk) ? last_ext : BN;
+#pragma unroll
+            for (int i = 0; i < 64; i++) {
+                const float x = __int_as_float((int)s[i >> 4][i & 15] + 0x4B400000) - 12582912.0f;
+                t[i] = (i < lim) ? fmaf(x, c1, c0) : -INFINITY;
+                mx = fmaxf(mx, t[i]);
+            }
+            m_true = fmaxf(m_true, mx);
+            if (j == 0) {
+                m_ref = mx;
+            } else if (mx > m_ref + 8.0f) {
+                // rebase O to the new reference: needs PV(j-1) complete
+                ptx::mbar_wait(&S.p_empty[(j - 1) & 1], (uint32_t)(((j - 1) >> 1) & 1));
+                ptx::tc_fence_after();
+                const float alpha = ex2(m_ref - mx);
+#pragma unroll 1
+                for (int c = 0; c < D; c += 16) {
+                    uint32_t o[16];
+                    ptx::tmem_ld16(TM_O + lane_base + c, o);
+                    ptx::tmem_wait_ld();
+#pragma unroll
+                    for (int i = 0; i < 16; i++) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+                    ptx::tmem_st16(TM_O + lane_base + c, o);
+                }
+                ptx::tmem_wait_st();
+                l *= alpha;
+                m_ref = mx;
+            }
+            float psum = 0.0f;
+            uint32_t pk[32];
+#pragma unroll
+            for (int i = 0; i < 64; i += 2) {
+                const float p0 = ex2(t[i] - m_ref), p1 = ex2(t[i + 1] - m_ref);
+                psum += p0 + p1;
+                __nv_bfloat162 pp = __floats2bfloat162_rn(p0, p1);
+                pk[i >> 1] = *reinterpret_cast<uint32_t *>(&pp);
+            }
+            l += psum;
+            if (j >= 2) ptx::mbar_wait(&S.p_empty[sb], (uint32_t)(((j >> 1) - 1) & 1));
+            uint8_t *prow = sb ? prow1 : prow0;
+#pragma unroll
+            for (int c = 0; c < 8; c++) {
+                const int phys = c ^ (r & 7);
+                *reinterpret_cast<uint4 *>(prow + phys * 16) =
+                    make_uint4(pk[c * 4], pk[c * 4 + 1], pk[c * 4 + 2], pk[c * 4 + 3]);
+            }
+            ptx::fence_async_smem();
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&S.p_full[sb]);
+        }
+        // ------------------------------------------------------- epilogue
+        ptx::mbar_wait(&S.o_final, 0);
+        ptx::tc_fence_after();
+        // rebase to the true row max (natural-log units for the combine)
+        const float f = ex2(m_ref - m_true);
+        const float m_nat = m_true * LN2;           // log2-domain max -> natural units
+        const float l_true = l * f;
+        const bool lin = a.num_l != nullptr && a.linear_mix != 0.0f;
+        float ss = f, shrink = 0.0f, den = l_true;
+        if (lin && row_ok) {
+            const float ref = fmaxf(m_nat, 0.0f);
+            const float e_ss = expf(m_nat - ref);
+            shrink = expf(-ref) * a.linear_mix;
+            den = l_true * e_ss + shrink * a.den_l[(int64_t)h * L + row];
+            ss = f * e_ss;
+        }
+        const float inv = 1.0f / den;
+        if (row_ok) {
+            if (a.row_max) a.row_max[(int64_t)h * L + row] = m_nat;
+            if (a.den) a.den[(int64_t)h * L + row] = l_true;
+        }
+#pragma unroll 1
+        for (int c = 0; c < D; c += 16) {
+            uint32_t o[16];
+            ptx::tmem_ld16(TM_O + lane_base + c, o);
+            ptx::tmem_wait_ld();
+            if (!row_ok) continue;
+            float v[16];
+            const int64_t off = ((int64_t)h * L + row) * D + c;
+            if (lin) {
+#pragma unroll
+                for (int i = 0; i < 16; i += 4) {
+                    const float4 nl = *reinterpret_cast<const float4 *>(a.num_l + off + i);
+                    v[i] = (__uint_as_float(o[i]) * ss + shrink * nl.x) * inv;
+                    v[i + 1] = (__uint_as_float(o[i + 1]) * ss + shrink * nl.y) * inv;
+                    v[i + 2] = (__uint_as_float(o[i + 2]) * ss + shrink * nl.z) * inv;
+                    v[i + 3] = (__uint_as_float(o[i + 3]) * ss + shrink * nl.w) * inv;
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < 16; i++) v[i] = __uint_as_float(o[i]) * f * inv;
+            }
+            if (a.out_dtype == TB_BF16) {
+                __nv_bfloat16 *dst = reinterpret_cast<__nv_bfloat16 *>(a.out) + off;
+#pragma unroll
+                for (int i = 0; i < 16; i += 8) {
+                    uint4 w;
+                    __nv_bfloat162 *p = reinterpret_cast<__nv_bfloat162 *>(&w);
+#pragma unroll
+                    for (int u = 0; u < 4; u++) p[u] = __floats2bfloat162_rn(v[i + 2 * u], v[i + 2 * u + 1]);
+                    *reinterpret_cast<uint4 *>(dst + i) = w;
+                }
+            } else {
+                float *dst = a.out + off;
+#pragma unroll
+                for (int i = 0; i < 16; i += 4) *reinterpret_cast<float4 *>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+            }
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 5) ptx::tmem_dealloc<256>(tmem);
+}
+
+int sla_simt(const tb_sla_args *a, cudaStream_t st);
+
+bool sla_tc_supported(const tb_sla_args *a) {
+    return a->quantized && a->d == 128 && a->q_block == 128 && a->kv_block == 64 && a->vt != nullptr &&
+           a->L >= 128 && a->l_pad % 64 == 0 && a->l_pad >= cdiv(a->L, 64) * 64 &&
+           (a->dtype == TB_BF16 || a->dtype == TB_F32) && a->count >= 1;
+}
+
+int sla_tc(const tb_sla_args *a, cudaStream_t st) {
+    using namespace sla;
+    const int64_t nq = cdiv(a->L, BM), nkv = cdiv(a->L, BN);
+    CUtensorMap tq, tk, tv;
+    bool ok = make_tmap_3d(&tq, a->q_codes, CU_TENSOR_MAP_DATA_TYPE_UINT8, D, a->L, a->H, D, a->L * D, D, BM, 1) &&
+              make_tmap_3d(&tk, a->k_codes, CU_TENSOR_MAP_DATA_TYPE_UINT8, D, a->L, a->H, D, a->L * D, D, BN, 1) &&
+              make_tmap_3d(&tv, a->vt, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, a->l_pad, D, a->H, a->l_pad * 2,
+                           a->l_pad * 2 * D, BN, D, 1);
+    if (!ok) return fail(TB_ECUDA, "cuTensorMapEncodeTiled failed (sla)");
+    dim3 grid((unsigned)nq, (unsigned)a->H);
+    if (a->dtype == TB_BF16) {
+        cudaFuncSetAttribute(sla_tc_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+        sla_tc_kernel<__nv_bfloat16><<<grid, THREADS, SMEM_BYTES, st>>>(tq, tk, tv, *a, (int)nq, (int)nkv);
+    } else {
+        cudaFuncSetAttribute(sla_tc_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+        sla_tc_kernel<float><<<grid, THREADS, SMEM_BYTES, st>>>(tq, tk, tv, *a, (int)nq, (int)nkv);
+    }
+    return check_launch("sla_tc");
+}
+
+}  // namespace tb
+
+using namespace tb;
+
+extern "C" int tb_sla_attention(const tb_sla_args *a, void *stream) {
+    TB_REQUIRE(a != nullptr, "null args");
+    TB_REQUIRE(a->H >= 0 && a->L >= 1 && a->d >= 1, "bad shape");
+    TB_REQUIRE(a->q_block >= 1 && a->kv_block >= 1, "block sizes must be >= 1");
+    TB_REQUIRE(a->q_block <= a->L && a->kv_block <= a->L, "block sizes exceed seq");
+    TB_REQUIRE(a->count >= 1 && a->count <= cdiv(a->L, a->kv_block), "bad count");
+    TB_REQUIRE(a->dtype == TB_F32 || a->dtype == TB_BF16, "dtype must be f32 or bf16");
+    TB_REQUIRE(!a->quantized || (a->q_codes && a->k_codes && a->q_scales && a->k_scales && a->k_mean),
+               "quantized branch needs codes, scales and k_mean");
+    if (a->H == 0) return TB_OK;
+    cudaStream_t st = as_stream(stream);
+    if (sla_tc_supported(a)) return sla_tc(a, st);
+    return sla_simt(a, st);
+}

@@ -1,0 +1,313 @@
+// w8a8.cu -- W8A8 INT8 GEMM with 128x128 block scales.
+//
+// Replaces w8a8_matmul (blockquant.py:132-161) and the GEMM of
+// quantized_linear_forward (blockquant.py:164-182):
+//   out[i,j] = sum_{kb ascending} (f32(seg_kb[i,j]) * sa[i/128,kb]) * sb[kb,j/128]
+//   (+ bias[j]),  seg_kb = exact integer code dot over k-block kb.
+//
+// tcgen05 path (block 128, K%128==0, N%128==0): persistent CTAs, one per SM,
+// warp-specialised: warp 0 issues TMA loads of 128x128 A / B^T code tiles
+// (128B swizzle) into a 4-stage ring; warp 1 issues 4 x tcgen05.mma
+// kind::i8 (M=128,N=128,K=32) per k-block into one of two s32 TMEM segment
+// buffers; 8 epilogue warps drain each segment (tcgen05.ld), promote it
+// into f32 register accumulators with the per-block scales, and store.
+// Exact mode reproduces the reference rounding sequence bit-for-bit (seg ->
+// f32 exactly via the 1.5*2^23 magic, then two RN multiplies and an RN add);
+// fast mode folds the two scales into one FMA (tolerance-level).
+#include "common.cuh"
+#include "ptx.cuh"
+#include "tmap.cuh"
+
+namespace tb {
+
+// ------------------------------------------------------------ tcgen05 path
+namespace gemm {
+constexpr int BM = 128, BN = 128, BK = 128, STAGES = 4;
+constexpr int EPI_WARPS = 8;
+constexpr int THREADS = 64 + EPI_WARPS * 32;
+constexpr uint32_t TILE_BYTES = BM * BK;  // A and B tiles are both 16 KiB
+
+struct Smem {
+    uint8_t a[STAGES][BM * BK];
+    uint8_t b[STAGES][BN * BK];
+    uint64_t full[STAGES], empty[STAGES];
+    uint64_t seg_full[2], seg_empty[2];
+    uint32_t tmem_base;
+};
+constexpr size_t SMEM_BYTES = sizeof(Smem) + 1024;
+}  // namespace gemm
+
+template <bool EXACT, bool OUT_BF16>
+__global__ void __launch_bounds__(gemm::THREADS, 1) w8a8_tc_kernel(
+    const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+    const float *__restrict__ sa, const float *__restrict__ sb, const float *__restrict__ bias,
+    void *__restrict__ out, int M, int N, int K) {
+    using namespace gemm;
+    extern __shared__ uint8_t smem_raw[];
+    Smem &S = *reinterpret_cast<Smem *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nmt = (M + BM - 1) / BM, nnt = N / BN, nkb = K / BK;
+    const int ntiles = nmt * nnt;
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < STAGES; s++) { ptx::mbar_init(&S.full[s], 1); ptx::mbar_init(&S.empty[s], 1); }
+        for (int b = 0; b < 2; b++) { ptx::mbar_init(&S.seg_full[b], 1); ptx::mbar_init(&S.seg_empty[b], EPI_WARPS * 32); }
+        ptx::fence_barrier_init();
+        ptx::prefetch_tmap(&tma_a);
+        ptx::prefetch_tmap(&tma_b);
+    }
+    if (warp == 1) ptx::tmem_alloc<256>(&S.tmem_base);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = S.tmem_base;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                const int mt = tile % nmt, nt = tile / nmt;
+                for (int kb = 0; kb < nkb; kb++) {
+                    ptx::mbar_wait(&S.empty[stage], phase ^ 1);
+                    ptx::mbar_arrive_expect_tx(&S.full[stage], 2 * TILE_BYTES);
+                    ptx::tma_load_2d(S.a[stage], &tma_a, kb * BK, mt * BM, &S.full[stage]);
+                    ptx::tma_load_2d(S.b[stage], &tma_b, kb * BK, nt * BN, &S.full[stage]);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            int stage = 0, buf = 0;
+            uint32_t phase = 0, bphase = 0;
+            constexpr uint32_t idesc = ptx::idesc_i8(BM, BN);
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                for (int kb = 0; kb < nkb; kb++) {
+                    ptx::mbar_wait(&S.seg_empty[buf], bphase ^ 1);
+                    ptx::mbar_wait(&S.full[stage], phase);
+                    ptx::tc_fence_after();
+                    const uint64_t ad = ptx::sdesc_sw128(ptx::smem_u32(S.a[stage]));
+                    const uint64_t bd = ptx::sdesc_sw128(ptx::smem_u32(S.b[stage]));
+#pragma unroll
+                    for (int k = 0; k < BK / 32; k++)   // K=32 bytes per kind::i8 MMA -> +2 in desc units
+                        ptx::mma_i8(tmem + buf * BN, ad + 2 * k, bd + 2 * k, idesc, k > 0 ? 1u : 0u);
+                    ptx::mma_commit(&S.empty[stage]);
+                    ptx::mma_commit(&S.seg_full[buf]);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    buf ^= 1;
+                    if (buf == 0) bphase ^= 1;
+                }
+            }
+        }
+    } else {
+        const int ew = warp - 2;
+        const int quarter = warp & 3;          // TMEM lanes this warp may touch
+        const int half = ew >> 2;              // column half of the 128-wide tile
+        const int trow = quarter * 32 + lane;
+        int buf = 0;
+        uint32_t bphase = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            const int mt = tile % nmt, nt = tile / nmt;
+            float acc[64];
+#pragma unroll
+            for (int i = 0; i < 64; i++) acc[i] = 0.0f;
+            for (int kb = 0; kb < nkb; kb++) {
+                const float s_a = __ldg(sa + (size_t)mt * nkb + kb);
+                const float s_b = __ldg(sb + (size_t)kb * nnt + nt);
+                ptx::mbar_wait(&S.seg_full[buf], bphase);
+                ptx::tc_fence_after();
+                uint32_t r[4][16];
+                const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + buf * BN + half * 64;
+#pragma unroll
+                for (int j = 0; j < 4; j++) ptx::tmem_ld16(taddr + j * 16, r[j]);
+                ptx::tmem_wait_ld();
+                ptx::tc_fence_before();
+                ptx::mbar_arrive(&S.seg_empty[buf]);
+                const float s_ab = s_a * s_b;
+#pragma unroll
+                for (int j = 0; j < 4; j++)
+#pragma unroll
+                    for (int i = 0; i < 16; i++) {
+                        // exact s32 -> f32 (|seg| <= 128*127^2 < 2^22)
+                        const float x = __int_as_float((int)r[j][i] + 0x4B400000) - 12582912.0f;
+                        if constexpr (EXACT)
+                            acc[j * 16 + i] = __fadd_rn(acc[j * 16 + i], __fmul_rn(__fmul_rn(x, s_a), s_b));
+                        else
+                            acc[j * 16 + i] = fmaf(x, s_ab, acc[j * 16 + i]);
+                    }
+                buf ^= 1;
+                if (buf == 0) bphase ^= 1;
+            }
+            const int row = mt * BM + trow;
+            if (row < M) {
+                const int col0 = nt * BN + half * 64;
+                if (bias) {
+#pragma unroll
+                    for (int i = 0; i < 64; i++) acc[i] = __fadd_rn(acc[i], __ldg(bias + col0 + i));
+                }
+                if constexpr (OUT_BF16) {
+                    __nv_bfloat16 *o = reinterpret_cast<__nv_bfloat16 *>(out) + (size_t)row * N + col0;
+#pragma unroll
+                    for (int i = 0; i < 64; i += 8) {
+                        uint4 w;
+                        __nv_bfloat162 *p = reinterpret_cast<__nv_bfloat162 *>(&w);
+#pragma unroll
+                        for (int j = 0; j < 4; j++) p[j] = __floats2bfloat162_rn(acc[i + 2 * j], acc[i + 2 * j + 1]);
+                        *reinterpret_cast<uint4 *>(o + i) = w;
+                    }
+                } else {
+                    float *o = reinterpret_cast<float *>(out) + (size_t)row * N + col0;
+#pragma unroll
+                    for (int i = 0; i < 64; i += 4)
+                        *reinterpret_cast<float4 *>(o + i) = make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
+                }
+            }
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) ptx::tmem_dealloc<256>(tmem);
+}
+
+// ------------------------------------------------------------ CUDA-core path
+// Any block size / shape.  64x64 output tile per CTA, 256 threads x 4x4
+// outputs, exact int32 segments via dp4a, identical promotion order.
+__global__ void __launch_bounds__(256) w8a8_simt_kernel(const int8_t *__restrict__ a, const float *__restrict__ sa,
+                                                        const int8_t *__restrict__ bt, const float *__restrict__ sb,
+                                                        const float *__restrict__ bias, int64_t M, int64_t N,
+                                                        int64_t K, int64_t block, int exact, void *out, int out_bf16) {
+    __shared__ __align__(16) int8_t as_[64][68];
+    __shared__ __align__(16) int8_t bs_[64][68];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int64_t m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+    const int64_t nkb = cdiv(K, block), nnb = cdiv(N, block);
+    float acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+#pragma unroll
+        for (int j = 0; j < 4; j++) acc[i][j] = 0.0f;
+    for (int64_t kb = 0; kb < nkb; kb++) {
+        const int64_t k0 = kb * block, k1 = min(k0 + block, K);
+        int seg[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+#pragma unroll
+            for (int j = 0; j < 4; j++) seg[i][j] = 0;
+        for (int64_t kc = k0; kc < k1; kc += 64) {
+            __syncthreads();
+            for (int i = threadIdx.x; i < 64 * 64; i += 256) {
+                int r = i >> 6, c = i & 63;
+                int64_t k = kc + c;
+                as_[r][c] = (m0 + r < M && k < k1) ? a[(m0 + r) * K + k] : (int8_t)0;
+                bs_[r][c] = (n0 + r < N && k < k1) ? bt[(n0 + r) * K + k] : (int8_t)0;
+            }
+            __syncthreads();
+#pragma unroll 4
+            for (int c = 0; c < 64; c += 4) {
+                int av[4], bv[4];
+#pragma unroll
+                for (int i = 0; i < 4; i++) av[i] = *reinterpret_cast<const int *>(&as_[ty * 4 + i][c]);
+#pragma unroll
+                for (int j = 0; j < 4; j++) bv[j] = *reinterpret_cast<const int *>(&bs_[tx * 4 + j][c]);
+#pragma unroll
+                for (int i = 0; i < 4; i++)
+#pragma unroll
+                    for (int j = 0; j < 4; j++) seg[i][j] = __dp4a(av[i], bv[j], seg[i][j]);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            const int64_t m = m0 + ty * 4 + i;
+            const float ra = (m < M) ? sa[(m / block) * nkb + kb] : 0.0f;
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const int64_t n = n0 + tx * 4 + j;
+                const float cb = (n < N) ? sb[kb * nnb + n / block] : 0.0f;
+                const float v = (float)seg[i][j];
+                acc[i][j] = exact ? __fadd_rn(acc[i][j], __fmul_rn(__fmul_rn(v, ra), cb)) : fmaf(v, ra * cb, acc[i][j]);
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        const int64_t m = m0 + ty * 4 + i;
+        if (m >= M) continue;
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const int64_t n = n0 + tx * 4 + j;
+            if (n >= N) continue;
+            float v = bias ? __fadd_rn(acc[i][j], bias[n]) : acc[i][j];
+            if (out_bf16) reinterpret_cast<__nv_bfloat16 *>(out)[m * N + n] = __float2bfloat16_rn(v);
+            else reinterpret_cast<float *>(out)[m * N + n] = v;
+        }
+    }
+}
+
+static int g_num_sms = 0;
+int num_sms() {
+    if (!g_num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0) g_num_sms = 148;
+    }
+    return g_num_sms;
+}
+
+int w8a8_dispatch(const int8_t *a, const float *sa, const int8_t *bt, const float *sb, const float *bias,
+                  int64_t M, int64_t N, int64_t K, int64_t block, void *out, int out_dtype, int exact,
+                  cudaStream_t st) {
+    TB_REQUIRE(block >= 1, "block must be >= 1");
+    TB_REQUIRE(block <= 1040, "block edge > 1040 (f32-exact segment bound) unsupported");
+    TB_REQUIRE(out_dtype == TB_F32 || out_dtype == TB_BF16, "out dtype must be f32 or bf16");
+    if (M == 0 || N == 0) return TB_OK;
+    const bool tc = block == 128 && K % 128 == 0 && N % 128 == 0 && K > 0 && M < (1ll << 31) &&
+                    ((uintptr_t)a % 16 == 0) && ((uintptr_t)bt % 16 == 0);
+    if (tc) {
+        CUtensorMap ta, tbm;
+        if (!make_tmap_2d(&ta, a, CU_TENSOR_MAP_DATA_TYPE_UINT8, K, M, K, 128, 128) ||
+            !make_tmap_2d(&tbm, bt, CU_TENSOR_MAP_DATA_TYPE_UINT8, K, N, K, 128, 128))
+            return fail(TB_ECUDA, "cuTensorMapEncodeTiled failed");
+        const int ntiles = (int)(cdiv(M, 128) * (N / 128));
+        const int grid = ntiles < num_sms() ? ntiles : num_sms();
+#define TB_GEMM_LAUNCH(E, B)                                                                               \
+    {                                                                                                      \
+        auto kern = w8a8_tc_kernel<E, B>;                                                                  \
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm::SMEM_BYTES);    \
+        kern<<<grid, gemm::THREADS, gemm::SMEM_BYTES, st>>>(ta, tbm, sa, sb, bias, out, (int)M, (int)N, (int)K); \
+    }
+        if (exact && out_dtype == TB_F32) TB_GEMM_LAUNCH(true, false)
+        else if (exact) TB_GEMM_LAUNCH(true, true)
+        else if (out_dtype == TB_F32) TB_GEMM_LAUNCH(false, false)
+        else TB_GEMM_LAUNCH(false, true)
+#undef TB_GEMM_LAUNCH
+        return check_launch("w8a8_tc");
+    }
+    dim3 grid((unsigned)cdiv(N, 64), (unsigned)cdiv(M, 64));
+    w8a8_simt_kernel<<<grid, 256, 0, st>>>(a, sa, bt, sb, bias, M, N, K, block, exact, out, out_dtype == TB_BF16);
+    return check_launch("w8a8_simt");
+}
+
+}  // namespace tb
+
+using namespace tb;
+
+extern "C" int tb_w8a8_gemm(const int8_t *a, const float *sa, const int8_t *bt, const float *sb, const float *bias,
+                            int64_t M, int64_t N, int64_t K, int64_t block, void *out, int out_dtype, void *stream) {
+    return w8a8_dispatch(a, sa, bt, sb, bias, M, N, K, block, out, out_dtype, 1, as_stream(stream));
+}
+
+extern "C" int tb_w8a8_gemm_fast(const int8_t *a, const float *sa, const int8_t *bt, const float *sb,
+                                 const float *bias, int64_t M, int64_t N, int64_t K, int64_t block, void *out,
+                                 int out_dtype, void *stream) {
+    return w8a8_dispatch(a, sa, bt, sb, bias, M, N, K, block, out, out_dtype, 0, as_stream(stream));
+}
+
+extern "C" int tb_quantized_linear(const void *x, int x_dtype, const int8_t *bt, const float *sb, const float *bias,
+                                   int64_t M, int64_t N, int64_t K, int64_t block, int8_t *xq_ws, float *xs_ws,
+                                   void *out, int out_dtype, void *stream) {
+    int rc = tb_quantize_blockwise(x, x_dtype, M, K, block, xq_ws, xs_ws, nullptr, stream);
+    if (rc) return rc;
+    return tb_w8a8_gemm(xq_ws, xs_ws, bt, sb, bias, M, N, K, block, out, out_dtype, stream);
+}

@@ -1,0 +1,299 @@
+"""Device-level operators: torch CUDA tensors in, torch CUDA tensors out.
+
+Each function is a thin shim over one C-ABI entry point (include/tb_capi.h);
+the CUDA kernels do the work.  The pipelines ``sla_attention`` and
+``quantized_linear`` are also registered as ``torch.library`` custom ops
+(``tb200::sla_attention``, ``tb200::quantized_linear``) so they compose with
+torch code and CUDA graphs.  Nothing here runs on the CPU: inputs must live on
+a CUDA device and the library must be built (no fallback).
+"""
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import _lib
+from ._lib import TB_BF16, TB_F32, call, dtype_code, ptr, stream_ptr
+
+
+def cdiv(a: int, b: int) -> int:
+    return -(-a // b)
+
+
+def _dev_tensor(t: torch.Tensor, name: str) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if t.dtype not in (torch.float32, torch.bfloat16):
+        t = t.float()
+    return t.contiguous()
+
+
+def _empty(shape, dtype, like: torch.Tensor):
+    return torch.empty(shape, dtype=dtype, device=like.device)
+
+
+# ------------------------------------------------------------------- quant
+
+def quantize_blockwise(x: torch.Tensor, block: int = 128, check_finite: bool = True):
+    """blockquant.py:91-110 -> (codes int8 [r,c], scales f32 [ceil(r/b),ceil(c/b)])."""
+    x = _dev_tensor(x, "x")
+    if x.dim() != 2:
+        raise ValueError(f"expected a matrix, got shape {tuple(x.shape)}")
+    r, c = x.shape
+    q = _empty((r, c), torch.int8, x)
+    s = _empty((cdiv(r, block), cdiv(c, block)), torch.float32, x)
+    flag = torch.zeros(1, dtype=torch.int32, device=x.device) if check_finite else None
+    call("tb_quantize_blockwise", ptr(x), dtype_code(x), r, c, block, ptr(q), ptr(s), ptr(flag), stream_ptr())
+    if check_finite and int(flag.item()) != 0:
+        raise ValueError("input contains non-finite values")
+    return q, s
+
+
+def dequantize_blockwise(q: torch.Tensor, scales: torch.Tensor, block: int):
+    r, c = q.shape
+    out = _empty((r, c), torch.float32, q)
+    call("tb_dequantize_blockwise", ptr(q), ptr(scales.contiguous()), r, c, block, ptr(out), stream_ptr())
+    return out
+
+
+def transpose_codes(q: torch.Tensor) -> torch.Tensor:
+    r, c = q.shape
+    out = _empty((c, r), torch.int8, q)
+    call("tb_transpose_codes", ptr(q.contiguous()), r, c, ptr(out), stream_ptr())
+    return out
+
+
+def w8a8_gemm(a_q, a_s, bt_q, b_s, block: int = 128, bias=None, out_dtype=torch.float32, exact: bool = True):
+    """blockquant.py:132-161 (+ bias).  bt_q is the TRANSPOSED weight code matrix [N, K]."""
+    M, K = a_q.shape
+    N = bt_q.shape[0]
+    if bt_q.shape[1] != K:
+        raise ValueError(f"inner dims differ: {K} vs {bt_q.shape[1]}")
+    out = _empty((M, N), out_dtype, a_q)
+    fn = "tb_w8a8_gemm" if exact else "tb_w8a8_gemm_fast"
+    call(fn, ptr(a_q.contiguous()), ptr(a_s.contiguous()), ptr(bt_q.contiguous()), ptr(b_s.contiguous()),
+         ptr(None if bias is None else bias.float().contiguous()), M, N, K, block, ptr(out),
+         TB_BF16 if out_dtype == torch.bfloat16 else TB_F32, stream_ptr())
+    return out
+
+
+def quantized_linear(x, bt_q, b_s, block: int = 128, bias=None, out_dtype=torch.float32, exact: bool = True,
+                     check_finite: bool = False):
+    """quantized_linear_forward (blockquant.py:164-182): activation quant + W8A8."""
+    xq, xs = quantize_blockwise(x, block, check_finite=check_finite)
+    return w8a8_gemm(xq, xs, bt_q, b_s, block, bias, out_dtype, exact)
+
+
+# ------------------------------------------------------ SLA block importance
+
+def pool_block_means(x: torch.Tensor, block: int) -> torch.Tensor:
+    """attention.py:256-266 (numpy reduceat order)."""
+    x = _dev_tensor(x, "x")
+    H, L, d = x.shape
+    out = _empty((H, cdiv(L, block), d), torch.float32, x)
+    call("tb_pool_block_means", ptr(x), dtype_code(x), H, L, d, block, ptr(out), stream_ptr())
+    return out
+
+
+def kmean(k: torch.Tensor) -> torch.Tensor:
+    """attention.py:187 (sequential chain over tokens)."""
+    k = _dev_tensor(k, "k")
+    H, L, d = k.shape
+    out = _empty((H, d), torch.float32, k)
+    call("tb_kmean", ptr(k), dtype_code(k), H, L, d, ptr(out), stream_ptr())
+    return out
+
+
+def pool_quant_tokens(x: torch.Tensor, block: int, center: torch.Tensor | None = None, pool: bool = True):
+    """attention.py:201-220 (+ fused pooling of raw x) -> (codes, scales, pooled|None)."""
+    x = _dev_tensor(x, "x")
+    H, L, d = x.shape
+    nb = cdiv(L, block)
+    codes = _empty((H, L, d), torch.int8, x)
+    scales = _empty((H, nb), torch.float32, x)
+    pooled = _empty((H, nb, d), torch.float32, x) if pool else None
+    call("tb_pool_quant_tokens", ptr(x), dtype_code(x), ptr(center), H, L, d, block, ptr(codes), ptr(scales),
+         ptr(pooled), stream_ptr())
+    return codes, scales, pooled
+
+
+def topk_count(ratio: float, nkv: int) -> int:
+    """attention.py:279."""
+    return math.ceil(ratio * nkv)
+
+
+def topk_blocks(qp: torch.Tensor, kp: torch.Tensor, count: int, want_comp: bool = True,
+                want_scores: bool = False):
+    """attention.py:269-284 + 122-132 -> (idx int32 [H,nq,count], comp uint8|None, scores|None)."""
+    qp, kp = qp.float().contiguous(), kp.float().contiguous()
+    H, nq, d = qp.shape
+    nkv = kp.shape[1]
+    idx = _empty((H, nq, count), torch.int32, qp)
+    comp = _empty((H, nq, nkv), torch.uint8, qp) if want_comp else None
+    scores = _empty((H, nq, nkv), torch.float32, qp) if want_scores else None
+    call("tb_topk_blocks", ptr(qp), ptr(kp), H, nq, nkv, d, count, ptr(idx), ptr(comp), ptr(scores), stream_ptr())
+    return idx, comp, scores
+
+
+def transpose_v(v: torch.Tensor, l_pad: int) -> torch.Tensor:
+    v = _dev_tensor(v, "v")
+    H, L, d = v.shape
+    vt = _empty((H, d, l_pad), torch.bfloat16, v)
+    call("tb_transpose_v", ptr(v), dtype_code(v), H, L, d, l_pad, ptr(vt), stream_ptr())
+    return vt
+
+
+def feature_map(x: torch.Tensor, l_pad: int, out_dtype=torch.float32) -> torch.Tensor:
+    """phi (attention.py:287-290) into [H, l_pad, d]; padding rows are 0."""
+    x = _dev_tensor(x, "x")
+    H, L, d = x.shape
+    out = _empty((H, l_pad, d), out_dtype, x)
+    call("tb_feature_map", ptr(x), dtype_code(x), H, L, d, l_pad, ptr(out),
+         TB_BF16 if out_dtype == torch.bfloat16 else TB_F32, stream_ptr())
+    return out
+
+
+def linear_branch(q, k, v, comp: torch.Tensor | None, q_block: int, kv_block: int, fast: bool = False):
+    """linear_attention over the complement mask (attention.py:293-335).
+
+    comp: uint8 [H, nq, nkv] (1 = block in the complement) or None for the
+    unmasked form.  Per-kv-block phi(K_b)^T V_b and sum phi(K_b), the
+    coverage GEMM cov . kv_part, then phi(Q_rows) . kv_sel per q block.  The
+    three batched GEMMs are plain cuBLAS GEMMs (bf16 operands with f32
+    accumulation when ``fast``, f32 otherwise); phi runs in tb_feature_map.
+    Returns (num f32 [H,L,d], den f32 [H,L]).
+    """
+    H, L, d = q.shape
+    dt = torch.bfloat16 if fast else torch.float32
+    if comp is None:
+        phik = feature_map(k, L, dt)
+        phiq = feature_map(q, L, dt)
+        kv = torch.bmm(phik.transpose(1, 2), v.to(dt))                      # [H, d, d]
+        k1 = phik.float().sum(dim=1)                                         # [H, d]
+        num = torch.bmm(phiq, kv).float()
+        den = torch.bmm(phiq.float(), k1[:, :, None])[..., 0]
+        return num, den
+    nq, nkv = comp.shape[1], comp.shape[2]
+    lk, lq = nkv * kv_block, nq * q_block
+    phik = feature_map(k, lk, dt)
+    phiq = feature_map(q, lq, dt)
+    vpad = torch.zeros((H, lk, d), dtype=dt, device=q.device)
+    vpad[:, :L] = v.to(dt)
+    kv_part = torch.bmm(phik.view(H * nkv, kv_block, d).transpose(1, 2), vpad.view(H * nkv, kv_block, d))
+    k1_part = phik.view(H, nkv, kv_block, d).float().sum(dim=2)             # [H, nkv, d]
+    cov = comp.to(dt)
+    kv_sel = torch.bmm(cov, kv_part.view(H, nkv, d * d))                     # [H, nq, d*d]
+    k1_sel = torch.bmm(cov.float(), k1_part)                                 # [H, nq, d]
+    num = torch.bmm(phiq.view(H * nq, q_block, d), kv_sel.view(H * nq, d, d)).view(H, lq, d)[:, :L]
+    den = torch.bmm(phiq.view(H * nq, q_block, d).float(), k1_sel.view(H * nq, d, 1)).view(H, lq)[:, :L]
+    return num.float().contiguous(), den.contiguous()
+
+
+def sla_args(**kw) -> _lib.SlaArgs:
+    a = _lib.SlaArgs()
+    for key, val in kw.items():
+        setattr(a, key, val)
+    return a
+
+
+def sla_attention(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: float = 0.1,
+                  linear_mix: float = 1.0, quantized: bool = True, scale: float | None = None,
+                  out_dtype=torch.float32, linear_fast: bool | None = None, return_parts: bool = False):
+    """sla_attention (attention.py:392-421) on device tensors [H, L, d]."""
+    q, k, v = _dev_tensor(q, "q"), _dev_tensor(k, "k"), _dev_tensor(v, "v")
+    if not (q.shape == k.shape == v.shape) or q.dim() != 3:
+        raise ValueError(f"q/k/v must share shape [heads, seq, head_dim], got "
+                         f"{tuple(q.shape)}, {tuple(k.shape)}, {tuple(v.shape)}")
+    if k.dtype != q.dtype or v.dtype != q.dtype:
+        k, v = k.to(q.dtype), v.to(q.dtype)
+    H, L, d = q.shape
+    if q_block > L or kv_block > L:
+        raise ValueError(f"block sizes {q_block}/{kv_block} exceed seq {L}")
+    scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+    nq, nkv = cdiv(L, q_block), cdiv(L, kv_block)
+    count = topk_count(topk_ratio, nkv)
+    parts = {}
+    if quantized:
+        qc, qs, qp = pool_quant_tokens(q, q_block, None, pool=True)
+        km = kmean(k)
+        kc, ks, kp = pool_quant_tokens(k, kv_block, km, pool=True)
+    else:
+        qc = qs = kc = ks = km = None
+        qp, kp = pool_block_means(q, q_block), pool_block_means(k, kv_block)
+    lin = count < nkv and linear_mix != 0.0
+    idx, comp, _ = topk_blocks(qp, kp, count, want_comp=lin or return_parts)
+    tc = quantized and d == 128 and q_block == 128 and kv_block == 64 and L >= 128
+    l_pad = nkv * 64
+    vt = transpose_v(v, l_pad) if tc else None
+    num_l = den_l = None
+    if lin:
+        fast = (H * L * d >= (1 << 22)) if linear_fast is None else linear_fast
+        num_l, den_l = linear_branch(q, k, v, comp, q_block, kv_block, fast=fast)
+    out = torch.empty((H, L, d), dtype=out_dtype, device=q.device)
+    row_max = torch.empty((H, L), dtype=torch.float32, device=q.device) if return_parts else None
+    den = torch.empty((H, L), dtype=torch.float32, device=q.device) if return_parts else None
+    args = sla_args(q=ptr(q), k=ptr(k), v=ptr(v), dtype=dtype_code(q), H=H, L=L, d=d, q_block=q_block,
+                    kv_block=kv_block, count=count, scale=scale, linear_mix=float(linear_mix),
+                    quantized=int(bool(quantized)), q_codes=ptr(qc), k_codes=ptr(kc), q_scales=ptr(qs),
+                    k_scales=ptr(ks), k_mean=ptr(km), idx=ptr(idx), vt=ptr(vt), l_pad=l_pad,
+                    num_l=ptr(num_l), den_l=ptr(den_l), out=ptr(out),
+                    out_dtype=TB_BF16 if out_dtype == torch.bfloat16 else TB_F32,
+                    row_max=ptr(row_max), den=ptr(den))
+    lib = _lib.load(require_device=True)
+    _lib.check(lib.tb_sla_attention(__import__("ctypes").byref(args), stream_ptr()), "tb_sla_attention")
+    if return_parts:
+        parts = dict(qp=qp, kp=kp, idx=idx, comp=comp, q_codes=qc, q_scales=qs, k_codes=kc, k_scales=ks,
+                     k_mean=km, num_l=num_l, den_l=den_l, row_max=row_max, den=den, count=count)
+        return out, parts
+    return out
+
+
+# ------------------------------------------------------------------ DiT rows
+
+def rmsnorm(x, gain, eps=1e-6):
+    x = x.float().contiguous()
+    out = torch.empty_like(x)
+    r, c = x.shape
+    call("tb_rmsnorm", ptr(x), ptr(gain.float().contiguous()), r, c, float(eps), ptr(out), stream_ptr())
+    return out
+
+
+def layernorm(x, gain, offset, eps=1e-6):
+    x = x.float().contiguous()
+    out = torch.empty_like(x)
+    r, c = x.shape
+    call("tb_layernorm", ptr(x), ptr(gain.float().contiguous()), ptr(offset.float().contiguous()), r, c,
+         float(eps), ptr(out), stream_ptr())
+    return out
+
+
+def gelu(x):
+    x = x.float().contiguous()
+    out = torch.empty_like(x)
+    call("tb_gelu", ptr(x), x.numel(), ptr(out), stream_ptr())
+    return out
+
+
+# --------------------------------------------------- torch.library registration
+
+@torch.library.custom_op("tb200::sla_attention", mutates_args=())
+def _sla_attention_op(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, q_block: int, kv_block: int,
+                      topk_ratio: float, linear_mix: float, quantized: bool) -> torch.Tensor:
+    return sla_attention(q, k, v, q_block, kv_block, topk_ratio, linear_mix, quantized)
+
+
+@_sla_attention_op.register_fake
+def _(q, k, v, q_block, kv_block, topk_ratio, linear_mix, quantized):
+    return torch.empty(q.shape, dtype=torch.float32, device=q.device)
+
+
+@torch.library.custom_op("tb200::quantized_linear", mutates_args=())
+def _quantized_linear_op(x: torch.Tensor, bt_q: torch.Tensor, b_s: torch.Tensor, block: int,
+                         bias: torch.Tensor | None, exact: bool) -> torch.Tensor:
+    return quantized_linear(x, bt_q, b_s, block, bias, torch.float32, exact)
+
+
+@_quantized_linear_op.register_fake
+def _(x, bt_q, b_s, block, bias, exact):
+    return torch.empty((x.shape[0], bt_q.shape[0]), dtype=torch.float32, device=x.device)

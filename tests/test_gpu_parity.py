@@ -1,0 +1,217 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the CPU oracle.
+
+Bit-exact for pools, k_mean, codes, scales, top-k indices and W8A8 (exact
+mode); cos >= 0.999 and rel-L1 <= 1e-2 for attention outputs (north-star
+tolerance), stated per assertion.
+"""
+import numpy as np
+import pytest
+import torch
+
+import gen
+from conftest import load_golden
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+COS_MIN, REL_L1_MAX = 0.999, 1e-2
+
+
+@pytest.fixture(scope="module")
+def tb():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2512_16093_b200 as pkg
+    from paper_2512_16093_b200 import _lib, ops
+    _lib.load(require_device=True)
+    return ops
+
+
+def dev(a, bf16=False):
+    t = torch.from_numpy(np.ascontiguousarray(a, np.float32)).cuda()
+    return t.to(torch.bfloat16) if bf16 else t
+
+
+def metrics(got, ref):
+    return O.error_metrics(np.asarray(got, np.float32), np.asarray(ref, np.float32))
+
+
+# ------------------------------------------------------------ quantization
+
+@pytest.mark.parametrize("case", gen.QUANT_CASES, ids=lambda c: c[0])
+def test_quantize_blockwise_bit_exact(tb, case):
+    name, seed, r, c, scale, block = case
+    m = gen.gaussian_matrix(seed, r, c, scale)
+    q, s = tb.quantize_blockwise(dev(m), block)
+    oq, os_ = O.quantize_blockwise(m, block)
+    assert np.array_equal(q.cpu().numpy(), oq)
+    assert np.array_equal(s.cpu().numpy(), os_)
+    g = load_golden("quant")
+    assert np.array_equal(s.cpu().numpy(), g[name + ".scales"])
+
+
+def test_quantize_blockwise_cfg2_activation_bf16(tb):
+    """cfg2 activation [32760, 1536] bf16 (last row block has 120 rows)."""
+    m = gen.gaussian_matrix(31, 32760, 1536, bf16=True)
+    q, s = tb.quantize_blockwise(dev(m, bf16=True), 128)
+    oq, os_ = O.quantize_blockwise(m, 128)
+    assert np.array_equal(s.cpu().numpy(), os_)
+    assert np.array_equal(q.cpu().numpy(), oq)
+    q32, s32 = tb.quantize_blockwise(dev(m), 128)     # same values as f32 -> same codes
+    assert torch.equal(q32, q) and torch.equal(s32, s)
+
+
+def test_quantize_rejects_nonfinite(tb):
+    m = np.zeros((4, 4), np.float32)
+    m[1, 2] = np.inf
+    with pytest.raises(ValueError):
+        tb.quantize_blockwise(dev(m), 128)
+
+
+def test_quantize_zero_and_constant_blocks(tb):
+    q, s = tb.quantize_blockwise(dev(np.zeros((130, 260), np.float32)), 128)
+    assert not q.any() and not s.any()
+    c = np.float32(0.731)
+    q, s = tb.quantize_blockwise(dev(np.full((128, 128), 127 * c, np.float32)), 128)
+    assert bool((q == 127).all()) and abs(float(s[0, 0]) - c) < 1e-6
+
+
+# ------------------------------------------------------------------- W8A8
+
+W8A8_TC = [("tc_300x512x256", 41, 300, 512, 256, 128), ("tc_128x1536x1536", 42, 128, 1536, 1536, 128),
+           ("tc_1000x256x384", 43, 1000, 256, 384, 128)]
+
+
+@pytest.mark.parametrize("case", gen.W8A8_CASES + [c + (True,) for c in W8A8_TC], ids=lambda c: c[0])
+def test_w8a8_bit_exact(tb, case):
+    name, seed, M, K, N, block, with_bias = case
+    x = gen.gaussian_matrix(seed, M, K)
+    w = gen.gaussian_matrix(seed + 1, K, N, 1.0 / np.sqrt(K))
+    bias = gen.gaussian_matrix(seed + 2, 1, N)[0] if with_bias else None
+    wq, ws = O.quantize_blockwise(w, block)
+    want = O.quantized_linear(x, wq, ws, block, bias)
+    bt = tb.transpose_codes(torch.from_numpy(wq).cuda())
+    got = tb.quantized_linear(dev(x), bt, dev(ws), block, None if bias is None else dev(bias), exact=True)
+    got = got.cpu().numpy()
+    assert np.array_equal(got, want), f"{int((got != want).sum())} mismatches"
+    fast = tb.quantized_linear(dev(x), bt, dev(ws), block, None if bias is None else dev(bias), exact=False)
+    cos, _, rel1 = metrics(fast.cpu().numpy(), want)
+    assert cos >= 0.99999 and rel1 <= 1e-4
+
+
+def test_w8a8_cfg2_shape_rows_exact(tb):
+    """cfg2 (M=32760, K=1536, N=4608) on the tensor cores; rows checked against the oracle."""
+    M, K, N = 32760, 1536, 4608
+    x = gen.gaussian_matrix(50, M, K, bf16=True)
+    w = gen.gaussian_matrix(51, K, N, 1.0 / np.sqrt(K))
+    wq, ws = O.quantize_blockwise(w, 128)
+    bt = tb.transpose_codes(torch.from_numpy(wq).cuda())
+    xq, xs = tb.quantize_blockwise(dev(x, bf16=True), 128)
+    got = tb.w8a8_gemm(xq, xs, bt, dev(ws), 128).cpu().numpy()
+    xq_n, xs_n = xq.cpu().numpy(), xs.cpu().numpy()
+    for rb in (0, 97, 255):                         # first, middle, ragged last row block
+        r0, r1 = rb * 128, min(rb * 128 + 128, M)
+        want = O.w8a8(xq_n[r0:r1], xs_n[rb:rb + 1], wq, ws, 128)
+        assert np.array_equal(got[r0:r1], want), rb
+
+
+# --------------------------------------------------------- SLA importance
+
+def _inputs(case):
+    name, g_, seed, h, s, d, qb, kvb, ratio = case
+    q, k, v = gen.make_inputs(g_, seed, h, s, d)
+    return q, k, v, g_ in ("G", "B")
+
+
+@pytest.mark.parametrize("case", gen.ATTN_CASES, ids=lambda c: c[0])
+def test_block_importance_bit_exact(tb, case):
+    name, g_, seed, h, s, d, qb, kvb, ratio = case
+    q, k, v, is_bf16 = _inputs(case)
+    g = load_golden("attn_" + name)
+    for use_bf16 in ([False, True] if is_bf16 else [False]):
+        qd, kd = dev(q, use_bf16), dev(k, use_bf16)
+        qc, qs, qp = tb.pool_quant_tokens(qd, qb, None, pool=True)
+        km = tb.kmean(kd)
+        kc, ks, kp = tb.pool_quant_tokens(kd, kvb, km, pool=True)
+        assert np.array_equal(qp.cpu().numpy(), O.pool_block_means(q, qb))
+        assert np.array_equal(kp.cpu().numpy(), O.pool_block_means(k, kvb))
+        assert np.array_equal(km.cpu().numpy(), g["k_mean"])
+        assert np.array_equal(qs.cpu().numpy(), g["q_scales"])
+        assert np.array_equal(ks.cpu().numpy(), g["k_scales"])
+        oqc, _ = O.quant_token_blocks(q, qb)
+        kcen, _ = O.smooth_keys(k)
+        okc, _ = O.quant_token_blocks(kcen, kvb)
+        assert np.array_equal(qc.cpu().numpy(), oqc)
+        assert np.array_equal(kc.cpu().numpy(), okc)
+        count = O.topk_count(ratio, kp.shape[1])
+        idx, comp, scores = tb.topk_blocks(qp, kp, count, want_comp=True, want_scores=True)
+        assert np.array_equal(scores.cpu().numpy(), O.block_scores(O.pool_block_means(q, qb),
+                                                                   O.pool_block_means(k, kvb)))
+        assert np.array_equal(idx.cpu().numpy().astype(np.int64), g["idx"])
+        cov = O.coverage(g["idx"], kp.shape[1])
+        assert np.array_equal(comp.cpu().numpy().astype(bool), ~cov)
+
+
+def test_topk_kats(tb):
+    scores = np.array([[[3, 1, 2, 0], [0, 0, 1, 5]]], dtype=np.float32)
+    idx, _, _ = tb.topk_blocks(dev(scores), dev(np.eye(4, dtype=np.float32)[None]), 2)
+    assert idx[0].tolist() == [[0, 2], [2, 3]]
+    idx, _, _ = tb.topk_blocks(dev(np.zeros((1, 1, 4))), dev(np.ones((1, 8, 4))), 2)
+    assert idx[0, 0].tolist() == [0, 1]
+    sc = np.array([[[0.0, -0.0, 1.0, -0.0]]], np.float32)
+    idx, _, _ = tb.topk_blocks(dev(sc), dev(np.eye(4, dtype=np.float32)[None]), 2)
+    assert idx[0, 0].tolist() == [0, 2]
+    idx, comp, _ = tb.topk_blocks(dev(np.random.default_rng(0).standard_normal((2, 3, 8))),
+                                  dev(np.random.default_rng(1).standard_normal((2, 5, 8))), 5)
+    assert np.array_equal(idx.cpu().numpy(), np.broadcast_to(np.arange(5), (2, 3, 5)))
+    assert not comp.any()
+
+
+def test_topk_random_ties_match_oracle(tb):
+    rng = np.random.default_rng(5)
+    qp = rng.integers(-2, 3, (3, 40, 16)).astype(np.float32)       # heavy ties
+    kp = rng.integers(-2, 3, (3, 300, 16)).astype(np.float32)
+    for ratio in (0.05, 0.1, 0.37, 0.99):
+        count = O.topk_count(ratio, 300)
+        idx, _, _ = tb.topk_blocks(dev(qp), dev(kp), count)
+        assert np.array_equal(idx.cpu().numpy().astype(np.int64), O.select_topk(qp, kp, ratio)), ratio
+
+
+# ---------------------------------------------------------- SLA attention
+
+SLA_CASES = [c for c in gen.ATTN_CASES if c[4] <= 4096]
+
+
+@pytest.mark.parametrize("case", SLA_CASES, ids=lambda c: c[0])
+@pytest.mark.parametrize("mix", [1.0, 0.0])
+def test_sla_attention_tolerance(tb, case, mix):
+    name, g_, seed, h, s, d, qb, kvb, ratio = case
+    q, k, v, is_bf16 = _inputs(case)
+    want = O.sla_attention(q, k, v, qb, kvb, ratio, mix)
+    g = load_golden("attn_" + name)
+    for use_bf16 in ([False, True] if is_bf16 else [False]):
+        got = tb.sla_attention(dev(q, use_bf16), dev(k, use_bf16), dev(v, use_bf16), qb, kvb, ratio, mix)
+        got = got.cpu().numpy()
+        cos, _, rel1 = metrics(got, want)
+        assert cos >= COS_MIN and rel1 <= REL_L1_MAX, (use_bf16, cos, rel1)
+        cos, _, rel1 = metrics(got[:, ::7, :], g[f"sla_mix{mix:g}.rows"])
+        assert cos >= COS_MIN and rel1 <= REL_L1_MAX, ("golden", cos, rel1)
+
+
+def test_sla_tensor_core_path_sparse_dominated(tb):
+    """Block-coherent inputs (sparse branch dominates): the tcgen05 kernel
+    with BF16 P/V must stay within rel-L1 1e-2 of the f32-PV oracle."""
+    q, k, v = gen.block_coherent_qkv(11, 4, 4096, 128, blk=64)
+    for mix in (1.0, 0.0):
+        want = O.sla_attention(q, k, v, 128, 64, 0.1, mix)
+        got = tb.sla_attention(dev(q, True), dev(k, True), dev(v, True), 128, 64, 0.1, mix).cpu().numpy()
+        cos, _, rel1 = metrics(got, want)
+        assert cos >= COS_MIN and rel1 <= REL_L1_MAX, (mix, cos, rel1)
+
+
+def test_sla_topk_one_equals_dense_unquantized(tb):
+    q, k, v = gen.gaussian_qkv(21, 2, 128, 16, bf16=False)
+    out = tb.sla_attention(dev(q), dev(k), dev(v), 32, 32, 1.0, 1.0, quantized=False).cpu().numpy()
+    ref = O.reference_attention(q, k, v)
+    _, rel2, _ = O.error_metrics(out, ref)
+    assert rel2 <= 1e-5
