@@ -184,23 +184,28 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             m_true = fmaxf(m_true, mx);
             if (j == 0) {
                 m_ref = mx;
-            } else if (mx > m_ref + 8.0f) {
-                // rebase O to the new reference: needs PV(j-1) complete
-                ptx::mbar_wait(&S.p_empty[(j - 1) & 1], (uint32_t)(((j - 1) >> 1) & 1));
-                ptx::tc_fence_after();
-                const float alpha = ex2(m_ref - mx);
+            } else {
+                // lazy rebase of O when a row's max outgrows its reference by
+                // > 8 (p <= 256).  tcgen05.ld/st are warp-collective, so the
+                // decision is made per warp; rows that do not need it use 1.
+                const bool need = mx > m_ref + 8.0f;
+                if (__any_sync(0xffffffffu, need)) {
+                    ptx::mbar_wait(&S.p_empty[(j - 1) & 1], (uint32_t)(((j - 1) >> 1) & 1));  // PV(j-1) done
+                    ptx::tc_fence_after();
+                    const float alpha = need ? ex2(m_ref - mx) : 1.0f;
 #pragma unroll 1
-                for (int c = 0; c < D; c += 16) {
-                    uint32_t o[16];
-                    ptx::tmem_ld16(TM_O + lane_base + c, o);
-                    ptx::tmem_wait_ld();
+                    for (int c = 0; c < D; c += 16) {
+                        uint32_t o[16];
+                        ptx::tmem_ld16(TM_O + lane_base + c, o);
+                        ptx::tmem_wait_ld();
 #pragma unroll
-                    for (int i = 0; i < 16; i++) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-                    ptx::tmem_st16(TM_O + lane_base + c, o);
+                        for (int i = 0; i < 16; i++) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+                        ptx::tmem_st16(TM_O + lane_base + c, o);
+                    }
+                    ptx::tmem_wait_st();
+                    l *= alpha;
+                    if (need) m_ref = mx;
                 }
-                ptx::tmem_wait_st();
-                l *= alpha;
-                m_ref = mx;
             }
             float psum = 0.0f;
             uint32_t pk[32];
