@@ -121,6 +121,10 @@ typedef struct tb_sla_args {
     int64_t l_pad;                     /* padded token stride of vt */
     /* linear branch over the complement (may be NULL -> no linear term) */
     const float *num_l, *den_l;        /* [H,L,d], [H,L] */
+    /* packed linear branch: when lin_ld != 0, row r of head h is
+     * num_l + h*lin_hs + r*lin_ld (d numerators followed by the
+     * denominator at column d; den_l is ignored) */
+    int64_t lin_ld, lin_hs;
     /* outputs */
     float *out;                        /* [H,L,d] f32 (or bf16 when out_dtype) */
     int out_dtype;
@@ -144,6 +148,16 @@ int tb_transpose_v(const void *v, int dtype, int64_t H, int64_t L, int64_t d, in
  * so padded kv blocks contribute nothing to phi(K)^T V (attention.py:320-325). */
 int tb_feature_map(const void *x, int dtype, int64_t H, int64_t L, int64_t d, int64_t l_pad,
                    void *out, int out_dtype, void *stream);
+
+/* Linear-branch and PV operands in one pass over q, k, v
+ * (attention.py:306-325): phiq [H,lq,d] = phi(q), phik [H,lk,d] = phi(k)
+ * (rows >= L zero), vext [H,lk,dx] = [v | 1 | 0..] so that phi(K_b)^T vext
+ * carries both phi(K_b)^T V_b and sum phi(K_b) (column d), and the bf16
+ * V^T [H,d,lvt] B operand of the PV MMA.  Any of phiq / phik(+vext) / vt may
+ * be NULL.  out_dtype bf16 or f32; d % 8 == 0, dx % 8 == 0, dx > d. */
+int tb_linear_operands(const void *q, const void *k, const void *v, int dtype, int64_t H, int64_t L,
+                       int64_t d, int64_t lq, int64_t lk, int64_t dx, void *phiq, void *phik,
+                       void *vext, int out_dtype, void *vt, int64_t lvt, void *stream);
 
 /* Fast-mode W8A8: identical operands, the two block scales folded into one
  * FMA per element (tolerance-level, not bit-exact); used by the DiT step. */

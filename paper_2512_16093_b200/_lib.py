@@ -40,6 +40,7 @@ SIGNATURES = {
     "tb_sla_attention": [_P, _P],
     "tb_transpose_v": [_P, _i, _I, _I, _I, _I, _P, _P],
     "tb_feature_map": [_P, _i, _I, _I, _I, _I, _P, _i, _P],
+    "tb_linear_operands": [_P, _P, _P, _i, _I, _I, _I, _I, _I, _I, _P, _P, _P, _i, _P, _I, _P],
     "tb_rmsnorm": [_P, _P, _I, _I, _f, _P, _P],
     "tb_layernorm": [_P, _P, _P, _I, _I, _f, _P, _P],
     "tb_gelu": [_P, _I, _P, _P],
@@ -62,6 +63,7 @@ class SlaArgs(ctypes.Structure):
         ("vt", _P),
         ("l_pad", _I),
         ("num_l", _P), ("den_l", _P),
+        ("lin_ld", _I), ("lin_hs", _I),
         ("out", _P),
         ("out_dtype", _i),
         ("row_max", _P), ("den", _P),

@@ -237,7 +237,7 @@ def linear_attention(inputs: AttnInputs, mask_complement: BlockMask | None = Non
     q, k, v = _dev(inputs.q), _dev(inputs.k), _dev(inputs.v)
     h, s, d = q.shape
     if mask_complement is None:
-        num, den = ops.linear_branch(q, k, v, None, s, s, fast=False)
+        pack = ops.linear_branch(q, k, v, None, s, s, fast=False)
     else:
         nkv = -(-s // mask_complement.kv_block)
         if nkv != mask_complement.num_kv_blocks:
@@ -246,8 +246,9 @@ def linear_attention(inputs: AttnInputs, mask_complement: BlockMask | None = Non
             z = torch.zeros((h, s, d), device=q.device)
             return _ret(z, inputs.numpy_io), _ret(z[..., 0], inputs.numpy_io)
         comp = _comp_from_mask(mask_complement, h)
-        num, den = ops.linear_branch(q, k, v, comp, mask_complement.q_block, mask_complement.kv_block, fast=False)
-    return _ret(num, inputs.numpy_io), _ret(den, inputs.numpy_io)
+        pack = ops.linear_branch(q, k, v, comp, mask_complement.q_block, mask_complement.kv_block, fast=False)
+    num, den = pack[:, :s, :d], pack[:, :s, d]
+    return _ret(num.contiguous(), inputs.numpy_io), _ret(den.contiguous(), inputs.numpy_io)
 
 
 def _gather_positions(sel_blocks, seq: int, block: int) -> np.ndarray:

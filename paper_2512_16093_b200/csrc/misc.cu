@@ -38,6 +38,105 @@ __global__ void feature_map_kernel(const T *__restrict__ x, int64_t H, int64_t L
     else out[i] = r;
 }
 
+// One pass over q, k, v producing every operand the SLA pipeline derives
+// from the raw tensors besides codes/pools (attention.py:306-334 and the PV
+// B operand), in the GEMM dtype O (bf16 or f32):
+//   phiq [H,lq,d]  phi(q), zero rows t >= L                  (may be NULL)
+//   phik [H,lk,d]  phi(k), zero rows t >= L: padding rows must contribute
+//                  nothing to phi(K)^T V (phi(0) = 1 != 0)     (may be NULL)
+//   vext [H,lk,dx] [v | 1 | 0...]: the ones column makes phi(K)^T vext carry
+//                  sum_t phi(k_t), the denominator term, in column d
+//   vt   [H,d,lvt] bf16 V^T, zero padded (K-major B operand of the PV MMA)
+// CTA = one head x 64 tokens; thread = 8 channels of one token row; V^T is
+// transposed through shared memory (row pitch d+2 keeps it conflict-free).
+template <typename T, typename O>
+__global__ void __launch_bounds__(256) linear_operands_kernel(
+    const T *__restrict__ q, const T *__restrict__ k, const T *__restrict__ v, int64_t L, int d, int64_t lq,
+    int64_t lk, int dx, O *__restrict__ phiq, O *__restrict__ phik, O *__restrict__ vext,
+    __nv_bfloat16 *__restrict__ vt, int64_t lvt) {
+    extern __shared__ __align__(16) __nv_bfloat16 vs[];   // [64][d+2]
+    const int64_t h = blockIdx.y;
+    const int64_t t0 = blockIdx.x * 64LL;
+    const int cg = d / 8;
+    const int rows = blockDim.x / cg;
+    const int tx = threadIdx.x % cg, ty = threadIdx.x / cg;
+    const int c0 = tx * 8;
+    auto st = [](O *dst, const float *x) {
+        if constexpr (sizeof(O) == 2) {
+            uint4 w;
+            __nv_bfloat162 *p = reinterpret_cast<__nv_bfloat162 *>(&w);
+#pragma unroll
+            for (int i = 0; i < 4; i++) p[i] = __floats2bfloat162_rn(x[2 * i], x[2 * i + 1]);
+            *reinterpret_cast<uint4 *>(dst) = w;
+        } else {
+            *reinterpret_cast<float4 *>(dst) = make_float4(x[0], x[1], x[2], x[3]);
+            *reinterpret_cast<float4 *>(dst + 4) = make_float4(x[4], x[5], x[6], x[7]);
+        }
+    };
+    auto ld = [&](const T *src, float *x, bool in) {
+        if (!in) {
+#pragma unroll
+            for (int i = 0; i < 8; i++) x[i] = 0.0f;
+            return;
+        }
+        if constexpr (sizeof(T) == 2) {
+            uint4 w = *reinterpret_cast<const uint4 *>(src);
+            const __nv_bfloat162 *p = reinterpret_cast<const __nv_bfloat162 *>(&w);
+#pragma unroll
+            for (int i = 0; i < 4; i++) { float2 f = __bfloat1622float2(p[i]); x[2 * i] = f.x; x[2 * i + 1] = f.y; }
+        } else {
+            float4 a = *reinterpret_cast<const float4 *>(src), b = *reinterpret_cast<const float4 *>(src + 4);
+            x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+        }
+    };
+    const int pitch = d + 2;
+    for (int tr = ty; tr < 64; tr += rows) {
+        const int64_t t = t0 + tr;
+        const bool in = t < L;
+        const int64_t off = (h * L + (in ? t : 0)) * d + c0;
+        float xv[8];
+        ld(v + off, xv, in);
+        if (vt) {
+#pragma unroll
+            for (int i = 0; i < 8; i++) vs[tr * pitch + c0 + i] = __float2bfloat16_rn(xv[i]);
+        }
+        if (phiq && t < lq) {
+            float xq[8];
+            ld(q + off, xq, in);
+#pragma unroll
+            for (int i = 0; i < 8; i++) xq[i] = in ? phi(xq[i]) : 0.0f;
+            st(phiq + (h * lq + t) * d + c0, xq);
+        }
+        if (phik && t < lk) {
+            float xk[8];
+            ld(k + off, xk, in);
+#pragma unroll
+            for (int i = 0; i < 8; i++) xk[i] = in ? phi(xk[i]) : 0.0f;
+            st(phik + (h * lk + t) * d + c0, xk);
+            st(vext + (h * lk + t) * dx + c0, xv);
+            if (tx == 0) {
+                float e[8] = {in ? 1.0f : 0.0f, 0, 0, 0, 0, 0, 0, 0};
+                for (int c = d; c < dx; c += 8) {
+                    st(vext + (h * lk + t) * dx + c, e);
+                    e[0] = 0.0f;
+                }
+            }
+        }
+    }
+    if (!vt || t0 >= lvt) return;
+    __syncthreads();
+    // V^T rows: channel c, 64 tokens = 8 chunks of 8 tokens (16 B each)
+    for (int i = threadIdx.x; i < d * 8; i += blockDim.x) {
+        const int c = i >> 3, tc = (i & 7) * 8;
+        if (t0 + tc >= lvt) continue;
+        uint4 w;
+        uint16_t *p = reinterpret_cast<uint16_t *>(&w);
+#pragma unroll
+        for (int j = 0; j < 8; j++) p[j] = __bfloat16_as_ushort(vs[(tc + j) * pitch + c]);
+        *reinterpret_cast<uint4 *>(vt + (h * d + c) * lvt + t0 + tc) = w;
+    }
+}
+
 // one warp per row
 __global__ void rmsnorm_kernel(const float *__restrict__ x, const float *__restrict__ g, int64_t rows,
                                int64_t cols, float eps, float *__restrict__ out) {
@@ -115,6 +214,36 @@ extern "C" int tb_feature_map(const void *x, int dtype, int64_t H, int64_t L, in
     else
         feature_map_kernel<__nv_bfloat16, float><<<grid, 256, 0, st>>>((const __nv_bfloat16 *)x, H, L, d, l_pad, (float *)out);
     return check_launch("feature_map");
+}
+
+extern "C" int tb_linear_operands(const void *q, const void *k, const void *v, int dtype, int64_t H, int64_t L,
+                                  int64_t d, int64_t lq, int64_t lk, int64_t dx, void *phiq, void *phik, void *vext,
+                                  int out_dtype, void *vt, int64_t lvt, void *stream) {
+    TB_REQUIRE(d % 8 == 0 && d <= 256, "head_dim must be a multiple of 8 (<= 256)");
+    TB_REQUIRE(!phik || (vext && dx >= d + 1 && dx % 8 == 0), "vext needs dx >= d+1, dx % 8 == 0");
+    TB_REQUIRE((!phiq || lq >= L) && (!phik || lk >= L) && (!vt || lvt >= L), "padded lengths must cover L");
+    TB_REQUIRE(!vt || lvt % 8 == 0, "lvt must be a multiple of 8");
+    if (H == 0) return TB_OK;
+    int64_t lmax = 0;
+    if (phiq && lq > lmax) lmax = lq;
+    if (phik && lk > lmax) lmax = lk;
+    if (vt && lvt > lmax) lmax = lvt;
+    if (lmax == 0) return TB_OK;
+    const int cg = (int)(d / 8);
+    const int threads = (256 / cg) * cg;
+    dim3 grid((unsigned)cdiv(lmax, 64), (unsigned)H);
+    const size_t smem = vt ? (size_t)64 * (d + 2) * 2 : 0;
+    cudaStream_t st = as_stream(stream);
+#define TB_LINOP(T, O)                                                                                           \
+    linear_operands_kernel<T, O><<<grid, threads, smem, st>>>((const T *)q, (const T *)k, (const T *)v, L, (int)d, \
+                                                              lq, lk, (int)dx, (O *)phiq, (O *)phik, (O *)vext,  \
+                                                              (__nv_bfloat16 *)vt, lvt)
+    if (dtype == TB_F32 && out_dtype == TB_BF16) TB_LINOP(float, __nv_bfloat16);
+    else if (dtype == TB_F32) TB_LINOP(float, float);
+    else if (out_dtype == TB_BF16) TB_LINOP(__nv_bfloat16, __nv_bfloat16);
+    else TB_LINOP(__nv_bfloat16, float);
+#undef TB_LINOP
+    return check_launch("linear_operands");
 }
 
 extern "C" int tb_rmsnorm(const float *x, const float *gain, int64_t rows, int64_t cols, float eps, float *out,

@@ -192,9 +192,11 @@ __global__ void __launch_bounds__(128) pool_quant_tokens_kernel(
 }
 
 // Fast path for d == 128, block <= 129 (the hot-path shapes): 128 threads,
-// thread c owns channel c; the tile is staged in registers once so the pool,
-// absmax and code passes read HBM a single time.  Codes are written by
-// transposing through shared memory so each warp stores contiguous 128 B rows.
+// thread c owns channel c.  Pass 1 streams the tile once in token order,
+// computing the numpy reduceat pooled sum (seed + pairwise of the rest, the
+// 8-accumulator body of FLOAT_pairwise_sum consumed as the values arrive) and
+// the absmax; pass 2 re-reads the (L1-resident) tile for the codes, which are
+// transposed through shared memory so each warp stores contiguous 128 B rows.
 template <typename T, int BLOCK>
 __global__ void __launch_bounds__(128) pool_quant_tokens_d128_kernel(
     const T *__restrict__ x, const float *__restrict__ center, int64_t L, int64_t nb,
@@ -207,52 +209,46 @@ __global__ void __launch_bounds__(128) pool_quant_tokens_d128_kernel(
     const int c = threadIdx.x;
     const T *xb = x + (h * L + lo) * 128 + c;
     const float ctr = center ? center[h * 128 + c] : 0.0f;
-    float v[BLOCK];
-#pragma unroll
-    for (int t = 0; t < BLOCK; t++) v[t] = (t < e) ? to_f32(xb[(int64_t)t * 128]) : 0.0f;
-    if (pooled) {
-        // x[lo] + pairwise(x[lo+1 : lo+e]) with n = e-1 <= 128
-        float acc = v[0];
-        const int n = e - 1;
-        if (n > 0) {
-            float res;
-            if (n < 8) {
-                res = -0.0f;
-#pragma unroll
-                for (int i = 0; i < 8; i++) if (i < n) res = __fadd_rn(res, v[1 + i]);
-            } else {
-                float r[8];
-#pragma unroll
-                for (int j = 0; j < 8; j++) r[j] = v[1 + j];
-                const int full = n - (n % 8);
-#pragma unroll
-                for (int i = 8; i + 8 <= BLOCK - 1; i += 8)
-                    if (i < full) {
-#pragma unroll
-                        for (int j = 0; j < 8; j++) r[j] = __fadd_rn(r[j], v[1 + i + j]);
-                    }
-                res = __fadd_rn(__fadd_rn(__fadd_rn(r[0], r[1]), __fadd_rn(r[2], r[3])),
-                                __fadd_rn(__fadd_rn(r[4], r[5]), __fadd_rn(r[6], r[7])));
-#pragma unroll
-                for (int i = 0; i < BLOCK - 1; i++)
-                    if (i >= full && i < n) res = __fadd_rn(res, v[1 + i]);
-            }
-            acc = __fadd_rn(acc, res);
-        }
-        pooled[(h * nb + b) * 128 + c] = __fdiv_rn(acc, (float)e);
-    }
+    auto ld = [&](int t) { return to_f32(xb[(int64_t)t * 128]); };
     float am = 0.0f;
+    const float seed = ld(0);
+    am = fabsf(seed - ctr);
+    const int n = e - 1;                               // values after the seed
+    float res = -0.0f;
+    if (n >= 8) {
+        float r[8];
 #pragma unroll
-    for (int t = 0; t < BLOCK; t++) {
-        if (center) v[t] = __fsub_rn(v[t], ctr);
-        if (t < e) am = fmaxf(am, fabsf(v[t]));
+        for (int j = 0; j < 8; j++) { r[j] = ld(1 + j); am = fmaxf(am, fabsf(r[j] - ctr)); }
+        const int full = n - (n % 8);
+        for (int i = 8; i < full; i += 8) {
+            float w[8];
+#pragma unroll
+            for (int j = 0; j < 8; j++) w[j] = ld(1 + i + j);
+#pragma unroll
+            for (int j = 0; j < 8; j++) { r[j] = __fadd_rn(r[j], w[j]); am = fmaxf(am, fabsf(w[j] - ctr)); }
+        }
+        res = __fadd_rn(__fadd_rn(__fadd_rn(r[0], r[1]), __fadd_rn(r[2], r[3])),
+                        __fadd_rn(__fadd_rn(r[4], r[5]), __fadd_rn(r[6], r[7])));
+        for (int i = full; i < n; i++) { const float w = ld(1 + i); res = __fadd_rn(res, w); am = fmaxf(am, fabsf(w - ctr)); }
+    } else {
+        for (int i = 0; i < n; i++) { const float w = ld(1 + i); res = __fadd_rn(res, w); am = fmaxf(am, fabsf(w - ctr)); }
+    }
+    if (pooled) {
+        const float acc = (n > 0) ? __fadd_rn(seed, res) : seed;
+        pooled[(h * nb + b) * 128 + c] = __fdiv_rn(acc, (float)e);
     }
     am = block_max_nonneg(am, red);
     const float s = quant_scale(am);
     if (threadIdx.x == 0) scales[h * nb + b] = s;
     const float safe = (s == 0.0f) ? 1.0f : s;
+    for (int t0 = 0; t0 < e; t0 += 8) {
+        float w[8];
 #pragma unroll
-    for (int t = 0; t < BLOCK; t++) stile[t][c] = quant_code(v[t], safe);
+        for (int j = 0; j < 8; j++) w[j] = (t0 + j < e) ? ld(t0 + j) : 0.0f;
+#pragma unroll
+        for (int j = 0; j < 8; j++)
+            if (t0 + j < e) stile[t0 + j][c] = quant_code(center ? __fsub_rn(w[j], ctr) : w[j], safe);
+    }
     __syncthreads();
     int8_t *cb = codes + (h * L + lo) * 128;
     const uint4 *st = reinterpret_cast<const uint4 *>(&stile[0][0]);

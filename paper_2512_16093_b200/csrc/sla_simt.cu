@@ -86,19 +86,26 @@ __global__ void __launch_bounds__(128) sla_simt_kernel(tb_sla_args a, int64_t nq
         }
         // combine with the linear branch (attention.py:410-421)
         const bool lin = a.num_l != nullptr && a.linear_mix != 0.0f;
+        const float *nl_row = nullptr;
         float ss = 1.0f, shrink = 0.0f, dl = 0.0f;
         if (lin) {
             const float ref = fmaxf(m, 0.0f);
             ss = expf(m - ref);
             shrink = expf(-ref) * a.linear_mix;
-            dl = a.den_l[h * L + row];
+            if (a.lin_ld) {
+                nl_row = a.num_l + h * a.lin_hs + row * a.lin_ld;
+                dl = nl_row[d];
+            } else {
+                nl_row = a.num_l + (h * L + row) * d;
+                dl = a.den_l[h * L + row];
+            }
         }
         const float den = lin ? (l * ss + shrink * dl) : l;
 #pragma unroll
         for (int i = 0; i < MAXC; i++) {
             const int64_t c = lane + 32 * i;
             if (c < d) {
-                float num = lin ? (acc[i] * ss + shrink * a.num_l[(h * L + row) * d + c]) : acc[i];
+                float num = lin ? (acc[i] * ss + shrink * nl_row[c]) : acc[i];
                 float o = num / den;
                 if (a.out_dtype == TB_BF16)
                     reinterpret_cast<__nv_bfloat16 *>(a.out)[(h * L + row) * d + c] = __float2bfloat16_rn(o);

@@ -7,19 +7,23 @@
 // One CTA per (head, 128-row q-block); two CTAs per SM so one CTA's softmax
 // overlaps the other's tensor-core work.  Warp roles (192 threads):
 //   warps 0-3  softmax/epilogue, thread = query row = TMEM lane
-//   warp 4     TMA producer: Q codes once, then for each selected kv block the
-//              K code tile (64x128 int8) and the V^T tile (128x64 bf16) into a
-//              2-stage ring (128B-swizzled, mbarrier complete_tx)
+//   warp 4     TMA producer: Q codes once; per selected kv block the K code
+//              tile (64x128 int8) into a 3-stage ring and the V^T tile
+//              (128x64 bf16) into a separate 3-stage ring (128B swizzle,
+//              mbarrier complete_tx), so K can run ahead of V
 //   warp 5     MMA issuer (one elected thread):
 //                S_j  = Qc . Kc_j^T   4 x tcgen05.mma kind::i8  (M128 N64 K32) -> s32 TMEM
-//                O   += P_j . V_j     4 x tcgen05.mma kind::f16 (M128 N128 K16) -> f32 TMEM
+//                O   += P_j . V_j     4 x tcgen05.mma kind::f16 (M128 N128 K16), A = P_j in TMEM
 //              issued as QK(j+1) before PV(j) so QK overlaps softmax(j).
+// TMEM (256 cols): two 64-col S buffers; P_j (bf16, 2 per column, 32 cols)
+// overwrites S_j in place (FA4-style), so PV reads A straight from TMEM and
+// the tensor pipe's in-order execution protects the S/P buffer reuse; O is
+// the f32 accumulator in cols 128-255.
 // Softmax per block (log2 domain): logit2 = s32 * (sq*sk*scale*log2e) +
 // corr*scale*log2e with corr = q_row . k_mean; running reference max with
 // lazy O rescaling (only when the block max exceeds it by > 8, i.e. p <=
-// 256); P in bf16 written straight into the 128B-swizzled K-major smem
-// layout the PV MMA reads.  Epilogue: O and l rebased to the true row max,
-// combined with the linear branch exactly as attention.py:416-421.
+// 256).  Epilogue: O and l rebased to the true row max, combined with the
+// linear branch exactly as attention.py:416-421.
 #include "common.cuh"
 #include "ptx.cuh"
 #include "tmap.cuh"
@@ -27,20 +31,19 @@
 namespace tb {
 
 namespace sla {
-constexpr int BM = 128, BN = 64, D = 128, STAGES = 2;
+constexpr int BM = 128, BN = 64, D = 128, KSTAGES = 3, VSTAGES = 3;
 constexpr int THREADS = 192;
 constexpr uint32_t Q_BYTES = BM * D;          // int8
 constexpr uint32_t K_BYTES = BN * D;          // int8
 constexpr uint32_t V_BYTES = D * BN * 2;      // bf16 V^T tile
-constexpr uint32_t P_BYTES = BM * BN * 2;     // bf16
 struct Smem {
     uint8_t q[Q_BYTES];
-    uint8_t p[2][P_BYTES];
-    uint8_t v[STAGES][V_BYTES];
-    uint8_t k[STAGES][K_BYTES];
+    uint8_t v[VSTAGES][V_BYTES];
+    uint8_t k[KSTAGES][K_BYTES];
     uint64_t q_full, o_final;
-    uint64_t kv_full[STAGES], kv_empty[STAGES];
-    uint64_t s_full[2], s_empty[2], p_full[2], p_empty[2];
+    uint64_t k_full[KSTAGES], k_empty[KSTAGES];
+    uint64_t v_full[VSTAGES], v_empty[VSTAGES];
+    uint64_t s_full[2], p_full[2], pv_done[2];
     uint32_t tmem_base;
 };
 constexpr size_t SMEM_BYTES = sizeof(Smem) + 1024;
@@ -70,12 +73,12 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
     if (warp == 4 && lane == 0) {
         ptx::mbar_init(&S.q_full, 1);
         ptx::mbar_init(&S.o_final, 1);
-        for (int s = 0; s < STAGES; s++) { ptx::mbar_init(&S.kv_full[s], 1); ptx::mbar_init(&S.kv_empty[s], 1); }
+        for (int s = 0; s < KSTAGES; s++) { ptx::mbar_init(&S.k_full[s], 1); ptx::mbar_init(&S.k_empty[s], 1); }
+        for (int s = 0; s < VSTAGES; s++) { ptx::mbar_init(&S.v_full[s], 1); ptx::mbar_init(&S.v_empty[s], 1); }
         for (int b = 0; b < 2; b++) {
             ptx::mbar_init(&S.s_full[b], 1);
-            ptx::mbar_init(&S.s_empty[b], 128);
             ptx::mbar_init(&S.p_full[b], 128);
-            ptx::mbar_init(&S.p_empty[b], 1);
+            ptx::mbar_init(&S.pv_done[b], 1);
         }
         ptx::fence_barrier_init();
         ptx::prefetch_tmap(&tm_q);
@@ -95,13 +98,14 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             ptx::mbar_arrive_expect_tx(&S.q_full, Q_BYTES);
             ptx::tma_load_3d(S.q, &tm_q, 0, n * BM, h, &S.q_full);
             for (int j = 0; j < count; j++) {
-                const int st = j % STAGES;
-                const uint32_t par = (uint32_t)((j / STAGES) & 1);
                 const int b = __ldg(sel + j);
-                ptx::mbar_wait(&S.kv_empty[st], par ^ 1);
-                ptx::mbar_arrive_expect_tx(&S.kv_full[st], K_BYTES + V_BYTES);
-                ptx::tma_load_3d(S.k[st], &tm_k, 0, b * BN, h, &S.kv_full[st]);
-                ptx::tma_load_3d(S.v[st], &tm_v, b * BN, 0, h, &S.kv_full[st]);
+                const int ks = j % KSTAGES, vs = j % VSTAGES;
+                ptx::mbar_wait_sleep(&S.k_empty[ks], (uint32_t)(((j / KSTAGES) & 1) ^ 1));
+                ptx::mbar_arrive_expect_tx(&S.k_full[ks], K_BYTES);
+                ptx::tma_load_3d(S.k[ks], &tm_k, 0, b * BN, h, &S.k_full[ks]);
+                ptx::mbar_wait_sleep(&S.v_empty[vs], (uint32_t)(((j / VSTAGES) & 1) ^ 1));
+                ptx::mbar_arrive_expect_tx(&S.v_full[vs], V_BYTES);
+                ptx::tma_load_3d(S.v[vs], &tm_v, b * BN, 0, h, &S.v_full[vs]);
             }
         }
     } else if (warp == 5) {
@@ -110,29 +114,30 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             constexpr uint32_t ID_QK = ptx::idesc_i8(BM, BN);
             constexpr uint32_t ID_PV = ptx::idesc_bf16(BM, D);
             const uint64_t qd = ptx::sdesc_sw128(ptx::smem_u32(S.q));
-            ptx::mbar_wait(&S.q_full, 0);
+            ptx::mbar_wait_sleep(&S.q_full, 0);
             auto pv = [&](int i) {
-                const int pb = i & 1, st = i % STAGES;
-                ptx::mbar_wait(&S.p_full[pb], (uint32_t)((i >> 1) & 1));
+                const int pb = i & 1, vs = i % VSTAGES;
+                ptx::mbar_wait_sleep(&S.v_full[vs], (uint32_t)((i / VSTAGES) & 1));
+                ptx::mbar_wait_sleep(&S.p_full[pb], (uint32_t)((i >> 1) & 1));
                 ptx::tc_fence_after();
-                const uint64_t pd = ptx::sdesc_sw128(ptx::smem_u32(S.p[pb]));
-                const uint64_t vd = ptx::sdesc_sw128(ptx::smem_u32(S.v[st]));
+                const uint64_t vd = ptx::sdesc_sw128(ptx::smem_u32(S.v[vs]));
 #pragma unroll
-                for (int k = 0; k < BN / 16; k++)   // K=16 bf16 = 32 B per MMA
-                    ptx::mma_f16(TM_O, pd + 2 * k, vd + 2 * k, ID_PV, (i > 0 || k > 0) ? 1u : 0u);
-                ptx::mma_commit(&S.p_empty[pb]);
-                ptx::mma_commit(&S.kv_empty[st]);
+                for (int k = 0; k < BN / 16; k++)   // K=16 bf16 per MMA: 8 TMEM cols of P, 32 B of V^T
+                    ptx::mma_f16_ts(TM_O, tmem + pb * BN + 8 * k, vd + 2 * k, ID_PV, (i > 0 || k > 0) ? 1u : 0u);
+                ptx::mma_commit(&S.pv_done[pb]);
+                ptx::mma_commit(&S.v_empty[vs]);
             };
             for (int j = 0; j < count; j++) {
-                const int st = j % STAGES, sb = j & 1;
-                ptx::mbar_wait(&S.kv_full[st], (uint32_t)((j / STAGES) & 1));
-                if (j >= 2) ptx::mbar_wait(&S.s_empty[sb], (uint32_t)(((j >> 1) - 1) & 1));
+                const int ks = j % KSTAGES, sb = j & 1;
+                ptx::mbar_wait_sleep(&S.k_full[ks], (uint32_t)((j / KSTAGES) & 1));
                 ptx::tc_fence_after();
-                const uint64_t kd = ptx::sdesc_sw128(ptx::smem_u32(S.k[st]));
+                const uint64_t kd = ptx::sdesc_sw128(ptx::smem_u32(S.k[ks]));
+                // S_sb last held P_{j-2}, read by PV(j-2), issued earlier: in-order tensor pipe
 #pragma unroll
                 for (int k = 0; k < D / 32; k++)    // K=32 int8 = 32 B per MMA
                     ptx::mma_i8(tmem + sb * BN, qd + 2 * k, kd + 2 * k, ID_QK, k > 0 ? 1u : 0u);
                 ptx::mma_commit(&S.s_full[sb]);
+                ptx::mma_commit(&S.k_empty[ks]);
                 if (j >= 1) pv(j - 1);
             }
             pv(count - 1);
@@ -155,31 +160,39 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
         }
         const float c0 = corr * scale2;
         const float sq = __ldg(a.q_scales + (int64_t)h * nq + n);
+        const float *ksc = a.k_scales + (int64_t)h * nkv;
         const int last_blk = nkv - 1;
         const int last_ext = L - last_blk * BN;
         float m_ref = -INFINITY, m_true = -INFINITY, l = 0.0f;
-        uint8_t *prow0 = S.p[0] + r * 128;
-        uint8_t *prow1 = S.p[1] + r * 128;
+        int b_next = __ldg(sel);
+        float sk_next = __ldg(ksc + b_next);
         for (int j = 0; j < count; j++) {
             const int sb = j & 1;
-            const int b = __ldg(sel + j);
-            const float c1 = sq * __ldg(a.k_scales + (int64_t)h * nkv + b) * scale2;
-            ptx::mbar_wait(&S.s_full[sb], (uint32_t)((j >> 1) & 1));
+            const int b = b_next;
+            const float c1 = sq * sk_next * scale2;
+            // s32 -> f32 via the 1.5*2^23 magic: x = M + s exactly; fold -M*c1 into the offset
+            const float c0m = fmaf(-12582912.0f, c1, c0);
+            if (j + 1 < count) { b_next = __ldg(sel + j + 1); sk_next = __ldg(ksc + b_next); }
+            ptx::mbar_wait_sleep(&S.s_full[sb], (uint32_t)((j >> 1) & 1));
             ptx::tc_fence_after();
             uint32_t s[4][16];
 #pragma unroll
             for (int q4 = 0; q4 < 4; q4++) ptx::tmem_ld16(tmem + lane_base + sb * BN + q4 * 16, s[q4]);
             ptx::tmem_wait_ld();
-            ptx::tc_fence_before();
-            ptx::mbar_arrive(&S.s_empty[sb]);
             float t[64];
             float mx = -INFINITY;
-            const int lim = (b == last_blk) ? last_ext : BN;
 #pragma unroll
             for (int i = 0; i < 64; i++) {
-                const float x = __int_as_float((int)s[i >> 4][i & 15] + 0x4B400000) - 12582912.0f;
-                t[i] = (i < lim) ? fmaf(x, c1, c0) : -INFINITY;
+                t[i] = fmaf(__int_as_float((int)s[i >> 4][i & 15] + 0x4B400000), c1, c0m);
                 mx = fmaxf(mx, t[i]);
+            }
+            if (b == last_blk && last_ext < BN) {   // ragged final kv block (uniform per CTA)
+                mx = -INFINITY;
+#pragma unroll
+                for (int i = 0; i < 64; i++) {
+                    if (i >= last_ext) t[i] = -INFINITY;
+                    mx = fmaxf(mx, t[i]);
+                }
             }
             m_true = fmaxf(m_true, mx);
             if (j == 0) {
@@ -190,7 +203,7 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
                 // decision is made per warp; rows that do not need it use 1.
                 const bool need = mx > m_ref + 8.0f;
                 if (__any_sync(0xffffffffu, need)) {
-                    ptx::mbar_wait(&S.p_empty[(j - 1) & 1], (uint32_t)(((j - 1) >> 1) & 1));  // PV(j-1) done
+                    ptx::mbar_wait_sleep(&S.pv_done[(j - 1) & 1], (uint32_t)(((j - 1) >> 1) & 1));
                     ptx::tc_fence_after();
                     const float alpha = need ? ex2(m_ref - mx) : 1.0f;
 #pragma unroll 1
@@ -202,47 +215,45 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
                         for (int i = 0; i < 16; i++) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
                         ptx::tmem_st16(TM_O + lane_base + c, o);
                     }
-                    ptx::tmem_wait_st();
                     l *= alpha;
                     if (need) m_ref = mx;
                 }
             }
             float psum = 0.0f;
-            uint32_t pk[32];
+            uint32_t pk[2][16];
 #pragma unroll
             for (int i = 0; i < 64; i += 2) {
                 const float p0 = ex2(t[i] - m_ref), p1 = ex2(t[i + 1] - m_ref);
                 psum += p0 + p1;
                 __nv_bfloat162 pp = __floats2bfloat162_rn(p0, p1);
-                pk[i >> 1] = *reinterpret_cast<uint32_t *>(&pp);
+                pk[i >> 5][(i >> 1) & 15] = *reinterpret_cast<uint32_t *>(&pp);
             }
             l += psum;
-            if (j >= 2) ptx::mbar_wait(&S.p_empty[sb], (uint32_t)(((j >> 1) - 1) & 1));
-            uint8_t *prow = sb ? prow1 : prow0;
-#pragma unroll
-            for (int c = 0; c < 8; c++) {
-                const int phys = c ^ (r & 7);
-                *reinterpret_cast<uint4 *>(prow + phys * 16) =
-                    make_uint4(pk[c * 4], pk[c * 4 + 1], pk[c * 4 + 2], pk[c * 4 + 3]);
-            }
-            ptx::fence_async_smem();
+            // P_j overwrites S_j's first 32 columns (A operand of PV, bf16x2 per column)
+            ptx::tmem_st16(tmem + lane_base + sb * BN, pk[0]);
+            ptx::tmem_st16(tmem + lane_base + sb * BN + 16, pk[1]);
+            ptx::tmem_wait_st();
             ptx::tc_fence_before();
             ptx::mbar_arrive(&S.p_full[sb]);
         }
         // ------------------------------------------------------- epilogue
-        ptx::mbar_wait(&S.o_final, 0);
+        ptx::mbar_wait_sleep(&S.o_final, 0);
         ptx::tc_fence_after();
         // rebase to the true row max (natural-log units for the combine)
         const float f = ex2(m_ref - m_true);
         const float m_nat = m_true * LN2;           // log2-domain max -> natural units
         const float l_true = l * f;
         const bool lin = a.num_l != nullptr && a.linear_mix != 0.0f;
+        const int64_t lin_ld = a.lin_ld ? a.lin_ld : D;
+        const int64_t lin_hs = a.lin_hs ? a.lin_hs : (int64_t)L * lin_ld;
+        const float *nl_row = lin ? a.num_l + (int64_t)h * lin_hs + (int64_t)row * lin_ld : nullptr;
+        const float *dl_ptr = lin ? (a.lin_ld ? nl_row + D : a.den_l + (int64_t)h * L + row) : nullptr;
         float ss = f, shrink = 0.0f, den = l_true;
         if (lin && row_ok) {
             const float ref = fmaxf(m_nat, 0.0f);
             const float e_ss = expf(m_nat - ref);
             shrink = expf(-ref) * a.linear_mix;
-            den = l_true * e_ss + shrink * a.den_l[(int64_t)h * L + row];
+            den = l_true * e_ss + shrink * *dl_ptr;
             ss = f * e_ss;
         }
         const float inv = 1.0f / den;
@@ -261,7 +272,7 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             if (lin) {
 #pragma unroll
                 for (int i = 0; i < 16; i += 4) {
-                    const float4 nl = *reinterpret_cast<const float4 *>(a.num_l + off + i);
+                    const float4 nl = *reinterpret_cast<const float4 *>(nl_row + c + i);
                     v[i] = (__uint_as_float(o[i]) * ss + shrink * nl.x) * inv;
                     v[i + 1] = (__uint_as_float(o[i + 1]) * ss + shrink * nl.y) * inv;
                     v[i + 2] = (__uint_as_float(o[i + 2]) * ss + shrink * nl.z) * inv;

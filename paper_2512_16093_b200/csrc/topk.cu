@@ -26,8 +26,7 @@ __global__ void __launch_bounds__(256) topk_kernel(
     int small_path, int32_t *__restrict__ idx, uint8_t *__restrict__ comp, float *__restrict__ scores_out) {
     extern __shared__ __align__(16) uint8_t smem[];
     uint32_t *keys = reinterpret_cast<uint32_t *>(smem);                    // [R][nkv]
-    float *qrow = reinterpret_cast<float *>(smem + (size_t)R * nkv * 4);    // [R][d]
-    __shared__ uint32_t hist[8][256];
+    float *qrow = reinterpret_cast<float *>(smem + (((size_t)R * nkv * 4 + 15) & ~(size_t)15));  // [R][d]
     const int h = blockIdx.y;
     const int row0 = blockIdx.x * R;
     const int nrows = min(R, nq - row0);
@@ -37,6 +36,46 @@ __global__ void __launch_bounds__(256) topk_kernel(
     }
     __syncthreads();
     const float *kph = kp + (int64_t)h * nkv * d;
+    if (!small_path && (d & 3) == 0 && (((uintptr_t)kph) & 15) == 0) {
+        // Regular-sgemm order (one fmaf chain per score over t ascending),
+        // register-tiled: each thread owns JT kv columns x R rows and steps t
+        // by 4 with float4 loads of kp and broadcast float4 reads of qp.
+        constexpr int JT = 4;
+        for (int j0 = threadIdx.x * JT; j0 < nkv; j0 += blockDim.x * JT) {
+            float acc[R][JT];
+#pragma unroll
+            for (int r = 0; r < R; r++)
+#pragma unroll
+                for (int u = 0; u < JT; u++) acc[r][u] = 0.0f;
+            const float *kr[JT];
+#pragma unroll
+            for (int u = 0; u < JT; u++) kr[u] = kph + (int64_t)min(j0 + u, nkv - 1) * d;
+            for (int t = 0; t < d; t += 4) {
+                float4 kv[JT];
+#pragma unroll
+                for (int u = 0; u < JT; u++) kv[u] = __ldg(reinterpret_cast<const float4 *>(kr[u] + t));
+#pragma unroll
+                for (int r = 0; r < R; r++) {
+                    const float4 qv = *reinterpret_cast<const float4 *>(qrow + r * d + t);
+#pragma unroll
+                    for (int u = 0; u < JT; u++) {
+                        acc[r][u] = __fmaf_rn(qv.x, kv[u].x, acc[r][u]);
+                        acc[r][u] = __fmaf_rn(qv.y, kv[u].y, acc[r][u]);
+                        acc[r][u] = __fmaf_rn(qv.z, kv[u].z, acc[r][u]);
+                        acc[r][u] = __fmaf_rn(qv.w, kv[u].w, acc[r][u]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < R; r++)
+#pragma unroll
+                for (int u = 0; u < JT; u++)
+                    if (r < nrows && j0 + u < nkv) {
+                        keys[r * nkv + j0 + u] = desc_key(acc[r][u]);
+                        if (scores_out) scores_out[((int64_t)h * nq + row0 + r) * nkv + j0 + u] = acc[r][u];
+                    }
+        }
+    } else
     for (int j = threadIdx.x; j < nkv; j += blockDim.x) {
         const float *kr = kph + (int64_t)j * d;
         float acc[R];
@@ -75,51 +114,29 @@ __global__ void __launch_bounds__(256) topk_kernel(
     for (int r = warp; r < nrows; r += 8) {
         const uint32_t *kr = keys + r * nkv;
         const int64_t row = (int64_t)h * nq + row0 + r;
-        uint32_t prefix = 0, pmask = 0;
-        int need = count;                         // how many still to take among keys matching prefix
-        uint32_t *hs = hist[warp];
-        for (int pass = 0; pass < 4 && count < nkv; pass++) {
-            const int shift = 24 - 8 * pass;
+        // Threshold key T = the count-th largest key: greedy bitwise search
+        // from the MSB (32 rounds of a warp-wide count of keys >= candidate),
+        // no atomics.  need = how many keys equal to T are taken.
+        uint32_t T = 0;
+        if (count < nkv) {
+            for (int bit = 31; bit >= 0; bit--) {
+                const uint32_t cand = T | (1u << bit);
+                int c = 0;
+                for (int j = lane; j < nkv; j += 32) c += kr[j] >= cand;
 #pragma unroll
-            for (int b = lane; b < 256; b += 32) hs[b] = 0;
-            __syncwarp();
-            for (int j = lane; j < nkv; j += 32) {
-                uint32_t k = kr[j];
-                if ((k & pmask) == prefix) atomicAdd(&hs[(k >> shift) & 255], 1u);
+                for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+                if (c >= count) T = cand;
             }
-            __syncwarp();
-            // lane l owns digits 255-8l .. 248-8l (descending)
-            uint32_t loc[8], tot = 0;
+        }
+        int need = count;
+        if (count < nkv) {
+            int gtc = 0;
+            for (int j = lane; j < nkv; j += 32) gtc += kr[j] > T;
 #pragma unroll
-            for (int q = 0; q < 8; q++) { loc[q] = hs[255 - 8 * lane - q]; tot += loc[q]; }
-            uint32_t incl = tot;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                uint32_t n = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += n;
-            }
-            const uint32_t excl = incl - tot;
-            const bool here = excl < (uint32_t)need && incl >= (uint32_t)need;
-            const unsigned ball = __ballot_sync(0xffffffffu, here);
-            const int src = __ffs(ball) - 1;
-            uint32_t digit = 0, above = 0;
-            if (lane == src) {
-                uint32_t run = excl;
-#pragma unroll
-                for (int q = 0; q < 8; q++) {
-                    if (run + loc[q] >= (uint32_t)need) { digit = 255 - 8 * lane - q; above = run; break; }
-                    run += loc[q];
-                }
-            }
-            digit = __shfl_sync(0xffffffffu, digit, src);
-            above = __shfl_sync(0xffffffffu, above, src);
-            need -= (int)above;
-            prefix |= digit << shift;
-            pmask |= 255u << shift;
-            __syncwarp();
+            for (int o = 16; o > 0; o >>= 1) gtc += __shfl_xor_sync(0xffffffffu, gtc, o);
+            need = count - gtc;
         }
         // compaction in ascending index order
-        const uint32_t T = prefix;
         const bool take_all = count >= nkv;
         int taken = 0, ties = 0;
         for (int base = 0; base < nkv; base += 32) {
@@ -155,7 +172,7 @@ extern "C" int tb_topk_blocks(const float *qp, const float *kp, int64_t H, int64
     cudaStream_t st = as_stream(stream);
 #define TB_TOPK(R)                                                                                 \
     {                                                                                              \
-        size_t smem = (size_t)(R) * nkv * 4 + (size_t)(R) * d * 4;                                 \
+        size_t smem = (((size_t)(R) * nkv * 4 + 15) & ~(size_t)15) + (size_t)(R) * d * 4;          \
         cudaFuncSetAttribute(topk_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
         dim3 grid((unsigned)cdiv(nq, R), (unsigned)H);                                             \
         topk_kernel<R><<<grid, 256, smem, st>>>(qp, kp, (int)nq, (int)nkv, (int)d, (int)count, small, \

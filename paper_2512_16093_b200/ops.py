@@ -154,40 +154,81 @@ def feature_map(x: torch.Tensor, l_pad: int, out_dtype=torch.float32) -> torch.T
     return out
 
 
-def linear_branch(q, k, v, comp: torch.Tensor | None, q_block: int, kv_block: int, fast: bool = False):
+def linear_operands(q, k, v, lq: int, lk: int, dx: int, dtype=torch.bfloat16, lvt: int = 0, linear: bool = True):
+    """tb_linear_operands -> (phiq [H,lq,d], phik [H,lk,d], vext [H,lk,dx] = [v | 1 | 0], vt [H,d,lvt] | None)."""
+    q, k, v = _dev_tensor(q, "q"), _dev_tensor(k, "k"), _dev_tensor(v, "v")
+    H, L, d = q.shape
+    phiq = _empty((H, lq, d), dtype, q) if linear else None
+    phik = _empty((H, lk, d), dtype, q) if linear else None
+    vext = _empty((H, lk, dx), dtype, q) if linear else None
+    vt = _empty((H, d, lvt), torch.bfloat16, q) if lvt else None
+    call("tb_linear_operands", ptr(q), ptr(k), ptr(v), dtype_code(q), H, L, d, lq, lk, dx, ptr(phiq), ptr(phik),
+         ptr(vext), TB_BF16 if dtype == torch.bfloat16 else TB_F32, ptr(vt), lvt, stream_ptr())
+    return phiq, phik, vext, vt
+
+
+def _phi_t(x, rows):
+    """phi on device for head dims outside the vectorised kernel (d % 8 != 0)."""
+    H, L, d = x.shape
+    out = torch.zeros((H, rows, d), dtype=torch.float32, device=x.device)
+    xf = x.float()
+    out[:, :L] = torch.where(xf >= 0, xf + 1.0, torch.exp(torch.clamp(xf, max=0.0)))
+    return out
+
+
+def linear_branch(q, k, v, comp: torch.Tensor | None, q_block: int, kv_block: int, fast: bool = False,
+                  lvt: int = 0):
     """linear_attention over the complement mask (attention.py:293-335).
 
     comp: uint8 [H, nq, nkv] (1 = block in the complement) or None for the
-    unmasked form.  Per-kv-block phi(K_b)^T V_b and sum phi(K_b), the
-    coverage GEMM cov . kv_part, then phi(Q_rows) . kv_sel per q block.  The
-    three batched GEMMs are plain cuBLAS GEMMs (bf16 operands with f32
-    accumulation when ``fast``, f32 otherwise); phi runs in tb_feature_map.
-    Returns (num f32 [H,L,d], den f32 [H,L]).
+    unmasked form.  One operand pass (tb_linear_operands: phi(Q), phi(K) and
+    V extended with a ones column, so the denominator rides along as column
+    d), then three batched GEMMs on cuBLAS: kv_part = phi(K_b)^T [V_b|1] per
+    kv block, kv_sel = cov . kv_part per q block, num = phi(Q_rows) . kv_sel
+    (f32 output).  bf16 operands with f32 accumulation when ``fast``, f32
+    otherwise.  Returns the packed f32 tensor [H, lq, dx] (columns 0..d-1 =
+    numerator, column d = denominator) with lq = nq*q_block (or L when comp is
+    None).
     """
     H, L, d = q.shape
     dt = torch.bfloat16 if fast else torch.float32
+    dx = -(-(d + 1) // 16) * 16
     if comp is None:
-        phik = feature_map(k, L, dt)
-        phiq = feature_map(q, L, dt)
-        kv = torch.bmm(phik.transpose(1, 2), v.to(dt))                      # [H, d, d]
-        k1 = phik.float().sum(dim=1)                                         # [H, d]
-        num = torch.bmm(phiq, kv).float()
-        den = torch.bmm(phiq.float(), k1[:, :, None])[..., 0]
-        return num, den
-    nq, nkv = comp.shape[1], comp.shape[2]
+        q_block = kv_block = L
+        nq = nkv = 1
+    else:
+        nq, nkv = comp.shape[1], comp.shape[2]
     lk, lq = nkv * kv_block, nq * q_block
-    phik = feature_map(k, lk, dt)
-    phiq = feature_map(q, lq, dt)
-    vpad = torch.zeros((H, lk, d), dtype=dt, device=q.device)
-    vpad[:, :L] = v.to(dt)
-    kv_part = torch.bmm(phik.view(H * nkv, kv_block, d).transpose(1, 2), vpad.view(H * nkv, kv_block, d))
-    k1_part = phik.view(H, nkv, kv_block, d).float().sum(dim=2)             # [H, nkv, d]
-    cov = comp.to(dt)
-    kv_sel = torch.bmm(cov, kv_part.view(H, nkv, d * d))                     # [H, nq, d*d]
-    k1_sel = torch.bmm(cov.float(), k1_part)                                 # [H, nq, d]
-    num = torch.bmm(phiq.view(H * nq, q_block, d), kv_sel.view(H * nq, d, d)).view(H, lq, d)[:, :L]
-    den = torch.bmm(phiq.view(H * nq, q_block, d).float(), k1_sel.view(H * nq, d, 1)).view(H, lq)[:, :L]
-    return num.float().contiguous(), den.contiguous()
+    vt = None
+    if d % 8 == 0:
+        phiq, phik, vext, vt = linear_operands(q, k, v, lq, lk, dx, dt, lvt=lvt)
+    else:
+        phiq, phik = _phi_t(q, lq).to(dt), _phi_t(k, lk).to(dt)
+        vext = torch.zeros((H, lk, dx), dtype=dt, device=q.device)
+        vext[:, :L, :d] = v.to(dt)
+        vext[:, :L, d] = 1.0
+    kv_part = torch.bmm(phik.view(H * nkv, kv_block, d).transpose(1, 2), vext.view(H * nkv, kv_block, dx))
+    if comp is None:
+        kv_sel = kv_part.view(H, d, dx)
+    else:
+        kv_sel = torch.bmm(comp.to(dt), kv_part.view(H, nkv, d * dx))           # [H, nq, d*dx]
+    out_dtype = torch.float32 if dt == torch.bfloat16 else None
+    num = torch.bmm(phiq.view(H * nq, q_block, d), kv_sel.reshape(H * nq, d, dx), out_dtype=out_dtype) \
+        if out_dtype else torch.bmm(phiq.view(H * nq, q_block, d), kv_sel.reshape(H * nq, d, dx))
+    if lvt:
+        return num.view(H, lq, dx), vt
+    return num.view(H, lq, dx)
+
+
+_SIDE = {}
+
+
+def _side_stream() -> torch.cuda.Stream:
+    dev = torch.cuda.current_device()
+    s = _SIDE.get(dev)
+    if s is None:
+        s = _SIDE[dev] = torch.cuda.Stream(device=dev)
+    return s
 
 
 def sla_args(**kw) -> _lib.SlaArgs:
@@ -214,22 +255,34 @@ def sla_attention(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: fl
     nq, nkv = cdiv(L, q_block), cdiv(L, kv_block)
     count = topk_count(topk_ratio, nkv)
     parts = {}
+    lin = count < nkv and linear_mix != 0.0
+    tc = quantized and d == 128 and q_block == 128 and kv_block == 64 and L >= 128
+    l_pad = nkv * 64
+    main = torch.cuda.current_stream()
     if quantized:
+        # k_mean is a latency-bound sequential chain on H CTAs: overlap it with
+        # the Q pass (and the V^T pass below) on a side stream
+        side = _side_stream()
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            km = kmean(k)
         qc, qs, qp = pool_quant_tokens(q, q_block, None, pool=True)
-        km = kmean(k)
-        kc, ks, kp = pool_quant_tokens(k, kv_block, km, pool=True)
     else:
         qc = qs = kc = ks = km = None
         qp, kp = pool_block_means(q, q_block), pool_block_means(k, kv_block)
-    lin = count < nkv and linear_mix != 0.0
+    vt = None
+    if tc and not lin:
+        _, _, _, vt = linear_operands(q, k, v, 0, 0, 0, lvt=l_pad, linear=False)
+    if quantized:
+        main.wait_stream(side)
+        km.record_stream(main)
+        kc, ks, kp = pool_quant_tokens(k, kv_block, km, pool=True)
     idx, comp, _ = topk_blocks(qp, kp, count, want_comp=lin or return_parts)
-    tc = quantized and d == 128 and q_block == 128 and kv_block == 64 and L >= 128
-    l_pad = nkv * 64
-    vt = transpose_v(v, l_pad) if tc else None
-    num_l = den_l = None
+    lin_pack = None
     if lin:
         fast = (H * L * d >= (1 << 22)) if linear_fast is None else linear_fast
-        num_l, den_l = linear_branch(q, k, v, comp, q_block, kv_block, fast=fast)
+        res = linear_branch(q, k, v, comp, q_block, kv_block, fast=fast, lvt=l_pad if tc else 0)
+        lin_pack, vt = res if tc else (res, None)
     out = torch.empty((H, L, d), dtype=out_dtype, device=q.device)
     row_max = torch.empty((H, L), dtype=torch.float32, device=q.device) if return_parts else None
     den = torch.empty((H, L), dtype=torch.float32, device=q.device) if return_parts else None
@@ -237,14 +290,16 @@ def sla_attention(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: fl
                     kv_block=kv_block, count=count, scale=scale, linear_mix=float(linear_mix),
                     quantized=int(bool(quantized)), q_codes=ptr(qc), k_codes=ptr(kc), q_scales=ptr(qs),
                     k_scales=ptr(ks), k_mean=ptr(km), idx=ptr(idx), vt=ptr(vt), l_pad=l_pad,
-                    num_l=ptr(num_l), den_l=ptr(den_l), out=ptr(out),
+                    num_l=ptr(lin_pack), den_l=None,
+                    lin_ld=0 if lin_pack is None else lin_pack.shape[2],
+                    lin_hs=0 if lin_pack is None else lin_pack.shape[1] * lin_pack.shape[2], out=ptr(out),
                     out_dtype=TB_BF16 if out_dtype == torch.bfloat16 else TB_F32,
                     row_max=ptr(row_max), den=ptr(den))
     lib = _lib.load(require_device=True)
     _lib.check(lib.tb_sla_attention(__import__("ctypes").byref(args), stream_ptr()), "tb_sla_attention")
     if return_parts:
         parts = dict(qp=qp, kp=kp, idx=idx, comp=comp, q_codes=qc, q_scales=qs, k_codes=kc, k_scales=ks,
-                     k_mean=km, num_l=num_l, den_l=den_l, row_max=row_max, den=den, count=count)
+                     k_mean=km, lin_pack=lin_pack, row_max=row_max, den=den, count=count)
         return out, parts
     return out
 
