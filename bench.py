@@ -237,8 +237,8 @@ def main():
                          q_codes=ops.ptr(parts["q_codes"]), k_codes=ops.ptr(parts["k_codes"]),
                          q_scales=ops.ptr(parts["q_scales"]), k_scales=ops.ptr(parts["k_scales"]),
                          k_mean=ops.ptr(parts["k_mean"]), idx=ops.ptr(parts["idx"]), vt=ops.ptr(vt),
-                         l_pad=(-(-L_ // 64)) * 64, num_l=ops.ptr(parts["lin_pack"]), den_l=None,
-                         lin_ld=parts["lin_pack"].shape[2], lin_hs=parts["lin_pack"].shape[1] * parts["lin_pack"].shape[2],
+                         l_pad=(-(-L_ // 64)) * 64, num_l=None, den_l=None, lin_ld=0, lin_hs=0,
+                         lin_kv=ops.ptr(parts["lin_kv"]), lin_dx=parts["lin_kv"].shape[2],
                          out=ops.ptr(out), out_dtype=1, row_max=None, den=None)
         import ctypes
         lib = _lib.load()

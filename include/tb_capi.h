@@ -125,6 +125,13 @@ typedef struct tb_sla_args {
      * num_l + h*lin_hs + r*lin_ld (d numerators followed by the
      * denominator at column d; den_l is ignored) */
     int64_t lin_ld, lin_hs;
+    /* fused linear branch (tensor-core path): when lin_kv != NULL, the
+     * kernel computes num_l = phi(Q) . KV_sel^T itself as one more tcgen05
+     * MMA in its epilogue.  lin_kv is bf16 [H, nq, lin_dx, d]: rows 0..d-1 of
+     * q-block n hold KV_sel[n]^T (= sum over complement blocks of
+     * V_b^T phi(K_b)), row d holds sum phi(K_b) (the denominator vector). */
+    const void *lin_kv;
+    int64_t lin_dx;
     /* outputs */
     float *out;                        /* [H,L,d] f32 (or bf16 when out_dtype) */
     int out_dtype;

@@ -64,6 +64,7 @@ class SlaArgs(ctypes.Structure):
         ("l_pad", _I),
         ("num_l", _P), ("den_l", _P),
         ("lin_ld", _I), ("lin_hs", _I),
+        ("lin_kv", _P), ("lin_dx", _I),
         ("out", _P),
         ("out_dtype", _i),
         ("row_max", _P), ("den", _P),

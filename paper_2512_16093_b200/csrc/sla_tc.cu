@@ -44,6 +44,7 @@ struct Smem {
     uint64_t k_full[KSTAGES], k_empty[KSTAGES];
     uint64_t v_full[VSTAGES], v_empty[VSTAGES];
     uint64_t s_full[2], p_full[2], pv_done[2];
+    uint64_t phiq_full, lin_full, lin_done;     // fused linear-branch epilogue
     uint32_t tmem_base;
 };
 constexpr size_t SMEM_BYTES = sizeof(Smem) + 1024;
@@ -60,7 +61,8 @@ __device__ __forceinline__ float ex2(float x) {
 template <typename T>
 __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
     const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-    const __grid_constant__ CUtensorMap tm_v, tb_sla_args a, int nq, int nkv) {
+    const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_kv, tb_sla_args a, int nq,
+    int nkv) {
     using namespace sla;
     extern __shared__ uint8_t smem_raw[];
     Smem &S = *reinterpret_cast<Smem *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -80,6 +82,9 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             ptx::mbar_init(&S.p_full[b], 128);
             ptx::mbar_init(&S.pv_done[b], 1);
         }
+        ptx::mbar_init(&S.phiq_full, 128);
+        ptx::mbar_init(&S.lin_full, 1);
+        ptx::mbar_init(&S.lin_done, 1);
         ptx::fence_barrier_init();
         ptx::prefetch_tmap(&tm_q);
         ptx::prefetch_tmap(&tm_k);
@@ -91,6 +96,11 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
     ptx::tc_fence_after();
     const uint32_t tmem = S.tmem_base;
     const uint32_t TM_O = tmem + 128;
+    // fused linear epilogue: after the last PV the V/K rings are free; phi(Q)
+    // (A, 2 x 16 KB swizzled K-halves) goes to v[0..1], KV_sel^T (B) to v[2]+k[0]
+    const bool fused = a.lin_kv != nullptr && a.linear_mix != 0.0f;
+    uint8_t *lin_a = S.v[0];
+    uint8_t *lin_b = S.v[2];
 
     if (warp == 4) {
         // ------------------------------------------------------ TMA producer
@@ -106,6 +116,13 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
                 ptx::mbar_wait_sleep(&S.v_empty[vs], (uint32_t)(((j / VSTAGES) & 1) ^ 1));
                 ptx::mbar_arrive_expect_tx(&S.v_full[vs], V_BYTES);
                 ptx::tma_load_3d(S.v[vs], &tm_v, b * BN, 0, h, &S.v_full[vs]);
+            }
+            if (fused) {
+                ptx::mbar_wait_sleep(&S.o_final, 0);        // every MMA reading the rings is done
+                const int row0 = (int)(((int64_t)h * nq + n) * a.lin_dx);
+                ptx::mbar_arrive_expect_tx(&S.lin_full, 2 * 16384);
+                ptx::tma_load_2d(lin_b, &tm_kv, 0, row0, &S.lin_full);
+                ptx::tma_load_2d(lin_b + 16384, &tm_kv, 64, row0, &S.lin_full);
             }
         }
     } else if (warp == 5) {
@@ -142,6 +159,20 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             }
             pv(count - 1);
             ptx::mma_commit(&S.o_final);
+            if (fused) {
+                // numL = phi(Q) . KV_sel  (M128 N128 K128, bf16) into the free S/P columns 0..127
+                ptx::mbar_wait_sleep(&S.phiq_full, 0);
+                ptx::mbar_wait_sleep(&S.lin_full, 0);
+                ptx::tc_fence_after();
+#pragma unroll
+                for (int ks = 0; ks < D / 16; ks++) {
+                    const int sub = ks >> 2, w = ks & 3;
+                    const uint64_t ad = ptx::sdesc_sw128(ptx::smem_u32(lin_a + sub * 16384)) + 2 * w;
+                    const uint64_t bd = ptx::sdesc_sw128(ptx::smem_u32(lin_b + sub * 16384)) + 2 * w;
+                    ptx::mma_f16(tmem, ad, bd, ID_PV, ks > 0 ? 1u : 0u);
+                }
+                ptx::mma_commit(&S.lin_done);
+            }
         }
     } else {
         // ------------------------------------------------ softmax + epilogue
@@ -239,21 +270,51 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
         // ------------------------------------------------------- epilogue
         ptx::mbar_wait_sleep(&S.o_final, 0);
         ptx::tc_fence_after();
+        float den_fused = 0.0f;
+        if (fused) {
+            // phi(q_row) -> bf16 A operand (128B-swizzled K halves); den = phi(q) . sum phi(K_b)
+            const __nv_bfloat16 *k1 = reinterpret_cast<const __nv_bfloat16 *>(a.lin_kv) +
+                                      (((int64_t)h * nq + n) * a.lin_dx + D) * D;
+            const T *qr = reinterpret_cast<const T *>(a.q) + ((int64_t)h * L + (row_ok ? row : 0)) * D;
+#pragma unroll 1
+            for (int kc = 0; kc < D / 8; kc++) {
+                uint32_t pk[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    float f0 = 0.0f, f1 = 0.0f;
+                    if (row_ok) {
+                        const float x0 = to_f32(qr[kc * 8 + 2 * u]), x1 = to_f32(qr[kc * 8 + 2 * u + 1]);
+                        f0 = x0 >= 0.0f ? x0 + 1.0f : __expf(x0);
+                        f1 = x1 >= 0.0f ? x1 + 1.0f : __expf(x1);
+                    }
+                    den_fused = fmaf(f0, __bfloat162float(k1[kc * 8 + 2 * u]), den_fused);
+                    den_fused = fmaf(f1, __bfloat162float(k1[kc * 8 + 2 * u + 1]), den_fused);
+                    __nv_bfloat162 pp = __floats2bfloat162_rn(f0, f1);
+                    pk[u] = *reinterpret_cast<uint32_t *>(&pp);
+                }
+                uint8_t *dst = lin_a + (kc >> 3) * 16384 + r * 128 + (((kc & 7) ^ (r & 7)) * 16);
+                *reinterpret_cast<uint4 *>(dst) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            }
+            ptx::fence_async_smem();
+            ptx::mbar_arrive(&S.phiq_full);
+            ptx::mbar_wait_sleep(&S.lin_done, 0);
+            ptx::tc_fence_after();
+        }
         // rebase to the true row max (natural-log units for the combine)
         const float f = ex2(m_ref - m_true);
         const float m_nat = m_true * LN2;           // log2-domain max -> natural units
         const float l_true = l * f;
-        const bool lin = a.num_l != nullptr && a.linear_mix != 0.0f;
+        const bool lin = fused || (a.num_l != nullptr && a.linear_mix != 0.0f);
         const int64_t lin_ld = a.lin_ld ? a.lin_ld : D;
         const int64_t lin_hs = a.lin_hs ? a.lin_hs : (int64_t)L * lin_ld;
-        const float *nl_row = lin ? a.num_l + (int64_t)h * lin_hs + (int64_t)row * lin_ld : nullptr;
-        const float *dl_ptr = lin ? (a.lin_ld ? nl_row + D : a.den_l + (int64_t)h * L + row) : nullptr;
+        const float *nl_row = (lin && !fused) ? a.num_l + (int64_t)h * lin_hs + (int64_t)row * lin_ld : nullptr;
+        const float *dl_ptr = (lin && !fused) ? (a.lin_ld ? nl_row + D : a.den_l + (int64_t)h * L + row) : nullptr;
         float ss = f, shrink = 0.0f, den = l_true;
         if (lin && row_ok) {
             const float ref = fmaxf(m_nat, 0.0f);
             const float e_ss = expf(m_nat - ref);
             shrink = expf(-ref) * a.linear_mix;
-            den = l_true * e_ss + shrink * *dl_ptr;
+            den = l_true * e_ss + shrink * (fused ? den_fused : *dl_ptr);
             ss = f * e_ss;
         }
         const float inv = 1.0f / den;
@@ -263,13 +324,18 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
         }
 #pragma unroll 1
         for (int c = 0; c < D; c += 16) {
-            uint32_t o[16];
+            uint32_t o[16], nlt[16];
             ptx::tmem_ld16(TM_O + lane_base + c, o);
+            if (fused) ptx::tmem_ld16(tmem + lane_base + c, nlt);
             ptx::tmem_wait_ld();
             if (!row_ok) continue;
             float v[16];
             const int64_t off = ((int64_t)h * L + row) * D + c;
-            if (lin) {
+            if (fused) {
+#pragma unroll
+                for (int i = 0; i < 16; i++)
+                    v[i] = (__uint_as_float(o[i]) * ss + shrink * __uint_as_float(nlt[i])) * inv;
+            } else if (lin) {
 #pragma unroll
                 for (int i = 0; i < 16; i += 4) {
                     const float4 nl = *reinterpret_cast<const float4 *>(nl_row + c + i);
@@ -309,7 +375,8 @@ int sla_simt(const tb_sla_args *a, cudaStream_t st);
 bool sla_tc_supported(const tb_sla_args *a) {
     return a->quantized && a->d == 128 && a->q_block == 128 && a->kv_block == 64 && a->vt != nullptr &&
            a->L >= 128 && a->l_pad % 64 == 0 && a->l_pad >= cdiv(a->L, 64) * 64 &&
-           (a->dtype == TB_BF16 || a->dtype == TB_F32) && a->count >= 1;
+           (a->dtype == TB_BF16 || a->dtype == TB_F32) && a->count >= 1 &&
+           (a->lin_kv == nullptr || a->lin_dx >= a->d + 1);
 }
 
 int sla_tc(const tb_sla_args *a, cudaStream_t st) {
@@ -320,14 +387,18 @@ int sla_tc(const tb_sla_args *a, cudaStream_t st) {
               make_tmap_3d(&tk, a->k_codes, CU_TENSOR_MAP_DATA_TYPE_UINT8, D, a->L, a->H, D, a->L * D, D, BN, 1) &&
               make_tmap_3d(&tv, a->vt, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, a->l_pad, D, a->H, a->l_pad * 2,
                            a->l_pad * 2 * D, BN, D, 1);
+    CUtensorMap tkv = tq;
+    if (a->lin_kv)
+        ok = ok && make_tmap_2d(&tkv, a->lin_kv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, D, a->H * nq * a->lin_dx, D * 2,
+                                64, 128);
     if (!ok) return fail(TB_ECUDA, "cuTensorMapEncodeTiled failed (sla)");
     dim3 grid((unsigned)nq, (unsigned)a->H);
     if (a->dtype == TB_BF16) {
         cudaFuncSetAttribute(sla_tc_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
-        sla_tc_kernel<__nv_bfloat16><<<grid, THREADS, SMEM_BYTES, st>>>(tq, tk, tv, *a, (int)nq, (int)nkv);
+        sla_tc_kernel<__nv_bfloat16><<<grid, THREADS, SMEM_BYTES, st>>>(tq, tk, tv, tkv, *a, (int)nq, (int)nkv);
     } else {
         cudaFuncSetAttribute(sla_tc_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
-        sla_tc_kernel<float><<<grid, THREADS, SMEM_BYTES, st>>>(tq, tk, tv, *a, (int)nq, (int)nkv);
+        sla_tc_kernel<float><<<grid, THREADS, SMEM_BYTES, st>>>(tq, tk, tv, tkv, *a, (int)nq, (int)nkv);
     }
     return check_launch("sla_tc");
 }
@@ -348,5 +419,6 @@ extern "C" int tb_sla_attention(const tb_sla_args *a, void *stream) {
     if (a->H == 0) return TB_OK;
     cudaStream_t st = as_stream(stream);
     if (sla_tc_supported(a)) return sla_tc(a, st);
+    TB_REQUIRE(a->lin_kv == nullptr, "fused linear epilogue needs the tensor-core envelope");
     return sla_simt(a, st);
 }

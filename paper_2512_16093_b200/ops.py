@@ -154,17 +154,39 @@ def feature_map(x: torch.Tensor, l_pad: int, out_dtype=torch.float32) -> torch.T
     return out
 
 
-def linear_operands(q, k, v, lq: int, lk: int, dx: int, dtype=torch.bfloat16, lvt: int = 0, linear: bool = True):
+def linear_operands(q, k, v, lq: int, lk: int, dx: int, dtype=torch.bfloat16, lvt: int = 0, linear: bool = True,
+                    want_phiq: bool = True):
     """tb_linear_operands -> (phiq [H,lq,d], phik [H,lk,d], vext [H,lk,dx] = [v | 1 | 0], vt [H,d,lvt] | None)."""
     q, k, v = _dev_tensor(q, "q"), _dev_tensor(k, "k"), _dev_tensor(v, "v")
     H, L, d = q.shape
-    phiq = _empty((H, lq, d), dtype, q) if linear else None
+    phiq = _empty((H, lq, d), dtype, q) if (linear and want_phiq) else None
     phik = _empty((H, lk, d), dtype, q) if linear else None
     vext = _empty((H, lk, dx), dtype, q) if linear else None
     vt = _empty((H, d, lvt), torch.bfloat16, q) if lvt else None
     call("tb_linear_operands", ptr(q), ptr(k), ptr(v), dtype_code(q), H, L, d, lq, lk, dx, ptr(phiq), ptr(phik),
          ptr(vext), TB_BF16 if dtype == torch.bfloat16 else TB_F32, ptr(vt), lvt, stream_ptr())
     return phiq, phik, vext, vt
+
+
+def linear_kv_sel(k, v, comp: torch.Tensor, kv_block: int, lvt: int = 0, q=None):
+    """Fused-epilogue form of the linear branch (attention.py:320-328).
+
+    Returns (kvsel [H, nq, dx, d] bf16, vt): per q block n, rows 0..d-1 hold
+    KV_sel[n]^T = sum over complement blocks b of V_b^T phi(K_b) and row d
+    holds sum phi(K_b); the attention kernel finishes the branch with one
+    tcgen05 MMA phi(Q_n) . KV_sel[n] in its epilogue (attention.py:329-334).
+    The two batched GEMMs (per-block V_b^T phi(K_b), then cov . kv_part) run
+    on cuBLAS with bf16 operands and f32 accumulation.
+    """
+    H, L, d = k.shape
+    nq, nkv = comp.shape[1], comp.shape[2]
+    dx = -(-(d + 1) // 16) * 16
+    lk = nkv * kv_block
+    _, phik, vext, vt = linear_operands(q if q is not None else k, k, v, 0, lk, dx, torch.bfloat16, lvt=lvt,
+                                        want_phiq=False)
+    kv_part = torch.bmm(vext.view(H * nkv, kv_block, dx).transpose(1, 2), phik.view(H * nkv, kv_block, d))
+    kvsel = torch.bmm(comp.to(torch.bfloat16), kv_part.view(H, nkv, dx * d))     # [H, nq, dx*d]
+    return kvsel.view(H, nq, dx, d), vt
 
 
 def _phi_t(x, rows):
@@ -278,11 +300,12 @@ def sla_attention(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: fl
         km.record_stream(main)
         kc, ks, kp = pool_quant_tokens(k, kv_block, km, pool=True)
     idx, comp, _ = topk_blocks(qp, kp, count, want_comp=lin or return_parts)
-    lin_pack = None
-    if lin:
+    lin_pack = lin_kv = None
+    if lin and tc:
+        lin_kv, vt = linear_kv_sel(k, v, comp, kv_block, lvt=l_pad, q=q)
+    elif lin:
         fast = (H * L * d >= (1 << 22)) if linear_fast is None else linear_fast
-        res = linear_branch(q, k, v, comp, q_block, kv_block, fast=fast, lvt=l_pad if tc else 0)
-        lin_pack, vt = res if tc else (res, None)
+        lin_pack = linear_branch(q, k, v, comp, q_block, kv_block, fast=fast)
     out = torch.empty((H, L, d), dtype=out_dtype, device=q.device)
     row_max = torch.empty((H, L), dtype=torch.float32, device=q.device) if return_parts else None
     den = torch.empty((H, L), dtype=torch.float32, device=q.device) if return_parts else None
@@ -292,14 +315,15 @@ def sla_attention(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: fl
                     k_scales=ptr(ks), k_mean=ptr(km), idx=ptr(idx), vt=ptr(vt), l_pad=l_pad,
                     num_l=ptr(lin_pack), den_l=None,
                     lin_ld=0 if lin_pack is None else lin_pack.shape[2],
-                    lin_hs=0 if lin_pack is None else lin_pack.shape[1] * lin_pack.shape[2], out=ptr(out),
+                    lin_hs=0 if lin_pack is None else lin_pack.shape[1] * lin_pack.shape[2],
+                    lin_kv=ptr(lin_kv), lin_dx=0 if lin_kv is None else lin_kv.shape[2], out=ptr(out),
                     out_dtype=TB_BF16 if out_dtype == torch.bfloat16 else TB_F32,
                     row_max=ptr(row_max), den=ptr(den))
     lib = _lib.load(require_device=True)
     _lib.check(lib.tb_sla_attention(__import__("ctypes").byref(args), stream_ptr()), "tb_sla_attention")
     if return_parts:
         parts = dict(qp=qp, kp=kp, idx=idx, comp=comp, q_codes=qc, q_scales=qs, k_codes=kc, k_scales=ks,
-                     k_mean=km, lin_pack=lin_pack, row_max=row_max, den=den, count=count)
+                     k_mean=km, lin_pack=lin_pack, lin_kv=lin_kv, row_max=row_max, den=den, count=count)
         return out, parts
     return out
 
