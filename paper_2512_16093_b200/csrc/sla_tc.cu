@@ -58,6 +58,30 @@ __device__ __forceinline__ float ex2(float x) {
     return y;
 }
 
+// 2^x on the FMA/ALU pipes (FA4-style MUFU offload): round-to-nearest split
+// x = j + f, f in [-0.5, 0.5], degree-3 minimax for 2^f (rel err 7.7e-5, well
+// under the bf16 rounding of P), exponent added with one LEA.
+__device__ __forceinline__ float ex2_poly(float x) {
+    x = fmaxf(x, -126.0f);
+    const float t = __fadd_rn(x, 12582912.0f);           // low bits = round(x)
+    const float f = __fsub_rn(x, __fsub_rn(t, 12582912.0f));
+    const float p = fmaf(fmaf(fmaf(0.055088773f, f, 0.24260406f), f, 0.69327623f), f, 0.99992895f);
+    return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
+template <typename T>
+__device__ __forceinline__ void load8(const T *p, float *x) {
+    if constexpr (sizeof(T) == 2) {
+        const uint4 w = *reinterpret_cast<const uint4 *>(p);
+        const __nv_bfloat162 *b = reinterpret_cast<const __nv_bfloat162 *>(&w);
+#pragma unroll
+        for (int i = 0; i < 4; i++) { const float2 f = __bfloat1622float2(b[i]); x[2 * i] = f.x; x[2 * i + 1] = f.y; }
+    } else {
+        const float4 a = *reinterpret_cast<const float4 *>(p), b = *reinterpret_cast<const float4 *>(p + 4);
+        x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+    }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
     const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -144,7 +168,7 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
                 ptx::mma_commit(&S.pv_done[pb]);
                 ptx::mma_commit(&S.v_empty[vs]);
             };
-            for (int j = 0; j < count; j++) {
+            auto qk = [&](int j) {
                 const int ks = j % KSTAGES, sb = j & 1;
                 ptx::mbar_wait_sleep(&S.k_full[ks], (uint32_t)((j / KSTAGES) & 1));
                 ptx::tc_fence_after();
@@ -155,9 +179,14 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
                     ptx::mma_i8(tmem + sb * BN, qd + 2 * k, kd + 2 * k, ID_QK, k > 0 ? 1u : 0u);
                 ptx::mma_commit(&S.s_full[sb]);
                 ptx::mma_commit(&S.k_empty[ks]);
-                if (j >= 1) pv(j - 1);
+            };
+            // QK(j+1) is queued before PV(j) waits for softmax(j): the tensor
+            // pipe computes the next scores while the softmax warps work
+            qk(0);
+            for (int j = 0; j < count; j++) {
+                if (j + 1 < count) qk(j + 1);
+                pv(j);
             }
-            pv(count - 1);
             ptx::mma_commit(&S.o_final);
             if (fused) {
                 // numL = phi(Q) . KV_sel  (M128 N128 K128, bf16) into the free S/P columns 0..127
@@ -186,8 +215,13 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
         if (row_ok) {
             const T *qr = reinterpret_cast<const T *>(a.q) + ((int64_t)h * L + row) * D;
             const float *km = a.k_mean + (int64_t)h * D;
-#pragma unroll 8
-            for (int c = 0; c < D; c++) corr = fmaf(to_f32(qr[c]), __ldg(km + c), corr);
+#pragma unroll 4
+            for (int c = 0; c < D; c += 8) {
+                float x[8];
+                load8(qr + c, x);
+#pragma unroll
+                for (int i = 0; i < 8; i++) corr = fmaf(x[i], __ldg(km + c + i), corr);
+            }
         }
         const float c0 = corr * scale2;
         const float sq = __ldg(a.q_scales + (int64_t)h * nq + n);
@@ -210,21 +244,19 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
 #pragma unroll
             for (int q4 = 0; q4 < 4; q4++) ptx::tmem_ld16(tmem + lane_base + sb * BN + q4 * 16, s[q4]);
             ptx::tmem_wait_ld();
-            float t[64];
-            float mx = -INFINITY;
+            // logit2 is affine in the exact s32 score with slope c1 (uniform
+            // sign per CTA), so the row max comes from an integer max/min
+            const bool ragged = (b == last_blk) && last_ext < BN;     // uniform per CTA
+            const int lim = ragged ? last_ext : BN;
+            int sx = (int)s[0][0];
+            if (c1 >= 0.0f) {
 #pragma unroll
-            for (int i = 0; i < 64; i++) {
-                t[i] = fmaf(__int_as_float((int)s[i >> 4][i & 15] + 0x4B400000), c1, c0m);
-                mx = fmaxf(mx, t[i]);
-            }
-            if (b == last_blk && last_ext < BN) {   // ragged final kv block (uniform per CTA)
-                mx = -INFINITY;
+                for (int i = 1; i < 64; i++) if (!ragged || i < lim) sx = max(sx, (int)s[i >> 4][i & 15]);
+            } else {
 #pragma unroll
-                for (int i = 0; i < 64; i++) {
-                    if (i >= last_ext) t[i] = -INFINITY;
-                    mx = fmaxf(mx, t[i]);
-                }
+                for (int i = 1; i < 64; i++) if (!ragged || i < lim) sx = min(sx, (int)s[i >> 4][i & 15]);
             }
+            const float mx = fmaf(__int_as_float(sx + 0x4B400000), c1, c0m);
             m_true = fmaxf(m_true, mx);
             if (j == 0) {
                 m_ref = mx;
@@ -252,9 +284,17 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             }
             float psum = 0.0f;
             uint32_t pk[2][16];
+            const float off = c0m - m_ref;
 #pragma unroll
             for (int i = 0; i < 64; i += 2) {
-                const float p0 = ex2(t[i] - m_ref), p1 = ex2(t[i + 1] - m_ref);
+                const float y0 = fmaf(__int_as_float((int)s[i >> 4][i & 15] + 0x4B400000), c1, off);
+                const float y1 = fmaf(__int_as_float((int)s[(i + 1) >> 4][(i + 1) & 15] + 0x4B400000), c1, off);
+                float p0 = ex2(y0);
+                float p1 = ((i & 7) == 6) ? ex2_poly(y1) : ex2(y1);   // 1/8 of exps on the FMA pipe
+                if (ragged) {
+                    if (i >= lim) p0 = 0.0f;
+                    if (i + 1 >= lim) p1 = 0.0f;
+                }
                 psum += p0 + p1;
                 __nv_bfloat162 pp = __floats2bfloat162_rn(p0, p1);
                 pk[i >> 5][(i >> 1) & 15] = *reinterpret_cast<uint32_t *>(&pp);
@@ -276,14 +316,16 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             const __nv_bfloat16 *k1 = reinterpret_cast<const __nv_bfloat16 *>(a.lin_kv) +
                                       (((int64_t)h * nq + n) * a.lin_dx + D) * D;
             const T *qr = reinterpret_cast<const T *>(a.q) + ((int64_t)h * L + (row_ok ? row : 0)) * D;
-#pragma unroll 1
+#pragma unroll 2
             for (int kc = 0; kc < D / 8; kc++) {
                 uint32_t pk[4];
+                float xq[8];
+                load8(qr + kc * 8, xq);
 #pragma unroll
                 for (int u = 0; u < 4; u++) {
                     float f0 = 0.0f, f1 = 0.0f;
                     if (row_ok) {
-                        const float x0 = to_f32(qr[kc * 8 + 2 * u]), x1 = to_f32(qr[kc * 8 + 2 * u + 1]);
+                        const float x0 = xq[2 * u], x1 = xq[2 * u + 1];
                         f0 = x0 >= 0.0f ? x0 + 1.0f : __expf(x0);
                         f1 = x1 >= 0.0f ? x1 + 1.0f : __expf(x1);
                     }
