@@ -24,6 +24,8 @@
 // lazy O rescaling (only when the block max exceeds it by > 8, i.e. p <=
 // 256).  Epilogue: O and l rebased to the true row max, combined with the
 // linear branch exactly as attention.py:416-421.
+#include <type_traits>
+
 #include "common.cuh"
 #include "ptx.cuh"
 #include "tmap.cuh"
@@ -248,15 +250,30 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             // sign per CTA), so the row max comes from an integer max/min
             const bool ragged = (b == last_blk) && last_ext < BN;     // uniform per CTA
             const int lim = ragged ? last_ext : BN;
-            int sx = (int)s[0][0];
-            if (c1 >= 0.0f) {
+            float xm[64];                   // M + s exactly (|s| < 2^22): monotone in s
 #pragma unroll
-                for (int i = 1; i < 64; i++) if (!ragged || i < lim) sx = max(sx, (int)s[i >> 4][i & 15]);
+            for (int i = 0; i < 64; i++) xm[i] = __int_as_float((int)s[i >> 4][i & 15] + 0x4B400000);
+            float sx;
+            if (!ragged) {
+                float a = xm[0], z = xm[0];
+                if (c1 >= 0.0f) {
+#pragma unroll
+                    for (int i = 1; i < 63; i += 2) a = fmaxf(a, fmaxf(xm[i], xm[i + 1]));
+                    a = fmaxf(a, xm[63]);
+                    sx = a;
+                } else {
+#pragma unroll
+                    for (int i = 1; i < 63; i += 2) z = fminf(z, fminf(xm[i], xm[i + 1]));
+                    z = fminf(z, xm[63]);
+                    sx = z;
+                }
             } else {
+                sx = xm[0];
 #pragma unroll
-                for (int i = 1; i < 64; i++) if (!ragged || i < lim) sx = min(sx, (int)s[i >> 4][i & 15]);
+                for (int i = 1; i < 64; i++)      // static indices keep xm[] in registers
+                    if (i < lim) sx = (c1 >= 0.0f) ? fmaxf(sx, xm[i]) : fminf(sx, xm[i]);
             }
-            const float mx = fmaf(__int_as_float(sx + 0x4B400000), c1, c0m);
+            const float mx = fmaf(sx, c1, c0m);
             m_true = fmaxf(m_true, mx);
             if (j == 0) {
                 m_ref = mx;
@@ -285,20 +302,25 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             float psum = 0.0f;
             uint32_t pk[2][16];
             const float off = c0m - m_ref;
+            auto make_p = [&](auto rg) {
+                constexpr bool RG = decltype(rg)::value;
 #pragma unroll
-            for (int i = 0; i < 64; i += 2) {
-                const float y0 = fmaf(__int_as_float((int)s[i >> 4][i & 15] + 0x4B400000), c1, off);
-                const float y1 = fmaf(__int_as_float((int)s[(i + 1) >> 4][(i + 1) & 15] + 0x4B400000), c1, off);
-                float p0 = ex2(y0);
-                float p1 = ((i & 7) == 6) ? ex2_poly(y1) : ex2(y1);   // 1/8 of exps on the FMA pipe
-                if (ragged) {
-                    if (i >= lim) p0 = 0.0f;
-                    if (i + 1 >= lim) p1 = 0.0f;
+                for (int i = 0; i < 64; i += 2) {
+                    const float y0 = fmaf(xm[i], c1, off);
+                    const float y1 = fmaf(xm[i + 1], c1, off);
+                    float p0 = ex2(y0);
+                    float p1 = ((i & 7) == 6) ? ex2_poly(y1) : ex2(y1);   // 1/8 of exps on the FMA pipe
+                    if (RG) {
+                        if (i >= lim) p0 = 0.0f;
+                        if (i + 1 >= lim) p1 = 0.0f;
+                    }
+                    psum += p0 + p1;
+                    __nv_bfloat162 pp = __floats2bfloat162_rn(p0, p1);
+                    pk[i >> 5][(i >> 1) & 15] = *reinterpret_cast<uint32_t *>(&pp);
                 }
-                psum += p0 + p1;
-                __nv_bfloat162 pp = __floats2bfloat162_rn(p0, p1);
-                pk[i >> 5][(i >> 1) & 15] = *reinterpret_cast<uint32_t *>(&pp);
-            }
+            };
+            if (ragged) make_p(std::integral_constant<bool, true>());
+            else make_p(std::integral_constant<bool, false>());
             l += psum;
             // P_j overwrites S_j's first 32 columns (A operand of PV, bf16x2 per column)
             ptx::tmem_st16(tmem + lane_base + sb * BN, pk[0]);
