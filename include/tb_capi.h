@@ -166,6 +166,14 @@ int tb_linear_operands(const void *q, const void *k, const void *v, int dtype, i
                        int64_t d, int64_t lq, int64_t lk, int64_t dx, void *phiq, void *phik,
                        void *vext, int out_dtype, void *vt, int64_t lvt, void *stream);
 
+/* Batched bf16 GEMM on tcgen05 (f32 accumulate): for each h < H,
+ * C[h] (MxN) = A[h] (MxK, row pitch lda, K contiguous) . B[h] (KxN, row
+ * pitch ldb, N contiguous); C row pitch ldc, bf16 or f32.  N % 256 == 0.
+ * Used for the linear branch's coverage GEMM kv_sel = cov . kv_part
+ * (attention.py:326-328). */
+int tb_gemm_bf16_batched(const void *A, const void *B, void *C, int64_t H, int64_t M, int64_t N,
+                         int64_t K, int64_t lda, int64_t ldb, int64_t ldc, int out_dtype, void *stream);
+
 /* Fast-mode W8A8: identical operands, the two block scales folded into one
  * FMA per element (tolerance-level, not bit-exact); used by the DiT step. */
 int tb_w8a8_gemm_fast(const int8_t *a, const float *sa, const int8_t *bt, const float *sb,

@@ -1,0 +1,204 @@
+// gemm_bf16.cu -- batched bf16 GEMM on tcgen05 for the SLA linear branch.
+//
+// C[h] (M x N) = A[h] (M x K, K-major) . B[h] (K x N, N-contiguous = MN-major)
+// with f32 accumulation in TMEM.  Used for kv_sel = cov . kv_part
+// (attention.py:326-328): A = the complement mask (0/1, exact in bf16),
+// B = the per-kv-block phi(K_b)^T [V_b|1] matrices; M = #q-blocks,
+// K = #kv-blocks, N = (d+16)*d.  Replaces a cuBLAS batched GEMM.
+//
+// Persistent CTAs (one per SM), warp-specialised like the W8A8 kernel:
+// warp 0 TMA producer (A tile 128x64 K-major SW128; B tile 64x256 as four
+// 64-column MN-major SW128 atoms), warp 1 single-thread MMA issuer
+// (4 x kind::f16 M128 N256 K16 per 64-deep stage), 8 epilogue warps draining
+// a double-buffered 2 x 256-column f32 TMEM accumulator to bf16/f32.
+#include "common.cuh"
+#include "ptx.cuh"
+#include "tmap.cuh"
+
+namespace tb {
+
+namespace gbf {
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int EPI_WARPS = 8;
+constexpr int THREADS = 64 + EPI_WARPS * 32;
+constexpr uint32_t A_BYTES = BM * BK * 2;   // 16 KiB
+constexpr uint32_t B_BYTES = BK * BN * 2;   // 32 KiB
+struct Smem {
+    uint8_t a[STAGES][A_BYTES];
+    uint8_t b[STAGES][B_BYTES];
+    uint64_t full[STAGES], empty[STAGES];
+    uint64_t acc_full[2], acc_empty[2];
+    uint32_t tmem_base;
+};
+constexpr size_t SMEM_BYTES = sizeof(Smem) + 1024;
+}  // namespace gbf
+
+// MN-major 128B-swizzled operand: atoms of 64 (MN) x 8 (K) bf16; LBO = byte
+// stride between 64-wide MN atoms, SBO = byte stride between 8-row K groups.
+__device__ __forceinline__ uint64_t sdesc_sw128_mn(uint32_t smem_addr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((smem_addr & 0x3FFFF) >> 4);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)2 << 61;
+    return d;
+}
+
+template <bool OUT_F32>
+__global__ void __launch_bounds__(gbf::THREADS, 1) gemm_bf16_kernel(
+    const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, void *__restrict__ C,
+    int H, int M, int N, int K, int64_t ldc, int64_t c_batch) {
+    using namespace gbf;
+    extern __shared__ uint8_t smem_raw[];
+    Smem &S = *reinterpret_cast<Smem *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nmt = (M + BM - 1) / BM, nnt = N / BN, nkb = (K + BK - 1) / BK;
+    const int tiles_per_head = nmt * nnt;
+    const int ntiles = H * tiles_per_head;
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < STAGES; s++) { ptx::mbar_init(&S.full[s], 1); ptx::mbar_init(&S.empty[s], 1); }
+        for (int b = 0; b < 2; b++) { ptx::mbar_init(&S.acc_full[b], 1); ptx::mbar_init(&S.acc_empty[b], EPI_WARPS * 32); }
+        ptx::fence_barrier_init();
+        ptx::prefetch_tmap(&tma_a);
+        ptx::prefetch_tmap(&tma_b);
+    }
+    if (warp == 1) ptx::tmem_alloc<512>(&S.tmem_base);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = S.tmem_base;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                const int h = tile / tiles_per_head, rem = tile % tiles_per_head;
+                const int nt = rem / nmt, mt = rem % nmt;       // m fastest: B tile reused from L2
+                for (int kb = 0; kb < nkb; kb++) {
+                    ptx::mbar_wait_sleep(&S.empty[stage], phase ^ 1);
+                    ptx::mbar_arrive_expect_tx(&S.full[stage], A_BYTES + B_BYTES);
+                    ptx::tma_load_3d(S.a[stage], &tma_a, kb * BK, mt * BM, h, &S.full[stage]);
+#pragma unroll
+                    for (int q = 0; q < BN / 64; q++)
+                        ptx::tma_load_3d(S.b[stage] + q * (BK * 128), &tma_b, nt * BN + q * 64, kb * BK, h,
+                                         &S.full[stage]);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            int stage = 0, buf = 0;
+            uint32_t phase = 0, bphase = 0;
+            constexpr uint32_t idesc = ptx::idesc_bf16(BM, BN) | (1u << 16);   // B MN-major
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                ptx::mbar_wait_sleep(&S.acc_empty[buf], bphase ^ 1);
+                ptx::tc_fence_after();
+                for (int kb = 0; kb < nkb; kb++) {
+                    ptx::mbar_wait_sleep(&S.full[stage], phase);
+                    ptx::tc_fence_after();
+                    const uint64_t ad = ptx::sdesc_sw128(ptx::smem_u32(S.a[stage]));
+                    const uint64_t bd = sdesc_sw128_mn(ptx::smem_u32(S.b[stage]), BK * 128, 1024);
+#pragma unroll
+                    for (int k = 0; k < BK / 16; k++)   // K=16: A +32 B in the row, B +16 rows (2048 B)
+                        ptx::mma_f16(tmem + buf * BN, ad + 2 * k, bd + 128 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+                    ptx::mma_commit(&S.empty[stage]);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+                ptx::mma_commit(&S.acc_full[buf]);
+                buf ^= 1;
+                if (buf == 0) bphase ^= 1;
+            }
+        }
+    } else {
+        const int ew = warp - 2;
+        const int quarter = warp & 3;
+        const int half = ew >> 2;                 // 128-column half of the 256-wide tile
+        const int trow = quarter * 32 + lane;
+        int buf = 0;
+        uint32_t bphase = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            const int h = tile / tiles_per_head, rem = tile % tiles_per_head;
+            const int nt = rem / nmt, mt = rem % nmt;
+            ptx::mbar_wait_sleep(&S.acc_full[buf], bphase);
+            ptx::tc_fence_after();
+            const int row = mt * BM + trow;
+            const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + buf * BN + half * 128;
+#pragma unroll 1
+            for (int c = 0; c < 128; c += 32) {
+                uint32_t r0[16], r1[16];
+                ptx::tmem_ld16(taddr + c, r0);
+                ptx::tmem_ld16(taddr + c + 16, r1);
+                ptx::tmem_wait_ld();
+                if (row < M) {
+                    const int64_t off = (int64_t)h * c_batch + (int64_t)row * ldc + nt * BN + half * 128 + c;
+                    if constexpr (OUT_F32) {
+                        float *o = reinterpret_cast<float *>(C) + off;
+#pragma unroll
+                        for (int i = 0; i < 16; i += 4) {
+                            *reinterpret_cast<float4 *>(o + i) = make_float4(__uint_as_float(r0[i]), __uint_as_float(r0[i + 1]),
+                                                                             __uint_as_float(r0[i + 2]), __uint_as_float(r0[i + 3]));
+                            *reinterpret_cast<float4 *>(o + 16 + i) = make_float4(__uint_as_float(r1[i]), __uint_as_float(r1[i + 1]),
+                                                                                  __uint_as_float(r1[i + 2]), __uint_as_float(r1[i + 3]));
+                        }
+                    } else {
+                        __nv_bfloat16 *o = reinterpret_cast<__nv_bfloat16 *>(C) + off;
+                        uint32_t w[16];
+#pragma unroll
+                        for (int i = 0; i < 8; i++) {
+                            __nv_bfloat162 a = __floats2bfloat162_rn(__uint_as_float(r0[2 * i]), __uint_as_float(r0[2 * i + 1]));
+                            __nv_bfloat162 b = __floats2bfloat162_rn(__uint_as_float(r1[2 * i]), __uint_as_float(r1[2 * i + 1]));
+                            w[i] = *reinterpret_cast<uint32_t *>(&a);
+                            w[8 + i] = *reinterpret_cast<uint32_t *>(&b);
+                        }
+#pragma unroll
+                        for (int i = 0; i < 16; i += 4)
+                            *reinterpret_cast<uint4 *>(o + 2 * i) = make_uint4(w[i], w[i + 1], w[i + 2], w[i + 3]);
+                    }
+                }
+            }
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&S.acc_empty[buf]);
+            buf ^= 1;
+            if (buf == 0) bphase ^= 1;
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) ptx::tmem_dealloc<512>(tmem);
+}
+
+int num_sms();
+
+}  // namespace tb
+
+using namespace tb;
+
+extern "C" int tb_gemm_bf16_batched(const void *A, const void *B, void *C, int64_t H, int64_t M, int64_t N, int64_t K,
+                                    int64_t lda, int64_t ldb, int64_t ldc, int out_dtype, void *stream) {
+    using namespace gbf;
+    TB_REQUIRE(N % BN == 0, "N must be a multiple of 256");
+    TB_REQUIRE(lda % 8 == 0 && ldb % 8 == 0 && ldc % 8 == 0, "leading dims must be multiples of 8");
+    TB_REQUIRE(lda >= K && ldb >= N && ldc >= N, "leading dims too small");
+    TB_REQUIRE(((uintptr_t)A % 16) == 0 && ((uintptr_t)B % 16) == 0 && ((uintptr_t)C % 16) == 0, "unaligned");
+    if (H == 0 || M == 0) return TB_OK;
+    CUtensorMap ta, tbm;
+    // A [H][M][K] (row pitch lda), B [H][K][N] (row pitch ldb), both bf16
+    if (!make_tmap_3d(&ta, A, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, K, M, H, lda * 2, lda * 2 * M, BK, BM, 1) ||
+        !make_tmap_3d(&tbm, B, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, N, K, H, ldb * 2, ldb * 2 * K, 64, BK, 1))
+        return fail(TB_ECUDA, "cuTensorMapEncodeTiled failed (gemm_bf16)");
+    const int64_t ntiles = H * cdiv(M, BM) * (N / BN);
+    const int grid = (int)(ntiles < num_sms() ? ntiles : num_sms());
+    cudaStream_t st = as_stream(stream);
+    if (out_dtype == TB_F32) {
+        cudaFuncSetAttribute(gemm_bf16_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+        gemm_bf16_kernel<true><<<grid, THREADS, SMEM_BYTES, st>>>(ta, tbm, C, (int)H, (int)M, (int)N, (int)K, ldc, ldc * M);
+    } else {
+        cudaFuncSetAttribute(gemm_bf16_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+        gemm_bf16_kernel<false><<<grid, THREADS, SMEM_BYTES, st>>>(ta, tbm, C, (int)H, (int)M, (int)N, (int)K, ldc, ldc * M);
+    }
+    return check_launch("gemm_bf16");
+}

@@ -185,8 +185,22 @@ def linear_kv_sel(k, v, comp: torch.Tensor, kv_block: int, lvt: int = 0, q=None)
     _, phik, vext, vt = linear_operands(q if q is not None else k, k, v, 0, lk, dx, torch.bfloat16, lvt=lvt,
                                         want_phiq=False)
     kv_part = torch.bmm(vext.view(H * nkv, kv_block, dx).transpose(1, 2), phik.view(H * nkv, kv_block, d))
-    kvsel = torch.bmm(comp.to(torch.bfloat16), kv_part.view(H, nkv, dx * d))     # [H, nq, dx*d]
+    nkv_pad = -(-nkv // 8) * 8                       # TMA row pitch must be a multiple of 16 B
+    cov = torch.zeros((H, nq, nkv_pad), dtype=torch.bfloat16, device=k.device)
+    cov[:, :, :nkv] = comp
+    kvsel = gemm_bf16_batched(cov, kv_part.view(H, nkv, dx * d), K=nkv)         # [H, nq, dx*d]
     return kvsel.view(H, nq, dx, d), vt
+
+
+def gemm_bf16_batched(a: torch.Tensor, b: torch.Tensor, K: int | None = None, out_dtype=torch.bfloat16):
+    """tb_gemm_bf16_batched: C[h] = A[h][:, :K] . B[h][:K] (tcgen05, f32 accumulate)."""
+    H, M, lda = a.shape
+    Kb, N = b.shape[1], b.shape[2]
+    K = Kb if K is None else K
+    c = torch.empty((H, M, N), dtype=out_dtype, device=a.device)
+    call("tb_gemm_bf16_batched", ptr(a), ptr(b), ptr(c), H, M, N, K, lda, N, N,
+         TB_F32 if out_dtype == torch.float32 else TB_BF16, stream_ptr())
+    return c
 
 
 def _phi_t(x, rows):
