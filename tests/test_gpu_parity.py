@@ -215,3 +215,20 @@ def test_sla_topk_one_equals_dense_unquantized(tb):
     ref = O.reference_attention(q, k, v)
     _, rel2, _ = O.error_metrics(out, ref)
     assert rel2 <= 1e-5
+
+
+def test_gemm_bf16_batched_mn_major(tb):
+    """tcgen05 bf16 GEMM with an MN-major B operand (linear-branch coverage GEMM)."""
+    g = torch.Generator(device="cuda").manual_seed(3)
+    for (H, M, K, N) in ((2, 200, 300, 512), (3, 591, 1182, 256), (1, 128, 64, 256)):
+        lda = -(-K // 8) * 8
+        a = torch.zeros((H, M, lda), dtype=torch.bfloat16, device="cuda")
+        a[:, :, :K] = torch.randn((H, M, K), generator=g, device="cuda").to(torch.bfloat16)
+        b = torch.randn((H, K, N), generator=g, device="cuda").to(torch.bfloat16)
+        want = torch.bmm(a[:, :, :K].float(), b.float())
+        got = tb.gemm_bf16_batched(a, b, K=K, out_dtype=torch.float32)
+        err = (got - want).abs().max().item() / want.abs().max().item()
+        assert err < 1e-5, (H, M, K, N, err)
+        got16 = tb.gemm_bf16_batched(a, b, K=K)
+        cos, _, rel1 = metrics(got16.float().cpu().numpy(), want.cpu().numpy())
+        assert cos > 0.99999 and rel1 < 5e-3
