@@ -22,11 +22,10 @@ namespace tb {
 
 // ------------------------------------------------------------ tcgen05 path
 namespace gemm {
-constexpr int BM = 128, BN = 128, BK = 128, STAGES = 4;
+constexpr int BM = 128, BK = 128, STAGES = 4;
 constexpr int EPI_WARPS = 8;
 constexpr int THREADS = 64 + EPI_WARPS * 32;
-constexpr uint32_t TILE_BYTES = BM * BK;  // A and B tiles are both 16 KiB
-
+template <int BN>
 struct Smem {
     uint8_t a[STAGES][BM * BK];
     uint8_t b[STAGES][BN * BK];
@@ -34,19 +33,25 @@ struct Smem {
     uint64_t seg_full[2], seg_empty[2];
     uint32_t tmem_base;
 };
-constexpr size_t SMEM_BYTES = sizeof(Smem) + 1024;
+template <int BN>
+constexpr size_t smem_bytes() { return sizeof(Smem<BN>) + 1024; }
 }  // namespace gemm
 
-template <bool EXACT, bool OUT_BF16>
+// BN = 128 or 256 (tile 128 x BN, s32 segment buffers 2 x BN TMEM columns).
+// Each epilogue warp owns 32 rows (its TMEM lane quarter) x BN/2 columns;
+// a BN/2 column span never crosses a 128-column scale block.
+template <int BN, bool EXACT, bool OUT_BF16>
 __global__ void __launch_bounds__(gemm::THREADS, 1) w8a8_tc_kernel(
     const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
     const float *__restrict__ sa, const float *__restrict__ sb, const float *__restrict__ bias,
     void *__restrict__ out, int M, int N, int K) {
     using namespace gemm;
+    constexpr int CW = BN / 2;
+    constexpr uint32_t TMEM_COLS = 2 * BN;
     extern __shared__ uint8_t smem_raw[];
-    Smem &S = *reinterpret_cast<Smem *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    Smem<BN> &S = *reinterpret_cast<Smem<BN> *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nmt = (M + BM - 1) / BM, nnt = N / BN, nkb = K / BK;
+    const int nmt = (M + BM - 1) / BM, nnt = N / BN, nkb = K / BK, nnb = N / 128;
     const int ntiles = nmt * nnt;
 
     if (warp == 0 && lane == 0) {
@@ -56,7 +61,7 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) w8a8_tc_kernel(
         ptx::prefetch_tmap(&tma_a);
         ptx::prefetch_tmap(&tma_b);
     }
-    if (warp == 1) ptx::tmem_alloc<256>(&S.tmem_base);
+    if (warp == 1) ptx::tmem_alloc<TMEM_COLS>(&S.tmem_base);
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
@@ -69,8 +74,8 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) w8a8_tc_kernel(
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
                 const int mt = tile % nmt, nt = tile / nmt;
                 for (int kb = 0; kb < nkb; kb++) {
-                    ptx::mbar_wait(&S.empty[stage], phase ^ 1);
-                    ptx::mbar_arrive_expect_tx(&S.full[stage], 2 * TILE_BYTES);
+                    ptx::mbar_wait_sleep(&S.empty[stage], phase ^ 1);
+                    ptx::mbar_arrive_expect_tx(&S.full[stage], (BM + BN) * BK);
                     ptx::tma_load_2d(S.a[stage], &tma_a, kb * BK, mt * BM, &S.full[stage]);
                     ptx::tma_load_2d(S.b[stage], &tma_b, kb * BK, nt * BN, &S.full[stage]);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -84,8 +89,8 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) w8a8_tc_kernel(
             constexpr uint32_t idesc = ptx::idesc_i8(BM, BN);
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
                 for (int kb = 0; kb < nkb; kb++) {
-                    ptx::mbar_wait(&S.seg_empty[buf], bphase ^ 1);
-                    ptx::mbar_wait(&S.full[stage], phase);
+                    ptx::mbar_wait_sleep(&S.seg_empty[buf], bphase ^ 1);
+                    ptx::mbar_wait_sleep(&S.full[stage], phase);
                     ptx::tc_fence_after();
                     const uint64_t ad = ptx::sdesc_sw128(ptx::smem_u32(S.a[stage]));
                     const uint64_t bd = ptx::sdesc_sw128(ptx::smem_u32(S.b[stage]));
@@ -103,53 +108,58 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) w8a8_tc_kernel(
     } else {
         const int ew = warp - 2;
         const int quarter = warp & 3;          // TMEM lanes this warp may touch
-        const int half = ew >> 2;              // column half of the 128-wide tile
+        const int half = ew >> 2;              // column half of the tile
         const int trow = quarter * 32 + lane;
         int buf = 0;
         uint32_t bphase = 0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
             const int mt = tile % nmt, nt = tile / nmt;
-            float acc[64];
+            const int col0 = nt * BN + half * CW;
+            const int nb = col0 / 128;
+            float acc[CW];
 #pragma unroll
-            for (int i = 0; i < 64; i++) acc[i] = 0.0f;
+            for (int i = 0; i < CW; i++) acc[i] = 0.0f;
             for (int kb = 0; kb < nkb; kb++) {
                 const float s_a = __ldg(sa + (size_t)mt * nkb + kb);
-                const float s_b = __ldg(sb + (size_t)kb * nnt + nt);
-                ptx::mbar_wait(&S.seg_full[buf], bphase);
-                ptx::tc_fence_after();
-                uint32_t r[4][16];
-                const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + buf * BN + half * 64;
-#pragma unroll
-                for (int j = 0; j < 4; j++) ptx::tmem_ld16(taddr + j * 16, r[j]);
-                ptx::tmem_wait_ld();
-                ptx::tc_fence_before();
-                ptx::mbar_arrive(&S.seg_empty[buf]);
+                const float s_b = __ldg(sb + (size_t)kb * nnb + nb);
                 const float s_ab = s_a * s_b;
+                ptx::mbar_wait_sleep(&S.seg_full[buf], bphase);
+                ptx::tc_fence_after();
+                const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + buf * BN + half * CW;
 #pragma unroll
-                for (int j = 0; j < 4; j++)
-#pragma unroll
-                    for (int i = 0; i < 16; i++) {
-                        // exact s32 -> f32 (|seg| <= 128*127^2 < 2^22)
-                        const float x = __int_as_float((int)r[j][i] + 0x4B400000) - 12582912.0f;
-                        if constexpr (EXACT)
-                            acc[j * 16 + i] = __fadd_rn(acc[j * 16 + i], __fmul_rn(__fmul_rn(x, s_a), s_b));
-                        else
-                            acc[j * 16 + i] = fmaf(x, s_ab, acc[j * 16 + i]);
+                for (int cc = 0; cc < CW; cc += 32) {
+                    uint32_t r[2][16];
+                    ptx::tmem_ld16(taddr + cc, r[0]);
+                    ptx::tmem_ld16(taddr + cc + 16, r[1]);
+                    ptx::tmem_wait_ld();
+                    if (cc + 32 == CW) {
+                        ptx::tc_fence_before();
+                        ptx::mbar_arrive(&S.seg_empty[buf]);     // segment buffer free for the MMA
                     }
+#pragma unroll
+                    for (int j = 0; j < 2; j++)
+#pragma unroll
+                        for (int i = 0; i < 16; i++) {
+                            // exact s32 -> f32 (|seg| <= 128*127^2 < 2^22)
+                            const float x = __int_as_float((int)r[j][i] + 0x4B400000) - 12582912.0f;
+                            float &o = acc[cc + j * 16 + i];
+                            if constexpr (EXACT) o = __fadd_rn(o, __fmul_rn(__fmul_rn(x, s_a), s_b));
+                            else o = fmaf(x, s_ab, o);
+                        }
+                }
                 buf ^= 1;
                 if (buf == 0) bphase ^= 1;
             }
             const int row = mt * BM + trow;
             if (row < M) {
-                const int col0 = nt * BN + half * 64;
                 if (bias) {
 #pragma unroll
-                    for (int i = 0; i < 64; i++) acc[i] = __fadd_rn(acc[i], __ldg(bias + col0 + i));
+                    for (int i = 0; i < CW; i++) acc[i] = __fadd_rn(acc[i], __ldg(bias + col0 + i));
                 }
                 if constexpr (OUT_BF16) {
                     __nv_bfloat16 *o = reinterpret_cast<__nv_bfloat16 *>(out) + (size_t)row * N + col0;
 #pragma unroll
-                    for (int i = 0; i < 64; i += 8) {
+                    for (int i = 0; i < CW; i += 8) {
                         uint4 w;
                         __nv_bfloat162 *p = reinterpret_cast<__nv_bfloat162 *>(&w);
 #pragma unroll
@@ -159,7 +169,7 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) w8a8_tc_kernel(
                 } else {
                     float *o = reinterpret_cast<float *>(out) + (size_t)row * N + col0;
 #pragma unroll
-                    for (int i = 0; i < 64; i += 4)
+                    for (int i = 0; i < CW; i += 4)
                         *reinterpret_cast<float4 *>(o + i) = make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
                 }
             }
@@ -167,7 +177,7 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) w8a8_tc_kernel(
     }
     ptx::tc_fence_before();
     __syncthreads();
-    if (warp == 1) ptx::tmem_dealloc<256>(tmem);
+    if (warp == 1) ptx::tmem_dealloc<TMEM_COLS>(tmem);
 }
 
 // ------------------------------------------------------------ CUDA-core path
@@ -263,24 +273,28 @@ int w8a8_dispatch(const int8_t *a, const float *sa, const int8_t *bt, const floa
     TB_REQUIRE(out_dtype == TB_F32 || out_dtype == TB_BF16, "out dtype must be f32 or bf16");
     if (M == 0 || N == 0) return TB_OK;
     const bool tc = block == 128 && K % 128 == 0 && N % 128 == 0 && K > 0 && M < (1ll << 31) &&
-                    ((uintptr_t)a % 16 == 0) && ((uintptr_t)bt % 16 == 0);
+                    ((uintptr_t)a % 16) == 0 && ((uintptr_t)bt % 16) == 0;
     if (tc) {
+        const int BN = (N % 256 == 0) ? 256 : 128;
         CUtensorMap ta, tbm;
         if (!make_tmap_2d(&ta, a, CU_TENSOR_MAP_DATA_TYPE_UINT8, K, M, K, 128, 128) ||
-            !make_tmap_2d(&tbm, bt, CU_TENSOR_MAP_DATA_TYPE_UINT8, K, N, K, 128, 128))
+            !make_tmap_2d(&tbm, bt, CU_TENSOR_MAP_DATA_TYPE_UINT8, K, N, K, 128, BN))
             return fail(TB_ECUDA, "cuTensorMapEncodeTiled failed");
-        const int ntiles = (int)(cdiv(M, 128) * (N / 128));
+        const int ntiles = (int)(cdiv(M, 128) * (N / BN));
         const int grid = ntiles < num_sms() ? ntiles : num_sms();
-#define TB_GEMM_LAUNCH(E, B)                                                                               \
+#define TB_GEMM_LAUNCH(BNV, E, B)                                                                          \
     {                                                                                                      \
-        auto kern = w8a8_tc_kernel<E, B>;                                                                  \
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm::SMEM_BYTES);    \
-        kern<<<grid, gemm::THREADS, gemm::SMEM_BYTES, st>>>(ta, tbm, sa, sb, bias, out, (int)M, (int)N, (int)K); \
+        auto kern = w8a8_tc_kernel<BNV, E, B>;                                                             \
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm::smem_bytes<BNV>()); \
+        kern<<<grid, gemm::THREADS, gemm::smem_bytes<BNV>(), st>>>(ta, tbm, sa, sb, bias, out, (int)M, (int)N, (int)K); \
     }
-        if (exact && out_dtype == TB_F32) TB_GEMM_LAUNCH(true, false)
-        else if (exact) TB_GEMM_LAUNCH(true, true)
-        else if (out_dtype == TB_F32) TB_GEMM_LAUNCH(false, false)
-        else TB_GEMM_LAUNCH(false, true)
+#define TB_GEMM_BN(BNV)                                                                                    \
+        if (exact && out_dtype == TB_F32) TB_GEMM_LAUNCH(BNV, true, false)                                 \
+        else if (exact) TB_GEMM_LAUNCH(BNV, true, true)                                                    \
+        else if (out_dtype == TB_F32) TB_GEMM_LAUNCH(BNV, false, false)                                    \
+        else TB_GEMM_LAUNCH(BNV, false, true)
+        if (BN == 256) { TB_GEMM_BN(256) } else { TB_GEMM_BN(128) }
+#undef TB_GEMM_BN
 #undef TB_GEMM_LAUNCH
         return check_launch("w8a8_tc");
     }
