@@ -152,6 +152,53 @@ def cpu_baseline_sample():
             "sample": f"1 of 40 heads of cfg4 (75600 tokens), {t:.1f} s, numpy/OpenBLAS oracle port"}
 
 
+DIT_DIM, DIT_FFN, DIT_STEPS = 5120, 13824, 4
+
+
+def dit_ops_per_layer(L=L_, dim=DIT_DIM, ffn=DIT_FFN, heads=H_):
+    """Per layer per step: W8A8 projections 2*L*(dim*3dim + dim*dim + 2*dim*ffn)
+    plus the SLA attention's executed work (attention_flop_report)."""
+    return 2 * L * (dim * 3 * dim + dim * dim + 2 * dim * ffn) + sparse_ops(H=heads, L=L)
+
+
+def bench_dit(world, rank, num_layers):
+    """cfg5 latency: one full rCM sample (4 steps x num_layers layers), seq-parallel
+    linears + Ulysses attention across ranks; max over ranks of CUDA-event time."""
+    import torch
+    import torch.distributed as dist
+    from paper_2512_16093_b200 import dit, ulysses
+    torch.cuda.empty_cache()
+    layers = dit.random_layers(DIT_DIM, DIT_FFN, num_layers, seed=0)
+    lo, hi = ulysses.token_bounds(L_, world, rank)
+    g = torch.Generator(device="cuda").manual_seed(77 + rank)
+    x_init = torch.randn((hi - lo, DIT_DIM), generator=g, device="cuda")
+    noises = [torch.randn((hi - lo, DIT_DIM), generator=g, device="cuda") for _ in range(DIT_STEPS - 1)]
+    sig = [80.0 * (0.5 / 80.0) ** (i / (DIT_STEPS - 1)) for i in range(DIT_STEPS)] + [0.0]   # make_schedule(4)
+    sla = dict(q_block=QB, kv_block=KVB, topk_ratio=RATIO, linear_mix=1.0)
+    dit.block_forward(x_init, sig[0], layers[0], H_, sla, L_)          # warm-up (one block)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    out = dit.rcm_sample(layers, H_, sla, x_init, noises, sig, L_global=L_)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ops_total = dit_ops_per_layer() * num_layers * DIT_STEPS
+    finite = bool(torch.isfinite(out).all().item())
+    del layers, noises, out
+    torch.cuda.empty_cache()
+    return {"workload": "cfg5: rCM 4-step sample, Wan2.1-14B-720P-shaped toy DiT (dim 5120, 40 heads, "
+                        f"FFN 13824, {num_layers} layers, L 75600), SLA 0.1 + Sage INT8 + W8A8",
+            "latency_s": ms / 1e3, "ops": ops_total, "TOPS": ops_total / (ms * 1e-3) / 1e12,
+            "weights": "random-init on device (N(0,1)/sqrt(fan_in), block-quantized)", "finite": finite}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -161,6 +208,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-w8a8", action="store_true")
     ap.add_argument("--heads", type=int, default=H_)
+    ap.add_argument("--no-dit", action="store_true")
+    ap.add_argument("--dit-layers", type=int, default=40)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -284,6 +333,13 @@ def main():
                 res[mode] = {"ms": gms, "TOPS": 2 * M * K * N / (gms * 1e-3) / 1e12}
             w8[f"{K}x{N}"] = res
 
+    # ---- cfg5: full rCM 4-step sampling of the Wan2.1-14B-720P-shaped toy DiT
+    dit_res = None
+    if not args.no_dit:
+        del shard
+        head_major = None if world > 1 else head_major
+        dit_res = bench_dit(world, rank, args.dit_layers)
+
     # ---- e2e through the public API with pinned host buffers
     e2e = None
     if world == 1:
@@ -318,7 +374,7 @@ def main():
                            "topk_ratio": RATIO, "parallelism": f"ulysses{world}",
                            "l2": "inputs 3 x 774 MB bf16 > 126 MB L2 (no flush needed)"},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "w8a8": w8,
-                "gpu_launches": 8 * args.steps, "clocks": clk.summary()}
+                "dit": dit_res, "gpu_launches": 8 * args.steps, "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -1,0 +1,139 @@
+"""Device-resident toy DiT + rCM few-step sampler (the cfg5 throughput path).
+
+Same block as ``sampler.toy_block_forward`` (/root/reference/pkg/src/turbobench/
+sampler.py:132-186): x + sigma*emb -> RMSNorm -> W8A8 qkv -> SLA attention ->
+W8A8 out_proj -> residual -> LayerNorm -> W8A8 mlp_in -> GELU(tanh) -> W8A8
+mlp_out -> residual, and the multistep consistency loop of sampler.py:281-302.
+Differences from the drop-in ``sampler`` module are throughput choices only:
+weights live on the device as transposed INT8 codes (the GEMM's K-major B
+operand) with 128x128 scales, the projections use the single-FMA promotion,
+and intermediate activations are bf16 (the residual stream stays f32).
+
+Sequence parallel with Ulysses attention when torch.distributed is
+initialised: each rank holds a token shard of x, weights are replicated, and
+attention exchanges q/k/v/o with one all-to-all each way (ulysses.py).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+from . import ops, ulysses
+
+
+@dataclass
+class DeviceLinear:
+    bt: torch.Tensor        # int8 [N, K] (transposed codes)
+    scales: torch.Tensor    # f32 [K/128, N/128]
+
+    @property
+    def shape(self):
+        return self.bt.shape[1], self.bt.shape[0]
+
+
+@dataclass
+class DeviceLayer:
+    rms_gain: torch.Tensor
+    ln_gain: torch.Tensor
+    ln_offset: torch.Tensor
+    sigma_emb: torch.Tensor
+    qkv: DeviceLinear
+    out_proj: DeviceLinear
+    mlp_in: DeviceLinear
+    mlp_out: DeviceLinear
+
+
+def quantize_device_weight(w: torch.Tensor, block: int = 128) -> DeviceLinear:
+    """blockquant.quantize_blockwise on device (bit-exact codes), stored transposed."""
+    q, s = ops.quantize_blockwise(w, block, check_finite=False)
+    return DeviceLinear(ops.transpose_codes(q), s)
+
+
+def from_toy_layers(layers) -> list[DeviceLayer]:
+    """ToyBlockWeights (f32 or BlockQuantized matrices) -> device layers."""
+    from .blockquant import BlockQuantized
+
+    def lin(m):
+        if isinstance(m, BlockQuantized):
+            return DeviceLinear(m.device_codes_t(), m.device_scales())
+        t = m if isinstance(m, torch.Tensor) else torch.from_numpy(m)
+        return quantize_device_weight(t.cuda().float())
+
+    def vec(v):
+        return (v if isinstance(v, torch.Tensor) else torch.from_numpy(v)).cuda().float().contiguous()
+
+    return [DeviceLayer(vec(w.rms_gain), vec(w.ln_gain), vec(w.ln_offset), vec(w.sigma_emb), lin(w.qkv),
+                        lin(w.out_proj), lin(w.mlp_in), lin(w.mlp_out)) for w in layers]
+
+
+def random_layers(model_dim: int, ffn: int, num_layers: int, seed: int = 0) -> list[DeviceLayer]:
+    """Random-init Wan-shaped toy DiT on device: N(0,1)/sqrt(fan_in) matrices
+    (sampler.py:244-246), block-quantized by the device quantizer."""
+    g = torch.Generator(device="cuda").manual_seed(seed)
+
+    def mat(rows, cols):
+        w = torch.randn((rows, cols), generator=g, device="cuda") / math.sqrt(rows)
+        lin = quantize_device_weight(w)
+        del w
+        return lin
+
+    def vec(scale, offset=0.0):
+        return torch.randn(model_dim, generator=g, device="cuda") * scale + offset
+
+    return [DeviceLayer(vec(0.1, 1.0), vec(0.1, 1.0), vec(0.1), vec(0.01), mat(model_dim, 3 * model_dim),
+                        mat(model_dim, model_dim), mat(model_dim, ffn), mat(ffn, model_dim))
+            for _ in range(num_layers)]
+
+
+def _linear(x: torch.Tensor, w: DeviceLinear, out_dtype=torch.bfloat16) -> torch.Tensor:
+    return ops.quantized_linear(x, w.bt, w.scales, 128, None, out_dtype, exact=False)
+
+
+def block_forward(x: torch.Tensor, sigma: float, w: DeviceLayer, heads: int, sla: dict, L_global: int,
+                  group=None) -> torch.Tensor:
+    """One block over the local token shard x [L_p, model_dim] (f32 residual stream)."""
+    Lp, dim = x.shape
+    hd = dim // heads
+    x = x + float(sigma) * w.sigma_emb
+    a = ops.rmsnorm(x, w.rms_gain)
+    qkv = _linear(a, w.qkv)                                   # [L_p, 3*dim] bf16
+    q, k, v = (t.view(Lp, heads, hd) for t in qkv.split(dim, dim=1))
+
+    def attn(qh, kh, vh):
+        return ops.sla_attention(qh, kh, vh, sla["q_block"], sla["kv_block"], sla["topk_ratio"],
+                                 sla.get("linear_mix", 1.0), True, out_dtype=torch.bfloat16)
+
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        o = ulysses.ulysses_sla_attention(q.contiguous(), k.contiguous(), v.contiguous(), L_global, attn, group)
+    else:
+        o = attn(q.permute(1, 0, 2).contiguous(), k.permute(1, 0, 2).contiguous(),
+                 v.permute(1, 0, 2).contiguous()).permute(1, 0, 2)
+    o = o.reshape(Lp, dim)
+    x = x + _linear(o.contiguous(), w.out_proj, torch.float32)
+    b = ops.layernorm(x, w.ln_gain, w.ln_offset)
+    h1 = _linear(b, w.mlp_in)
+    h1 = torch.nn.functional.gelu(h1, approximate="tanh")     # sampler.py:55-58
+    return x + _linear(h1, w.mlp_out, torch.float32)
+
+
+def model_forward(x, sigma, layers, heads, sla, L_global, group=None):
+    for w in layers:
+        x = block_forward(x, sigma, w, heads, sla, L_global, group)
+    return x
+
+
+def rcm_sample(layers, heads: int, sla: dict, x_init: torch.Tensor, noises: list, sigmas, group=None,
+               L_global: int | None = None):
+    """sampler.py:281-302 over device tensors: x = sigma0*eps0; x0 = f(x, s_i);
+    x = x0 + s_{i+1}*eps_{i+1}; exactly len(sigmas)-1 model calls."""
+    L_global = x_init.shape[0] if L_global is None else L_global
+    x = float(sigmas[0]) * x_init
+    x0 = x
+    for i in range(len(sigmas) - 1):
+        x0 = model_forward(x, float(sigmas[i]), layers, heads, sla, L_global, group)
+        if sigmas[i + 1] > 0:
+            x = x0 + float(sigmas[i + 1]) * noises[i]
+    return x0
