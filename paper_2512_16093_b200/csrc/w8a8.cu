@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) w8a8_tc_kernel(
 #pragma unroll
                         for (int i = 0; i < 16; i++) {
                             // exact s32 -> f32 (|seg| <= 128*127^2 < 2^22)
-                            const float x = __int_as_float((int)r[j][i] + 0x4B400000) - 12582912.0f;
+                            const float x = __int2float_rn((int)r[j][i]);   // I2FP, exact (|seg| < 2^24)
                             float &o = acc[cc + j * 16 + i];
                             if constexpr (EXACT) o = __fadd_rn(o, __fmul_rn(__fmul_rn(x, s_a), s_b));
                             else o = fmaf(x, s_ab, o);
