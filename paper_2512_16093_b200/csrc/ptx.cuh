@@ -160,6 +160,26 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
         : "memory");
 }
 
+// --------------------------------------------- packed f32x2 math (sm_100)
+// FFMA2 / FMUL2 / FADD2: two IEEE RN operations per instruction (each lane of
+// the pair rounds exactly like the scalar op), halving FP issue slots.
+union f2u { float2 f; unsigned long long u; };
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    f2u A{a}, B{b}, C{c}, D;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(D.u) : "l"(A.u), "l"(B.u), "l"(C.u));
+    return D.f;
+}
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+    f2u A{a}, B{b}, D;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(D.u) : "l"(A.u), "l"(B.u));
+    return D.f;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+    f2u A{a}, B{b}, D;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(D.u) : "l"(A.u), "l"(B.u));
+    return D.f;
+}
+
 // ------------------------------------------------- UMMA descriptors
 // Shared-memory matrix descriptor (sm_100): K-major operand, 128B swizzle,
 // 8-row core groups 1024 B apart (SBO), version 1.

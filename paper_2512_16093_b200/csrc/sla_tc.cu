@@ -299,28 +299,29 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
                     if (need) m_ref = mx;
                 }
             }
-            float psum = 0.0f;
+            float2 psum2 = make_float2(0.0f, 0.0f);
             uint32_t pk[2][16];
             const float off = c0m - m_ref;
+            const float2 c12 = make_float2(c1, c1), off2 = make_float2(off, off);
             auto make_p = [&](auto rg) {
                 constexpr bool RG = decltype(rg)::value;
 #pragma unroll
                 for (int i = 0; i < 64; i += 2) {
-                    const float y0 = fmaf(xm[i], c1, off);
-                    const float y1 = fmaf(xm[i + 1], c1, off);
-                    float p0 = ex2(y0);
-                    float p1 = ((i & 7) == 6) ? ex2_poly(y1) : ex2(y1);   // 1/8 of exps on the FMA pipe
+                    const float2 y = ptx::ffma2(make_float2(xm[i], xm[i + 1]), c12, off2);   // FFMA2
+                    float p0 = ex2(y.x);
+                    float p1 = ((i & 7) == 6) ? ex2_poly(y.y) : ex2(y.y);   // 1/8 of exps on the FMA pipe
                     if (RG) {
                         if (i >= lim) p0 = 0.0f;
                         if (i + 1 >= lim) p1 = 0.0f;
                     }
-                    psum += p0 + p1;
+                    psum2 = ptx::fadd2(psum2, make_float2(p0, p1));
                     __nv_bfloat162 pp = __floats2bfloat162_rn(p0, p1);
                     pk[i >> 5][(i >> 1) & 15] = *reinterpret_cast<uint32_t *>(&pp);
                 }
             };
             if (ragged) make_p(std::integral_constant<bool, true>());
             else make_p(std::integral_constant<bool, false>());
+            const float psum = psum2.x + psum2.y;
             l += psum;
             // P_j overwrites S_j's first 32 columns (A operand of PV, bf16x2 per column)
             ptx::tmem_st16(tmem + lane_base + sb * BN, pk[0]);

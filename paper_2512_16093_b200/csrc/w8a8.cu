@@ -116,13 +116,17 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) w8a8_tc_kernel(
             const int mt = tile % nmt, nt = tile / nmt;
             const int col0 = nt * BN + half * CW;
             const int nb = col0 / 128;
-            float acc[CW];
+            float2 acc2[CW / 2];
 #pragma unroll
-            for (int i = 0; i < CW; i++) acc[i] = 0.0f;
+            for (int i = 0; i < CW / 2; i++) acc2[i] = make_float2(0.0f, 0.0f);
+            float s_a = __ldg(sa + (size_t)mt * nkb), s_b = __ldg(sb + nb);
             for (int kb = 0; kb < nkb; kb++) {
-                const float s_a = __ldg(sa + (size_t)mt * nkb + kb);
-                const float s_b = __ldg(sb + (size_t)kb * nnb + nb);
-                const float s_ab = s_a * s_b;
+                const float2 sa2 = make_float2(s_a, s_a), sb2 = make_float2(s_b, s_b);
+                const float2 sab2 = make_float2(s_a * s_b, s_a * s_b);
+                if (kb + 1 < nkb) {                     // prefetch next k-block's scales
+                    s_a = __ldg(sa + (size_t)mt * nkb + kb + 1);
+                    s_b = __ldg(sb + (size_t)(kb + 1) * nnb + nb);
+                }
                 ptx::mbar_wait_sleep(&S.seg_full[buf], bphase);
                 ptx::tc_fence_after();
                 const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + buf * BN + half * CW;
@@ -139,17 +143,20 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) w8a8_tc_kernel(
 #pragma unroll
                     for (int j = 0; j < 2; j++)
 #pragma unroll
-                        for (int i = 0; i < 16; i++) {
-                            // exact s32 -> f32 (|seg| <= 128*127^2 < 2^22)
-                            const float x = __int2float_rn((int)r[j][i]);   // I2FP, exact (|seg| < 2^24)
-                            float &o = acc[cc + j * 16 + i];
-                            if constexpr (EXACT) o = __fadd_rn(o, __fmul_rn(__fmul_rn(x, s_a), s_b));
-                            else o = fmaf(x, s_ab, o);
+                        for (int i = 0; i < 16; i += 2) {
+                            // exact s32 -> f32 (I2FP; |seg| <= 128*127^2 < 2^24), then packed f32x2 math
+                            const float2 x = make_float2(__int2float_rn((int)r[j][i]), __int2float_rn((int)r[j][i + 1]));
+                            float2 &o = acc2[(cc + j * 16 + i) >> 1];
+                            if constexpr (EXACT) o = ptx::fadd2(o, ptx::fmul2(ptx::fmul2(x, sa2), sb2));
+                            else o = ptx::ffma2(x, sab2, o);
                         }
                 }
                 buf ^= 1;
                 if (buf == 0) bphase ^= 1;
             }
+            float acc[CW];
+#pragma unroll
+            for (int i = 0; i < CW / 2; i++) { acc[2 * i] = acc2[i].x; acc[2 * i + 1] = acc2[i].y; }
             const int row = mt * BM + trow;
             if (row < M) {
                 if (bias) {
