@@ -147,8 +147,14 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) w8a8_tc_kernel(
                             // exact s32 -> f32 (I2FP; |seg| <= 128*127^2 < 2^24), then packed f32x2 math
                             const float2 x = make_float2(__int2float_rn((int)r[j][i]), __int2float_rn((int)r[j][i + 1]));
                             float2 &o = acc2[(cc + j * 16 + i) >> 1];
-                            if constexpr (EXACT) o = ptx::fadd2(o, ptx::fmul2(ptx::fmul2(x, sa2), sb2));
-                            else o = ptx::ffma2(x, sab2, o);
+                            if constexpr (EXACT) {
+                                // scalar RN ops: the reference rounding sequence bit-for-bit (the
+                                // packed f32x2 forms differ in the last bits on sm_100a)
+                                o.x = __fadd_rn(o.x, __fmul_rn(__fmul_rn(x.x, sa2.x), sb2.x));
+                                o.y = __fadd_rn(o.y, __fmul_rn(__fmul_rn(x.y, sa2.y), sb2.y));
+                            } else {
+                                o = ptx::ffma2(x, sab2, o);
+                            }
                         }
                 }
                 buf ^= 1;
