@@ -255,17 +255,24 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             for (int i = 0; i < 64; i++) xm[i] = __int_as_float((int)s[i >> 4][i & 15] + 0x4B400000);
             float sx;
             if (!ragged) {
-                float a = xm[0], z = xm[0];
+                // 4 independent 3-input max/min chains (depth 8 instead of 31)
+                float a[4];
                 if (c1 >= 0.0f) {
 #pragma unroll
-                    for (int i = 1; i < 63; i += 2) a = fmaxf(a, fmaxf(xm[i], xm[i + 1]));
-                    a = fmaxf(a, xm[63]);
-                    sx = a;
+                    for (int u = 0; u < 4; u++) a[u] = xm[u];
+#pragma unroll
+                    for (int i = 4; i < 64; i += 8)
+#pragma unroll
+                        for (int u = 0; u < 4; u++) a[u] = fmaxf(a[u], fmaxf(xm[i + 2 * u], xm[i + 2 * u + 1]));
+                    sx = fmaxf(fmaxf(a[0], a[1]), fmaxf(a[2], a[3]));
                 } else {
 #pragma unroll
-                    for (int i = 1; i < 63; i += 2) z = fminf(z, fminf(xm[i], xm[i + 1]));
-                    z = fminf(z, xm[63]);
-                    sx = z;
+                    for (int u = 0; u < 4; u++) a[u] = xm[u];
+#pragma unroll
+                    for (int i = 4; i < 64; i += 8)
+#pragma unroll
+                        for (int u = 0; u < 4; u++) a[u] = fminf(a[u], fminf(xm[i + 2 * u], xm[i + 2 * u + 1]));
+                    sx = fminf(fminf(a[0], a[1]), fminf(a[2], a[3]));
                 }
             } else {
                 sx = xm[0];
@@ -299,7 +306,8 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
                     if (need) m_ref = mx;
                 }
             }
-            float2 psum2 = make_float2(0.0f, 0.0f);
+            float2 psum2[4] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f),
+                               make_float2(0.0f, 0.0f)};
             uint32_t pk[2][16];
             const float off = c0m - m_ref;
             const float2 c12 = make_float2(c1, c1), off2 = make_float2(off, off);
@@ -309,19 +317,20 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
                 for (int i = 0; i < 64; i += 2) {
                     const float2 y = ptx::ffma2(make_float2(xm[i], xm[i + 1]), c12, off2);   // FFMA2
                     float p0 = ex2(y.x);
-                    float p1 = ((i & 7) == 6) ? ex2_poly(y.y) : ex2(y.y);   // 1/8 of exps on the FMA pipe
+                    float p1 = ((i & 3) == 2) ? ex2_poly(y.y) : ex2(y.y);   // 1/4 of exps on the FMA pipe
                     if (RG) {
                         if (i >= lim) p0 = 0.0f;
                         if (i + 1 >= lim) p1 = 0.0f;
                     }
-                    psum2 = ptx::fadd2(psum2, make_float2(p0, p1));
+                    psum2[(i >> 1) & 3] = ptx::fadd2(psum2[(i >> 1) & 3], make_float2(p0, p1));
                     __nv_bfloat162 pp = __floats2bfloat162_rn(p0, p1);
                     pk[i >> 5][(i >> 1) & 15] = *reinterpret_cast<uint32_t *>(&pp);
                 }
             };
             if (ragged) make_p(std::integral_constant<bool, true>());
             else make_p(std::integral_constant<bool, false>());
-            const float psum = psum2.x + psum2.y;
+            const float2 ps = ptx::fadd2(ptx::fadd2(psum2[0], psum2[1]), ptx::fadd2(psum2[2], psum2[3]));
+            const float psum = ps.x + ps.y;
             l += psum;
             // P_j overwrites S_j's first 32 columns (A operand of PV, bf16x2 per column)
             ptx::tmem_st16(tmem + lane_base + sb * BN, pk[0]);
