@@ -54,6 +54,17 @@ constexpr float LOG2E = 1.4426950408889634f;
 constexpr float LN2 = 0.6931471805599453f;
 }  // namespace sla
 
+#ifdef TB_SLA_TRACE
+// diagnostic timestamps (clock64) of one CTA: [block][event]
+__device__ unsigned long long tb_sla_trace[64][8];
+#define TB_TRACE(j, e)                                                                                   \
+    do {                                                                                                 \
+        if (blockIdx.x == 100 && blockIdx.y == 5 && (j) < 64) tb_sla_trace[(j)][(e)] = clock64();        \
+    } while (0)
+#else
+#define TB_TRACE(j, e) do {} while (0)
+#endif
+
 __device__ __forceinline__ float ex2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -161,7 +172,9 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             auto pv = [&](int i) {
                 const int pb = i & 1, vs = i % VSTAGES;
                 ptx::mbar_wait_sleep(&S.v_full[vs], (uint32_t)((i / VSTAGES) & 1));
+                TB_TRACE(i, 4);
                 ptx::mbar_wait_sleep(&S.p_full[pb], (uint32_t)((i >> 1) & 1));
+                TB_TRACE(i, 5);
                 ptx::tc_fence_after();
                 const uint64_t vd = ptx::sdesc_sw128(ptx::smem_u32(S.v[vs]));
 #pragma unroll
@@ -172,7 +185,9 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             };
             auto qk = [&](int j) {
                 const int ks = j % KSTAGES, sb = j & 1;
+                TB_TRACE(j, 6);
                 ptx::mbar_wait_sleep(&S.k_full[ks], (uint32_t)((j / KSTAGES) & 1));
+                TB_TRACE(j, 7);
                 ptx::tc_fence_after();
                 const uint64_t kd = ptx::sdesc_sw128(ptx::smem_u32(S.k[ks]));
                 // S_sb last held P_{j-2}, read by PV(j-2), issued earlier: in-order tensor pipe
@@ -240,8 +255,10 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             // s32 -> f32 via the 1.5*2^23 magic: x = M + s exactly; fold -M*c1 into the offset
             const float c0m = fmaf(-12582912.0f, c1, c0);
             if (j + 1 < count) { b_next = __ldg(sel + j + 1); sk_next = __ldg(ksc + b_next); }
+            if (threadIdx.x == 0) TB_TRACE(j, 0);
             ptx::mbar_wait_sleep(&S.s_full[sb], (uint32_t)((j >> 1) & 1));
             ptx::tc_fence_after();
+            if (threadIdx.x == 0) TB_TRACE(j, 1);
             uint32_t s[4][16];
 #pragma unroll
             for (int q4 = 0; q4 < 4; q4++) ptx::tmem_ld16(tmem + lane_base + sb * BN + q4 * 16, s[q4]);
@@ -281,6 +298,7 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
                     if (i < lim) sx = (c1 >= 0.0f) ? fmaxf(sx, xm[i]) : fminf(sx, xm[i]);
             }
             const float mx = fmaf(sx, c1, c0m);
+            if (threadIdx.x == 0) TB_TRACE(j, 2);
             m_true = fmaxf(m_true, mx);
             if (j == 0) {
                 m_ref = mx;
@@ -338,6 +356,7 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             ptx::tmem_wait_st();
             ptx::tc_fence_before();
             ptx::mbar_arrive(&S.p_full[sb]);
+            if (threadIdx.x == 0) TB_TRACE(j, 3);
         }
         // ------------------------------------------------------- epilogue
         ptx::mbar_wait_sleep(&S.o_final, 0);
@@ -496,3 +515,9 @@ extern "C" int tb_sla_attention(const tb_sla_args *a, void *stream) {
     TB_REQUIRE(a->lin_kv == nullptr, "fused linear epilogue needs the tensor-core envelope");
     return sla_simt(a, st);
 }
+
+#ifdef TB_SLA_TRACE
+extern "C" int tb_sla_trace_read(unsigned long long *host) {
+    return cudaMemcpyFromSymbol(host, tb_sla_trace, sizeof(tb_sla_trace)) == cudaSuccess ? 0 : -2;
+}
+#endif
