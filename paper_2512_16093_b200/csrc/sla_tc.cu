@@ -82,6 +82,21 @@ __device__ __forceinline__ float ex2_poly(float x) {
     return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
+// Packed form for two exponents: FFMA2/FADD2 carry the split and the Horner
+// chain, so one pair costs ~10 issue slots and no MUFU/XU cycles.
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+    x.x = fmaxf(x.x, -126.0f);
+    x.y = fmaxf(x.y, -126.0f);
+    const float2 M = make_float2(12582912.0f, 12582912.0f), NM = make_float2(-12582912.0f, -12582912.0f);
+    const float2 t = ptx::fadd2(x, M);                                    // low mantissa bits = round(x)
+    const float2 f = ptx::ffma2(ptx::fadd2(t, NM), make_float2(-1.0f, -1.0f), x);   // x - round(x)
+    float2 p = ptx::ffma2(make_float2(0.055088773f, 0.055088773f), f, make_float2(0.24260406f, 0.24260406f));
+    p = ptx::ffma2(p, f, make_float2(0.69327623f, 0.69327623f));
+    p = ptx::ffma2(p, f, make_float2(0.99992895f, 0.99992895f));
+    return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                       __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+
 template <typename T>
 __device__ __forceinline__ void load8(const T *p, float *x) {
     if constexpr (sizeof(T) == 2) {
@@ -334,8 +349,17 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
 #pragma unroll
                 for (int i = 0; i < 64; i += 2) {
                     const float2 y = ptx::ffma2(make_float2(xm[i], xm[i + 1]), c12, off2);   // FFMA2
-                    float p0 = ex2(y.x);
-                    float p1 = ((i & 3) == 2) ? ex2_poly(y.y) : ex2(y.y);   // 1/4 of exps on the FMA pipe
+                    // 3 of every 8 pairs (3/8 of the exponentials) on the FMA pipe, the rest on MUFU
+                    constexpr int PP = 0x52;                        // pair-slot mask {1, 4, 6} of 8
+                    float p0, p1;
+                    if ((PP >> ((i >> 1) & 7)) & 1) {
+                        const float2 e = ex2_poly2(y);
+                        p0 = e.x;
+                        p1 = e.y;
+                    } else {
+                        p0 = ex2(y.x);
+                        p1 = ex2(y.y);
+                    }
                     if (RG) {
                         if (i >= lim) p0 = 0.0f;
                         if (i + 1 >= lim) p1 = 0.0f;
