@@ -20,7 +20,7 @@ lib.tb_sla_trace_read.argtypes = [ctypes.c_void_p]
 assert lib.tb_sla_trace_read(ctypes.cast(buf, ctypes.c_void_p)) == 0
 t = np.array(buf, dtype=np.int64).reshape(64, 8)
 t0 = t[0, 0]
-names = ["sm_wait_s", "sm_s_ready", "sm_max_done", "sm_p_arrived", "mma_wait_p", "mma_p_ready", "mma_wait_k", "mma_k_ready"]
+names = ["wait_s", "s_ready", "max_done", "p_arrived", "ld_done", "exp_done", "st_done", "-"]
 print("block " + " ".join(f"{n:>12s}" for n in names))
 for j in range(40):
     print(f"{j:5d} " + " ".join(f"{int(x - t0):12d}" for x in t[j]))
@@ -29,3 +29,5 @@ print("softmax period (cycles/block): median", np.median(d), "mean", d.mean())
 print("softmax busy (s_ready -> p_arrived): median", np.median(t[5:40, 3] - t[5:40, 1]))
 print("wait for S (wait_s -> s_ready): median", np.median(t[5:40, 1] - t[5:40, 0]))
 print("S ready after P(j-1) arrival: median", np.median(t[6:40, 1] - t[5:39, 3]))
+for a_, b_, nm in ((1, 4, "ldtm"), (4, 2, "max"), (2, 5, "exp"), (5, 6, "sttm"), (6, 3, "arrive")):
+    print(f"phase {nm}: median {np.median(t[5:40, b_] - t[5:40, a_])}")
