@@ -12,7 +12,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtb200.so")
+# TB200_LIB selects an alternative in-tree build (e.g. the phase-trace variant)
+LIB_PATH = os.environ.get("TB200_LIB") or os.path.join(_HERE, "libtb200.so")
 
 TB_OK, TB_EINVAL, TB_ECUDA, TB_EUNSUPPORTED = 0, -1, -2, -3
 TB_F32, TB_BF16, TB_I8 = 0, 1, 2

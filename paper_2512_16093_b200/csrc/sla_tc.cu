@@ -32,6 +32,16 @@
 
 namespace tb {
 
+#ifndef TB_SLA_PP
+#define TB_SLA_PP 0x52
+#endif
+// TB_SLA_BIAS: seed each S tile with the float bits of 1.5*2^23 through one
+// kind::f16 MMA, so the s32 scores come out of TMEM already as the floats
+// M + s (no per-element integer add in the softmax)
+#ifndef TB_SLA_BIAS
+#define TB_SLA_BIAS 1
+#endif
+
 namespace sla {
 constexpr int BM = 128, BN = 64, D = 128, KSTAGES = 3, VSTAGES = 3;
 constexpr int THREADS = 192;
@@ -47,16 +57,20 @@ struct Smem {
     uint64_t v_full[VSTAGES], v_empty[VSTAGES];
     uint64_t s_full[2], p_full[2], pv_done[2];
     uint64_t phiq_full, lin_full, lin_done;     // fused linear-branch epilogue
+    alignas(128) uint16_t bias_a[128], bias_b[128];  // bias-MMA operands (2 core matrices each)
+    float c1[2048];                             // per selected block: sq * sk * scale * log2e
+    uint8_t rag[2048];                          // per selected block: ragged last kv block
     uint32_t tmem_base;
 };
-constexpr size_t SMEM_BYTES = sizeof(Smem) + 1024;
+constexpr int MAX_SEL = 2048;                  // selected kv blocks per q-block (c1 / ragged tables)
+constexpr size_t SMEM_BYTES = sizeof(Smem);
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float LN2 = 0.6931471805599453f;
 }  // namespace sla
 
 #ifdef TB_SLA_TRACE
 // diagnostic timestamps (clock64) of one CTA: [block][event]
-__device__ unsigned long long tb_sla_trace[64][8];
+__device__ unsigned long long tb_sla_trace[64][16];
 #define TB_TRACE(j, e)                                                                                   \
     do {                                                                                                 \
         if (blockIdx.x == 100 && blockIdx.y == 5 && (j) < 64) tb_sla_trace[(j)][(e)] = clock64();        \
@@ -110,14 +124,14 @@ __device__ __forceinline__ void load8(const T *p, float *x) {
     }
 }
 
-template <typename T>
+template <typename T, bool EXACT>
 __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
     const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_kv, tb_sla_args a, int nq,
     int nkv) {
     using namespace sla;
-    extern __shared__ uint8_t smem_raw[];
-    Smem &S = *reinterpret_cast<Smem *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    Smem &S = *reinterpret_cast<Smem *>(smem_raw);    // dynamic smem starts 1024-aligned (no static smem)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n = blockIdx.x, h = blockIdx.y;
     const int count = (int)a.count;
@@ -125,6 +139,7 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
     const int32_t *sel = a.idx + ((int64_t)h * nq + n) * count;
 
     if (warp == 4 && lane == 0) {
+        if (ptx::smem_u32(smem_raw) & 1023) __trap();     // SW128 tiles need 1024-B alignment
         ptx::mbar_init(&S.q_full, 1);
         ptx::mbar_init(&S.o_final, 1);
         for (int s = 0; s < KSTAGES; s++) { ptx::mbar_init(&S.k_full[s], 1); ptx::mbar_init(&S.k_empty[s], 1); }
@@ -137,6 +152,12 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
         ptx::mbar_init(&S.phiq_full, 128);
         ptx::mbar_init(&S.lin_full, 1);
         ptx::mbar_init(&S.lin_done, 1);
+        // bias-MMA operands: A rows [1, 0 x7 | 1, 0 x7], B rows [M/2, 0 x7 | M/2, 0 x7]
+        for (int i = 0; i < 128; i++) {
+            S.bias_a[i] = (i % 8 == 0) ? 0x3F80 : 0;    // bf16 1.0
+            S.bias_b[i] = (i % 8 == 0) ? 0x4AC0 : 0;    // bf16 6291456 = 1.5 * 2^22
+        }
+        ptx::fence_async_smem();
         ptx::fence_barrier_init();
         ptx::prefetch_tmap(&tm_q);
         ptx::prefetch_tmap(&tm_k);
@@ -156,71 +177,101 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
 
     if (warp == 4) {
         // ------------------------------------------------------ TMA producer
-        if (lane == 0) {
+        // the whole warp walks the loop (warp-uniform values, no waterfall
+        // loops around the uniform-operand TMA instructions); one lane issues
+        if (ptx::elect_one()) {
             ptx::mbar_arrive_expect_tx(&S.q_full, Q_BYTES);
             ptx::tma_load_3d(S.q, &tm_q, 0, n * BM, h, &S.q_full);
-            for (int j = 0; j < count; j++) {
-                const int b = __ldg(sel + j);
-                const int ks = j % KSTAGES, vs = j % VSTAGES;
-                ptx::mbar_wait_sleep(&S.k_empty[ks], (uint32_t)(((j / KSTAGES) & 1) ^ 1));
+        }
+        __syncwarp();
+        for (int j = 0; j < count; j++) {
+            const int b = __ldg(sel + j);
+            const int ks = j % KSTAGES, vs = j % VSTAGES;
+            ptx::mbar_wait_sleep(&S.k_empty[ks], (uint32_t)(((j / KSTAGES) & 1) ^ 1));
+            if (lane == 0) TB_TRACE(j, 10);
+            if (ptx::elect_one()) {
                 ptx::mbar_arrive_expect_tx(&S.k_full[ks], K_BYTES);
                 ptx::tma_load_3d(S.k[ks], &tm_k, 0, b * BN, h, &S.k_full[ks]);
-                ptx::mbar_wait_sleep(&S.v_empty[vs], (uint32_t)(((j / VSTAGES) & 1) ^ 1));
+            }
+            __syncwarp();
+            ptx::mbar_wait_sleep(&S.v_empty[vs], (uint32_t)(((j / VSTAGES) & 1) ^ 1));
+            if (lane == 0) TB_TRACE(j, 11);
+            if (ptx::elect_one()) {
                 ptx::mbar_arrive_expect_tx(&S.v_full[vs], V_BYTES);
                 ptx::tma_load_3d(S.v[vs], &tm_v, b * BN, 0, h, &S.v_full[vs]);
             }
-            if (fused) {
-                ptx::mbar_wait_sleep(&S.o_final, 0);        // every MMA reading the rings is done
-                const int row0 = (int)(((int64_t)h * nq + n) * a.lin_dx);
+            __syncwarp();
+        }
+        if (fused) {
+            ptx::mbar_wait_sleep(&S.o_final, 0);        // every MMA reading the rings is done
+            const int row0 = (int)(((int64_t)h * nq + n) * a.lin_dx);
+            if (ptx::elect_one()) {
                 ptx::mbar_arrive_expect_tx(&S.lin_full, 2 * 16384);
                 ptx::tma_load_2d(lin_b, &tm_kv, 0, row0, &S.lin_full);
                 ptx::tma_load_2d(lin_b + 16384, &tm_kv, 64, row0, &S.lin_full);
             }
+            __syncwarp();
         }
     } else if (warp == 5) {
         // ------------------------------------------------------- MMA issuer
-        if (lane == 0) {
-            constexpr uint32_t ID_QK = ptx::idesc_i8(BM, BN);
-            constexpr uint32_t ID_PV = ptx::idesc_bf16(BM, D);
-            const uint64_t qd = ptx::sdesc_sw128(ptx::smem_u32(S.q));
-            ptx::mbar_wait_sleep(&S.q_full, 0);
-            auto pv = [&](int i) {
-                const int pb = i & 1, vs = i % VSTAGES;
-                ptx::mbar_wait_sleep(&S.v_full[vs], (uint32_t)((i / VSTAGES) & 1));
-                ptx::mbar_wait_sleep(&S.p_full[pb], (uint32_t)((i >> 1) & 1));
-                ptx::tc_fence_after();
-                const uint64_t vd = ptx::sdesc_sw128(ptx::smem_u32(S.v[vs]));
+        // whole warp in the loop, one elected lane issues each MMA group
+        constexpr uint32_t ID_QK = ptx::idesc_i8(BM, BN);
+        constexpr uint32_t ID_PV = ptx::idesc_bf16(BM, D);
+        constexpr uint32_t ID_BIAS = ptx::idesc_bf16(BM, BN);
+        const uint64_t qd = ptx::sdesc_sw128(ptx::smem_u32(S.q));
+        // no-swizzle K-major 8x16 bf16 tiles; SBO = 0 makes every 8-row group alias the same rows
+        const uint64_t bias_a = ptx::sdesc_noswz_alias(ptx::smem_u32(S.bias_a));
+        const uint64_t bias_b = ptx::sdesc_noswz_alias(ptx::smem_u32(S.bias_b));
+        ptx::mbar_wait_sleep(&S.q_full, 0);
+        auto pv = [&](int i) {
+            const int pb = i & 1, vs = i % VSTAGES;
+            ptx::mbar_wait_sleep(&S.v_full[vs], (uint32_t)((i / VSTAGES) & 1));
+            ptx::mbar_wait_sleep(&S.p_full[pb], (uint32_t)((i >> 1) & 1));
+            ptx::tc_fence_after();
+            if (lane == 0) TB_TRACE(i, 9);
+            const uint64_t vd = ptx::sdesc_sw128(ptx::smem_u32(S.v[vs]));
+            if (ptx::elect_one()) {
 #pragma unroll
                 for (int k = 0; k < BN / 16; k++)   // K=16 bf16 per MMA: 8 TMEM cols of P, 32 B of V^T
                     ptx::mma_f16_ts(TM_O, tmem + pb * BN + 8 * k, vd + 2 * k, ID_PV, (i > 0 || k > 0) ? 1u : 0u);
                 ptx::mma_commit(&S.pv_done[pb]);
                 ptx::mma_commit(&S.v_empty[vs]);
-            };
-            auto qk = [&](int j) {
-                const int ks = j % KSTAGES, sb = j & 1;
-                ptx::mbar_wait_sleep(&S.k_full[ks], (uint32_t)((j / KSTAGES) & 1));
-                ptx::tc_fence_after();
-                const uint64_t kd = ptx::sdesc_sw128(ptx::smem_u32(S.k[ks]));
-                // S_sb last held P_{j-2}, read by PV(j-2), issued earlier: in-order tensor pipe
+            }
+            __syncwarp();
+        };
+        auto qk = [&](int j) {
+            const int ks = j % KSTAGES, sb = j & 1;
+            ptx::mbar_wait_sleep(&S.k_full[ks], (uint32_t)((j / KSTAGES) & 1));
+            ptx::tc_fence_after();
+            if (lane == 0) TB_TRACE(j, 8);
+            const uint64_t kd = ptx::sdesc_sw128(ptx::smem_u32(S.k[ks]));
+            // S_sb last held P_{j-2}, read by PV(j-2), issued earlier: in-order tensor pipe
+            if (ptx::elect_one()) {
+                // D = 1 x 6291456 + 1 x 6291456 = 1.5*2^23 (bf16 operands, f32 bits) in every cell
+                if (TB_SLA_BIAS) ptx::mma_f16(tmem + sb * BN, bias_a, bias_b, ID_BIAS, 0u);
 #pragma unroll
                 for (int k = 0; k < D / 32; k++)    // K=32 int8 = 32 B per MMA
-                    ptx::mma_i8(tmem + sb * BN, qd + 2 * k, kd + 2 * k, ID_QK, k > 0 ? 1u : 0u);
+                    ptx::mma_i8(tmem + sb * BN, qd + 2 * k, kd + 2 * k, ID_QK, (TB_SLA_BIAS || k > 0) ? 1u : 0u);
                 ptx::mma_commit(&S.s_full[sb]);
                 ptx::mma_commit(&S.k_empty[ks]);
-            };
-            // QK(j+1) is queued before PV(j) waits for softmax(j): the tensor
-            // pipe computes the next scores while the softmax warps work
-            qk(0);
-            for (int j = 0; j < count; j++) {
-                if (j + 1 < count) qk(j + 1);
-                pv(j);
             }
-            ptx::mma_commit(&S.o_final);
-            if (fused) {
-                // numL = phi(Q) . KV_sel  (M128 N128 K128, bf16) into the free S/P columns 0..127
-                ptx::mbar_wait_sleep(&S.phiq_full, 0);
-                ptx::mbar_wait_sleep(&S.lin_full, 0);
-                ptx::tc_fence_after();
+            __syncwarp();
+        };
+        // QK(j+1) is queued before PV(j) waits for softmax(j): the tensor
+        // pipe computes the next scores while the softmax warps work
+        qk(0);
+        for (int j = 0; j < count; j++) {
+            if (j + 1 < count) qk(j + 1);
+            pv(j);
+        }
+        if (ptx::elect_one()) ptx::mma_commit(&S.o_final);
+        __syncwarp();
+        if (fused) {
+            // numL = phi(Q) . KV_sel  (M128 N128 K128, bf16) into the free S/P columns 0..127
+            ptx::mbar_wait_sleep(&S.phiq_full, 0);
+            ptx::mbar_wait_sleep(&S.lin_full, 0);
+            ptx::tc_fence_after();
+            if (ptx::elect_one()) {
 #pragma unroll
                 for (int ks = 0; ks < D / 16; ks++) {
                     const int sub = ks >> 2, w = ks & 3;
@@ -230,6 +281,7 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
                 }
                 ptx::mma_commit(&S.lin_done);
             }
+            __syncwarp();
         }
     } else {
         // ------------------------------------------------ softmax + epilogue
@@ -256,16 +308,30 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
         const float *ksc = a.k_scales + (int64_t)h * nkv;
         const int last_blk = nkv - 1;
         const int last_ext = L - last_blk * BN;
+        // m_ref: the running reference (log2 units) the exponentials are taken
+        // against.  Fast path (EXACT == false): no per-block row max at all --
+        // p = 2^(logit2 - m_ref) is computed straight away and the block is
+        // accepted when its row sum stays <= 2^60 (finite, far from f32 / bf16
+        // overflow); otherwise (first block: m_ref = -inf gives inf / NaN) the
+        // warp takes the exact path below: row max, lazy O rebase when the max
+        // outgrows m_ref by > 8, recompute.  The softmax and the SLA combine
+        // are invariant to the reference (attention.py:416-421: num and den
+        // carry the same exp(-ref)), so only rounding differs.  EXACT == true
+        // (row_max / den outputs requested) runs the exact path every block
+        // and reports the true row max like _sparse_branch (attention.py:385-389).
+        // per selected block: logit slope and ragged flag (smem, read once per block)
+        for (int j = r; j < count; j += BM) {
+            const int b = __ldg(sel + j);
+            S.c1[j] = sq * __ldg(ksc + b) * scale2;
+            S.rag[j] = (b == last_blk) && last_ext < BN;
+        }
+        ptx::named_bar_sync(1, BM);
         float m_ref = -INFINITY, m_true = -INFINITY, l = 0.0f;
-        int b_next = __ldg(sel);
-        float sk_next = __ldg(ksc + b_next);
         for (int j = 0; j < count; j++) {
             const int sb = j & 1;
-            const int b = b_next;
-            const float c1 = sq * sk_next * scale2;
-            // s32 -> f32 via the 1.5*2^23 magic: x = M + s exactly; fold -M*c1 into the offset
+            const float c1 = S.c1[j];
+            // s32 scores as the floats M + s (M = 1.5*2^23, exact): fold -M*c1 into the offset
             const float c0m = fmaf(-12582912.0f, c1, c0);
-            if (j + 1 < count) { b_next = __ldg(sel + j + 1); sk_next = __ldg(ksc + b_next); }
             if (threadIdx.x == 0) TB_TRACE(j, 0);
             ptx::mbar_wait_sleep(&S.s_full[sb], (uint32_t)((j >> 1) & 1));
             ptx::tc_fence_after();
@@ -275,79 +341,24 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             for (int q4 = 0; q4 < 4; q4++) ptx::tmem_ld16(tmem + lane_base + sb * BN + q4 * 16, s[q4]);
             ptx::tmem_wait_ld();
             if (threadIdx.x == 0) TB_TRACE(j, 4);
-            // logit2 is affine in the exact s32 score with slope c1 (uniform
-            // sign per CTA), so the row max comes from an integer max/min
-            const bool ragged = (b == last_blk) && last_ext < BN;     // uniform per CTA
+            const bool ragged = S.rag[j] != 0;                        // uniform per CTA
             const int lim = ragged ? last_ext : BN;
             float xm[64];                   // M + s exactly (|s| < 2^22): monotone in s
 #pragma unroll
-            for (int i = 0; i < 64; i++) xm[i] = __int_as_float((int)s[i >> 4][i & 15] + 0x4B400000);
-            float sx;
-            if (!ragged) {
-                // 4 independent 3-input max/min chains (depth 8 instead of 31)
-                float a[4];
-                if (c1 >= 0.0f) {
-#pragma unroll
-                    for (int u = 0; u < 4; u++) a[u] = xm[u];
-#pragma unroll
-                    for (int i = 4; i < 64; i += 8)
-#pragma unroll
-                        for (int u = 0; u < 4; u++) a[u] = fmaxf(a[u], fmaxf(xm[i + 2 * u], xm[i + 2 * u + 1]));
-                    sx = fmaxf(fmaxf(a[0], a[1]), fmaxf(a[2], a[3]));
-                } else {
-#pragma unroll
-                    for (int u = 0; u < 4; u++) a[u] = xm[u];
-#pragma unroll
-                    for (int i = 4; i < 64; i += 8)
-#pragma unroll
-                        for (int u = 0; u < 4; u++) a[u] = fminf(a[u], fminf(xm[i + 2 * u], xm[i + 2 * u + 1]));
-                    sx = fminf(fminf(a[0], a[1]), fminf(a[2], a[3]));
-                }
-            } else {
-                sx = xm[0];
-#pragma unroll
-                for (int i = 1; i < 64; i++)      // static indices keep xm[] in registers
-                    if (i < lim) sx = (c1 >= 0.0f) ? fmaxf(sx, xm[i]) : fminf(sx, xm[i]);
-            }
-            const float mx = fmaf(sx, c1, c0m);
-            if (threadIdx.x == 0) TB_TRACE(j, 2);
-            m_true = fmaxf(m_true, mx);
-            if (j == 0) {
-                m_ref = mx;
-            } else {
-                // lazy rebase of O when a row's max outgrows its reference by
-                // > 8 (p <= 256).  tcgen05.ld/st are warp-collective, so the
-                // decision is made per warp; rows that do not need it use 1.
-                const bool need = mx > m_ref + 8.0f;
-                if (__any_sync(0xffffffffu, need)) {
-                    ptx::mbar_wait_sleep(&S.pv_done[(j - 1) & 1], (uint32_t)(((j - 1) >> 1) & 1));
-                    ptx::tc_fence_after();
-                    const float alpha = need ? ex2(m_ref - mx) : 1.0f;
-#pragma unroll 1
-                    for (int c = 0; c < D; c += 16) {
-                        uint32_t o[16];
-                        ptx::tmem_ld16(TM_O + lane_base + c, o);
-                        ptx::tmem_wait_ld();
-#pragma unroll
-                        for (int i = 0; i < 16; i++) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-                        ptx::tmem_st16(TM_O + lane_base + c, o);
-                    }
-                    l *= alpha;
-                    if (need) m_ref = mx;
-                }
-            }
-            float2 psum2[4] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f),
-                               make_float2(0.0f, 0.0f)};
+            for (int i = 0; i < 64; i++)
+                xm[i] = __int_as_float((int)s[i >> 4][i & 15] + (TB_SLA_BIAS ? 0 : 0x4B400000));
+            float2 psum2[4];
             uint32_t pk[2][16];
-            const float off = c0m - m_ref;
-            const float2 c12 = make_float2(c1, c1), off2 = make_float2(off, off);
-            auto make_p = [&](auto rg) {
+            auto make_p = [&](auto rg, float off) {
                 constexpr bool RG = decltype(rg)::value;
+                const float2 c12 = make_float2(c1, c1), off2 = make_float2(off, off);
+#pragma unroll
+                for (int u = 0; u < 4; u++) psum2[u] = make_float2(0.0f, 0.0f);
 #pragma unroll
                 for (int i = 0; i < 64; i += 2) {
                     const float2 y = ptx::ffma2(make_float2(xm[i], xm[i + 1]), c12, off2);   // FFMA2
                     // 3 of every 8 pairs (3/8 of the exponentials) on the FMA pipe, the rest on MUFU
-                    constexpr int PP = 0x52;                        // pair-slot mask {1, 4, 6} of 8
+                    constexpr int PP = TB_SLA_PP;                   // pair-slot mask {1, 4, 6} of 8
                     float p0, p1;
                     if ((PP >> ((i >> 1) & 7)) & 1) {
                         const float2 e = ex2_poly2(y);
@@ -365,12 +376,79 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
                     __nv_bfloat162 pp = __floats2bfloat162_rn(p0, p1);
                     pk[i >> 5][(i >> 1) & 15] = *reinterpret_cast<uint32_t *>(&pp);
                 }
+                const float2 ps = ptx::fadd2(ptx::fadd2(psum2[0], psum2[1]), ptx::fadd2(psum2[2], psum2[3]));
+                return ps.x + ps.y;
             };
-            if (ragged) make_p(std::integral_constant<bool, true>());
-            else make_p(std::integral_constant<bool, false>());
+            auto run_p = [&](float off) {
+                return ragged ? make_p(std::integral_constant<bool, true>(), off)
+                              : make_p(std::integral_constant<bool, false>(), off);
+            };
+            float psum = 0.0f;
+            bool slow = EXACT;
+            if (!EXACT) {
+                psum = run_p(c0m - m_ref);
+                slow = __any_sync(0xffffffffu, !(psum <= 0x1p60f));
+            }
+            if (slow) {
+                // exact row max of the block: logit2 is affine in the exact s32
+                // score with slope c1 (uniform sign per CTA) -> max/min of M + s
+                float sx;
+                if (!ragged) {
+                    // 4 independent 3-input max/min chains (depth 8 instead of 31)
+                    float a4[4];
+                    if (c1 >= 0.0f) {
+#pragma unroll
+                        for (int u = 0; u < 4; u++) a4[u] = xm[u];
+#pragma unroll
+                        for (int i = 4; i < 64; i += 8)
+#pragma unroll
+                            for (int u = 0; u < 4; u++) a4[u] = fmaxf(a4[u], fmaxf(xm[i + 2 * u], xm[i + 2 * u + 1]));
+                        sx = fmaxf(fmaxf(a4[0], a4[1]), fmaxf(a4[2], a4[3]));
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < 4; u++) a4[u] = xm[u];
+#pragma unroll
+                        for (int i = 4; i < 64; i += 8)
+#pragma unroll
+                            for (int u = 0; u < 4; u++) a4[u] = fminf(a4[u], fminf(xm[i + 2 * u], xm[i + 2 * u + 1]));
+                        sx = fminf(fminf(a4[0], a4[1]), fminf(a4[2], a4[3]));
+                    }
+                } else {
+                    sx = xm[0];
+#pragma unroll
+                    for (int i = 1; i < 64; i++)      // static indices keep xm[] in registers
+                        if (i < lim) sx = (c1 >= 0.0f) ? fmaxf(sx, xm[i]) : fminf(sx, xm[i]);
+                }
+                const float mx = fmaf(sx, c1, c0m);
+                if (threadIdx.x == 0) TB_TRACE(j, 2);
+                m_true = fmaxf(m_true, mx);
+                if (m_ref == -INFINITY) {
+                    m_ref = mx;                       // first block of the row: nothing accumulated yet
+                } else {
+                    // lazy rebase of O when a row's max outgrows its reference by
+                    // > 8 (p <= 256).  tcgen05.ld/st are warp-collective, so the
+                    // decision is made per warp; rows that do not need it use 1.
+                    const bool need = mx > m_ref + 8.0f;
+                    if (__any_sync(0xffffffffu, need)) {
+                        ptx::mbar_wait_sleep(&S.pv_done[(j - 1) & 1], (uint32_t)(((j - 1) >> 1) & 1));
+                        ptx::tc_fence_after();
+                        const float alpha = need ? ex2(m_ref - mx) : 1.0f;
+#pragma unroll 1
+                        for (int c = 0; c < D; c += 16) {
+                            uint32_t o[16];
+                            ptx::tmem_ld16(TM_O + lane_base + c, o);
+                            ptx::tmem_wait_ld();
+#pragma unroll
+                            for (int i = 0; i < 16; i++) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+                            ptx::tmem_st16(TM_O + lane_base + c, o);
+                        }
+                        l *= alpha;
+                        if (need) m_ref = mx;
+                    }
+                }
+                psum = run_p(c0m - m_ref);
+            }
             if (threadIdx.x == 0) TB_TRACE(j, 5);
-            const float2 ps = ptx::fadd2(ptx::fadd2(psum2[0], psum2[1]), ptx::fadd2(psum2[2], psum2[3]));
-            const float psum = ps.x + ps.y;
             l += psum;
             // P_j overwrites S_j's first 32 columns (A operand of PV, bf16x2 per column)
             ptx::tmem_st16(tmem + lane_base + sb * BN, pk[0]);
@@ -380,7 +458,9 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             ptx::tc_fence_before();
             ptx::mbar_arrive(&S.p_full[sb]);
             if (threadIdx.x == 0) TB_TRACE(j, 3);
+            if (threadIdx.x == 96) TB_TRACE(j, 12);
         }
+        if (!EXACT) m_true = m_ref;                  // combine against the reference (exact in math)
         // ------------------------------------------------------- epilogue
         ptx::mbar_wait_sleep(&S.o_final, 0);
         ptx::tc_fence_after();
@@ -491,7 +571,7 @@ int sla_simt(const tb_sla_args *a, cudaStream_t st);
 bool sla_tc_supported(const tb_sla_args *a) {
     return a->quantized && a->d == 128 && a->q_block == 128 && a->kv_block == 64 && a->vt != nullptr &&
            a->L >= 128 && a->l_pad % 64 == 0 && a->l_pad >= cdiv(a->L, 64) * 64 &&
-           (a->dtype == TB_BF16 || a->dtype == TB_F32) && a->count >= 1 &&
+           (a->dtype == TB_BF16 || a->dtype == TB_F32) && a->count >= 1 && a->count <= sla::MAX_SEL &&
            (a->lin_kv == nullptr || a->lin_dx >= a->d + 1);
 }
 
@@ -509,12 +589,18 @@ int sla_tc(const tb_sla_args *a, cudaStream_t st) {
                                 64, 128);
     if (!ok) return fail(TB_ECUDA, "cuTensorMapEncodeTiled failed (sla)");
     dim3 grid((unsigned)nq, (unsigned)a->H);
+    // the exact-max variant only when the caller asks for the sparse-branch stats
+    const bool exact = a->row_max != nullptr || a->den != nullptr;
+    auto launch = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+        kern<<<grid, THREADS, SMEM_BYTES, st>>>(tq, tk, tv, tkv, *a, (int)nq, (int)nkv);
+    };
     if (a->dtype == TB_BF16) {
-        cudaFuncSetAttribute(sla_tc_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
-        sla_tc_kernel<__nv_bfloat16><<<grid, THREADS, SMEM_BYTES, st>>>(tq, tk, tv, tkv, *a, (int)nq, (int)nkv);
+        if (exact) launch(sla_tc_kernel<__nv_bfloat16, true>);
+        else launch(sla_tc_kernel<__nv_bfloat16, false>);
     } else {
-        cudaFuncSetAttribute(sla_tc_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
-        sla_tc_kernel<float><<<grid, THREADS, SMEM_BYTES, st>>>(tq, tk, tv, tkv, *a, (int)nq, (int)nkv);
+        if (exact) launch(sla_tc_kernel<float, true>);
+        else launch(sla_tc_kernel<float, false>);
     }
     return check_launch("sla_tc");
 }

@@ -209,6 +209,23 @@ def test_sla_tensor_core_path_sparse_dominated(tb):
         assert cos >= COS_MIN and rel1 <= REL_L1_MAX, (mix, cos, rel1)
 
 
+def test_sla_tensor_core_path_peaky_logits(tb):
+    """Logit jumps of 40+ (natural units) between selected blocks of a row:
+    the kernel's fast path (no per-block row max) must detect the overflow
+    risk and fall back to the exact rebase, matching the oracle."""
+    q, k, v = gen.gaussian_qkv(12, 2, 4096, 128, bf16=True)
+    k = k.copy()
+    for b in (3, 17, 40, 63):                      # a few "hot" kv blocks, 16x the logits (powers of two keep bf16 exact)
+        k[:, b * 64:(b + 1) * 64] *= 16.0
+    for hb in range(2):
+        k[hb, 5 * 64:6 * 64] *= -32.0                 # and a very negative one
+    for mix in (1.0, 0.0):
+        want = O.sla_attention(q, k, v, 128, 64, 0.1, mix)
+        got = tb.sla_attention(dev(q, True), dev(k, True), dev(v, True), 128, 64, 0.1, mix).cpu().numpy()
+        cos, _, rel1 = metrics(got, want)
+        assert cos >= COS_MIN and rel1 <= REL_L1_MAX, (mix, cos, rel1)
+
+
 def test_sla_topk_one_equals_dense_unquantized(tb):
     q, k, v = gen.gaussian_qkv(21, 2, 128, 16, bf16=False)
     out = tb.sla_attention(dev(q), dev(k), dev(v), 32, 32, 1.0, 1.0, quantized=False).cpu().numpy()

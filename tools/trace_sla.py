@@ -1,11 +1,17 @@
-"""Per-block phase timeline of one sla_tc CTA (build with -DTB_SLA_TRACE)."""
+"""Per-block phase timeline of one sla_tc CTA (clock64, SM cycles).
+
+Build the trace variant and run on the GPU box:
+    make -C paper_2512_16093_b200/csrc trace      # -> paper_2512_16093_b200/libtb200_trace.so
+    TB200_LIB=paper_2512_16093_b200/libtb200_trace.so python tools/trace_sla.py
+"""
 import ctypes
+import os
 import sys
 
 import numpy as np
 import torch
 
-sys.path.insert(0, ".")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2512_16093_b200 import _lib, ops  # noqa: E402
 
 H, L, D = 40, 75600, 128
@@ -14,20 +20,23 @@ q, k, v = (torch.randn((H, L, D), generator=g, device="cuda").to(torch.bfloat16)
 for _ in range(2):
     ops.sla_attention(q, k, v, 128, 64, 0.1, 1.0, out_dtype=torch.bfloat16)
 torch.cuda.synchronize()
-buf = (ctypes.c_ulonglong * (64 * 8))()
+buf = (ctypes.c_ulonglong * (64 * 16))()
 lib = _lib.load()
 lib.tb_sla_trace_read.argtypes = [ctypes.c_void_p]
 assert lib.tb_sla_trace_read(ctypes.cast(buf, ctypes.c_void_p)) == 0
-t = np.array(buf, dtype=np.int64).reshape(64, 8)
-t0 = t[0, 0]
-names = ["wait_s", "s_ready", "max_done", "p_arrived", "ld_done", "exp_done", "st_done", "-"]
-print("block " + " ".join(f"{n:>12s}" for n in names))
-for j in range(40):
-    print(f"{j:5d} " + " ".join(f"{int(x - t0):12d}" for x in t[j]))
-d = np.diff(t[5:40, 3])
-print("softmax period (cycles/block): median", np.median(d), "mean", d.mean())
-print("softmax busy (s_ready -> p_arrived): median", np.median(t[5:40, 3] - t[5:40, 1]))
-print("wait for S (wait_s -> s_ready): median", np.median(t[5:40, 1] - t[5:40, 0]))
-print("S ready after P(j-1) arrival: median", np.median(t[6:40, 1] - t[5:39, 3]))
-for a_, b_, nm in ((1, 4, "ldtm"), (4, 2, "max"), (2, 5, "exp"), (5, 6, "sttm"), (6, 3, "arrive")):
-    print(f"phase {nm}: median {np.median(t[5:40, b_] - t[5:40, a_])}")
+t = np.array(buf, dtype=np.int64).reshape(64, 16)
+t0 = t[0, 10]
+names = {10: "tma_k", 11: "tma_v", 8: "mma_qk", 0: "sm_wait", 1: "s_ready", 4: "ld_done", 5: "exp_done",
+         6: "st_done", 3: "p_arr0", 12: "p_arr3", 9: "mma_pv"}
+cols = [10, 11, 8, 0, 1, 4, 5, 6, 3, 12, 9]
+print("block " + " ".join(f"{names[c]:>9s}" for c in cols))
+for j in range(48):
+    print(f"{j:5d} " + " ".join(f"{int(t[j, c] - t0):9d}" for c in cols))
+sl = slice(8, 40)
+med = lambda a, b: float(np.median(t[sl, b] - t[sl, a]))
+print("period (p_arr0 j -> j+1):", float(np.median(np.diff(t[8:41, 3]))))
+print("softmax: wait S", med(0, 1), " ldtm", med(1, 4), " exp", med(4, 5), " sttm", med(5, 6), " arrive", med(6, 3))
+print("S ready after P(j-1) arrival:", float(np.median(t[9:41, 1] - t[8:40, 3])))
+print("PV(j) issue after P(j) arrival:", med(3, 9), "  warp-3 arrival lag:", med(3, 12))
+print("QK(j) issue -> S(j) seen by softmax:", float(np.median(t[sl, 1] - t[sl, 8])))
+print("QK(j+1) issue after PV(j-1) issue:", float(np.median(t[9:41, 8] - t[7:39, 9])))
