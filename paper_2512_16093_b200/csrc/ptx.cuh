@@ -237,6 +237,13 @@ __device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
     asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(D.u) : "l"(A.u), "l"(B.u));
     return D.f;
 }
+// fma.sat has no f32x2 form: two scalar saturating FMAs (clamp to [0, 1])
+__device__ __forceinline__ float2 ffma2_sat(float2 a, float2 b, float2 c) {
+    float2 d;
+    asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(d.x) : "f"(a.x), "f"(b.x), "f"(c.x));
+    asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(d.y) : "f"(a.y), "f"(b.y), "f"(c.y));
+    return d;
+}
 __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
     f2u A{a}, B{b}, D;
     asm("add.rn.f32x2 %0, %1, %2;" : "=l"(D.u) : "l"(A.u), "l"(B.u));

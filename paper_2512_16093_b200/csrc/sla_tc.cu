@@ -111,6 +111,25 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
                        __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
+// 2^y for two exponents entirely on the FMA pipe, from u = sat(y/256 + 125/256)
+// (one saturating FFMA2 computes u from the score, so the clamp of y to
+// [-125, 131] is free): t = M + round(y_c) with y_c = 256u - 125, f = y_c -
+// round(y_c) in [-0.5, 0.5], degree-3 minimax for 2^f (rel err 7.7e-5, far
+// under the bf16 rounding of P), exponent added with one integer op.  y_c >
+// 127 gives inf/NaN, which the caller's row-sum check rejects.
+__device__ __forceinline__ float2 ex2_poly2_sat(float2 u) {
+    const float2 C = make_float2(12582912.0f - 125.0f, 12582912.0f - 125.0f);
+    const float2 S256 = make_float2(256.0f, 256.0f);
+    const float2 t = ptx::ffma2(u, S256, C);                                  // M + round(y_c)
+    const float2 w = ptx::ffma2(t, make_float2(-1.0f, -1.0f), C);            // -round(y_c) - 125 (exact)
+    const float2 f = ptx::ffma2(u, S256, w);                                  // y_c - round(y_c)
+    float2 p = ptx::ffma2(make_float2(0.055088773f, 0.055088773f), f, make_float2(0.24260406f, 0.24260406f));
+    p = ptx::ffma2(p, f, make_float2(0.69327623f, 0.69327623f));
+    p = ptx::ffma2(p, f, make_float2(0.99992895f, 0.99992895f));
+    return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                       __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+
 template <typename T>
 __device__ __forceinline__ void load8(const T *p, float *x) {
     if constexpr (sizeof(T) == 2) {
@@ -337,34 +356,42 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             ptx::tc_fence_after();
             if (threadIdx.x == 0) TB_TRACE(j, 1);
             uint32_t s[4][16];
+            auto load_s = [&]() {
 #pragma unroll
-            for (int q4 = 0; q4 < 4; q4++) ptx::tmem_ld16(tmem + lane_base + sb * BN + q4 * 16, s[q4]);
-            ptx::tmem_wait_ld();
+                for (int q4 = 0; q4 < 4; q4++) ptx::tmem_ld16(tmem + lane_base + sb * BN + q4 * 16, s[q4]);
+                ptx::tmem_wait_ld();
+            };
+            load_s();
             if (threadIdx.x == 0) TB_TRACE(j, 4);
             const bool ragged = S.rag[j] != 0;                        // uniform per CTA
             const int lim = ragged ? last_ext : BN;
-            float xm[64];                   // M + s exactly (|s| < 2^22): monotone in s
-#pragma unroll
-            for (int i = 0; i < 64; i++)
-                xm[i] = __int_as_float((int)s[i >> 4][i & 15] + (TB_SLA_BIAS ? 0 : 0x4B400000));
+            // scores as floats M + s (exact, |s| < 2^22), monotone in s
+            auto xm = [&](int i) {
+                return __int_as_float((int)s[i >> 4][i & 15] + (TB_SLA_BIAS ? 0 : 0x4B400000));
+            };
             float2 psum2[4];
             uint32_t pk[2][16];
+            // P from the registers s[] (consumed as it goes, so the exact path
+            // below reloads S from TMEM instead of keeping 64 values alive)
             auto make_p = [&](auto rg, float off) {
                 constexpr bool RG = decltype(rg)::value;
                 const float2 c12 = make_float2(c1, c1), off2 = make_float2(off, off);
+                const float2 cu = make_float2(c1 * 0.00390625f, c1 * 0.00390625f);
+                const float ou = fmaf(off, 0.00390625f, 0.48828125f);        // off/256 + 125/256
+                const float2 ou2 = make_float2(ou, ou);
 #pragma unroll
                 for (int u = 0; u < 4; u++) psum2[u] = make_float2(0.0f, 0.0f);
 #pragma unroll
                 for (int i = 0; i < 64; i += 2) {
-                    const float2 y = ptx::ffma2(make_float2(xm[i], xm[i + 1]), c12, off2);   // FFMA2
                     // 3 of every 8 pairs (3/8 of the exponentials) on the FMA pipe, the rest on MUFU
                     constexpr int PP = TB_SLA_PP;                   // pair-slot mask {1, 4, 6} of 8
                     float p0, p1;
                     if ((PP >> ((i >> 1) & 7)) & 1) {
-                        const float2 e = ex2_poly2(y);
+                        const float2 e = ex2_poly2_sat(ptx::ffma2_sat(make_float2(xm(i), xm(i + 1)), cu, ou2));
                         p0 = e.x;
                         p1 = e.y;
                     } else {
+                        const float2 y = ptx::ffma2(make_float2(xm(i), xm(i + 1)), c12, off2);   // FFMA2
                         p0 = ex2(y.x);
                         p1 = ex2(y.y);
                     }
@@ -390,6 +417,7 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
                 slow = __any_sync(0xffffffffu, !(psum <= 0x1p60f));
             }
             if (slow) {
+                if (!EXACT) load_s();         // S is intact in TMEM until P is stored
                 // exact row max of the block: logit2 is affine in the exact s32
                 // score with slope c1 (uniform sign per CTA) -> max/min of M + s
                 float sx;
@@ -398,26 +426,26 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
                     float a4[4];
                     if (c1 >= 0.0f) {
 #pragma unroll
-                        for (int u = 0; u < 4; u++) a4[u] = xm[u];
+                        for (int u = 0; u < 4; u++) a4[u] = xm(u);
 #pragma unroll
                         for (int i = 4; i < 64; i += 8)
 #pragma unroll
-                            for (int u = 0; u < 4; u++) a4[u] = fmaxf(a4[u], fmaxf(xm[i + 2 * u], xm[i + 2 * u + 1]));
+                            for (int u = 0; u < 4; u++) a4[u] = fmaxf(a4[u], fmaxf(xm(i + 2 * u), xm(i + 2 * u + 1)));
                         sx = fmaxf(fmaxf(a4[0], a4[1]), fmaxf(a4[2], a4[3]));
                     } else {
 #pragma unroll
-                        for (int u = 0; u < 4; u++) a4[u] = xm[u];
+                        for (int u = 0; u < 4; u++) a4[u] = xm(u);
 #pragma unroll
                         for (int i = 4; i < 64; i += 8)
 #pragma unroll
-                            for (int u = 0; u < 4; u++) a4[u] = fminf(a4[u], fminf(xm[i + 2 * u], xm[i + 2 * u + 1]));
+                            for (int u = 0; u < 4; u++) a4[u] = fminf(a4[u], fminf(xm(i + 2 * u), xm(i + 2 * u + 1)));
                         sx = fminf(fminf(a4[0], a4[1]), fminf(a4[2], a4[3]));
                     }
                 } else {
-                    sx = xm[0];
+                    sx = xm(0);
 #pragma unroll
-                    for (int i = 1; i < 64; i++)      // static indices keep xm[] in registers
-                        if (i < lim) sx = (c1 >= 0.0f) ? fmaxf(sx, xm[i]) : fminf(sx, xm[i]);
+                    for (int i = 1; i < 64; i++)      // static indices keep s[] in registers
+                        if (i < lim) sx = (c1 >= 0.0f) ? fmaxf(sx, xm(i)) : fminf(sx, xm(i));
                 }
                 const float mx = fmaf(sx, c1, c0m);
                 if (threadIdx.x == 0) TB_TRACE(j, 2);
