@@ -279,13 +279,12 @@ def main():
     if world == 1:
         qh, kh, vh = head_major
         _, parts = ops.sla_attention(qh, kh, vh, QB, KVB, RATIO, 1.0, out_dtype=torch.bfloat16, return_parts=True)
-        vt = ops.transpose_v(vh, (-(-L_ // 64)) * 64)
         out = torch.empty((H, L_, D_), dtype=torch.bfloat16, device="cuda")
         a = ops.sla_args(q=ops.ptr(qh), k=ops.ptr(kh), v=ops.ptr(vh), dtype=1, H=H, L=L_, d=D_, q_block=QB,
                          kv_block=KVB, count=parts["count"], scale=1.0 / math.sqrt(D_), linear_mix=1.0, quantized=1,
                          q_codes=ops.ptr(parts["q_codes"]), k_codes=ops.ptr(parts["k_codes"]),
                          q_scales=ops.ptr(parts["q_scales"]), k_scales=ops.ptr(parts["k_scales"]),
-                         k_mean=ops.ptr(parts["k_mean"]), idx=ops.ptr(parts["idx"]), vt=ops.ptr(vt),
+                         k_mean=ops.ptr(parts["k_mean"]), idx=ops.ptr(parts["idx"]), vt=None,
                          l_pad=(-(-L_ // 64)) * 64, num_l=None, den_l=None, lin_ld=0, lin_hs=0,
                          lin_kv=ops.ptr(parts["lin_kv"]), lin_dx=parts["lin_kv"].shape[2],
                          out=ops.ptr(out), out_dtype=1, row_max=None, den=None)

@@ -117,8 +117,9 @@ typedef struct tb_sla_args {
     const float *q_scales, *k_scales;  /* [H,nq], [H,nkv] */
     const float *k_mean;               /* [H,d] */
     const int32_t *idx;                /* [H,nq,count] ascending */
-    const void *vt;                    /* bf16 V^T [H,d,Lpad] (tensor-core path) */
-    int64_t l_pad;                     /* padded token stride of vt */
+    const void *vt;                    /* bf16 copy of V [H,L,d] for the tensor-core path when
+                                          dtype is f32 (ignored for bf16 inputs: v is read directly) */
+    int64_t l_pad;                     /* unused (kept for ABI stability) */
     /* linear branch over the complement (may be NULL -> no linear term) */
     const float *num_l, *den_l;        /* [H,L,d], [H,L] */
     /* packed linear branch: when lin_ld != 0, row r of head h is
@@ -173,6 +174,14 @@ int tb_linear_operands(const void *q, const void *k, const void *v, int dtype, i
  * (attention.py:326-328). */
 int tb_gemm_bf16_batched(const void *A, const void *B, void *C, int64_t H, int64_t M, int64_t N,
                          int64_t K, int64_t lda, int64_t ldb, int64_t ldc, int out_dtype, void *stream);
+
+/* Per-kv-block linear-branch operand (attention.py:320-325) straight from
+ * bf16 k, v [H,L,d] on tcgen05: kv_part [H, nkv, dx, d] bf16 with rows
+ * 0..d-1 = V_b^T phi(K_b), row d = sum_t phi(K_b), rows d+1.. zero (padded
+ * tokens contribute nothing).  d == 128, kv_block == 64, dx*d % 256 == 0.
+ * Replaces linear_attention's per-block einsums (attention.py:322-325). */
+int tb_linear_kv_part(const void *k, const void *v, int64_t H, int64_t L, int64_t d, int64_t kv_block,
+                      int64_t dx, void *kv_part, void *stream);
 
 /* Fast-mode W8A8: identical operands, the two block scales folded into one
  * FMA per element (tolerance-level, not bit-exact); used by the DiT step. */

@@ -33,18 +33,6 @@ struct Smem {
 constexpr size_t SMEM_BYTES = sizeof(Smem) + 1024;
 }  // namespace gbf
 
-// MN-major 128B-swizzled operand: atoms of 64 (MN) x 8 (K) bf16; LBO = byte
-// stride between 64-wide MN atoms, SBO = byte stride between 8-row K groups.
-__device__ __forceinline__ uint64_t sdesc_sw128_mn(uint32_t smem_addr, uint32_t lbo, uint32_t sbo) {
-    uint64_t d = 0;
-    d |= (uint64_t)((smem_addr & 0x3FFFF) >> 4);
-    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
-    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
-    d |= (uint64_t)1 << 46;
-    d |= (uint64_t)2 << 61;
-    return d;
-}
-
 template <bool OUT_F32>
 __global__ void __launch_bounds__(gbf::THREADS, 1) gemm_bf16_kernel(
     const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, void *__restrict__ C,
@@ -101,7 +89,7 @@ __global__ void __launch_bounds__(gbf::THREADS, 1) gemm_bf16_kernel(
                     ptx::mbar_wait_sleep(&S.full[stage], phase);
                     ptx::tc_fence_after();
                     const uint64_t ad = ptx::sdesc_sw128(ptx::smem_u32(S.a[stage]));
-                    const uint64_t bd = sdesc_sw128_mn(ptx::smem_u32(S.b[stage]), BK * 128, 1024);
+                    const uint64_t bd = ptx::sdesc_sw128_mn(ptx::smem_u32(S.b[stage]), BK * 128, 1024);
 #pragma unroll
                     for (int k = 0; k < BK / 16; k++)   // K=16: A +32 B in the row, B +16 rows (2048 B)
                         ptx::mma_f16(tmem + buf * BN, ad + 2 * k, bd + 128 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);

@@ -81,6 +81,13 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, i
         " [%0], [%1, {%2, %3, %4}], [%5];"
         :: "r"(smem_u32(dst)), "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar)) : "memory");
 }
+// shared -> global tensor store (bulk-group completion)
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap *map, const void *src, int32_t x, int32_t y) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
+                 :: "l"(map), "r"(x), "r"(y), "r"(smem_u32(src)) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
     asm volatile("prefetch.tensormap [%0];" :: "l"(map) : "memory");
 }
@@ -260,6 +267,18 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t smem_addr) {
     d |= (uint64_t)(1024 >> 4) << 32;                   // SBO
     d |= (uint64_t)1 << 46;                             // descriptor version (sm_100)
     d |= (uint64_t)2 << 61;                             // SWIZZLE_128B
+    return d;
+}
+
+// MN-major 128B-swizzled operand: atoms of 64 (MN) x 8 (K) bf16; LBO = byte
+// stride between 64-wide MN atoms, SBO = byte stride between 8-row K groups.
+__device__ __forceinline__ uint64_t sdesc_sw128_mn(uint32_t smem_addr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((smem_addr & 0x3FFFF) >> 4);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)2 << 61;
     return d;
 }
 

@@ -47,7 +47,7 @@ constexpr int BM = 128, BN = 64, D = 128, KSTAGES = 3, VSTAGES = 3;
 constexpr int THREADS = 192;
 constexpr uint32_t Q_BYTES = BM * D;          // int8
 constexpr uint32_t K_BYTES = BN * D;          // int8
-constexpr uint32_t V_BYTES = D * BN * 2;      // bf16 V^T tile
+constexpr uint32_t V_BYTES = D * BN * 2;      // bf16 V tile: two 64-channel x 64-token SW128 boxes
 struct Smem {
     uint8_t q[Q_BYTES];
     uint8_t v[VSTAGES][V_BYTES];
@@ -217,7 +217,8 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             if (lane == 0) TB_TRACE(j, 11);
             if (ptx::elect_one()) {
                 ptx::mbar_arrive_expect_tx(&S.v_full[vs], V_BYTES);
-                ptx::tma_load_3d(S.v[vs], &tm_v, b * BN, 0, h, &S.v_full[vs]);
+                ptx::tma_load_3d(S.v[vs], &tm_v, 0, b * BN, h, &S.v_full[vs]);
+                ptx::tma_load_3d(S.v[vs] + V_BYTES / 2, &tm_v, 64, b * BN, h, &S.v_full[vs]);
             }
             __syncwarp();
         }
@@ -236,6 +237,7 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
         // whole warp in the loop, one elected lane issues each MMA group
         constexpr uint32_t ID_QK = ptx::idesc_i8(BM, BN);
         constexpr uint32_t ID_PV = ptx::idesc_bf16(BM, D);
+        constexpr uint32_t ID_PV_MN = ptx::idesc_bf16(BM, D) | (1u << 16);   // B = V tile, MN-major
         constexpr uint32_t ID_BIAS = ptx::idesc_bf16(BM, BN);
         const uint64_t qd = ptx::sdesc_sw128(ptx::smem_u32(S.q));
         // no-swizzle K-major 8x16 bf16 tiles; SBO = 0 makes every 8-row group alias the same rows
@@ -248,11 +250,12 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             ptx::mbar_wait_sleep(&S.p_full[pb], (uint32_t)((i >> 1) & 1));
             ptx::tc_fence_after();
             if (lane == 0) TB_TRACE(i, 9);
-            const uint64_t vd = ptx::sdesc_sw128(ptx::smem_u32(S.v[vs]));
+            // V [tokens][channels]: channel-contiguous = MN-major B; atoms 64 ch x 8 tokens
+            const uint64_t vd = ptx::sdesc_sw128_mn(ptx::smem_u32(S.v[vs]), V_BYTES / 2, 1024);
             if (ptx::elect_one()) {
 #pragma unroll
-                for (int k = 0; k < BN / 16; k++)   // K=16 bf16 per MMA: 8 TMEM cols of P, 32 B of V^T
-                    ptx::mma_f16_ts(TM_O, tmem + pb * BN + 8 * k, vd + 2 * k, ID_PV, (i > 0 || k > 0) ? 1u : 0u);
+                for (int k = 0; k < BN / 16; k++)   // K=16 bf16 per MMA: 8 TMEM cols of P, 16 token rows of V
+                    ptx::mma_f16_ts(TM_O, tmem + pb * BN + 8 * k, vd + 128 * k, ID_PV_MN, (i > 0 || k > 0) ? 1u : 0u);
                 ptx::mma_commit(&S.pv_done[pb]);
                 ptx::mma_commit(&S.v_empty[vs]);
             }
@@ -597,8 +600,8 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
 int sla_simt(const tb_sla_args *a, cudaStream_t st);
 
 bool sla_tc_supported(const tb_sla_args *a) {
-    return a->quantized && a->d == 128 && a->q_block == 128 && a->kv_block == 64 && a->vt != nullptr &&
-           a->L >= 128 && a->l_pad % 64 == 0 && a->l_pad >= cdiv(a->L, 64) * 64 &&
+    return a->quantized && a->d == 128 && a->q_block == 128 && a->kv_block == 64 &&
+           (a->dtype == TB_BF16 || a->vt != nullptr) && a->L >= 128 &&
            (a->dtype == TB_BF16 || a->dtype == TB_F32) && a->count >= 1 && a->count <= sla::MAX_SEL &&
            (a->lin_kv == nullptr || a->lin_dx >= a->d + 1);
 }
@@ -609,8 +612,8 @@ int sla_tc(const tb_sla_args *a, cudaStream_t st) {
     CUtensorMap tq, tk, tv;
     bool ok = make_tmap_3d(&tq, a->q_codes, CU_TENSOR_MAP_DATA_TYPE_UINT8, D, a->L, a->H, D, a->L * D, D, BM, 1) &&
               make_tmap_3d(&tk, a->k_codes, CU_TENSOR_MAP_DATA_TYPE_UINT8, D, a->L, a->H, D, a->L * D, D, BN, 1) &&
-              make_tmap_3d(&tv, a->vt, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, a->l_pad, D, a->H, a->l_pad * 2,
-                           a->l_pad * 2 * D, BN, D, 1);
+              make_tmap_3d(&tv, a->dtype == TB_BF16 ? a->v : a->vt, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, D, a->L, a->H,
+                           D * 2, a->L * D * 2, 64, BN, 1);
     CUtensorMap tkv = tq;
     if (a->lin_kv)
         ok = ok && make_tmap_2d(&tkv, a->lin_kv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, D, a->H * nq * a->lin_dx, D * 2,

@@ -168,28 +168,37 @@ def linear_operands(q, k, v, lq: int, lk: int, dx: int, dtype=torch.bfloat16, lv
     return phiq, phik, vext, vt
 
 
-def linear_kv_sel(k, v, comp: torch.Tensor, kv_block: int, lvt: int = 0, q=None):
+def linear_kv_dx(d: int) -> int:
+    """Rows of a kv_part block: d numerator rows, the denominator row, and
+    zero padding up to the smallest dx with dx*d a multiple of 256 (the
+    coverage GEMM's N tile)."""
+    dx = d + 1
+    while (dx * d) % 256:
+        dx += 1
+    return dx
+
+
+def linear_kv_sel(k, v, comp: torch.Tensor, kv_block: int):
     """Fused-epilogue form of the linear branch (attention.py:320-328).
 
-    Returns (kvsel [H, nq, dx, d] bf16, vt): per q block n, rows 0..d-1 hold
-    KV_sel[n]^T = sum over complement blocks b of V_b^T phi(K_b) and row d
-    holds sum phi(K_b); the attention kernel finishes the branch with one
-    tcgen05 MMA phi(Q_n) . KV_sel[n] in its epilogue (attention.py:329-334).
-    The two batched GEMMs (per-block V_b^T phi(K_b), then cov . kv_part) run
-    on cuBLAS with bf16 operands and f32 accumulation.
+    k, v: bf16 [H, L, d].  Returns kvsel [H, nq, dx, d] bf16: per q block n,
+    rows 0..d-1 hold KV_sel[n]^T = sum over complement blocks b of
+    V_b^T phi(K_b), row d holds sum phi(K_b); the attention kernel finishes
+    the branch with one tcgen05 MMA phi(Q_n) . KV_sel[n] in its epilogue
+    (attention.py:329-334).  kv_part (one tcgen05 kernel straight from k and
+    v) and the coverage GEMM cov . kv_part are both ours (tb_linear_kv_part,
+    tb_gemm_bf16_batched), bf16 operands with f32 accumulation.
     """
     H, L, d = k.shape
     nq, nkv = comp.shape[1], comp.shape[2]
-    dx = -(-(d + 1) // 16) * 16
-    lk = nkv * kv_block
-    _, phik, vext, vt = linear_operands(q if q is not None else k, k, v, 0, lk, dx, torch.bfloat16, lvt=lvt,
-                                        want_phiq=False)
-    kv_part = torch.bmm(vext.view(H * nkv, kv_block, dx).transpose(1, 2), phik.view(H * nkv, kv_block, d))
+    dx = linear_kv_dx(d)
+    kv_part = torch.empty((H, nkv, dx, d), dtype=torch.bfloat16, device=k.device)
+    call("tb_linear_kv_part", ptr(k), ptr(v), H, L, d, kv_block, dx, ptr(kv_part), stream_ptr())
     nkv_pad = -(-nkv // 8) * 8                       # TMA row pitch must be a multiple of 16 B
     cov = torch.zeros((H, nq, nkv_pad), dtype=torch.bfloat16, device=k.device)
     cov[:, :, :nkv] = comp
     kvsel = gemm_bf16_batched(cov, kv_part.view(H, nkv, dx * d), K=nkv)         # [H, nq, dx*d]
-    return kvsel.view(H, nq, dx, d), vt
+    return kvsel.view(H, nq, dx, d)
 
 
 def gemm_bf16_batched(a: torch.Tensor, b: torch.Tensor, K: int | None = None, out_dtype=torch.bfloat16):
@@ -306,9 +315,9 @@ def sla_attention(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: fl
     else:
         qc = qs = kc = ks = km = None
         qp, kp = pool_block_means(q, q_block), pool_block_means(k, kv_block)
-    vt = None
-    if tc and not lin:
-        _, _, _, vt = linear_operands(q, k, v, 0, 0, 0, lvt=l_pad, linear=False)
+    # the tensor-core path reads V (and the linear-branch kernel K and V) as bf16
+    kb, vb = (k, v) if q.dtype == torch.bfloat16 else (k.to(torch.bfloat16), v.to(torch.bfloat16))
+    vt = None if q.dtype == torch.bfloat16 else vb
     if quantized:
         main.wait_stream(side)
         km.record_stream(main)
@@ -316,7 +325,7 @@ def sla_attention(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: fl
     idx, comp, _ = topk_blocks(qp, kp, count, want_comp=lin or return_parts)
     lin_pack = lin_kv = None
     if lin and tc:
-        lin_kv, vt = linear_kv_sel(k, v, comp, kv_block, lvt=l_pad, q=q)
+        lin_kv = linear_kv_sel(kb, vb, comp, kv_block)
     elif lin:
         fast = (H * L * d >= (1 << 22)) if linear_fast is None else linear_fast
         lin_pack = linear_branch(q, k, v, comp, q_block, kv_block, fast=fast)

@@ -249,3 +249,27 @@ def test_gemm_bf16_batched_mn_major(tb):
         got16 = tb.gemm_bf16_batched(a, b, K=K)
         cos, _, rel1 = metrics(got16.float().cpu().numpy(), want.cpu().numpy())
         assert cos > 0.99999 and rel1 < 5e-3
+
+
+def test_linear_kv_part_blocks(tb):
+    """tb_linear_kv_part vs the per-block einsums of linear_attention
+    (attention.py:320-325): V_b^T phi(K_b) and sum phi(K_b), padded tokens
+    contributing nothing (ragged last block: L = 15*64 + 40)."""
+    H, L, d = 2, 1000, 128
+    _, k, v = gen.gaussian_qkv(31, H, L, d, bf16=True)
+    nkv = -(-L // 64)
+    dx = tb.linear_kv_dx(d)
+    kv_part = torch.empty((H, nkv, dx, d), dtype=torch.bfloat16, device="cuda")
+    kd, vd = dev(k, True), dev(v, True)              # keep the inputs alive across the async launch
+    tb.call("tb_linear_kv_part", tb.ptr(kd), tb.ptr(vd), H, L, d, 64, dx, tb.ptr(kv_part), tb.stream_ptr())
+    got = kv_part.float().cpu().numpy()
+    pk = np.where(k >= 0, k + 1.0, np.exp(np.minimum(k, 0.0))).astype(np.float32)
+    for h in range(H):
+        for b in range(nkv):
+            lo, hi = b * 64, min(L, b * 64 + 64)
+            num = v[h, lo:hi].T.astype(np.float64) @ pk[h, lo:hi].astype(np.float64)
+            den = pk[h, lo:hi].sum(axis=0)
+            cos, _, rel1 = metrics(got[h, b, :d], num)
+            assert cos >= 0.9999 and rel1 <= 1e-2, (h, b, cos, rel1)
+            assert np.allclose(got[h, b, d], den, rtol=1e-2, atol=1e-2), (h, b)
+            assert not got[h, b, d + 1:].any()

@@ -15,13 +15,12 @@ g = torch.Generator(device="cuda").manual_seed(0)
 q, k, v = (torch.randn((H, L, D), generator=g, device="cuda").to(torch.bfloat16) for _ in range(3))
 _, parts = ops.sla_attention(q, k, v, 128, 64, 0.1, 1.0, out_dtype=torch.bfloat16, return_parts=True)
 l_pad = -(-L // 64) * 64
-vt = ops.transpose_v(v, l_pad)
 out = torch.empty((H, L, D), dtype=torch.bfloat16, device="cuda")
 a = ops.sla_args(q=ops.ptr(q), k=ops.ptr(k), v=ops.ptr(v), dtype=1, H=H, L=L, d=D, q_block=128, kv_block=64,
                  count=parts["count"], scale=1.0 / math.sqrt(D), linear_mix=1.0, quantized=1,
                  q_codes=ops.ptr(parts["q_codes"]), k_codes=ops.ptr(parts["k_codes"]),
                  q_scales=ops.ptr(parts["q_scales"]), k_scales=ops.ptr(parts["k_scales"]),
-                 k_mean=ops.ptr(parts["k_mean"]), idx=ops.ptr(parts["idx"]), vt=ops.ptr(vt), l_pad=l_pad,
+                 k_mean=ops.ptr(parts["k_mean"]), idx=ops.ptr(parts["idx"]), vt=None, l_pad=l_pad,
                  num_l=None, den_l=None, lin_ld=0, lin_hs=0, lin_kv=ops.ptr(parts["lin_kv"]),
                  lin_dx=parts["lin_kv"].shape[2], out=ops.ptr(out), out_dtype=1, row_max=None, den=None)
 lib = _lib.load()
