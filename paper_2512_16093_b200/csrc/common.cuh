@@ -36,6 +36,20 @@ __device__ __forceinline__ int8_t quant_code(float x, float safe) {
     return (int8_t)(int)r;
 }
 
+// Same code as quant_code for |x| <= 127 * safe, from one FMA against inv =
+// __frcp_rn(safe): u = M + rint(x * inv) (M = 1.5*2^23); x * inv is within
+// 1.2e-5 of the IEEE quotient fl(x / safe), so unless x * inv lands within
+// 2^-15 of a rounding boundary (probability ~6e-5) both round to the same
+// integer; near a boundary the exact division decides.  Returns the int8
+// code in the low byte.
+__device__ __forceinline__ uint32_t quant_code_fast(float x, float safe, float inv) {
+    const float u = __fmaf_rn(x, inv, 12582912.0f);
+    const float w = __fsub_rn(u, 12582912.0f);
+    const float dlt = __fmaf_rn(x, inv, -w);
+    if (fabsf(dlt) > 0.5f - 0x1p-15f) return (uint32_t)(uint8_t)quant_code(x, safe);
+    return (uint32_t)__float_as_int(u) & 0xFFu;
+}
+
 template <int N>
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll

@@ -8,6 +8,7 @@
 //   attention._quantize_token_blocks   attention.py:201-220
 #include "common.cuh"
 #include "ptx.cuh"
+#include "tmap.cuh"
 
 namespace tb {
 
@@ -255,6 +256,125 @@ __global__ void __launch_bounds__(128) pool_quant_tokens_d128_kernel(
     for (int i = threadIdx.x; i < e * 8; i += 128) reinterpret_cast<uint4 *>(cb)[i] = st[i];
 }
 
+// Tile kernel for bf16 inputs, d == 128, block 64 or 128 (the hot path):
+// one CTA per 128-token tile of one head (one Q block of 128 or two K blocks
+// of 64), 256 threads.  The 32 KB tile arrives in shared memory with one bulk
+// copy and is read twice from there:
+//   pass 1 (64 threads per block, one channel pair each): numpy's reduceat
+//          order for the pooled sum (seed + 8-accumulator pairwise body +
+//          sequential tail, both channels in f32x2 lanes) and the absmax of
+//          the (centered) values
+//   pass 2 (all threads, 16 channels x one token each): codes via
+//          quant_code_fast (bit-exact with the IEEE division), 16-B stores.
+template <int BLOCK>
+__global__ void __launch_bounds__(256) pool_quant_tile_kernel(
+    const __nv_bfloat16 *__restrict__ x, const float *__restrict__ center, int64_t L, int64_t nb,
+    int8_t *__restrict__ codes, float *__restrict__ scales, float *__restrict__ pooled) {
+    constexpr int TT = 128, NBLK = TT / BLOCK;
+    __shared__ __align__(128) __nv_bfloat16 tile[TT * 128];
+    __shared__ __align__(8) uint64_t full;
+    __shared__ float red[NBLK][4];
+    __shared__ float bsafe[NBLK], binv[NBLK];
+    __shared__ int bexact[NBLK];
+    const int64_t h = blockIdx.y;
+    const int64_t lo = (int64_t)blockIdx.x * TT;
+    const int et = (int)imin64(TT, L - lo);                    // tokens in this tile
+    if (threadIdx.x == 0) {
+        ptx::mbar_init(&full, 1);
+        ptx::fence_barrier_init();
+        ptx::mbar_arrive_expect_tx(&full, (uint32_t)et * 256u);
+        ptx::bulk_g2s(tile, x + (h * L + lo) * 128, (uint32_t)et * 256u, &full);
+    }
+    __syncthreads();
+    ptx::mbar_wait(&full, 0);
+    const int tid = threadIdx.x;
+    // ---- pass 1: pooled sums (raw x) + absmax (centered), one channel pair per thread
+    if (tid < 64 * NBLK) {
+        const int blk = tid >> 6, cp = tid & 63;
+        const int t0 = blk * BLOCK;
+        const int e = min(BLOCK, et - t0);
+        if (e > 0) {
+            const float2 ctr = center ? *reinterpret_cast<const float2 *>(center + h * 128 + 2 * cp)
+                                      : make_float2(0.0f, 0.0f);
+            const uint32_t *col = reinterpret_cast<const uint32_t *>(tile) + cp;   // row stride 64 words
+            auto ld = [&](int t) {
+                const uint32_t w = col[(t0 + t) * 64];
+                return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+            };
+            float am0 = 0.0f, am1 = 0.0f;
+            auto amax = [&](float2 v) {
+                am0 = fmaxf(am0, fabsf(__fsub_rn(v.x, ctr.x)));
+                am1 = fmaxf(am1, fabsf(__fsub_rn(v.y, ctr.y)));
+            };
+            const float2 seed = ld(0);
+            amax(seed);
+            const int n = e - 1;
+            float2 res = make_float2(-0.0f, -0.0f);
+            if (n >= 8) {
+                float2 r[8];
+#pragma unroll
+                for (int j = 0; j < 8; j++) { r[j] = ld(1 + j); amax(r[j]); }
+                const int full8 = n - (n % 8);
+                for (int i = 8; i < full8; i += 8) {
+#pragma unroll
+                    for (int j = 0; j < 8; j++) { const float2 w = ld(1 + i + j); r[j] = ptx::fadd2(r[j], w); amax(w); }
+                }
+                res = ptx::fadd2(ptx::fadd2(ptx::fadd2(r[0], r[1]), ptx::fadd2(r[2], r[3])),
+                                 ptx::fadd2(ptx::fadd2(r[4], r[5]), ptx::fadd2(r[6], r[7])));
+                for (int i = full8; i < n; i++) { const float2 w = ld(1 + i); res = ptx::fadd2(res, w); amax(w); }
+            } else {
+                for (int i = 0; i < n; i++) { const float2 w = ld(1 + i); res = ptx::fadd2(res, w); amax(w); }
+            }
+            if (pooled) {
+                const float2 acc = (n > 0) ? ptx::fadd2(seed, res) : seed;
+                const int64_t b = lo / BLOCK + blk;
+                *reinterpret_cast<float2 *>(pooled + (h * nb + b) * 128 + 2 * cp) =
+                    make_float2(__fdiv_rn(acc.x, (float)e), __fdiv_rn(acc.y, (float)e));
+            }
+            float am = fmaxf(am0, am1);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
+            if ((tid & 31) == 0) red[blk][(tid >> 5) & 1] = am;
+        }
+    }
+    __syncthreads();
+    if (tid < NBLK && tid * BLOCK < et) {
+        const float am = fmaxf(red[tid][0], red[tid][1]);
+        const float s = quant_scale(am);
+        scales[h * nb + lo / BLOCK + tid] = s;
+        const float safe = (s == 0.0f) ? 1.0f : s;
+        const float inv = __frcp_rn(safe);
+        bsafe[tid] = safe;
+        binv[tid] = inv;
+        bexact[tid] = !(safe >= 1.17549435e-38f && inv <= 3.0e38f);   // subnormal scale: exact division
+    }
+    __syncthreads();
+    // ---- pass 2: codes, 16 channels of one token per work item
+    const int g = tid & 7;                                   // 16-channel group
+    float cg[16];
+#pragma unroll
+    for (int i = 0; i < 16; i++) cg[i] = center ? __ldg(center + h * 128 + 16 * g + i) : 0.0f;
+    for (int t = tid >> 3; t < et; t += 32) {
+        const int blk = t / BLOCK;
+        const float safe = bsafe[blk], inv = binv[blk];
+        const bool exact = bexact[blk] != 0;
+        const uint4 *src = reinterpret_cast<const uint4 *>(tile + t * 128 + 16 * g);
+        uint32_t wv[8];
+        *reinterpret_cast<uint4 *>(&wv[0]) = src[0];
+        *reinterpret_cast<uint4 *>(&wv[4]) = src[1];
+        uint32_t out[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+        for (int i = 0; i < 16; i++) {
+            const uint32_t w = wv[i >> 1];
+            float v = __uint_as_float((i & 1) ? (w & 0xFFFF0000u) : (w << 16));
+            if (center) v = __fsub_rn(v, cg[i]);
+            const uint32_t c8 = exact ? (uint32_t)(uint8_t)quant_code(v, safe) : quant_code_fast(v, safe, inv);
+            out[i >> 2] |= c8 << ((i & 3) * 8);
+        }
+        *reinterpret_cast<uint4 *>(codes + (h * L + lo + t) * 128 + 16 * g) = make_uint4(out[0], out[1], out[2], out[3]);
+    }
+}
+
 // ------------------------------------------------------------------ k_mean
 // Sequential f32 chain over all L tokens per (head, channel) -- the numpy
 // strided-reduce order.  The chain is latency-bound
@@ -315,6 +435,52 @@ __global__ void __launch_bounds__(128) kmean_bulk_kernel(const T *__restrict__ k
         }
     }
     if (c < d) kmean[h * d + c] = __fdiv_rn(acc, (float)L);
+}
+
+// bf16, d == 128: one warp per (head, 32-channel quarter) so 4*H CTAs stream
+// the heads in parallel; a 2-D TMA ring of [256 tokens x 32 channels] tiles
+// (16 KB) feeds the chains, each lane one channel, summing in token order.
+constexpr int KM_CH = 256, KM_STAGES = 6;
+__global__ void __launch_bounds__(32) kmean_split_kernel(const __grid_constant__ CUtensorMap tm, int64_t L,
+                                                         float *__restrict__ kmean) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ __align__(8) uint64_t full[KM_STAGES];
+    const int qc = blockIdx.x, h = blockIdx.y, lane = threadIdx.x;
+    const __nv_bfloat16 *ring = reinterpret_cast<const __nv_bfloat16 *>(smem);
+    const int64_t nch = cdiv(L, KM_CH);
+    const int64_t row0 = (int64_t)h * L;
+    if (lane == 0) {
+        for (int s = 0; s < KM_STAGES; s++) ptx::mbar_init(&full[s], 1);
+        ptx::fence_barrier_init();
+        for (int64_t i = 0; i < imin64(KM_STAGES, nch); i++) {
+            ptx::mbar_arrive_expect_tx(&full[i], KM_CH * 64);
+            ptx::tma_load_2d(smem + i * KM_CH * 64, &tm, qc * 32, (int)(row0 + i * KM_CH), &full[i]);
+        }
+    }
+    __syncwarp();
+    float acc = 0.0f;
+    for (int64_t i = 0; i < nch; i++) {
+        const int s = (int)(i % KM_STAGES);
+        ptx::mbar_wait(&full[s], (uint32_t)((i / KM_STAGES) & 1));
+        const int toks = (int)imin64(KM_CH, L - i * KM_CH);
+        const __nv_bfloat16 *buf = ring + (size_t)s * KM_CH * 32 + lane;
+        int t = 0;
+        for (; t + 16 <= toks; t += 16) {
+            float w[16];
+#pragma unroll
+            for (int j = 0; j < 16; j++) w[j] = __bfloat162float(buf[(t + j) * 32]);
+#pragma unroll
+            for (int j = 0; j < 16; j++) acc = __fadd_rn(acc, w[j]);
+        }
+        for (; t < toks; t++) acc = __fadd_rn(acc, __bfloat162float(buf[t * 32]));
+        __syncwarp();
+        if (lane == 0 && i + KM_STAGES < nch) {
+            ptx::fence_async_smem();          // the warp's reads of stage s before the TMA overwrite
+            ptx::mbar_arrive_expect_tx(&full[s], KM_CH * 64);
+            ptx::tma_load_2d(smem + s * KM_CH * 64, &tm, qc * 32, (int)(row0 + (i + KM_STAGES) * KM_CH), &full[s]);
+        }
+    }
+    kmean[h * 128 + qc * 32 + lane] = __fdiv_rn(acc, (float)L);
 }
 
 // Generic fallback (unaligned rows / large d): same order, direct loads.
@@ -417,6 +583,15 @@ extern "C" int tb_pool_quant_tokens(const void *x, int dtype, const float *cente
     dim3 grid((unsigned)nb, (unsigned)H);
     cudaStream_t st = as_stream(stream);
     const bool fast = d == 128 && codes != nullptr && (block == 64 || block == 128);
+    if (fast && dtype == TB_BF16 && ((uintptr_t)x % 16) == 0 && ((uintptr_t)codes % 16) == 0 &&
+        (pooled == nullptr || ((uintptr_t)pooled % 8) == 0) && (center == nullptr || ((uintptr_t)center % 8) == 0)) {
+        dim3 tgrid((unsigned)cdiv(L, 128), (unsigned)H);
+        if (block == 64)
+            pool_quant_tile_kernel<64><<<tgrid, 256, 0, st>>>((const __nv_bfloat16 *)x, center, L, nb, codes, scales, pooled);
+        else
+            pool_quant_tile_kernel<128><<<tgrid, 256, 0, st>>>((const __nv_bfloat16 *)x, center, L, nb, codes, scales, pooled);
+        return check_launch("pool_quant_tile");
+    }
 #define TB_POOLQ(T)                                                                                      \
     if (fast && block == 64)                                                                             \
         pool_quant_tokens_d128_kernel<T, 64><<<grid, 128, 0, st>>>((const T *)x, center, L, nb, codes, scales, pooled); \
@@ -436,7 +611,15 @@ extern "C" int tb_kmean(const void *k, int dtype, int64_t H, int64_t L, int64_t 
     cudaStream_t st = as_stream(stream);
     const size_t es = dtype == TB_F32 ? 4 : 2;
     const bool aligned = ((uintptr_t)k % 16 == 0) && ((L * d * es) % 16 == 0) && ((d * es) % 16 == 0);
-    if (aligned && d <= 128) {
+    if (aligned && d == 128 && dtype == TB_BF16 && H * L < (1ll << 31)) {
+        CUtensorMap tm;
+        if (!make_tmap_2d(&tm, k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 128, H * L, 256, 32, KM_CH,
+                          CU_TENSOR_MAP_SWIZZLE_NONE))
+            return fail(TB_ECUDA, "cuTensorMapEncodeTiled failed (kmean)");
+        const int smem = KM_STAGES * KM_CH * 64;
+        cudaFuncSetAttribute(kmean_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        kmean_split_kernel<<<dim3(4, (unsigned)H), 32, smem, st>>>(tm, L, kmean);
+    } else if (aligned && d <= 128) {
         constexpr int STAGES = 6;
         int chunk = (int)(16384 / (d * es));          // 16 KiB per stage
         if (chunk < 8) chunk = 8;
