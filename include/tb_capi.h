@@ -102,6 +102,22 @@ int tb_topk_blocks(const float *qp, const float *kp, int64_t H, int64_t nq, int6
                    int64_t d, int64_t count, int32_t *idx, uint8_t *comp, float *scores_out,
                    void *stream);
 
+/* tb_pool_quant_tokens plus a transposed copy of the pooled means,
+ * pooled_t [H, d, ldt] (ldt >= blocks): the coalesced kp operand of
+ * tb_topk_blocks_cov. */
+int tb_pool_quant_tokens_t(const void *x, int dtype, const float *center, int64_t H, int64_t L, int64_t d,
+                           int64_t block, int8_t *codes, float *scales, float *pooled, float *pooled_t,
+                           int64_t ldt, void *stream);
+
+/* tb_topk_blocks plus the complement written as the bf16 coverage matrix
+ * cov [H, nq, cov_ld] (1.0 = kv block in the complement, padding columns
+ * 0) -- the A operand of the linear branch's GEMM (attention.py:326-328).
+ * kpt (optional, from tb_pool_quant_tokens_t, row pitch ldk) enables the
+ * coalesced fast path.  comp may be NULL. */
+int tb_topk_blocks_cov(const float *qp, const float *kp, const float *kpt, int64_t ldk, int64_t H, int64_t nq,
+                       int64_t nkv, int64_t d, int64_t count, int32_t *idx, uint8_t *comp, void *cov,
+                       int64_t cov_ld, void *stream);
+
 /* ------------------------------------------------------- SLA attention */
 
 typedef struct tb_sla_args {

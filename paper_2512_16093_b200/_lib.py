@@ -38,6 +38,8 @@ SIGNATURES = {
     "tb_kmean": [_P, _i, _I, _I, _I, _P, _P],
     "tb_pool_quant_tokens": [_P, _i, _P, _I, _I, _I, _I, _P, _P, _P, _P],
     "tb_topk_blocks": [_P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P],
+    "tb_topk_blocks_cov": [_P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _I, _P],
+    "tb_pool_quant_tokens_t": [_P, _i, _P, _I, _I, _I, _I, _P, _P, _P, _P, _I, _P],
     "tb_sla_attention": [_P, _P],
     "tb_transpose_v": [_P, _i, _I, _I, _I, _I, _P, _P],
     "tb_feature_map": [_P, _i, _I, _I, _I, _I, _P, _i, _P],

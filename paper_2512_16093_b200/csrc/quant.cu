@@ -269,7 +269,8 @@ __global__ void __launch_bounds__(128) pool_quant_tokens_d128_kernel(
 template <int BLOCK>
 __global__ void __launch_bounds__(256) pool_quant_tile_kernel(
     const __nv_bfloat16 *__restrict__ x, const float *__restrict__ center, int64_t L, int64_t nb,
-    int8_t *__restrict__ codes, float *__restrict__ scales, float *__restrict__ pooled) {
+    int8_t *__restrict__ codes, float *__restrict__ scales, float *__restrict__ pooled,
+    float *__restrict__ pooled_t, int64_t ldt) {
     constexpr int TT = 128, NBLK = TT / BLOCK;
     __shared__ __align__(128) __nv_bfloat16 tile[TT * 128];
     __shared__ __align__(8) uint64_t full;
@@ -328,8 +329,12 @@ __global__ void __launch_bounds__(256) pool_quant_tile_kernel(
             if (pooled) {
                 const float2 acc = (n > 0) ? ptx::fadd2(seed, res) : seed;
                 const int64_t b = lo / BLOCK + blk;
-                *reinterpret_cast<float2 *>(pooled + (h * nb + b) * 128 + 2 * cp) =
-                    make_float2(__fdiv_rn(acc.x, (float)e), __fdiv_rn(acc.y, (float)e));
+                const float2 pm = make_float2(__fdiv_rn(acc.x, (float)e), __fdiv_rn(acc.y, (float)e));
+                *reinterpret_cast<float2 *>(pooled + (h * nb + b) * 128 + 2 * cp) = pm;
+                if (pooled_t) {                 // [H][d][ldt] copy: the top-k kernel's coalesced operand
+                    pooled_t[(h * 128 + 2 * cp) * ldt + b] = pm.x;
+                    pooled_t[(h * 128 + 2 * cp + 1) * ldt + b] = pm.y;
+                }
             }
             float am = fmaxf(am0, am1);
 #pragma unroll
@@ -571,9 +576,9 @@ extern "C" int tb_pool_block_means(const void *x, int dtype, int64_t H, int64_t 
     return tb_pool_quant_tokens(x, dtype, nullptr, H, L, d, block, nullptr, nullptr, out, stream);
 }
 
-extern "C" int tb_pool_quant_tokens(const void *x, int dtype, const float *center, int64_t H, int64_t L,
-                                    int64_t d, int64_t block, int8_t *codes, float *scales, float *pooled,
-                                    void *stream) {
+static int pool_quant_launch(const void *x, int dtype, const float *center, int64_t H, int64_t L, int64_t d,
+                             int64_t block, int8_t *codes, float *scales, float *pooled, float *pooled_t,
+                             int64_t ldt, void *stream) {
     TB_REQUIRE(block >= 1, "block must be >= 1");
     TB_REQUIRE(dtype == TB_F32 || dtype == TB_BF16, "dtype must be f32 or bf16");
     TB_REQUIRE((codes == nullptr) == (scales == nullptr), "codes and scales go together");
@@ -587,9 +592,11 @@ extern "C" int tb_pool_quant_tokens(const void *x, int dtype, const float *cente
         (pooled == nullptr || ((uintptr_t)pooled % 8) == 0) && (center == nullptr || ((uintptr_t)center % 8) == 0)) {
         dim3 tgrid((unsigned)cdiv(L, 128), (unsigned)H);
         if (block == 64)
-            pool_quant_tile_kernel<64><<<tgrid, 256, 0, st>>>((const __nv_bfloat16 *)x, center, L, nb, codes, scales, pooled);
+            pool_quant_tile_kernel<64><<<tgrid, 256, 0, st>>>((const __nv_bfloat16 *)x, center, L, nb, codes, scales, pooled,
+                                                              pooled_t, ldt);
         else
-            pool_quant_tile_kernel<128><<<tgrid, 256, 0, st>>>((const __nv_bfloat16 *)x, center, L, nb, codes, scales, pooled);
+            pool_quant_tile_kernel<128><<<tgrid, 256, 0, st>>>((const __nv_bfloat16 *)x, center, L, nb, codes, scales, pooled,
+                                                               pooled_t, ldt);
         return check_launch("pool_quant_tile");
     }
 #define TB_POOLQ(T)                                                                                      \
@@ -599,9 +606,23 @@ extern "C" int tb_pool_quant_tokens(const void *x, int dtype, const float *cente
         pool_quant_tokens_d128_kernel<T, 128><<<grid, 128, 0, st>>>((const T *)x, center, L, nb, codes, scales, pooled); \
     else                                                                                                 \
         pool_quant_tokens_kernel<T><<<grid, 128, 0, st>>>((const T *)x, center, L, d, block, nb, codes, scales, pooled);
+    TB_REQUIRE(pooled_t == nullptr, "the transposed pooled copy needs the bf16 tile path");
     if (dtype == TB_F32) { TB_POOLQ(float) } else { TB_POOLQ(__nv_bfloat16) }
 #undef TB_POOLQ
     return check_launch("pool_quant_tokens");
+}
+
+extern "C" int tb_pool_quant_tokens(const void *x, int dtype, const float *center, int64_t H, int64_t L,
+                                    int64_t d, int64_t block, int8_t *codes, float *scales, float *pooled,
+                                    void *stream) {
+    return pool_quant_launch(x, dtype, center, H, L, d, block, codes, scales, pooled, nullptr, 0, stream);
+}
+
+extern "C" int tb_pool_quant_tokens_t(const void *x, int dtype, const float *center, int64_t H, int64_t L,
+                                      int64_t d, int64_t block, int8_t *codes, float *scales, float *pooled,
+                                      float *pooled_t, int64_t ldt, void *stream) {
+    TB_REQUIRE(pooled != nullptr && pooled_t != nullptr && ldt >= cdiv(L, block), "pooled_t needs ldt >= blocks");
+    return pool_quant_launch(x, dtype, center, H, L, d, block, codes, scales, pooled, pooled_t, ldt, stream);
 }
 
 extern "C" int tb_kmean(const void *k, int dtype, int64_t H, int64_t L, int64_t d, float *kmean, void *stream) {

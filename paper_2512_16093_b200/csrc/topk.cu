@@ -11,6 +11,7 @@
 //    lower index, -0.0 == +0.0; output ascending.  Radix select (4 x 8-bit
 //    digits on order-preserving uint keys) per row, one warp per row.
 #include "common.cuh"
+#include "ptx.cuh"
 
 namespace tb {
 
@@ -23,7 +24,8 @@ __device__ __forceinline__ uint32_t desc_key(float s) {
 template <int R>
 __global__ void __launch_bounds__(256) topk_kernel(
     const float *__restrict__ qp, const float *__restrict__ kp, int nq, int nkv, int d, int count,
-    int small_path, int32_t *__restrict__ idx, uint8_t *__restrict__ comp, float *__restrict__ scores_out) {
+    int small_path, int32_t *__restrict__ idx, uint8_t *__restrict__ comp, float *__restrict__ scores_out,
+    __nv_bfloat16 *__restrict__ cov, int64_t cov_ld) {
     extern __shared__ __align__(16) uint8_t smem[];
     uint32_t *keys = reinterpret_cast<uint32_t *>(smem);                    // [R][nkv]
     float *qrow = reinterpret_cast<float *>(smem + (((size_t)R * nkv * 4 + 15) & ~(size_t)15));  // [R][d]
@@ -151,9 +153,168 @@ __global__ void __launch_bounds__(256) topk_kernel(
             const unsigned selb = __ballot_sync(0xffffffffu, sel);
             if (sel) idx[row * count + taken + __popc(selb & ((1u << lane) - 1u))] = j;
             if (comp && valid) comp[row * nkv + j] = sel ? 0 : 1;
+            if (cov && valid) cov[row * cov_ld + j] = __float2bfloat16_rn(sel ? 0.0f : 1.0f);
             taken += __popc(selb);
             ties += __popc(eqb);
         }
+        if (cov)
+            for (int j = nkv + lane; j < cov_ld; j += 32) cov[row * cov_ld + j] = __float2bfloat16_rn(0.0f);
+    }
+}
+
+// Fast path for the regular-sgemm order (d % 4 == 0, not the small-matrix
+// kernel): 16 q rows per CTA, each thread JT kv columns x 16 rows with the
+// chains packed in pairs of rows (fma.rn.f32x2 = two IEEE fmaf, bit-identical
+// to the scalar chain), q staged transposed so a row pair is one 8-B load.
+// Selection: 4-pass radix select (8-bit digits, warp-private histograms in
+// shared memory) for the threshold key, then the same ballot compaction.
+// Optional bf16 coverage output (1 = block in the complement) with row pitch
+// cov_ld, zero-padded, the A operand of the linear branch's GEMM.
+template <int JT>
+__global__ void __launch_bounds__(320, 1) topk16_kernel(
+    const float *__restrict__ qp, const float *__restrict__ kpt, int64_t ldk, int nq, int nkv, int d, int count,
+    int32_t *__restrict__ idx, uint8_t *__restrict__ comp, float *__restrict__ scores_out,
+    __nv_bfloat16 *__restrict__ cov, int64_t cov_ld) {
+    constexpr int R = 16;
+    extern __shared__ __align__(16) uint8_t smem[];
+    uint32_t *keys = reinterpret_cast<uint32_t *>(smem);                          // [R][nkv]
+    float *qt = reinterpret_cast<float *>(smem + (((size_t)R * nkv * 4 + 15) & ~(size_t)15));   // [d][R]
+    uint32_t *hist = reinterpret_cast<uint32_t *>(qt + (size_t)d * R);             // [warps][256]
+    const int h = blockIdx.y;
+    const int row0 = blockIdx.x * R;
+    const int nrows = min(R, nq - row0);
+    for (int i = threadIdx.x; i < R * d; i += blockDim.x) {
+        const int r = i / d, t = i - r * d;
+        qt[t * R + r] = (r < nrows) ? qp[((int64_t)h * nq + row0 + r) * d + t] : 0.0f;
+    }
+    __syncthreads();
+    // kp transposed ([d][ldk] per head): a warp's float4 loads of 4 kv columns are contiguous
+    const float *kth = kpt + (int64_t)h * d * ldk;
+    for (int j0 = threadIdx.x * JT; j0 < nkv; j0 += blockDim.x * JT) {
+        float2 acc[R / 2][JT];
+#pragma unroll
+        for (int r = 0; r < R / 2; r++)
+#pragma unroll
+            for (int u = 0; u < JT; u++) acc[r][u] = make_float2(0.0f, 0.0f);
+        // 8 dims per batch: the 8 coalesced float4 loads are all in flight before the FFMA2s
+        auto step = [&](int t, const float4 kv) {
+            const float4 *qrow = reinterpret_cast<const float4 *>(qt + t * R);
+            float2 qpair[R / 2];
+#pragma unroll
+            for (int r4 = 0; r4 < R / 4; r4++) {
+                const float4 q4 = qrow[r4];
+                qpair[2 * r4] = make_float2(q4.x, q4.y);
+                qpair[2 * r4 + 1] = make_float2(q4.z, q4.w);
+            }
+            const float kvu[4] = {kv.x, kv.y, kv.z, kv.w};
+#pragma unroll
+            for (int u = 0; u < JT; u++) {
+                const float2 k2 = make_float2(kvu[u], kvu[u]);
+#pragma unroll
+                for (int r = 0; r < R / 2; r++) acc[r][u] = ptx::ffma2(qpair[r], k2, acc[r][u]);
+            }
+        };
+        int t = 0;
+        for (; t + 8 <= d; t += 8) {
+            float4 kv[8];
+#pragma unroll
+            for (int i = 0; i < 8; i++) kv[i] = __ldg(reinterpret_cast<const float4 *>(kth + (int64_t)(t + i) * ldk + j0));
+#pragma unroll
+            for (int i = 0; i < 8; i++) step(t + i, kv[i]);
+        }
+        for (; t < d; t++) step(t, __ldg(reinterpret_cast<const float4 *>(kth + (int64_t)t * ldk + j0)));
+#pragma unroll
+        for (int r = 0; r < R / 2; r++)
+#pragma unroll
+            for (int u = 0; u < JT; u++) {
+                const int j = j0 + u;
+                if (j < nkv) {
+                    if (2 * r < nrows) keys[(2 * r) * nkv + j] = desc_key(acc[r][u].x);
+                    if (2 * r + 1 < nrows) keys[(2 * r + 1) * nkv + j] = desc_key(acc[r][u].y);
+                    if (scores_out) {
+                        if (2 * r < nrows) scores_out[((int64_t)h * nq + row0 + 2 * r) * nkv + j] = acc[r][u].x;
+                        if (2 * r + 1 < nrows) scores_out[((int64_t)h * nq + row0 + 2 * r + 1) * nkv + j] = acc[r][u].y;
+                    }
+                }
+            }
+    }
+    __syncthreads();
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t *hw = hist + warp * 256;
+    const int nwarps = blockDim.x >> 5;
+    for (int r = warp; r < nrows; r += nwarps) {
+        const uint32_t *kr = keys + r * nkv;
+        const int64_t row = (int64_t)h * nq + row0 + r;
+        // threshold T = the count-th largest key, digit by digit from the top;
+        // need = how many keys equal to T are taken
+        uint32_t prefix = 0;
+        int need = count;
+        if (count < nkv) {
+#pragma unroll 1
+            for (int shift = 24; shift >= 0; shift -= 8) {
+                for (int i = lane; i < 256; i += 32) hw[i] = 0;
+                __syncwarp();
+                const uint32_t hi_mask = shift == 24 ? 0u : (0xFFFFFFFFu << (shift + 8));
+                for (int j = lane; j < nkv; j += 32) {
+                    const uint32_t k = kr[j];
+                    if ((k & hi_mask) == (prefix & hi_mask)) atomicAdd(&hw[(k >> shift) & 0xFF], 1u);
+                }
+                __syncwarp();
+                // lane owns bins 255-8*lane .. 248-8*lane (descending); suffix counts from the top
+                uint32_t c8[8], tot = 0;
+#pragma unroll
+                for (int i = 0; i < 8; i++) { c8[i] = hw[255 - 8 * lane - i]; tot += c8[i]; }
+                uint32_t incl = tot;                       // inclusive scan over lanes (higher bins first)
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += v;
+                }
+                const uint32_t before = incl - tot;        // keys in bins above this lane's range
+                // the bin where the running count first reaches need
+                int hit = -1;
+                uint32_t above = before;
+                if (before < (uint32_t)need && incl >= (uint32_t)need) {
+#pragma unroll
+                    for (int i = 0; i < 8; i++) {
+                        if (hit < 0) {
+                            if (above + c8[i] >= (uint32_t)need) hit = i;
+                            else above += c8[i];
+                        }
+                    }
+                }
+                const unsigned who = __ballot_sync(0xffffffffu, hit >= 0);
+                const int src = __ffs(who) - 1;
+                const int bin = __shfl_sync(0xffffffffu, 255 - 8 * lane - hit, src);
+                const uint32_t ab = __shfl_sync(0xffffffffu, above, src);
+                prefix |= (uint32_t)bin << shift;
+                need -= (int)ab;
+                __syncwarp();
+            }
+        }
+        const uint32_t T = prefix;
+        // compaction in ascending index order
+        const bool take_all = count >= nkv;
+        int taken = 0, ties = 0;
+        for (int base = 0; base < nkv; base += 32) {
+            const int j = base + lane;
+            const uint32_t k = (j < nkv) ? kr[j] : 0u;
+            const bool valid = j < nkv;
+            const bool gt = valid && (take_all || k > T);
+            const bool eq = valid && !take_all && k == T;
+            const unsigned eqb = __ballot_sync(0xffffffffu, eq);
+            const int tie_rank = ties + __popc(eqb & ((1u << lane) - 1u));
+            const bool sel = gt || (eq && tie_rank < need);
+            const unsigned selb = __ballot_sync(0xffffffffu, sel);
+            if (sel) idx[row * count + taken + __popc(selb & ((1u << lane) - 1u))] = j;
+            if (comp && valid) comp[row * nkv + j] = sel ? 0 : 1;
+            if (cov && valid) cov[row * cov_ld + j] = __float2bfloat16_rn(sel ? 0.0f : 1.0f);
+            taken += __popc(selb);
+            ties += __popc(eqb);
+        }
+        if (cov)
+            for (int j = nkv + lane; j < cov_ld; j += 32) cov[row * cov_ld + j] = __float2bfloat16_rn(0.0f);
     }
 }
 
@@ -161,24 +322,48 @@ __global__ void __launch_bounds__(256) topk_kernel(
 
 using namespace tb;
 
-extern "C" int tb_topk_blocks(const float *qp, const float *kp, int64_t H, int64_t nq, int64_t nkv, int64_t d,
-                              int64_t count, int32_t *idx, uint8_t *comp, float *scores_out, void *stream) {
+static int topk_launch(const float *qp, const float *kp, const float *kpt, int64_t ldk, int64_t H, int64_t nq,
+                       int64_t nkv, int64_t d, int64_t count, int32_t *idx, uint8_t *comp, float *scores_out,
+                       __nv_bfloat16 *cov, int64_t cov_ld, cudaStream_t st) {
     TB_REQUIRE(count >= 1 && count <= nkv, "count must be in [1, num_kv_blocks]");
     TB_REQUIRE(nkv <= 16384, "num_kv_blocks > 16384 unsupported");
     TB_REQUIRE(d >= 1 && d <= 1024, "head_dim out of range");
     if (H == 0 || nq == 0) return TB_OK;
     const double mnk = (double)nq * (double)nkv * (double)d;
     const int small = (nq * nkv <= 1200 && d >= 32 && mnk <= 1e6) ? 1 : 0;
-    cudaStream_t st = as_stream(stream);
+    const bool fast16 = !small && kpt != nullptr && ldk % 4 == 0 && ldk >= cdiv(nkv, 4) * 4 &&
+                        (((uintptr_t)kpt) % 16) == 0 && nkv <= 2560;
+    if (fast16) {
+        constexpr int JT = 4;                        // 320 threads x 4 columns >= 1182 kv blocks (cfg4) in one pass
+        const size_t smem = (((size_t)16 * nkv * 4 + 15) & ~(size_t)15) + (size_t)d * 16 * 4 + 10 * 256 * 4;
+        cudaFuncSetAttribute(topk16_kernel<JT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        dim3 grid((unsigned)cdiv(nq, 16), (unsigned)H);
+        topk16_kernel<JT><<<grid, 320, smem, st>>>(qp, kpt, ldk, (int)nq, (int)nkv, (int)d, (int)count, idx, comp,
+                                                  scores_out, cov, cov_ld);
+        return check_launch("topk16");
+    }
 #define TB_TOPK(R)                                                                                 \
     {                                                                                              \
         size_t smem = (((size_t)(R) * nkv * 4 + 15) & ~(size_t)15) + (size_t)(R) * d * 4;          \
         cudaFuncSetAttribute(topk_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
         dim3 grid((unsigned)cdiv(nq, R), (unsigned)H);                                             \
         topk_kernel<R><<<grid, 256, smem, st>>>(qp, kp, (int)nq, (int)nkv, (int)d, (int)count, small, \
-                                                idx, comp, scores_out);                            \
+                                                idx, comp, scores_out, cov, cov_ld);               \
     }
     if (nkv <= 2048) TB_TOPK(8) else if (nkv <= 4096) TB_TOPK(4) else TB_TOPK(1)
 #undef TB_TOPK
     return check_launch("topk_blocks");
+}
+
+extern "C" int tb_topk_blocks(const float *qp, const float *kp, int64_t H, int64_t nq, int64_t nkv, int64_t d,
+                              int64_t count, int32_t *idx, uint8_t *comp, float *scores_out, void *stream) {
+    return topk_launch(qp, kp, nullptr, 0, H, nq, nkv, d, count, idx, comp, scores_out, nullptr, 0, as_stream(stream));
+}
+
+extern "C" int tb_topk_blocks_cov(const float *qp, const float *kp, const float *kpt, int64_t ldk, int64_t H,
+                                  int64_t nq, int64_t nkv, int64_t d, int64_t count, int32_t *idx, uint8_t *comp,
+                                  void *cov, int64_t cov_ld, void *stream) {
+    TB_REQUIRE(cov != nullptr && cov_ld >= nkv && cov_ld % 8 == 0, "cov needs a row pitch >= nkv, multiple of 8");
+    return topk_launch(qp, kp, kpt, ldk, H, nq, nkv, d, count, idx, comp, nullptr, (__nv_bfloat16 *)cov, cov_ld,
+                       as_stream(stream));
 }

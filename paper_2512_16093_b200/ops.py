@@ -118,6 +118,22 @@ def pool_quant_tokens(x: torch.Tensor, block: int, center: torch.Tensor | None =
     return codes, scales, pooled
 
 
+def pool_quant_tokens_t(x: torch.Tensor, block: int, center: torch.Tensor | None = None):
+    """pool_quant_tokens plus the pooled means transposed [H, d, ldt] (the
+    top-k kernel's coalesced kp operand) -> (codes, scales, pooled, pooled_t)."""
+    x = _dev_tensor(x, "x")
+    H, L, d = x.shape
+    nb = cdiv(L, block)
+    ldt = -(-nb // 4) * 4
+    codes = _empty((H, L, d), torch.int8, x)
+    scales = _empty((H, nb), torch.float32, x)
+    pooled = _empty((H, nb, d), torch.float32, x)
+    pooled_t = _empty((H, d, ldt), torch.float32, x)
+    call("tb_pool_quant_tokens_t", ptr(x), dtype_code(x), ptr(center), H, L, d, block, ptr(codes), ptr(scales),
+         ptr(pooled), ptr(pooled_t), ldt, stream_ptr())
+    return codes, scales, pooled, pooled_t
+
+
 def topk_count(ratio: float, nkv: int) -> int:
     """attention.py:279."""
     return math.ceil(ratio * nkv)
@@ -134,6 +150,23 @@ def topk_blocks(qp: torch.Tensor, kp: torch.Tensor, count: int, want_comp: bool 
     scores = _empty((H, nq, nkv), torch.float32, qp) if want_scores else None
     call("tb_topk_blocks", ptr(qp), ptr(kp), H, nq, nkv, d, count, ptr(idx), ptr(comp), ptr(scores), stream_ptr())
     return idx, comp, scores
+
+
+def topk_blocks_cov(qp: torch.Tensor, kp: torch.Tensor, count: int, want_comp: bool = False,
+                    kpt: torch.Tensor | None = None):
+    """select_topk_blocks + the complement as the bf16 coverage matrix of the
+    linear branch's GEMM -> (idx, comp uint8|None, cov bf16 [H, nq, nkv_pad]).
+    kpt: kp transposed [H, d, ldk] (pool_quant_tokens_t) for the fast path."""
+    qp, kp = qp.float().contiguous(), kp.float().contiguous()
+    H, nq, d = qp.shape
+    nkv = kp.shape[1]
+    ld = -(-nkv // 8) * 8                            # TMA row pitch must be a multiple of 16 B
+    idx = _empty((H, nq, count), torch.int32, qp)
+    comp = _empty((H, nq, nkv), torch.uint8, qp) if want_comp else None
+    cov = _empty((H, nq, ld), torch.bfloat16, qp)
+    call("tb_topk_blocks_cov", ptr(qp), ptr(kp), ptr(kpt), 0 if kpt is None else kpt.shape[2], H, nq, nkv, d,
+         count, ptr(idx), ptr(comp), ptr(cov), ld, stream_ptr())
+    return idx, comp, cov
 
 
 def transpose_v(v: torch.Tensor, l_pad: int) -> torch.Tensor:
@@ -178,25 +211,29 @@ def linear_kv_dx(d: int) -> int:
     return dx
 
 
-def linear_kv_sel(k, v, comp: torch.Tensor, kv_block: int):
-    """Fused-epilogue form of the linear branch (attention.py:320-328).
-
-    k, v: bf16 [H, L, d].  Returns kvsel [H, nq, dx, d] bf16: per q block n,
-    rows 0..d-1 hold KV_sel[n]^T = sum over complement blocks b of
-    V_b^T phi(K_b), row d holds sum phi(K_b); the attention kernel finishes
-    the branch with one tcgen05 MMA phi(Q_n) . KV_sel[n] in its epilogue
-    (attention.py:329-334).  kv_part (one tcgen05 kernel straight from k and
-    v) and the coverage GEMM cov . kv_part are both ours (tb_linear_kv_part,
-    tb_gemm_bf16_batched), bf16 operands with f32 accumulation.
-    """
+def linear_kv_part(k, v, kv_block: int):
+    """tb_linear_kv_part: per kv block [V_b | 1]^T phi(K_b) (attention.py:320-325)
+    straight from bf16 k, v -> [H, nkv, dx, d] bf16 (one tcgen05 kernel)."""
     H, L, d = k.shape
-    nq, nkv = comp.shape[1], comp.shape[2]
+    nkv = cdiv(L, kv_block)
     dx = linear_kv_dx(d)
     kv_part = torch.empty((H, nkv, dx, d), dtype=torch.bfloat16, device=k.device)
     call("tb_linear_kv_part", ptr(k), ptr(v), H, L, d, kv_block, dx, ptr(kv_part), stream_ptr())
-    nkv_pad = -(-nkv // 8) * 8                       # TMA row pitch must be a multiple of 16 B
-    cov = torch.zeros((H, nq, nkv_pad), dtype=torch.bfloat16, device=k.device)
-    cov[:, :, :nkv] = comp
+    return kv_part
+
+
+def linear_kv_sel(kv_part: torch.Tensor, cov: torch.Tensor, nkv: int):
+    """Fused-epilogue form of the linear branch (attention.py:320-328).
+
+    Returns kvsel [H, nq, dx, d] bf16: per q block n, rows 0..d-1 hold
+    KV_sel[n]^T = sum over complement blocks b of V_b^T phi(K_b), row d holds
+    sum phi(K_b); the attention kernel finishes the branch with one tcgen05
+    MMA phi(Q_n) . KV_sel[n] in its epilogue (attention.py:329-334).  The
+    coverage GEMM cov . kv_part is ours (tb_gemm_bf16_batched), bf16 operands
+    with f32 accumulation.
+    """
+    H, _, dx, d = kv_part.shape
+    nq = cov.shape[1]
     kvsel = gemm_bf16_batched(cov, kv_part.view(H, nkv, dx * d), K=nkv)         # [H, nq, dx*d]
     return kvsel.view(H, nq, dx, d)
 
@@ -268,6 +305,15 @@ def linear_branch(q, k, v, comp: torch.Tensor | None, q_block: int, kv_block: in
 _SIDE = {}
 
 
+def _km_event(side: torch.cuda.Stream) -> torch.cuda.Event:
+    """An event recorded on the side stream right after k_mean was enqueued
+    (sla_attention records it before the kv_part launch)."""
+    return _KM_EVENT[torch.cuda.current_device()]
+
+
+_KM_EVENT = {}
+
+
 def _side_stream() -> torch.cuda.Stream:
     dev = torch.cuda.current_device()
     s = _SIDE.get(dev)
@@ -304,31 +350,50 @@ def sla_attention(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: fl
     tc = quantized and d == 128 and q_block == 128 and kv_block == 64 and L >= 128
     l_pad = nkv * 64
     main = torch.cuda.current_stream()
-    if quantized:
-        # k_mean is a latency-bound sequential chain on H CTAs: overlap it with
-        # the Q pass (and the V^T pass below) on a side stream
-        side = _side_stream()
-        side.wait_stream(main)
-        with torch.cuda.stream(side):
-            km = kmean(k)
-        qc, qs, qp = pool_quant_tokens(q, q_block, None, pool=True)
-    else:
-        qc = qs = kc = ks = km = None
-        qp, kp = pool_block_means(q, q_block), pool_block_means(k, kv_block)
+    # bf16 tensor-core path with the linear branch: the pool pass also emits
+    # kp transposed for the coalesced top-k kernel, which writes the bf16
+    # coverage matrix for the branch's GEMM
+    fast_lin = lin and tc and quantized and q.dtype == torch.bfloat16
+    kpt = None
     # the tensor-core path reads V (and the linear-branch kernel K and V) as bf16
     kb, vb = (k, v) if q.dtype == torch.bfloat16 else (k.to(torch.bfloat16), v.to(torch.bfloat16))
     vt = None if q.dtype == torch.bfloat16 else vb
+    # Side stream: k_mean (a latency-bound sequential chain) and the linear
+    # branch's per-block operand kv_part (HBM-bound, needs only k and v) run
+    # under the Q / K passes and the (issue-bound) top-k selection.
+    side = _side_stream()
+    side.wait_stream(main)
+    kv_part = None
+    with torch.cuda.stream(side):
+        km = kmean(k) if quantized else None
+        ev = _KM_EVENT.setdefault(torch.cuda.current_device(), torch.cuda.Event())
+        ev.record(side)
+        if lin and tc:
+            kv_part = linear_kv_part(kb, vb, kv_block)
     if quantized:
-        main.wait_stream(side)
+        qc, qs, qp = pool_quant_tokens(q, q_block, None, pool=True)
+    else:
+        qc = qs = kc = ks = None
+        qp, kp = pool_block_means(q, q_block), pool_block_means(k, kv_block)
+    if quantized:
+        main.wait_stream(side) if not (lin and tc) else main.wait_event(_km_event(side))
         km.record_stream(main)
-        kc, ks, kp = pool_quant_tokens(k, kv_block, km, pool=True)
-    idx, comp, _ = topk_blocks(qp, kp, count, want_comp=lin or return_parts)
+        if fast_lin:
+            kc, ks, kp, kpt = pool_quant_tokens_t(k, kv_block, km)
+        else:
+            kc, ks, kp = pool_quant_tokens(k, kv_block, km, pool=True)
     lin_pack = lin_kv = None
+    cov = None
     if lin and tc:
-        lin_kv = linear_kv_sel(kb, vb, comp, kv_block)
-    elif lin:
-        fast = (H * L * d >= (1 << 22)) if linear_fast is None else linear_fast
-        lin_pack = linear_branch(q, k, v, comp, q_block, kv_block, fast=fast)
+        idx, comp, cov = topk_blocks_cov(qp, kp, count, want_comp=return_parts, kpt=kpt)
+        main.wait_stream(side)
+        kv_part.record_stream(main)
+        lin_kv = linear_kv_sel(kv_part, cov, nkv)
+    else:
+        idx, comp, _ = topk_blocks(qp, kp, count, want_comp=lin or return_parts)
+        if lin:
+            fast = (H * L * d >= (1 << 22)) if linear_fast is None else linear_fast
+            lin_pack = linear_branch(q, k, v, comp, q_block, kv_block, fast=fast)
     out = torch.empty((H, L, d), dtype=out_dtype, device=q.device)
     row_max = torch.empty((H, L), dtype=torch.float32, device=q.device) if return_parts else None
     den = torch.empty((H, L), dtype=torch.float32, device=q.device) if return_parts else None
