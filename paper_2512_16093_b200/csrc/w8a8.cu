@@ -32,6 +32,7 @@ struct Smem {
     uint64_t full[STAGES], empty[STAGES];
     uint64_t seg_full[2], seg_empty[2];
     uint32_t tmem_base;
+    alignas(1024) uint8_t stage_out[EPI_WARPS][32 * 128];   // per-warp 32 rows x 128 B output chunk (SW128)
 };
 template <int BN>
 constexpr size_t smem_bytes() { return sizeof(Smem<BN>) + 1024; }
@@ -43,6 +44,7 @@ constexpr size_t smem_bytes() { return sizeof(Smem<BN>) + 1024; }
 template <int BN, bool EXACT, bool OUT_BF16>
 __global__ void __launch_bounds__(gemm::THREADS, 1) w8a8_tc_kernel(
     const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+    const __grid_constant__ CUtensorMap tma_out,
     const float *__restrict__ sa, const float *__restrict__ sb, const float *__restrict__ bias,
     void *__restrict__ out, int M, int N, int K) {
     using namespace gemm;
@@ -163,30 +165,42 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) w8a8_tc_kernel(
             float acc[CW];
 #pragma unroll
             for (int i = 0; i < CW / 2; i++) { acc[2 * i] = acc2[i].x; acc[2 * i + 1] = acc2[i].y; }
-            const int row = mt * BM + trow;
-            if (row < M) {
-                if (bias) {
+            if (bias) {
 #pragma unroll
-                    for (int i = 0; i < CW; i++) acc[i] = __fadd_rn(acc[i], __ldg(bias + col0 + i));
-                }
-                if constexpr (OUT_BF16) {
-                    __nv_bfloat16 *o = reinterpret_cast<__nv_bfloat16 *>(out) + (size_t)row * N + col0;
+                for (int i = 0; i < CW; i++) acc[i] = __fadd_rn(acc[i], __ldg(bias + col0 + i));
+            }
+            // stores: each warp stages 32 rows x 128 B (32 f32 or 64 bf16 columns) in a
+            // 128B-swizzled smem chunk and one lane TMA-stores it (rows >= M are clipped)
+            constexpr int CPC = OUT_BF16 ? 64 : 32;             // columns per chunk
+            uint8_t *stg = S.stage_out[ew];
+            const int row0 = mt * BM + quarter * 32;
 #pragma unroll
-                    for (int i = 0; i < CW; i += 8) {
-                        uint4 w;
+            for (int ch = 0; ch < CW / CPC; ch++) {
+                if (lane == 0) ptx::bulk_wait_read0();          // previous chunk has left the buffer
+                __syncwarp();
+#pragma unroll
+                for (int u = 0; u < 8; u++) {                   // 8 x 16-byte units per 128-B row
+                    uint4 w;
+                    if constexpr (OUT_BF16) {
                         __nv_bfloat162 *p = reinterpret_cast<__nv_bfloat162 *>(&w);
 #pragma unroll
-                        for (int j = 0; j < 4; j++) p[j] = __floats2bfloat162_rn(acc[i + 2 * j], acc[i + 2 * j + 1]);
-                        *reinterpret_cast<uint4 *>(o + i) = w;
+                        for (int j = 0; j < 4; j++)
+                            p[j] = __floats2bfloat162_rn(acc[ch * CPC + 8 * u + 2 * j], acc[ch * CPC + 8 * u + 2 * j + 1]);
+                    } else {
+                        w = make_uint4(__float_as_uint(acc[ch * CPC + 4 * u]), __float_as_uint(acc[ch * CPC + 4 * u + 1]),
+                                       __float_as_uint(acc[ch * CPC + 4 * u + 2]), __float_as_uint(acc[ch * CPC + 4 * u + 3]));
                     }
-                } else {
-                    float *o = reinterpret_cast<float *>(out) + (size_t)row * N + col0;
-#pragma unroll
-                    for (int i = 0; i < CW; i += 4)
-                        *reinterpret_cast<float4 *>(o + i) = make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
+                    *reinterpret_cast<uint4 *>(stg + lane * 128 + ((u ^ (lane & 7)) * 16)) = w;
+                }
+                ptx::fence_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    ptx::tma_store_2d(&tma_out, stg, col0 + ch * CPC, row0);
+                    ptx::bulk_commit();
                 }
             }
         }
+        if (lane == 0) ptx::bulk_wait_read0();
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -286,12 +300,16 @@ int w8a8_dispatch(const int8_t *a, const float *sa, const int8_t *bt, const floa
     TB_REQUIRE(out_dtype == TB_F32 || out_dtype == TB_BF16, "out dtype must be f32 or bf16");
     if (M == 0 || N == 0) return TB_OK;
     const bool tc = block == 128 && K % 128 == 0 && N % 128 == 0 && K > 0 && M < (1ll << 31) &&
-                    ((uintptr_t)a % 16) == 0 && ((uintptr_t)bt % 16) == 0;
+                    ((uintptr_t)a % 16) == 0 && ((uintptr_t)bt % 16) == 0 && ((uintptr_t)out % 16) == 0;
     if (tc) {
         const int BN = (N % 256 == 0) ? 256 : 128;
         CUtensorMap ta, tbm;
+        CUtensorMap tout;
+        const bool obf = out_dtype == TB_BF16;
         if (!make_tmap_2d(&ta, a, CU_TENSOR_MAP_DATA_TYPE_UINT8, K, M, K, 128, 128) ||
-            !make_tmap_2d(&tbm, bt, CU_TENSOR_MAP_DATA_TYPE_UINT8, K, N, K, 128, BN))
+            !make_tmap_2d(&tbm, bt, CU_TENSOR_MAP_DATA_TYPE_UINT8, K, N, K, 128, BN) ||
+            !make_tmap_2d(&tout, out, obf ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, N, M,
+                          N * (obf ? 2 : 4), obf ? 64 : 32, 32))
             return fail(TB_ECUDA, "cuTensorMapEncodeTiled failed");
         const int ntiles = (int)(cdiv(M, 128) * (N / BN));
         const int grid = ntiles < num_sms() ? ntiles : num_sms();
@@ -299,7 +317,7 @@ int w8a8_dispatch(const int8_t *a, const float *sa, const int8_t *bt, const floa
     {                                                                                                      \
         auto kern = w8a8_tc_kernel<BNV, E, B>;                                                             \
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm::smem_bytes<BNV>()); \
-        kern<<<grid, gemm::THREADS, gemm::smem_bytes<BNV>(), st>>>(ta, tbm, sa, sb, bias, out, (int)M, (int)N, (int)K); \
+        kern<<<grid, gemm::THREADS, gemm::smem_bytes<BNV>(), st>>>(ta, tbm, tout, sa, sb, bias, out, (int)M, (int)N, (int)K); \
     }
 #define TB_GEMM_BN(BNV)                                                                                    \
         if (exact && out_dtype == TB_F32) TB_GEMM_LAUNCH(BNV, true, false)                                 \
