@@ -37,6 +37,10 @@ sys.path.insert(0, ROOT)
 H_, L_, D_ = 40, 75600, 128
 QB, KVB, RATIO = 128, 64, 0.1
 METRIC = "SLA-Sage attn TOPS & W8A8 GEMM TOPS at Wan2.1-14B-720P shapes, 1/2/4/8 B200"
+# kernels one sla_attention step launches (bf16 tensor-core path with the linear branch):
+# k_mean + kv_part (side stream), Q pool/quant, K pool/quant (+ transposed kp), top-k
+# (+ coverage matrix), coverage GEMM, fused attention
+LAUNCHES_PER_STEP = 7
 UNIT = "TOPS"
 
 
@@ -301,8 +305,14 @@ def main():
         torch.cuda.synchronize()
         kms = e0.elapsed_time(e1) / reps
         ach = total_ops / (kms * 1e-3) / 1e12
+        traffic = None
+        try:        # dram read+write bytes per launch from the committed ncu --set full capture
+            with open(os.path.join(ROOT, "profiles", "r01_sla_tc_traffic.json")) as f:
+                traffic = json.load(f)["traffic_bytes"]
+        except Exception:
+            pass
         roof = {"bound": "tensor", "achieved": ach, "peak": mixed_peak, "unit": "TFLOP/s",
-                "frac": ach / mixed_peak, "traffic": None, "kernel": "sla_tc_kernel",
+                "frac": ach / mixed_peak, "traffic": traffic, "kernel": "sla_tc_kernel",
                 "kernel_ms": kms, "share_of_step": kms / ms,
                 "peak_note": f"INT8 QK^T (2x) + BF16 PV at {peak_kind} bf16 burst {bf16_peak} TFLOP/s x 4/3; "
                              "INT8 dense peak not in MEASURED_PEAKS.json"}
@@ -373,7 +383,7 @@ def main():
                            "topk_ratio": RATIO, "parallelism": f"ulysses{world}",
                            "l2": "inputs 3 x 774 MB bf16 > 126 MB L2 (no flush needed)"},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "w8a8": w8,
-                "dit": dit_res, "gpu_launches": 8 * args.steps, "clocks": clk.summary()}
+                "dit": dit_res, "gpu_launches": LAUNCHES_PER_STEP * args.steps, "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
