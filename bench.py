@@ -355,9 +355,8 @@ def main():
         hq = [t.cpu().pin_memory() for t in head_major]
         hout = torch.empty((H, L_, D_), dtype=torch.bfloat16).pin_memory()
         def e2e_step():
-            dq = [t.to("cuda", non_blocking=True) for t in hq]
-            o = ops.sla_attention(dq[0], dq[1], dq[2], QB, KVB, RATIO, 1.0, out_dtype=torch.bfloat16)
-            hout.copy_(o, non_blocking=True)
+            # public API on pinned host buffers: per-head-chunk H2D / attention / D2H pipeline
+            ops.sla_attention_host(hq[0], hq[1], hq[2], QB, KVB, RATIO, 1.0, out=hout)
         e2e_step()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -416,6 +416,69 @@ def sla_attention(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: fl
     return out
 
 
+_AUX = {}
+
+
+def _aux_stream(name: str) -> torch.cuda.Stream:
+    key = (torch.cuda.current_device(), name)
+    s = _AUX.get(key)
+    if s is None:
+        s = _AUX[key] = torch.cuda.Stream()
+    return s
+
+
+def sla_attention_host(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: float = 0.1,
+                       linear_mix: float = 1.0, quantized: bool = True, scale: float | None = None,
+                       out: torch.Tensor | None = None, out_dtype=torch.bfloat16, chunk_heads: int = 4):
+    """sla_attention on HOST tensors [H, L, d] (pinned for overlap): every
+    hot-path quantity is per head (attention.py:370), so the heads are
+    processed in chunks and the host->device copy of chunk i+1, the attention
+    of chunk i and the device->host copy of chunk i-1 run on three streams at
+    once.  Returns the (pinned) host output."""
+    if q.is_cuda or k.is_cuda or v.is_cuda:
+        raise ValueError("sla_attention_host takes host tensors; use sla_attention for device tensors")
+    if not (q.shape == k.shape == v.shape) or q.dim() != 3:
+        raise ValueError(f"q/k/v must share shape [heads, seq, head_dim], got "
+                         f"{tuple(q.shape)}, {tuple(k.shape)}, {tuple(v.shape)}")
+    H, L, d = q.shape
+    if out is None:
+        out = torch.empty((H, L, d), dtype=out_dtype, pin_memory=True)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    compute = torch.cuda.current_stream()
+    h2d, d2h = _aux_stream("h2d"), _aux_stream("d2h")
+    h2d.wait_stream(compute)
+    d2h.wait_stream(compute)
+    ch = max(1, min(chunk_heads, H))
+    bufs = [[torch.empty((ch, L, d), dtype=x.dtype, device=dev) for x in (q, k, v)] for _ in range(2)]
+    ev_in = [torch.cuda.Event() for _ in range(2)]
+    ev_done = [torch.cuda.Event() for _ in range(2)]
+    ev_out = [torch.cuda.Event() for _ in range(2)]
+    for i, h0 in enumerate(range(0, H, ch)):
+        h1 = min(H, h0 + ch)
+        n, b = h1 - h0, i % 2
+        if i >= 2:
+            h2d.wait_event(ev_done[b])                  # chunk i-2 has consumed buffer b
+        with torch.cuda.stream(h2d):
+            for dst, src in zip(bufs[b], (q, k, v)):
+                dst[:n].copy_(src[h0:h1], non_blocking=True)
+            ev_in[b].record(h2d)
+        compute.wait_event(ev_in[b])
+        o = sla_attention(bufs[b][0][:n], bufs[b][1][:n], bufs[b][2][:n], q_block, kv_block, topk_ratio,
+                          linear_mix, quantized, scale, out_dtype=out.dtype)
+        ev_done[b].record(compute)
+        d2h.wait_event(ev_done[b])
+        with torch.cuda.stream(d2h):
+            out[h0:h1].copy_(o, non_blocking=True)
+            ev_out[b].record(d2h)
+        o.record_stream(d2h)
+    for bb in bufs:
+        for t in bb:
+            t.record_stream(compute)
+            t.record_stream(h2d)
+    compute.wait_stream(d2h)                            # the caller's stream covers the output copy
+    return out
+
+
 # ------------------------------------------------------------------ DiT rows
 
 def rmsnorm(x, gain, eps=1e-6):

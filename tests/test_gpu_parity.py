@@ -273,3 +273,14 @@ def test_linear_kv_part_blocks(tb):
             assert cos >= 0.9999 and rel1 <= 1e-2, (h, b, cos, rel1)
             assert np.allclose(got[h, b, d], den, rtol=1e-2, atol=1e-2), (h, b)
             assert not got[h, b, d + 1:].any()
+
+
+def test_sla_attention_host_pipeline_matches_device(tb):
+    """The host-buffer API (per-head-chunk H2D / attention / D2H on three
+    streams) returns exactly the device path's output: every quantity is per head."""
+    q, k, v = gen.gaussian_qkv(41, 5, 1024, 128, bf16=True)
+    hq, hk, hv = (torch.from_numpy(x).to(torch.bfloat16).pin_memory() for x in (q, k, v))
+    want = tb.sla_attention(hq.cuda(), hk.cuda(), hv.cuda(), 128, 64, 0.1, 1.0, out_dtype=torch.bfloat16).cpu()
+    got = tb.sla_attention_host(hq, hk, hv, 128, 64, 0.1, 1.0, chunk_heads=2)
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)
