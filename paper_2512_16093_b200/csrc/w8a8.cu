@@ -132,47 +132,64 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) w8a8_tc_kernel(
                 ptx::mbar_wait_sleep(&S.seg_full[buf], bphase);
                 ptx::tc_fence_after();
                 const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + buf * BN + half * CW;
+                // 16-column chunks, double-buffered: the tcgen05.ld of chunk c+1 is in
+                // flight while chunk c is promoted (wait::ld covers all outstanding loads)
+#ifdef TB_W8_NOEPI
+                ptx::tc_fence_before();
+                ptx::mbar_arrive(&S.seg_empty[buf]);
+                buf ^= 1;
+                if (buf == 0) bphase ^= 1;
+                continue;
+#endif
+                uint32_t rb[2][16];
+                ptx::tmem_ld16(taddr, rb[0]);
+                ptx::tmem_wait_ld();
 #pragma unroll
-                for (int cc = 0; cc < CW; cc += 32) {
-                    uint32_t r[2][16];
-                    ptx::tmem_ld16(taddr + cc, r[0]);
-                    ptx::tmem_ld16(taddr + cc + 16, r[1]);
-                    ptx::tmem_wait_ld();
-                    if (cc + 32 == CW) {
-                        ptx::tc_fence_before();
-                        ptx::mbar_arrive(&S.seg_empty[buf]);     // segment buffer free for the MMA
-                    }
+                for (int c = 0; c < CW / 16; c++) {
+                    if (c + 1 < CW / 16) ptx::tmem_ld16(taddr + (c + 1) * 16, rb[(c + 1) & 1]);
+                    const uint32_t (&r)[16] = rb[c & 1];
 #pragma unroll
-                    for (int j = 0; j < 2; j++)
-#pragma unroll
-                        for (int i = 0; i < 16; i += 2) {
-                            // exact s32 -> f32 (I2FP; |seg| <= 128*127^2 < 2^24), then packed f32x2 math
-                            const float2 x = make_float2(__int2float_rn((int)r[j][i]), __int2float_rn((int)r[j][i + 1]));
-                            float2 &o = acc2[(cc + j * 16 + i) >> 1];
-                            if constexpr (EXACT) {
-                                // scalar RN ops: the reference rounding sequence bit-for-bit (the
-                                // packed f32x2 forms differ in the last bits on sm_100a)
-                                o.x = __fadd_rn(o.x, __fmul_rn(__fmul_rn(x.x, sa2.x), sb2.x));
-                                o.y = __fadd_rn(o.y, __fmul_rn(__fmul_rn(x.y, sa2.y), sb2.y));
-                            } else {
-                                o = ptx::ffma2(x, sab2, o);
-                            }
+                    for (int i = 0; i < 16; i += 2) {
+                        // exact s32 -> f32 (|seg| <= 128*127^2 < 2^22).  Fast mode splits the
+                        // conversion between pipes: 3 of 4 pairs by I2FP (ALU), 1 of 4 by the
+                        // 1.5*2^23 magic + FADD2 (FMA pipe)
+                        float2 x;
+                        if (!EXACT && (i & 6) == 6) {
+                            const float2 m = make_float2(__int_as_float((int)r[i] + 0x4B400000),
+                                                         __int_as_float((int)r[i + 1] + 0x4B400000));
+                            x = ptx::fadd2(m, make_float2(-12582912.0f, -12582912.0f));
+                        } else {
+                            x = make_float2(__int2float_rn((int)r[i]), __int2float_rn((int)r[i + 1]));
                         }
+                        float2 &o = acc2[(c * 16 + i) >> 1];
+                        if constexpr (EXACT) {
+                            // scalar RN ops: the reference rounding sequence bit-for-bit (the
+                            // packed f32x2 forms differ in the last bits on sm_100a)
+                            o.x = __fadd_rn(o.x, __fmul_rn(__fmul_rn(x.x, sa2.x), sb2.x));
+                            o.y = __fadd_rn(o.y, __fmul_rn(__fmul_rn(x.y, sa2.y), sb2.y));
+                        } else {
+                            o = ptx::ffma2(x, sab2, o);
+                        }
+                    }
+                    ptx::tmem_wait_ld();
                 }
+                ptx::tc_fence_before();
+                ptx::mbar_arrive(&S.seg_empty[buf]);             // segment buffer free for the MMA
                 buf ^= 1;
                 if (buf == 0) bphase ^= 1;
             }
-            float acc[CW];
-#pragma unroll
-            for (int i = 0; i < CW / 2; i++) { acc[2 * i] = acc2[i].x; acc[2 * i + 1] = acc2[i].y; }
             if (bias) {
 #pragma unroll
-                for (int i = 0; i < CW; i++) acc[i] = __fadd_rn(acc[i], __ldg(bias + col0 + i));
+                for (int i = 0; i < CW / 2; i++) {
+                    acc2[i].x = __fadd_rn(acc2[i].x, __ldg(bias + col0 + 2 * i));
+                    acc2[i].y = __fadd_rn(acc2[i].y, __ldg(bias + col0 + 2 * i + 1));
+                }
             }
             // stores: each warp stages 32 rows x 128 B (32 f32 or 64 bf16 columns) in a
             // 128B-swizzled smem chunk and one lane TMA-stores it (rows >= M are clipped)
             constexpr int CPC = OUT_BF16 ? 64 : 32;             // columns per chunk
             uint8_t *stg = S.stage_out[ew];
+            const uint32_t stg_s = ptx::smem_u32(stg);
             const int row0 = mt * BM + quarter * 32;
 #pragma unroll
             for (int ch = 0; ch < CW / CPC; ch++) {
@@ -180,17 +197,23 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) w8a8_tc_kernel(
                 __syncwarp();
 #pragma unroll
                 for (int u = 0; u < 8; u++) {                   // 8 x 16-byte units per 128-B row
-                    uint4 w;
+                    uint32_t w0, w1, w2, w3;
                     if constexpr (OUT_BF16) {
-                        __nv_bfloat162 *p = reinterpret_cast<__nv_bfloat162 *>(&w);
-#pragma unroll
-                        for (int j = 0; j < 4; j++)
-                            p[j] = __floats2bfloat162_rn(acc[ch * CPC + 8 * u + 2 * j], acc[ch * CPC + 8 * u + 2 * j + 1]);
+                        const int p = (ch * CPC + 8 * u) >> 1;     // first float2 of the unit
+                        __nv_bfloat162 b0 = __floats2bfloat162_rn(acc2[p].x, acc2[p].y);
+                        __nv_bfloat162 b1 = __floats2bfloat162_rn(acc2[p + 1].x, acc2[p + 1].y);
+                        __nv_bfloat162 b2 = __floats2bfloat162_rn(acc2[p + 2].x, acc2[p + 2].y);
+                        __nv_bfloat162 b3 = __floats2bfloat162_rn(acc2[p + 3].x, acc2[p + 3].y);
+                        w0 = *reinterpret_cast<uint32_t *>(&b0); w1 = *reinterpret_cast<uint32_t *>(&b1);
+                        w2 = *reinterpret_cast<uint32_t *>(&b2); w3 = *reinterpret_cast<uint32_t *>(&b3);
                     } else {
-                        w = make_uint4(__float_as_uint(acc[ch * CPC + 4 * u]), __float_as_uint(acc[ch * CPC + 4 * u + 1]),
-                                       __float_as_uint(acc[ch * CPC + 4 * u + 2]), __float_as_uint(acc[ch * CPC + 4 * u + 3]));
+                        const int p = (ch * CPC + 4 * u) >> 1;
+                        w0 = __float_as_uint(acc2[p].x); w1 = __float_as_uint(acc2[p].y);
+                        w2 = __float_as_uint(acc2[p + 1].x); w3 = __float_as_uint(acc2[p + 1].y);
                     }
-                    *reinterpret_cast<uint4 *>(stg + lane * 128 + ((u ^ (lane & 7)) * 16)) = w;
+                    const uint32_t dst = stg_s + lane * 128 + ((u ^ (lane & 7)) * 16);
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" :: "r"(dst), "r"(w0), "r"(w1), "r"(w2),
+                                 "r"(w3) : "memory");
                 }
                 ptx::fence_async_smem();
                 __syncwarp();
