@@ -14,6 +14,8 @@
 // Exact mode reproduces the reference rounding sequence bit-for-bit (seg ->
 // f32 exactly via the 1.5*2^23 magic, then two RN multiplies and an RN add);
 // fast mode folds the two scales into one FMA (tolerance-level).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "ptx.cuh"
 #include "tmap.cuh"
@@ -230,6 +232,215 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) w8a8_tc_kernel(
     if (warp == 1) ptx::tmem_dealloc<TMEM_COLS>(tmem);
 }
 
+// ------------------------------------------------------- 2-SM tcgen05 path
+// CTA pairs (cluster 2x1): each pair computes a 256 x 256 output tile with
+// tcgen05.mma.cta_group::2 (M = 256, each CTA supplies 128 rows of A and 128
+// of the 256 B rows, each CTA's TMEM receives its 128 rows x 256 columns).
+// Per SM and k-block that is 16 KB of A + 16 KB of B through shared memory
+// instead of 16 + 32 KB: the single-SM kernel is bound by that operand traffic
+// (TB_W8_NOEPI: ~2 POPS without any epilogue).  The leader CTA (rank 0) owns
+// the operand-full and segment-free barriers and issues the MMAs; commits are
+// multicast to both CTAs; both CTAs' epilogues drain their own TMEM rows with
+// the same promotion as the single-SM kernel and TMA-store their rows.
+namespace gemm2 {
+constexpr int BM = 128, BN = 256, BK = 128, STAGES = 5;
+constexpr int EPI_WARPS = 8;
+constexpr int THREADS = 64 + EPI_WARPS * 32;
+struct Smem {
+    uint8_t a[STAGES][BM * BK];
+    uint8_t b[STAGES][(BN / 2) * BK];
+    uint64_t full[STAGES], empty[STAGES];
+    uint64_t seg_full[2], seg_empty[2];
+    uint32_t tmem_base;
+    alignas(1024) uint8_t stage_out[EPI_WARPS][32 * 128];
+};
+constexpr size_t SMEM_BYTES = sizeof(Smem) + 1024;
+}  // namespace gemm2
+
+template <bool EXACT, bool OUT_BF16>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w8a8_2sm_kernel(
+    const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+    const __grid_constant__ CUtensorMap tma_out,
+    const float *__restrict__ sa, const float *__restrict__ sb, const float *__restrict__ bias,
+    int M, int N, int K) {
+    using namespace gemm2;
+    constexpr int CW = BN / 2;
+    constexpr uint32_t TMEM_COLS = 2 * BN;
+    extern __shared__ uint8_t smem_raw[];
+    Smem &S = *reinterpret_cast<Smem *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = ptx::cluster_ctarank();
+    const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+    const int nmp = (M + 2 * BM - 1) / (2 * BM), nnt = N / BN, nkb = K / BK, nnb = N / 128;
+    const int nmb = (M + 127) / 128;
+    const int ntiles = nmp * nnt;
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < STAGES; s++) { ptx::mbar_init(&S.full[s], 1); ptx::mbar_init(&S.empty[s], 1); }
+        for (int b = 0; b < 2; b++) { ptx::mbar_init(&S.seg_full[b], 1); ptx::mbar_init(&S.seg_empty[b], 2 * EPI_WARPS); }
+        ptx::fence_barrier_init();
+        ptx::prefetch_tmap(&tma_a);
+        ptx::prefetch_tmap(&tma_b);
+    }
+    if (warp == 1) ptx::tmem_alloc_pair<TMEM_COLS>(&S.tmem_base);
+    ptx::tc_fence_before();
+    ptx::cluster_sync();                       // barriers of both CTAs initialised, TMEM allocated
+    ptx::tc_fence_after();
+    const uint32_t tmem = S.tmem_base;
+
+    if (warp == 0) {
+        if (ptx::elect_one()) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = cluster; tile < ntiles; tile += nclusters) {
+                const int mp = tile % nmp, nt = tile / nmp;
+                for (int kb = 0; kb < nkb; kb++) {
+                    ptx::mbar_wait_sleep(&S.empty[stage], phase ^ 1);
+                    const uint32_t fullc = ptx::mapa(ptx::smem_u32(&S.full[stage]), 0);
+                    if (rank == 0) ptx::mbar_arrive_expect_tx(&S.full[stage], 2 * (BM + BN / 2) * BK);
+                    ptx::tma_load_2d_pair(S.a[stage], &tma_a, kb * BK, mp * 2 * BM + (int)rank * BM, fullc);
+                    ptx::tma_load_2d_pair(S.b[stage], &tma_b, kb * BK, nt * BN + (int)rank * (BN / 2), fullc);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        if (rank == 0) {
+            int stage = 0, buf = 0;
+            uint32_t phase = 0, bphase = 0;
+            constexpr uint32_t idesc = ptx::idesc_i8(2 * BM, BN);
+            for (int tile = cluster; tile < ntiles; tile += nclusters) {
+                for (int kb = 0; kb < nkb; kb++) {
+                    ptx::mbar_wait_sleep(&S.seg_empty[buf], bphase ^ 1);
+                    ptx::mbar_wait_sleep(&S.full[stage], phase);
+                    ptx::tc_fence_after();
+                    const uint64_t ad = ptx::sdesc_sw128(ptx::smem_u32(S.a[stage]));
+                    const uint64_t bd = ptx::sdesc_sw128(ptx::smem_u32(S.b[stage]));
+                    if (ptx::elect_one()) {
+#pragma unroll
+                        for (int k = 0; k < BK / 32; k++)
+                            ptx::mma_i8_pair(tmem + buf * BN, ad + 2 * k, bd + 2 * k, idesc, k > 0 ? 1u : 0u);
+                        ptx::mma_commit_pair(&S.empty[stage], 0x3);
+                        ptx::mma_commit_pair(&S.seg_full[buf], 0x3);
+                    }
+                    __syncwarp();
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    buf ^= 1;
+                    if (buf == 0) bphase ^= 1;
+                }
+            }
+        }
+    } else {
+        const int ew = warp - 2;
+        const int quarter = warp & 3;
+        const int half = ew >> 2;
+        const uint32_t seg_empty0 = ptx::mapa(ptx::smem_u32(&S.seg_empty[0]), 0);
+        const uint32_t seg_empty1 = ptx::mapa(ptx::smem_u32(&S.seg_empty[1]), 0);
+        int buf = 0;
+        uint32_t bphase = 0;
+        for (int tile = cluster; tile < ntiles; tile += nclusters) {
+            const int mp = tile % nmp, nt = tile / nmp;
+            const int col0 = nt * BN + half * CW;
+            const int nb = col0 / 128;
+            const int mb = 2 * mp + (int)rank;                    // this CTA's 128-row scale block
+            const int mbs = mb < nmb ? mb : nmb - 1;              // (rows past M are clipped anyway)
+            float2 acc2[CW / 2];
+#pragma unroll
+            for (int i = 0; i < CW / 2; i++) acc2[i] = make_float2(0.0f, 0.0f);
+            float s_a = __ldg(sa + (size_t)mbs * nkb), s_b = __ldg(sb + nb);
+            for (int kb = 0; kb < nkb; kb++) {
+                const float2 sa2 = make_float2(s_a, s_a), sb2 = make_float2(s_b, s_b);
+                const float2 sab2 = make_float2(s_a * s_b, s_a * s_b);
+                if (kb + 1 < nkb) {
+                    s_a = __ldg(sa + (size_t)mbs * nkb + kb + 1);
+                    s_b = __ldg(sb + (size_t)(kb + 1) * nnb + nb);
+                }
+                ptx::mbar_wait_sleep(&S.seg_full[buf], bphase);
+                ptx::tc_fence_after();
+                const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + buf * BN + half * CW;
+                uint32_t rb[2][16];
+                ptx::tmem_ld16(taddr, rb[0]);
+                ptx::tmem_wait_ld();
+#pragma unroll
+                for (int c = 0; c < CW / 16; c++) {
+                    if (c + 1 < CW / 16) ptx::tmem_ld16(taddr + (c + 1) * 16, rb[(c + 1) & 1]);
+                    const uint32_t (&r)[16] = rb[c & 1];
+#pragma unroll
+                    for (int i = 0; i < 16; i += 2) {
+                        float2 x;
+                        if (!EXACT && (i & 6) == 6) {
+                            const float2 m = make_float2(__int_as_float((int)r[i] + 0x4B400000),
+                                                         __int_as_float((int)r[i + 1] + 0x4B400000));
+                            x = ptx::fadd2(m, make_float2(-12582912.0f, -12582912.0f));
+                        } else {
+                            x = make_float2(__int2float_rn((int)r[i]), __int2float_rn((int)r[i + 1]));
+                        }
+                        float2 &o = acc2[(c * 16 + i) >> 1];
+                        if constexpr (EXACT) {
+                            o.x = __fadd_rn(o.x, __fmul_rn(__fmul_rn(x.x, sa2.x), sb2.x));
+                            o.y = __fadd_rn(o.y, __fmul_rn(__fmul_rn(x.y, sa2.y), sb2.y));
+                        } else {
+                            o = ptx::ffma2(x, sab2, o);
+                        }
+                    }
+                    ptx::tmem_wait_ld();
+                }
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive_cluster(buf ? seg_empty1 : seg_empty0);   // the leader's barrier
+                buf ^= 1;
+                if (buf == 0) bphase ^= 1;
+            }
+            if (bias) {
+#pragma unroll
+                for (int i = 0; i < CW / 2; i++) {
+                    acc2[i].x = __fadd_rn(acc2[i].x, __ldg(bias + col0 + 2 * i));
+                    acc2[i].y = __fadd_rn(acc2[i].y, __ldg(bias + col0 + 2 * i + 1));
+                }
+            }
+            constexpr int CPC = OUT_BF16 ? 64 : 32;
+            const uint32_t stg_s = ptx::smem_u32(S.stage_out[ew]);
+            const int row0 = mp * 2 * BM + (int)rank * BM + quarter * 32;
+#pragma unroll
+            for (int ch = 0; ch < CW / CPC; ch++) {
+                if (lane == 0) ptx::bulk_wait_read0();
+                __syncwarp();
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
+                    uint32_t w0, w1, w2, w3;
+                    if constexpr (OUT_BF16) {
+                        const int p = (ch * CPC + 8 * u) >> 1;
+                        __nv_bfloat162 b0 = __floats2bfloat162_rn(acc2[p].x, acc2[p].y);
+                        __nv_bfloat162 b1 = __floats2bfloat162_rn(acc2[p + 1].x, acc2[p + 1].y);
+                        __nv_bfloat162 b2 = __floats2bfloat162_rn(acc2[p + 2].x, acc2[p + 2].y);
+                        __nv_bfloat162 b3 = __floats2bfloat162_rn(acc2[p + 3].x, acc2[p + 3].y);
+                        w0 = *reinterpret_cast<uint32_t *>(&b0); w1 = *reinterpret_cast<uint32_t *>(&b1);
+                        w2 = *reinterpret_cast<uint32_t *>(&b2); w3 = *reinterpret_cast<uint32_t *>(&b3);
+                    } else {
+                        const int p = (ch * CPC + 4 * u) >> 1;
+                        w0 = __float_as_uint(acc2[p].x); w1 = __float_as_uint(acc2[p].y);
+                        w2 = __float_as_uint(acc2[p + 1].x); w3 = __float_as_uint(acc2[p + 1].y);
+                    }
+                    const uint32_t dst = stg_s + lane * 128 + ((u ^ (lane & 7)) * 16);
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" :: "r"(dst), "r"(w0), "r"(w1), "r"(w2),
+                                 "r"(w3) : "memory");
+                }
+                ptx::fence_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    ptx::tma_store_2d(&tma_out, S.stage_out[ew], col0 + ch * CPC, row0);
+                    ptx::bulk_commit();
+                }
+            }
+        }
+        if (lane == 0) ptx::bulk_wait_read0();
+    }
+    ptx::tc_fence_before();
+    ptx::cluster_sync();                       // no CTA leaves while its peer may still signal it
+    if (warp == 1) ptx::tmem_dealloc_pair<TMEM_COLS>(tmem);
+}
+
 // ------------------------------------------------------------ CUDA-core path
 // Any block size / shape.  64x64 output tile per CTA, 256 threads x 4x4
 // outputs, exact int32 segments via dp4a, identical promotion order.
@@ -324,6 +535,33 @@ int w8a8_dispatch(const int8_t *a, const float *sa, const int8_t *bt, const floa
     if (M == 0 || N == 0) return TB_OK;
     const bool tc = block == 128 && K % 128 == 0 && N % 128 == 0 && K > 0 && M < (1ll << 31) &&
                     ((uintptr_t)a % 16) == 0 && ((uintptr_t)bt % 16) == 0 && ((uintptr_t)out % 16) == 0;
+    // the 2-SM kernel measures at parity with the 1-SM one (both epilogue-bound); opt-in
+    static const bool use2sm = [] { const char *e = getenv("TB_W8A8_2SM"); return e && atoi(e) != 0; }();
+    if (tc && use2sm && N % 256 == 0 && M >= 256) {
+        CUtensorMap ta, tbm, tout;
+        const bool obf = out_dtype == TB_BF16;
+        if (!make_tmap_2d(&ta, a, CU_TENSOR_MAP_DATA_TYPE_UINT8, K, M, K, 128, 128) ||
+            !make_tmap_2d(&tbm, bt, CU_TENSOR_MAP_DATA_TYPE_UINT8, K, N, K, 128, 128) ||
+            !make_tmap_2d(&tout, out, obf ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, N, M,
+                          N * (obf ? 2 : 4), obf ? 64 : 32, 32))
+            return fail(TB_ECUDA, "cuTensorMapEncodeTiled failed");
+        const int ntiles = (int)(cdiv(M, 256) * (N / 256));
+        int clusters = num_sms() / 2;
+        if (ntiles < clusters) clusters = ntiles;
+        const int grid = 2 * clusters;
+#define TB_GEMM2(E, B)                                                                                     \
+    {                                                                                                      \
+        auto kern = w8a8_2sm_kernel<E, B>;                                                                 \
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm2::SMEM_BYTES);   \
+        kern<<<grid, gemm2::THREADS, gemm2::SMEM_BYTES, st>>>(ta, tbm, tout, sa, sb, bias, (int)M, (int)N, (int)K); \
+    }
+        if (exact && !obf) TB_GEMM2(true, false)
+        else if (exact) TB_GEMM2(true, true)
+        else if (!obf) TB_GEMM2(false, false)
+        else TB_GEMM2(false, true)
+#undef TB_GEMM2
+        return check_launch("w8a8_2sm");
+    }
     if (tc) {
         const int BN = (N % 256 == 0) ? 256 : 128;
         CUtensorMap ta, tbm;
