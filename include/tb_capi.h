@@ -199,6 +199,20 @@ int tb_gemm_bf16_batched(const void *A, const void *B, void *C, int64_t H, int64
 int tb_linear_kv_part(const void *k, const void *v, int64_t H, int64_t L, int64_t d, int64_t kv_block,
                       int64_t dx, void *kv_part, void *stream);
 
+/* quantize_blockwise (block 128) of a logical [rows, cols] matrix stored as
+ * cols/128 planes [rows, 128] (a head-major attention output [H, L, 128]);
+ * codes [rows, cols] row-major, scales [ceil(rows/128), cols/128]. */
+int tb_quantize_blockwise_planar(const void *x, int dtype, int64_t rows, int64_t cols, int8_t *q, float *scales,
+                                 void *stream);
+
+/* tb_w8a8_gemm_fast with epilogue options for the DiT block:
+ * plane > 0 (divides 128 and N, bf16 out): the output is stored as N/plane
+ * planes [M, plane] -- the qkv projection lands head-major [3, H, M, head_dim];
+ * act == 1: GELU (tanh form, sampler.py:55-58) applied to the result. */
+int tb_w8a8_gemm_fast_ex(const int8_t *a, const float *sa, const int8_t *bt, const float *sb, const float *bias,
+                         int64_t M, int64_t N, int64_t K, int64_t block, void *out, int out_dtype, int64_t plane,
+                         int act, void *stream);
+
 /* Fast-mode W8A8: identical operands, the two block scales folded into one
  * FMA per element (tolerance-level, not bit-exact); used by the DiT step. */
 int tb_w8a8_gemm_fast(const int8_t *a, const float *sa, const int8_t *bt, const float *sb,

@@ -46,7 +46,10 @@ __global__ void __launch_bounds__(256) quantize_blockwise_kernel(
 // Fast path: block == 128, cols % 8 == 0.  Each thread owns 8 consecutive
 // columns of a row (16 B of bf16 / 32 B of f32 loaded as vectors), codes
 // stored as one 8-byte word.
-template <typename T>
+// PLANAR: x is stored as cols/128 planes [rows, 128] (a head-major attention
+// output [H, L, head_dim]); codes and scales are written for the logical
+// [rows, cols] matrix (the out-projection's A operand).
+template <typename T, bool PLANAR = false>
 __global__ void __launch_bounds__(256) quantize_blockwise128_kernel(
     const T *__restrict__ x, int64_t rows, int64_t cols, int64_t nbc,
     int8_t *__restrict__ q, float *__restrict__ scales, int32_t *__restrict__ nonfinite) {
@@ -64,7 +67,8 @@ __global__ void __launch_bounds__(256) quantize_blockwise128_kernel(
     for (int p = 0; p < 8; p++) {
         int r = rsub + p * 16;
         if (col_ok && r < nr) {
-            const T *src = x + (r0 + r) * cols + c0 + lane16 * 8;
+            const T *src = PLANAR ? x + (c0 / 128) * rows * 128 + (r0 + r) * 128 + lane16 * 8
+                                  : x + (r0 + r) * cols + c0 + lane16 * 8;
             if constexpr (sizeof(T) == 2) {
                 uint4 raw = *reinterpret_cast<const uint4 *>(src);
                 const __nv_bfloat16 *b = reinterpret_cast<const __nv_bfloat16 *>(&raw);
@@ -88,14 +92,19 @@ __global__ void __launch_bounds__(256) quantize_blockwise128_kernel(
     const float s = quant_scale(am);
     if (threadIdx.x == 0) scales[bi * nbc + bj] = s;
     const float safe = (s == 0.0f) ? 1.0f : s;
+    const float inv = __frcp_rn(safe);
+    const bool exact = !(safe >= 1.17549435e-38f && inv <= 3.0e38f);   // subnormal scale: exact division
 #pragma unroll
     for (int p = 0; p < 8; p++) {
         int r = rsub + p * 16;
         if (col_ok && r < nr) {
             uint32_t w[2] = {0, 0};
 #pragma unroll
-            for (int j = 0; j < 8; j++)
-                w[j >> 2] |= (uint32_t)(uint8_t)quant_code(v[p][j], safe) << ((j & 3) * 8);
+            for (int j = 0; j < 8; j++) {
+                const uint32_t c8 = exact ? (uint32_t)(uint8_t)quant_code(v[p][j], safe)
+                                          : quant_code_fast(v[p][j], safe, inv);    // bit-identical
+                w[j >> 2] |= c8 << ((j & 3) * 8);
+            }
             *reinterpret_cast<uint2 *>(q + (r0 + r) * cols + c0 + lane16 * 8) = make_uint2(w[0], w[1]);
         }
     }
@@ -669,4 +678,21 @@ extern "C" int tb_transpose_v(const void *v, int dtype, int64_t H, int64_t L, in
     if (dtype == TB_F32) transpose_v_kernel<float><<<grid, dim3(32, 8), 0, st>>>((const float *)v, L, d, l_pad, (__nv_bfloat16 *)vt);
     else transpose_v_kernel<__nv_bfloat16><<<grid, dim3(32, 8), 0, st>>>((const __nv_bfloat16 *)v, L, d, l_pad, (__nv_bfloat16 *)vt);
     return check_launch("transpose_v");
+}
+
+extern "C" int tb_quantize_blockwise_planar(const void *x, int dtype, int64_t rows, int64_t cols, int8_t *q,
+                                            float *scales, void *stream) {
+    TB_REQUIRE(dtype == TB_F32 || dtype == TB_BF16, "dtype must be f32 or bf16");
+    TB_REQUIRE(cols % 128 == 0 && ((uintptr_t)x % 16) == 0, "planar input needs cols % 128 == 0, 16-B aligned");
+    if (rows == 0 || cols == 0) return TB_OK;
+    const int64_t nbr = cdiv(rows, 128), nbc = cols / 128;
+    TB_REQUIRE(nbr < 65536, "too many row blocks");
+    dim3 grid((unsigned)nbc, (unsigned)nbr);
+    cudaStream_t st = as_stream(stream);
+    if (dtype == TB_F32)
+        quantize_blockwise128_kernel<float, true><<<grid, 256, 0, st>>>((const float *)x, rows, cols, nbc, q, scales, nullptr);
+    else
+        quantize_blockwise128_kernel<__nv_bfloat16, true><<<grid, 256, 0, st>>>((const __nv_bfloat16 *)x, rows, cols, nbc, q,
+                                                                                scales, nullptr);
+    return check_launch("quantize_blockwise_planar");
 }

@@ -43,12 +43,22 @@ constexpr size_t smem_bytes() { return sizeof(Smem<BN>) + 1024; }
 // BN = 128 or 256 (tile 128 x BN, s32 segment buffers 2 x BN TMEM columns).
 // Each epilogue warp owns 32 rows (its TMEM lane quarter) x BN/2 columns;
 // a BN/2 column span never crosses a 128-column scale block.
+// plane > 0: the output is stored as N/plane planes [M, plane] (plane | 128):
+// a qkv projection lands head-major ([3, H, M, head_dim]) for the attention
+// with no permute.  act == 1: GELU (tanh form, sampler.py:55-58) on the result.
+__device__ __forceinline__ float gelu_tanh(float x) {
+    float t;
+    const float u = 0.7978845608028654f * fmaf(0.044715f * x, x * x, x);
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(u));
+    return 0.5f * x * (1.0f + t);
+}
+
 template <int BN, bool EXACT, bool OUT_BF16>
 __global__ void __launch_bounds__(gemm::THREADS, 1) w8a8_tc_kernel(
     const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
     const __grid_constant__ CUtensorMap tma_out,
     const float *__restrict__ sa, const float *__restrict__ sb, const float *__restrict__ bias,
-    void *__restrict__ out, int M, int N, int K) {
+    void *__restrict__ out, int M, int N, int K, int plane, int act) {
     using namespace gemm;
     constexpr int CW = BN / 2;
     constexpr uint32_t TMEM_COLS = 2 * BN;
@@ -189,6 +199,10 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) w8a8_tc_kernel(
             }
             // stores: each warp stages 32 rows x 128 B (32 f32 or 64 bf16 columns) in a
             // 128B-swizzled smem chunk and one lane TMA-stores it (rows >= M are clipped)
+            if (act == 1) {
+#pragma unroll
+                for (int i = 0; i < CW / 2; i++) { acc2[i].x = gelu_tanh(acc2[i].x); acc2[i].y = gelu_tanh(acc2[i].y); }
+            }
             constexpr int CPC = OUT_BF16 ? 64 : 32;             // columns per chunk
             uint8_t *stg = S.stage_out[ew];
             const uint32_t stg_s = ptx::smem_u32(stg);
@@ -220,7 +234,9 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) w8a8_tc_kernel(
                 ptx::fence_async_smem();
                 __syncwarp();
                 if (lane == 0) {
-                    ptx::tma_store_2d(&tma_out, stg, col0 + ch * CPC, row0);
+                    const int c = col0 + ch * CPC;
+                    if (plane) ptx::tma_store_3d(&tma_out, stg, c % plane, row0, c / plane);
+                    else ptx::tma_store_2d(&tma_out, stg, c, row0);
                     ptx::bulk_commit();
                 }
             }
@@ -528,7 +544,10 @@ int num_sms() {
 
 int w8a8_dispatch(const int8_t *a, const float *sa, const int8_t *bt, const float *sb, const float *bias,
                   int64_t M, int64_t N, int64_t K, int64_t block, void *out, int out_dtype, int exact,
-                  cudaStream_t st) {
+                  cudaStream_t st, int64_t plane = 0, int act = 0) {
+    TB_REQUIRE(plane == 0 || (plane > 0 && 128 % plane == 0 && N % plane == 0 && out_dtype == TB_BF16 && plane >= 64),
+               "plane must divide 128 and N, be >= 64, with bf16 output");
+    TB_REQUIRE(act == 0 || act == 1, "act must be 0 (none) or 1 (gelu-tanh)");
     TB_REQUIRE(block >= 1, "block must be >= 1");
     TB_REQUIRE(block <= 1040, "block edge > 1040 (f32-exact segment bound) unsupported");
     TB_REQUIRE(out_dtype == TB_F32 || out_dtype == TB_BF16, "out dtype must be f32 or bf16");
@@ -537,7 +556,7 @@ int w8a8_dispatch(const int8_t *a, const float *sa, const int8_t *bt, const floa
                     ((uintptr_t)a % 16) == 0 && ((uintptr_t)bt % 16) == 0 && ((uintptr_t)out % 16) == 0;
     // the 2-SM kernel measures at parity with the 1-SM one (both epilogue-bound); opt-in
     static const bool use2sm = [] { const char *e = getenv("TB_W8A8_2SM"); return e && atoi(e) != 0; }();
-    if (tc && use2sm && N % 256 == 0 && M >= 256) {
+    if (tc && use2sm && N % 256 == 0 && M >= 256 && plane == 0 && act == 0) {
         CUtensorMap ta, tbm, tout;
         const bool obf = out_dtype == TB_BF16;
         if (!make_tmap_2d(&ta, a, CU_TENSOR_MAP_DATA_TYPE_UINT8, K, M, K, 128, 128) ||
@@ -567,18 +586,23 @@ int w8a8_dispatch(const int8_t *a, const float *sa, const int8_t *bt, const floa
         CUtensorMap ta, tbm;
         CUtensorMap tout;
         const bool obf = out_dtype == TB_BF16;
-        if (!make_tmap_2d(&ta, a, CU_TENSOR_MAP_DATA_TYPE_UINT8, K, M, K, 128, 128) ||
-            !make_tmap_2d(&tbm, bt, CU_TENSOR_MAP_DATA_TYPE_UINT8, K, N, K, 128, BN) ||
-            !make_tmap_2d(&tout, out, obf ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, N, M,
-                          N * (obf ? 2 : 4), obf ? 64 : 32, 32))
-            return fail(TB_ECUDA, "cuTensorMapEncodeTiled failed");
+        bool okm = make_tmap_2d(&ta, a, CU_TENSOR_MAP_DATA_TYPE_UINT8, K, M, K, 128, 128) &&
+                   make_tmap_2d(&tbm, bt, CU_TENSOR_MAP_DATA_TYPE_UINT8, K, N, K, 128, BN);
+        if (plane)       // planes [N/plane][M][plane] (bf16), box 64 columns x 32 rows
+            okm = okm && make_tmap_3d(&tout, out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, plane, M, N / plane, plane * 2,
+                                      M * plane * 2, 64, 32, 1);
+        else
+            okm = okm && make_tmap_2d(&tout, out, obf ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                      N, M, N * (obf ? 2 : 4), obf ? 64 : 32, 32);
+        if (!okm) return fail(TB_ECUDA, "cuTensorMapEncodeTiled failed");
         const int ntiles = (int)(cdiv(M, 128) * (N / BN));
         const int grid = ntiles < num_sms() ? ntiles : num_sms();
 #define TB_GEMM_LAUNCH(BNV, E, B)                                                                          \
     {                                                                                                      \
         auto kern = w8a8_tc_kernel<BNV, E, B>;                                                             \
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm::smem_bytes<BNV>()); \
-        kern<<<grid, gemm::THREADS, gemm::smem_bytes<BNV>(), st>>>(ta, tbm, tout, sa, sb, bias, out, (int)M, (int)N, (int)K); \
+        kern<<<grid, gemm::THREADS, gemm::smem_bytes<BNV>(), st>>>(ta, tbm, tout, sa, sb, bias, out, (int)M, (int)N, (int)K, \
+                                                                  (int)plane, act);                                        \
     }
 #define TB_GEMM_BN(BNV)                                                                                    \
         if (exact && out_dtype == TB_F32) TB_GEMM_LAUNCH(BNV, true, false)                                 \
@@ -590,6 +614,7 @@ int w8a8_dispatch(const int8_t *a, const float *sa, const int8_t *bt, const floa
 #undef TB_GEMM_LAUNCH
         return check_launch("w8a8_tc");
     }
+    TB_REQUIRE(plane == 0 && act == 0, "planar output / fused activation need the tensor-core path");
     dim3 grid((unsigned)cdiv(N, 64), (unsigned)cdiv(M, 64));
     w8a8_simt_kernel<<<grid, 256, 0, st>>>(a, sa, bt, sb, bias, M, N, K, block, exact, out, out_dtype == TB_BF16);
     return check_launch("w8a8_simt");
@@ -616,4 +641,10 @@ extern "C" int tb_quantized_linear(const void *x, int x_dtype, const int8_t *bt,
     int rc = tb_quantize_blockwise(x, x_dtype, M, K, block, xq_ws, xs_ws, nullptr, stream);
     if (rc) return rc;
     return tb_w8a8_gemm(xq_ws, xs_ws, bt, sb, bias, M, N, K, block, out, out_dtype, stream);
+}
+
+extern "C" int tb_w8a8_gemm_fast_ex(const int8_t *a, const float *sa, const int8_t *bt, const float *sb,
+                                    const float *bias, int64_t M, int64_t N, int64_t K, int64_t block, void *out,
+                                    int out_dtype, int64_t plane, int act, void *stream) {
+    return w8a8_dispatch(a, sa, bt, sb, bias, M, N, K, block, out, out_dtype, 0, as_stream(stream), plane, act);
 }

@@ -99,23 +99,28 @@ def block_forward(x: torch.Tensor, sigma: float, w: DeviceLayer, heads: int, sla
     hd = dim // heads
     x = x + float(sigma) * w.sigma_emb
     a = ops.rmsnorm(x, w.rms_gain)
-    qkv = _linear(a, w.qkv)                                   # [L_p, 3*dim] bf16
-    q, k, v = (t.view(Lp, heads, hd) for t in qkv.split(dim, dim=1))
 
     def attn(qh, kh, vh):
         return ops.sla_attention(qh, kh, vh, sla["q_block"], sla["kv_block"], sla["topk_ratio"],
                                  sla.get("linear_mix", 1.0), True, out_dtype=torch.bfloat16)
 
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        qkv = _linear(a, w.qkv)                               # [L_p, 3*dim] bf16
+        q, k, v = (t.view(Lp, heads, hd) for t in qkv.split(dim, dim=1))
         o = ulysses.ulysses_sla_attention(q.contiguous(), k.contiguous(), v.contiguous(), L_global, attn, group)
+        o = o.reshape(Lp, dim)
+        oq, osc = ops.quantize_blockwise(o.contiguous(), 128, check_finite=False)
     else:
-        o = attn(q.permute(1, 0, 2).contiguous(), k.permute(1, 0, 2).contiguous(),
-                 v.permute(1, 0, 2).contiguous()).permute(1, 0, 2)
-    o = o.reshape(Lp, dim)
-    x = x + _linear(o.contiguous(), w.out_proj, torch.float32)
+        # qkv lands head-major [3H, L, hd] straight from the GEMM epilogue (no permute);
+        # the out-projection quantizes the head-major attention output in place
+        aq, asc = ops.quantize_blockwise(a, 128, check_finite=False)
+        qkv = ops.w8a8_gemm_ex(aq, asc, w.qkv.bt, w.qkv.scales, 128, None, torch.bfloat16, plane=hd)
+        o = attn(qkv[:heads], qkv[heads:2 * heads], qkv[2 * heads:])           # [H, L, hd]
+        oq, osc = ops.quantize_blockwise_planar(o)
+    x = x + ops.w8a8_gemm(oq, osc, w.out_proj.bt, w.out_proj.scales, 128, None, torch.float32, exact=False)
     b = ops.layernorm(x, w.ln_gain, w.ln_offset)
-    h1 = _linear(b, w.mlp_in)
-    h1 = torch.nn.functional.gelu(h1, approximate="tanh")     # sampler.py:55-58
+    bq, bsc = ops.quantize_blockwise(b, 128, check_finite=False)
+    h1 = ops.w8a8_gemm_ex(bq, bsc, w.mlp_in.bt, w.mlp_in.scales, 128, None, torch.bfloat16, act=1)  # GELU fused
     return x + _linear(h1, w.mlp_out, torch.float32)
 
 

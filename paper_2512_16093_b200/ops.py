@@ -50,6 +50,19 @@ def quantize_blockwise(x: torch.Tensor, block: int = 128, check_finite: bool = T
     return q, s
 
 
+def quantize_blockwise_planar(x: torch.Tensor):
+    """quantize_blockwise (block 128) of the logical [L, P*128] matrix stored as
+    P planes [L, 128] (a head-major attention output) -> (codes [L, P*128], scales)."""
+    P, r, w = x.shape
+    if w != 128:
+        raise ValueError("planes must be 128 wide")
+    c = P * 128
+    q = _empty((r, c), torch.int8, x)
+    s = _empty((cdiv(r, 128), P), torch.float32, x)
+    call("tb_quantize_blockwise_planar", ptr(x.contiguous()), dtype_code(x), r, c, ptr(q), ptr(s), stream_ptr())
+    return q, s
+
+
 def dequantize_blockwise(q: torch.Tensor, scales: torch.Tensor, block: int):
     r, c = q.shape
     out = _empty((r, c), torch.float32, q)
@@ -75,6 +88,22 @@ def w8a8_gemm(a_q, a_s, bt_q, b_s, block: int = 128, bias=None, out_dtype=torch.
     call(fn, ptr(a_q.contiguous()), ptr(a_s.contiguous()), ptr(bt_q.contiguous()), ptr(b_s.contiguous()),
          ptr(None if bias is None else bias.float().contiguous()), M, N, K, block, ptr(out),
          TB_BF16 if out_dtype == torch.bfloat16 else TB_F32, stream_ptr())
+    return out
+
+
+def w8a8_gemm_ex(a_q, a_s, bt_q, b_s, block: int = 128, bias=None, out_dtype=torch.bfloat16, plane: int = 0,
+                 act: int = 0):
+    """Fast-mode W8A8 with epilogue options: plane > 0 stores the output as
+    N/plane planes [M, plane] (qkv -> head-major [3, H, M, head_dim]); act=1
+    applies GELU-tanh."""
+    M, K = a_q.shape
+    N = bt_q.shape[0]
+    if bt_q.shape[1] != K:
+        raise ValueError(f"inner dims differ: {K} vs {bt_q.shape[1]}")
+    out = _empty((N // plane, M, plane) if plane else (M, N), out_dtype, a_q)
+    call("tb_w8a8_gemm_fast_ex", ptr(a_q.contiguous()), ptr(a_s.contiguous()), ptr(bt_q.contiguous()),
+         ptr(b_s.contiguous()), ptr(None if bias is None else bias.float().contiguous()), M, N, K, block, ptr(out),
+         TB_BF16 if out_dtype == torch.bfloat16 else TB_F32, plane, act, stream_ptr())
     return out
 
 

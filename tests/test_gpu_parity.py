@@ -284,3 +284,31 @@ def test_sla_attention_host_pipeline_matches_device(tb):
     got = tb.sla_attention_host(hq, hk, hv, 128, 64, 0.1, 1.0, chunk_heads=2)
     torch.cuda.synchronize()
     assert torch.equal(got, want)
+
+
+def test_w8a8_planar_output_and_gelu_epilogue(tb):
+    """tb_w8a8_gemm_fast_ex: the planar (head-major) store equals the row-major
+    result split into 128-column planes, and the fused GELU equals GELU-tanh of
+    the plain result."""
+    M, K, N = 640, 512, 768
+    g = torch.Generator(device="cuda").manual_seed(5)
+    xq = torch.randint(-127, 128, (M, K), dtype=torch.int8, device="cuda", generator=g)
+    xs = torch.rand((M // 128, K // 128), device="cuda", generator=g) * 0.01
+    bt = torch.randint(-127, 128, (N, K), dtype=torch.int8, device="cuda", generator=g)
+    bs = torch.rand((K // 128, N // 128), device="cuda", generator=g) * 0.01
+    ref = tb.w8a8_gemm(xq, xs, bt, bs, 128, None, torch.bfloat16, exact=False)
+    planes = tb.w8a8_gemm_ex(xq, xs, bt, bs, 128, None, torch.bfloat16, plane=128)
+    assert torch.equal(planes, ref.view(M, N // 128, 128).permute(1, 0, 2))
+    ref32 = tb.w8a8_gemm(xq, xs, bt, bs, 128, None, torch.float32, exact=False)
+    gel = tb.w8a8_gemm_ex(xq, xs, bt, bs, 128, None, torch.bfloat16, act=1).float()
+    want = torch.nn.functional.gelu(ref32, approximate="tanh")
+    assert torch.allclose(gel, want, rtol=2e-2, atol=2e-2)
+
+
+def test_quantize_blockwise_planar_matches_row_major(tb):
+    H, L = 6, 1000
+    g = torch.Generator(device="cuda").manual_seed(6)
+    o = torch.randn((H, L, 128), device="cuda", generator=g).to(torch.bfloat16)
+    q1, s1 = tb.quantize_blockwise_planar(o)
+    q2, s2 = tb.quantize_blockwise(o.permute(1, 0, 2).reshape(L, H * 128).contiguous(), 128, check_finite=False)
+    assert torch.equal(q1, q2) and torch.equal(s1, s2)
