@@ -199,6 +199,13 @@ int tb_gemm_bf16_batched(const void *A, const void *B, void *C, int64_t H, int64
 int tb_linear_kv_part(const void *k, const void *v, int64_t H, int64_t L, int64_t d, int64_t kv_block,
                       int64_t dx, void *kv_part, void *stream);
 
+/* DiT glue in one pass: s = x (+ y) (+ alpha * emb[cols]) -> sum_out (f32,
+ * optional, may alias x or y) and RMSNorm(s) * gain (layer_norm = 0) or
+ * LayerNorm(s) * gain + offset (layer_norm = 1) as bf16 norm_out
+ * (sampler.py:34-53 semantics, eps added inside the root). */
+int tb_add_norm(const float *x, const float *y, const float *emb, float alpha, const float *gain, const float *offset,
+                int64_t rows, int64_t cols, float eps, int layer_norm, float *sum_out, void *norm_out, void *stream);
+
 /* quantize_blockwise (block 128) of a logical [rows, cols] matrix stored as
  * cols/128 planes [rows, 128] (a head-major attention output [H, L, 128]);
  * codes [rows, cols] row-major, scales [ceil(rows/128), cols/128]. */

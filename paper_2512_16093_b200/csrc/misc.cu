@@ -172,6 +172,99 @@ __global__ void layernorm_kernel(const float *__restrict__ x, const float *__res
     for (int64_t c = lane; c < cols; c += 32) out[row * cols + c] = (xr[c] - mu) * inv * g[c] + b[c];
 }
 
+// DiT glue in one pass (dit.py): s = x (+ y) (+ alpha * emb), optionally
+// stored (f32), and its RMSNorm (MODE 0, sampler.py:34-44) or LayerNorm
+// (MODE 1, sampler.py:47-53) as bf16 for the next W8A8 projection.  One CTA
+// per row, 256 threads, each thread 4-float chunks kept in registers
+// (cols <= 256 * 4 * ADD_NORM_CHUNKS).
+constexpr int ADD_NORM_CHUNKS = 8;
+template <int MODE>
+__global__ void __launch_bounds__(256) add_norm_kernel(
+    const float *__restrict__ x, const float *__restrict__ y, const float *__restrict__ emb, float alpha,
+    const float *__restrict__ g, const float *__restrict__ b, int64_t cols, float eps, float *__restrict__ sum_out,
+    __nv_bfloat16 *__restrict__ norm_out) {
+    __shared__ float red[2][8];
+    const int64_t row = blockIdx.x;
+    const int nc4 = (int)(cols >> 2);
+    float4 v[ADD_NORM_CHUNKS];
+    float s1 = 0.0f, s2 = 0.0f;
+#pragma unroll
+    for (int i = 0; i < ADD_NORM_CHUNKS; i++) {
+        const int c4 = threadIdx.x + i * 256;
+        if (c4 < nc4) {
+            float4 a = reinterpret_cast<const float4 *>(x + row * cols)[c4];
+            if (y) {
+                const float4 t = reinterpret_cast<const float4 *>(y + row * cols)[c4];
+                a.x += t.x; a.y += t.y; a.z += t.z; a.w += t.w;
+            }
+            if (emb) {
+                const float4 e = reinterpret_cast<const float4 *>(emb)[c4];
+                a.x = fmaf(alpha, e.x, a.x); a.y = fmaf(alpha, e.y, a.y);
+                a.z = fmaf(alpha, e.z, a.z); a.w = fmaf(alpha, e.w, a.w);
+            }
+            if (sum_out) reinterpret_cast<float4 *>(sum_out + row * cols)[c4] = a;
+            v[i] = a;
+            s1 += (a.x + a.y) + (a.z + a.w);
+            s2 = fmaf(a.x, a.x, fmaf(a.y, a.y, fmaf(a.z, a.z, fmaf(a.w, a.w, s2))));
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) { red[0][w] = s1; red[1][w] = s2; }
+    __syncthreads();
+    s1 = 0.0f; s2 = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 8; i++) { s1 += red[0][i]; s2 += red[1][i]; }
+    const float n = (float)cols;
+    float mu = 0.0f, inv;
+    if (MODE == 0) {
+        inv = rsqrtf(s2 / n + eps);
+    } else {
+        // population variance in a second pass over the registers (no E[x^2] - mu^2 cancellation)
+        mu = s1 / n;
+        float s3 = 0.0f;
+#pragma unroll
+        for (int i = 0; i < ADD_NORM_CHUNKS; i++) {
+            if (threadIdx.x + i * 256 < nc4) {
+                const float dx = v[i].x - mu, dy = v[i].y - mu, dz = v[i].z - mu, dw = v[i].w - mu;
+                s3 = fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, fmaf(dw, dw, s3))));
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s3 += __shfl_xor_sync(0xffffffffu, s3, o);
+        __syncthreads();
+        if ((threadIdx.x & 31) == 0) red[0][w] = s3;
+        __syncthreads();
+        s3 = 0.0f;
+#pragma unroll
+        for (int i = 0; i < 8; i++) s3 += red[0][i];
+        inv = rsqrtf(s3 / n + eps);
+    }
+#pragma unroll
+    for (int i = 0; i < ADD_NORM_CHUNKS; i++) {
+        const int c4 = threadIdx.x + i * 256;
+        if (c4 < nc4) {
+            const float4 gg = reinterpret_cast<const float4 *>(g)[c4];
+            float4 o;
+            o.x = (v[i].x - mu) * inv * gg.x; o.y = (v[i].y - mu) * inv * gg.y;
+            o.z = (v[i].z - mu) * inv * gg.z; o.w = (v[i].w - mu) * inv * gg.w;
+            if (MODE == 1) {
+                const float4 bb = reinterpret_cast<const float4 *>(b)[c4];
+                o.x += bb.x; o.y += bb.y; o.z += bb.z; o.w += bb.w;
+            }
+            __nv_bfloat162 p0 = __floats2bfloat162_rn(o.x, o.y), p1 = __floats2bfloat162_rn(o.z, o.w);
+            uint2 wv;
+            wv.x = *reinterpret_cast<uint32_t *>(&p0);
+            wv.y = *reinterpret_cast<uint32_t *>(&p1);
+            reinterpret_cast<uint2 *>(norm_out + row * cols)[c4] = wv;
+        }
+    }
+}
+
 __global__ void gelu_kernel(const float *__restrict__ x, int64_t n, float *__restrict__ out) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -266,4 +359,21 @@ extern "C" int tb_gelu(const float *x, int64_t n, float *out, void *stream) {
     if (n == 0) return TB_OK;
     gelu_kernel<<<(unsigned)cdiv(n, 256), 256, 0, as_stream(stream)>>>(x, n, out);
     return check_launch("gelu");
+}
+
+extern "C" int tb_add_norm(const float *x, const float *y, const float *emb, float alpha, const float *gain,
+                           const float *offset, int64_t rows, int64_t cols, float eps, int layer_norm,
+                           float *sum_out, void *norm_out, void *stream) {
+    TB_REQUIRE(eps > 0.0f, "eps must be > 0");
+    TB_REQUIRE(cols % 4 == 0 && cols <= 4 * 256 * ADD_NORM_CHUNKS, "cols must be a multiple of 4, <= 8192");
+    TB_REQUIRE(!layer_norm || offset != nullptr, "layer norm needs an offset");
+    if (rows == 0) return TB_OK;
+    cudaStream_t st = as_stream(stream);
+    if (layer_norm)
+        add_norm_kernel<1><<<(unsigned)rows, 256, 0, st>>>(x, y, emb, alpha, gain, offset, cols, eps, sum_out,
+                                                          (__nv_bfloat16 *)norm_out);
+    else
+        add_norm_kernel<0><<<(unsigned)rows, 256, 0, st>>>(x, y, emb, alpha, gain, offset, cols, eps, sum_out,
+                                                          (__nv_bfloat16 *)norm_out);
+    return check_launch("add_norm");
 }

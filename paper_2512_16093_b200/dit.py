@@ -93,41 +93,47 @@ def _linear(x: torch.Tensor, w: DeviceLinear, out_dtype=torch.bfloat16) -> torch
 
 
 def block_forward(x: torch.Tensor, sigma: float, w: DeviceLayer, heads: int, sla: dict, L_global: int,
-                  group=None) -> torch.Tensor:
-    """One block over the local token shard x [L_p, model_dim] (f32 residual stream)."""
+                  group=None, pending: torch.Tensor | None = None):
+    """One block over the local token shard x [L_p, model_dim] (f32 residual stream).
+
+    Returns (x2, p2): the block output is x2 + p2 -- the last residual add is
+    left to the next block's fused add+norm (or to ``model_forward``)."""
     Lp, dim = x.shape
     hd = dim // heads
-    x = x + float(sigma) * w.sigma_emb
-    a = ops.rmsnorm(x, w.rms_gain)
+    # x1 = x (+ pending residual) + sigma*emb and a = RMSNorm(x1), one pass (bf16 a)
+    x1, a = ops.add_norm(x, pending, w.sigma_emb, float(sigma), w.rms_gain)
 
     def attn(qh, kh, vh):
         return ops.sla_attention(qh, kh, vh, sla["q_block"], sla["kv_block"], sla["topk_ratio"],
                                  sla.get("linear_mix", 1.0), True, out_dtype=torch.bfloat16)
 
+    aq, asc = ops.quantize_blockwise(a, 128, check_finite=False)
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        qkv = _linear(a, w.qkv)                               # [L_p, 3*dim] bf16
+        qkv = ops.w8a8_gemm(aq, asc, w.qkv.bt, w.qkv.scales, 128, None, torch.bfloat16, exact=False)
         q, k, v = (t.view(Lp, heads, hd) for t in qkv.split(dim, dim=1))
         o = ulysses.ulysses_sla_attention(q.contiguous(), k.contiguous(), v.contiguous(), L_global, attn, group)
-        o = o.reshape(Lp, dim)
-        oq, osc = ops.quantize_blockwise(o.contiguous(), 128, check_finite=False)
+        oq, osc = ops.quantize_blockwise(o.reshape(Lp, dim).contiguous(), 128, check_finite=False)
     else:
         # qkv lands head-major [3H, L, hd] straight from the GEMM epilogue (no permute);
         # the out-projection quantizes the head-major attention output in place
-        aq, asc = ops.quantize_blockwise(a, 128, check_finite=False)
         qkv = ops.w8a8_gemm_ex(aq, asc, w.qkv.bt, w.qkv.scales, 128, None, torch.bfloat16, plane=hd)
         o = attn(qkv[:heads], qkv[heads:2 * heads], qkv[2 * heads:])           # [H, L, hd]
         oq, osc = ops.quantize_blockwise_planar(o)
-    x = x + ops.w8a8_gemm(oq, osc, w.out_proj.bt, w.out_proj.scales, 128, None, torch.float32, exact=False)
-    b = ops.layernorm(x, w.ln_gain, w.ln_offset)
+    po = ops.w8a8_gemm(oq, osc, w.out_proj.bt, w.out_proj.scales, 128, None, torch.float32, exact=False)
+    # x2 = x1 + po and b = LayerNorm(x2), one pass (x2 overwrites x1)
+    x2, b = ops.add_norm(x1, po, None, 0.0, w.ln_gain, w.ln_offset, layer_norm=True, sum_out=x1)
     bq, bsc = ops.quantize_blockwise(b, 128, check_finite=False)
     h1 = ops.w8a8_gemm_ex(bq, bsc, w.mlp_in.bt, w.mlp_in.scales, 128, None, torch.bfloat16, act=1)  # GELU fused
-    return x + _linear(h1, w.mlp_out, torch.float32)
+    hq, hsc = ops.quantize_blockwise(h1, 128, check_finite=False)
+    p2 = ops.w8a8_gemm(hq, hsc, w.mlp_out.bt, w.mlp_out.scales, 128, None, torch.float32, exact=False)
+    return x2, p2
 
 
 def model_forward(x, sigma, layers, heads, sla, L_global, group=None):
+    pending = None
     for w in layers:
-        x = block_forward(x, sigma, w, heads, sla, L_global, group)
-    return x
+        x, pending = block_forward(x, sigma, w, heads, sla, L_global, group, pending)
+    return x + pending
 
 
 def rcm_sample(layers, heads: int, sla: dict, x_init: torch.Tensor, noises: list, sigmas, group=None,

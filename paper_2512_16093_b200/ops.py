@@ -527,6 +527,18 @@ def layernorm(x, gain, offset, eps=1e-6):
     return out
 
 
+def add_norm(x, y=None, emb=None, alpha: float = 0.0, gain=None, offset=None, layer_norm: bool = False,
+             eps: float = 1e-6, sum_out=None, write_sum: bool = True):
+    """s = x (+ y) (+ alpha*emb) -> (s f32 | None, norm(s) bf16) in one pass (DiT glue)."""
+    rows, cols = x.shape
+    if write_sum and sum_out is None:
+        sum_out = torch.empty_like(x)
+    norm = torch.empty((rows, cols), dtype=torch.bfloat16, device=x.device)
+    call("tb_add_norm", ptr(x), ptr(y), ptr(emb), float(alpha), ptr(gain), ptr(offset), rows, cols, float(eps),
+         int(layer_norm), ptr(sum_out if write_sum else None), ptr(norm), stream_ptr())
+    return (sum_out if write_sum else None), norm
+
+
 def gelu(x):
     x = x.float().contiguous()
     out = torch.empty_like(x)

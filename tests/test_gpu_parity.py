@@ -312,3 +312,25 @@ def test_quantize_blockwise_planar_matches_row_major(tb):
     q1, s1 = tb.quantize_blockwise_planar(o)
     q2, s2 = tb.quantize_blockwise(o.permute(1, 0, 2).reshape(L, H * 128).contiguous(), 128, check_finite=False)
     assert torch.equal(q1, q2) and torch.equal(s1, s2)
+
+
+@pytest.mark.parametrize("layer_norm", [False, True])
+def test_add_norm_matches_reference_norms(tb, layer_norm):
+    """tb_add_norm: s = x + y + alpha*emb and its RMSNorm / LayerNorm
+    (sampler.py:34-53) in bf16, against the f32 torch formulas."""
+    g = torch.Generator(device="cuda").manual_seed(8)
+    rows, cols = 300, 5120
+    x = torch.randn((rows, cols), device="cuda", generator=g) * 3 + 1
+    y = torch.randn((rows, cols), device="cuda", generator=g)
+    emb = torch.randn(cols, device="cuda", generator=g)
+    gain = torch.rand(cols, device="cuda", generator=g) + 0.5
+    off = torch.randn(cols, device="cuda", generator=g)
+    s, n = tb.add_norm(x, y, emb, 0.7, gain, off if layer_norm else None, layer_norm=layer_norm)
+    ref_s = x + y + 0.7 * emb
+    assert torch.allclose(s, ref_s, rtol=1e-6, atol=1e-5)
+    if layer_norm:
+        mu = ref_s.mean(-1, keepdim=True)
+        ref = (ref_s - mu) / torch.sqrt(((ref_s - mu) ** 2).mean(-1, keepdim=True) + 1e-6) * gain + off
+    else:
+        ref = ref_s / torch.sqrt((ref_s ** 2).mean(-1, keepdim=True) + 1e-6) * gain
+    assert torch.allclose(n.float(), ref, rtol=1e-2, atol=1e-2)
