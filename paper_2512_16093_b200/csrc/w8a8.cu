@@ -24,8 +24,11 @@ namespace tb {
 
 // ------------------------------------------------------------ tcgen05 path
 namespace gemm {
-constexpr int BM = 128, BK = 128, STAGES = 4;
-constexpr int EPI_WARPS = 8;
+#ifndef TB_W8_EPI_WARPS
+#define TB_W8_EPI_WARPS 8
+#endif
+constexpr int EPI_WARPS = TB_W8_EPI_WARPS;       // 8 or 16 (column groups of BN / (EPI_WARPS / 4))
+constexpr int BM = 128, BK = 128, STAGES = EPI_WARPS == 16 ? 3 : 4;
 constexpr int THREADS = 64 + EPI_WARPS * 32;
 template <int BN>
 struct Smem {
@@ -60,7 +63,7 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) w8a8_tc_kernel(
     const float *__restrict__ sa, const float *__restrict__ sb, const float *__restrict__ bias,
     void *__restrict__ out, int M, int N, int K, int plane, int act) {
     using namespace gemm;
-    constexpr int CW = BN / 2;
+    constexpr int CW = BN / (EPI_WARPS / 4);
     constexpr uint32_t TMEM_COLS = 2 * BN;
     extern __shared__ uint8_t smem_raw[];
     Smem<BN> &S = *reinterpret_cast<Smem<BN> *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -86,7 +89,7 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) w8a8_tc_kernel(
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-                const int mt = tile % nmt, nt = tile / nmt;
+                const int mt = tile / nnt, nt = tile % nnt;   // n fastest: A band reused from L2, B (weights) L2-resident
                 for (int kb = 0; kb < nkb; kb++) {
                     ptx::mbar_wait_sleep(&S.empty[stage], phase ^ 1);
                     ptx::mbar_arrive_expect_tx(&S.full[stage], (BM + BN) * BK);
@@ -122,12 +125,12 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) w8a8_tc_kernel(
     } else {
         const int ew = warp - 2;
         const int quarter = warp & 3;          // TMEM lanes this warp may touch
-        const int half = ew >> 2;              // column half of the tile
+        const int half = ew >> 2;              // column group of the tile
         const int trow = quarter * 32 + lane;
         int buf = 0;
         uint32_t bphase = 0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-            const int mt = tile % nmt, nt = tile / nmt;
+            const int mt = tile / nnt, nt = tile % nnt;   // n fastest: A band reused from L2, B (weights) L2-resident
             const int col0 = nt * BN + half * CW;
             const int nb = col0 / 128;
             float2 acc2[CW / 2];
@@ -309,7 +312,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = cluster; tile < ntiles; tile += nclusters) {
-                const int mp = tile % nmp, nt = tile / nmp;
+                const int mp = tile / nnt, nt = tile % nnt;
                 for (int kb = 0; kb < nkb; kb++) {
                     ptx::mbar_wait_sleep(&S.empty[stage], phase ^ 1);
                     const uint32_t fullc = ptx::mapa(ptx::smem_u32(&S.full[stage]), 0);
@@ -356,7 +359,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
         int buf = 0;
         uint32_t bphase = 0;
         for (int tile = cluster; tile < ntiles; tile += nclusters) {
-            const int mp = tile % nmp, nt = tile / nmp;
+            const int mp = tile / nnt, nt = tile % nnt;
             const int col0 = nt * BN + half * CW;
             const int nb = col0 / 128;
             const int mb = 2 * mp + (int)rank;                    // this CTA's 128-row scale block
@@ -374,6 +377,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
                 }
                 ptx::mbar_wait_sleep(&S.seg_full[buf], bphase);
                 ptx::tc_fence_after();
+#ifdef TB_W8_NOEPI
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive_cluster(buf ? seg_empty1 : seg_empty0);
+                buf ^= 1;
+                if (buf == 0) bphase ^= 1;
+                continue;
+#endif
                 const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + buf * BN + half * CW;
                 uint32_t rb[2][16];
                 ptx::tmem_ld16(taddr, rb[0]);
