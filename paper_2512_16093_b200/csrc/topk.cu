@@ -13,6 +13,10 @@
 #include "common.cuh"
 #include "ptx.cuh"
 
+#ifndef TB_TOPK_ROWS
+#define TB_TOPK_ROWS 8
+#endif
+
 namespace tb {
 
 __device__ __forceinline__ uint32_t desc_key(float s) {
@@ -170,12 +174,11 @@ __global__ void __launch_bounds__(256) topk_kernel(
 // shared memory) for the threshold key, then the same ballot compaction.
 // Optional bf16 coverage output (1 = block in the complement) with row pitch
 // cov_ld, zero-padded, the A operand of the linear branch's GEMM.
-template <int JT>
-__global__ void __launch_bounds__(320, 1) topk16_kernel(
+template <int JT, int R, int MINB>
+__global__ void __launch_bounds__(320, MINB) topk16_kernel(
     const float *__restrict__ qp, const float *__restrict__ kpt, int64_t ldk, int nq, int nkv, int d, int count,
     int32_t *__restrict__ idx, uint8_t *__restrict__ comp, float *__restrict__ scores_out,
     __nv_bfloat16 *__restrict__ cov, int64_t cov_ld) {
-    constexpr int R = 16;
     extern __shared__ __align__(16) uint8_t smem[];
     uint32_t *keys = reinterpret_cast<uint32_t *>(smem);                          // [R][nkv]
     float *qt = reinterpret_cast<float *>(smem + (((size_t)R * nkv * 4 + 15) & ~(size_t)15));   // [d][R]
@@ -335,10 +338,11 @@ static int topk_launch(const float *qp, const float *kp, const float *kpt, int64
                         (((uintptr_t)kpt) % 16) == 0 && nkv <= 2560;
     if (fast16) {
         constexpr int JT = 4;                        // 320 threads x 4 columns >= 1182 kv blocks (cfg4) in one pass
-        const size_t smem = (((size_t)16 * nkv * 4 + 15) & ~(size_t)15) + (size_t)d * 16 * 4 + 10 * 256 * 4;
-        cudaFuncSetAttribute(topk16_kernel<JT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        dim3 grid((unsigned)cdiv(nq, 16), (unsigned)H);
-        topk16_kernel<JT><<<grid, 320, smem, st>>>(qp, kpt, ldk, (int)nq, (int)nkv, (int)d, (int)count, idx, comp,
+        constexpr int R = TB_TOPK_ROWS;              // q rows per CTA (8: two CTAs per SM)
+        const size_t smem = (((size_t)R * nkv * 4 + 15) & ~(size_t)15) + (size_t)d * R * 4 + 10 * 256 * 4;
+        dim3 grid((unsigned)cdiv(nq, R), (unsigned)H);
+        cudaFuncSetAttribute(topk16_kernel<JT, R, R == 16 ? 1 : (R == 8 ? 2 : 3)>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        topk16_kernel<JT, R, R == 16 ? 1 : (R == 8 ? 2 : 3)><<<grid, 320, smem, st>>>(qp, kpt, ldk, (int)nq, (int)nkv, (int)d, (int)count, idx, comp,
                                                   scores_out, cov, cov_ld);
         return check_launch("topk16");
     }
