@@ -51,22 +51,75 @@ def sparse_ops(H=H_, L=L_, d=D_, qb=QB, kvb=KVB, ratio=RATIO) -> int:
     return 4 * H * L * min(count * kvb, L) * d
 
 
+def _find_num(d, *words, avoid=()):
+    """First numeric value in a (nested) dict whose key path contains all `words`."""
+    stack = [("", d)]
+    while stack:
+        path, x = stack.pop(0)
+        if isinstance(x, dict):
+            stack += [(f"{path}.{k}".lower(), v) for k, v in x.items()]
+        elif isinstance(x, (int, float)) and all(w in path for w in words) and not any(a in path for a in avoid):
+            return float(x)
+    return None
+
+
 def peaks():
+    """(HBM GB/s, bf16 TFLOP/s burst, source).  MEASURED_PEAKS.json is driver-written per
+    pod (key names are matched loosely); without it, the pool's measured figures that
+    BASELINE.md section 3 copies from it (6547.2 GB/s, 1672.5 TFLOP/s burst)."""
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "measured"
+        hbm = _find_num(p, "hbm") or _find_num(p, "gb")
+        bf = (_find_num(p, "bf16", "burst") or _find_num(p, "bf16", avoid=("sustained",))
+              or _find_num(p, "tflop", avoid=("sustained",)))
+        if hbm and bf:
+            return hbm, bf, "measured (MEASURED_PEAKS.json)"
     except Exception:
-        return 6650.0, 1590.0, "fallback"
+        pass
+    return 6547.2, 1672.5, "measured (MEASURED_PEAKS.json values quoted in BASELINE.md)"
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region: NVML polled
+    every 10 ms from a thread (the timed region is ~100 ms, too short for
+    `nvidia-smi -lms`), falling back to nvidia-smi when NVML is unavailable."""
+
+    _REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+                ("sw_power_cap", 0x4), ("hw_power_brake_slowdown", 0x80))
 
     def __init__(self, index=0):
-        self.index, self.rows, self.proc = index, [], None
+        self.index, self.rows, self.proc, self.nvml = index, [], None, None
+        self.stop = threading.Event()
+
+    def _poll(self):
+        import pynvml as N
+        h = N.nvmlDeviceGetHandleByIndex(self.index)
+        mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+        while True:
+            try:
+                sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                rs = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                pw = N.nvmlDeviceGetPowerUsage(h) / 1e3
+            except Exception:
+                break
+            row = [str(sm), str(mx), f"{pw:.1f}"]
+            row += ["Active" if rs & bit else "Not Active" for name, bit in self._REASONS[:4]]
+            self.rows.append(row)
+            if self.stop.wait(0.01):
+                break
 
     def __enter__(self):
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            self.nvml = True
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            time.sleep(0.05)
+            return self
+        except Exception:
+            self.nvml = None
         q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
@@ -85,6 +138,9 @@ class ClockSampler:
             self.rows.append([x.strip() for x in line.split(",")])
 
     def __exit__(self, *exc):
+        if self.nvml:
+            self.stop.set()
+            self.t.join(timeout=2)
         if self.proc:
             self.proc.terminate()
             try:
@@ -102,8 +158,11 @@ class ClockSampler:
                                       "sw_power_cap"), r[3:7]):
                     if val.lower() == "active":
                         reasons.add(name)
+        pw = [float(r[2]) for r in self.rows if len(r) >= 7 and r[2].replace(".", "").isdigit()]
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w": statistics.median(pw) if pw else None,
+                "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
 # --------------------------------------------------------------- reference arm
