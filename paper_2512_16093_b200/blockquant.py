@@ -175,3 +175,23 @@ def pack_blockquantized(bq: BlockQuantized, name: str) -> dict:
     """blockquant.py:193-195."""
     return {f"{name}.q": bq.q_numpy(), f"{name}.scales": np.asarray(
         bq.scales.cpu() if isinstance(bq.scales, torch.Tensor) else bq.scales)}
+
+
+def unpack_blockquantized(manifest, name: str, block: int, device: bool = False) -> BlockQuantized:
+    """blockquant.py:198-202: rebuild from the ``<name>.q`` / ``<name>.scales`` entries.
+
+    ``device=True`` streams the codes from disk into HBM already in
+    the GEMM's K-major B layout ([N, K], tensor_store.read_tensor_device) and the
+    scales next to them; ``q`` is then the [K, N] view of those codes, so nothing
+    is staged through a host ndarray or transposed again at first use."""
+    from .tensor_store import read_tensor, read_tensor_device
+    qp, sp = manifest.tensors[f"{name}.q"], manifest.tensors[f"{name}.scales"]   # KeyError, as the reference
+    if not device:
+        q, s = read_tensor(qp), read_tensor(sp)
+        return BlockQuantized(rows=q.shape[0], cols=q.shape[1], block=block, q=q, scales=s)
+    qt = read_tensor_device(qp, layout="kmajor_t")
+    s = read_tensor_device(sp)
+    bq = BlockQuantized(rows=qt.shape[1], cols=qt.shape[0], block=block, q=qt.t(), scales=s)
+    object.__setattr__(bq, "_dev_qt", qt)
+    object.__setattr__(bq, "_dev_s", s)
+    return bq
