@@ -8,9 +8,11 @@
 // overlaps the other's tensor-core work.  Warp roles (192 threads):
 //   warps 0-3  softmax/epilogue, thread = query row = TMEM lane
 //   warp 4     TMA producer: Q codes once; per selected kv block the K code
-//              tile (64x128 int8) into a 3-stage ring and the V^T tile
-//              (128x64 bf16) into a separate 3-stage ring (128B swizzle,
-//              mbarrier complete_tx), so K can run ahead of V
+//              tile (64x128 int8) into a 3-stage ring (128B swizzle,
+//              mbarrier complete_tx)
+//   warp 6     TMA producer: per selected kv block the V tile (64 tokens x
+//              128 channels bf16, two SW128 boxes) into its own 3-stage ring,
+//              so K runs ahead of V
 //   warp 5     MMA issuer (one elected thread):
 //                S_j  = Qc . Kc_j^T   4 x tcgen05.mma kind::i8  (M128 N64 K32) -> s32 TMEM
 //                O   += P_j . V_j     4 x tcgen05.mma kind::f16 (M128 N128 K16), A = P_j in TMEM
@@ -44,8 +46,30 @@ namespace tb {
 #endif
 
 namespace sla {
-constexpr int BM = 128, BN = 64, D = 128, KSTAGES = 3, VSTAGES = 3;
-constexpr int THREADS = 192;
+// MMA-warp barrier waits: 0 = try_wait with suspend hint, 1 = try_wait, 2 = test_wait poll
+#ifndef TB_SLA_MMA_WAIT
+#define TB_SLA_MMA_WAIT 0
+#endif
+#if TB_SLA_MMA_WAIT == 0
+#define MMA_WAIT ptx::mbar_wait_sleep
+#elif TB_SLA_MMA_WAIT == 1
+#define MMA_WAIT ptx::mbar_wait
+#else
+#define MMA_WAIT ptx::mbar_wait_spin
+#endif
+#ifndef TB_SLA_SM_SPIN
+#define TB_SLA_SM_SPIN 0
+#endif
+#if TB_SLA_SM_SPIN
+#define SM_WAIT ptx::mbar_wait_spin
+#else
+#define SM_WAIT ptx::mbar_wait_sleep
+#endif
+#ifndef TB_SLA_KST
+#define TB_SLA_KST 3
+#endif
+constexpr int BM = 128, BN = 64, D = 128, KSTAGES = TB_SLA_KST, VSTAGES = 3;
+constexpr int THREADS = 224;   // 4 softmax + K producer + MMA + V producer warps
 constexpr uint32_t Q_BYTES = BM * D;          // int8
 constexpr uint32_t K_BYTES = BN * D;          // int8
 constexpr uint32_t V_BYTES = D * BN * 2;      // bf16 V tile: two 64-channel x 64-token SW128 boxes
@@ -58,7 +82,10 @@ struct Smem {
     uint64_t v_full[VSTAGES], v_empty[VSTAGES];
     uint64_t s_full[2], p_full[2], pv_done[2];
     uint64_t phiq_full, lin_full, lin_done;     // fused linear-branch epilogue
+    uint64_t k1_full;                           // den row of KV_sel (sum phi(K_b) over the complement)
     alignas(128) uint16_t bias_a[128], bias_b[128];  // bias-MMA operands (2 core matrices each)
+    alignas(16) __nv_bfloat16 k1[128];
+    float corr_s[128], den_s[128];              // prologue: per-row q . k_mean and den_L
     float c1[2048];                             // per selected block: sq * sk * scale * log2e
     uint8_t rag[2048];                          // per selected block: ragged last kv block
     uint32_t tmem_base;
@@ -71,13 +98,45 @@ constexpr float LN2 = 0.6931471805599453f;
 
 #ifdef TB_SLA_TRACE
 // diagnostic timestamps (clock64) of one CTA: [block][event]
-__device__ unsigned long long tb_sla_trace[64][16];
+__device__ unsigned long long tb_sla_trace[80][16];
+// whole-launch phase accounting: [0..2] summed prologue / main loop / epilogue
+// cycles of thread 0 over all CTAs, [3] CTA count; per SM: min entry / max exit
+// clock64 and %globaltimer (ns)
+__device__ unsigned long long tb_sla_phase[4];
+__device__ unsigned long long tb_sla_sm[160][4];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void tb_phase_done(unsigned long long t0, unsigned long long g0, unsigned long long t1,
+                                              unsigned long long t2) {
+    const unsigned long long t3 = clock64(), g3 = gtimer();
+    atomicAdd(&tb_sla_phase[0], t1 - t0);
+    atomicAdd(&tb_sla_phase[1], t2 - t1);
+    atomicAdd(&tb_sla_phase[2], t3 - t2);
+    atomicAdd(&tb_sla_phase[3], 1ull);
+    uint32_t sm;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(sm));
+    atomicMin(&tb_sla_sm[sm][0], t0);
+    atomicMax(&tb_sla_sm[sm][1], t3);
+    atomicMin(&tb_sla_sm[sm][2], g0);
+    atomicMax(&tb_sla_sm[sm][3], g3);
+}
+#define TB_PH(x) x
 #define TB_TRACE(j, e)                                                                                   \
     do {                                                                                                 \
         if (blockIdx.x == 100 && blockIdx.y == 5 && (j) < 64) tb_sla_trace[(j)][(e)] = clock64();        \
     } while (0)
+// rows 64.. : one-off events (prologue 70, epilogue 71)
+#define TB_TRACE_X(row, e)                                                                               \
+    do {                                                                                                 \
+        if (blockIdx.x == 100 && blockIdx.y == 5) tb_sla_trace[(row)][(e)] = clock64();                  \
+    } while (0)
 #else
 #define TB_TRACE(j, e) do {} while (0)
+#define TB_TRACE_X(row, e) do {} while (0)
+#define TB_PH(x) do {} while (0)
 #endif
 
 __device__ __forceinline__ float ex2(float x) {
@@ -158,6 +217,27 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
     const int L = (int)a.L;
     const int32_t *sel = a.idx + ((int64_t)h * nq + n) * count;
 
+#ifdef TB_SLA_TRACE
+    unsigned long long ph_t0 = clock64(), ph_g0 = gtimer(), ph_t1 = 0, ph_t2 = 0;
+#endif
+    if (threadIdx.x == 0) TB_TRACE_X(70, 0);
+    // softmax threads: their q row is pulled into L2 before the setup barrier,
+    // so the DRAM latency overlaps barrier init / TMEM alloc
+    if (warp < 4 && n * BM + (int)threadIdx.x < L) {
+        const char *src = reinterpret_cast<const char *>(reinterpret_cast<const T *>(a.q) +
+                                                         ((int64_t)h * L + n * BM + threadIdx.x) * D);
+#pragma unroll
+        for (int c = 0; c < (int)(D * sizeof(T)); c += 128) asm volatile("prefetch.global.L2 [%0];" :: "l"(src + c));
+    }
+    if (warp == 6) {
+        // bias-MMA operands: A rows [1, 0 x7 | 1, 0 x7], B rows [M/2, 0 x7 | M/2, 0 x7]
+#pragma unroll
+        for (int i = lane; i < 128; i += 32) {
+            S.bias_a[i] = (i % 8 == 0) ? 0x3F80 : 0;    // bf16 1.0
+            S.bias_b[i] = (i % 8 == 0) ? 0x4AC0 : 0;    // bf16 6291456 = 1.5 * 2^22
+        }
+        ptx::fence_async_smem();
+    }
     if (warp == 4 && lane == 0) {
         if (ptx::smem_u32(smem_raw) & 1023) __trap();     // SW128 tiles need 1024-B alignment
         ptx::mbar_init(&S.q_full, 1);
@@ -172,12 +252,7 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
         ptx::mbar_init(&S.phiq_full, 128);
         ptx::mbar_init(&S.lin_full, 1);
         ptx::mbar_init(&S.lin_done, 1);
-        // bias-MMA operands: A rows [1, 0 x7 | 1, 0 x7], B rows [M/2, 0 x7 | M/2, 0 x7]
-        for (int i = 0; i < 128; i++) {
-            S.bias_a[i] = (i % 8 == 0) ? 0x3F80 : 0;    // bf16 1.0
-            S.bias_b[i] = (i % 8 == 0) ? 0x4AC0 : 0;    // bf16 6291456 = 1.5 * 2^22
-        }
-        ptx::fence_async_smem();
+        ptx::mbar_init(&S.k1_full, 1);
         ptx::fence_barrier_init();
         ptx::prefetch_tmap(&tm_q);
         ptx::prefetch_tmap(&tm_k);
@@ -187,26 +262,51 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
+    if (threadIdx.x == 0) TB_TRACE_X(70, 1);
     const uint32_t tmem = S.tmem_base;
     const uint32_t TM_O = tmem + 128;
-    // fused linear epilogue: after the last PV the V/K rings are free; phi(Q)
-    // (A, 2 x 16 KB swizzled K-halves) goes to v[0..1], KV_sel^T (B) to v[2]+k[0]
+    // fused linear branch numL = phi(Q) . KV_sel: phi(Q) (A, 2 x 16 KB swizzled
+    // K-halves) in v[0..1], KV_sel^T (B) in v[2] + k[0..1].  Linear-first mode
+    // (lf: no row_max / den outputs, complement non-empty) runs it BEFORE the
+    // main loop, straight into the O accumulator, which then starts as numL at
+    // the reference m_ref = log2(linear_mix) (l starts as den_L): the SLA
+    // combine (attention.py:416-421) becomes out = O / l, and the prologue
+    // already holds the q row that phi(Q) needs.  The producers start once
+    // that MMA has released the rings.  Otherwise the same MMA runs after the
+    // last PV into the free S columns (end-of-kernel combine).
     const bool fused = a.lin_kv != nullptr && a.linear_mix != 0.0f;
+    const bool lf = fused && !EXACT && count < nkv;
+    const bool fused_end = fused && !lf;
     uint8_t *lin_a = S.v[0];
     uint8_t *lin_b = S.v[2];
 
     if (warp == 4) {
-        // ------------------------------------------------------ TMA producer
+        // ---------------------------------------------------- TMA producer (K)
         // the whole warp walks the loop (warp-uniform values, no waterfall
-        // loops around the uniform-operand TMA instructions); one lane issues
+        // loops around the uniform-operand TMA instructions); one lane issues.
+        // K and V have their own producer warps, so a K slot freed by QK(j-3)
+        // is refilled at once instead of queueing behind the wait for the V
+        // slot that PV(j-4) frees.
         if (ptx::elect_one()) {
             ptx::mbar_arrive_expect_tx(&S.q_full, Q_BYTES);
             ptx::tma_load_3d(S.q, &tm_q, 0, n * BM, h, &S.q_full);
+            if (fused) {      // den row of KV_sel: 256 B
+                ptx::mbar_arrive_expect_tx(&S.k1_full, D * 2);
+                ptx::bulk_g2s(S.k1, reinterpret_cast<const __nv_bfloat16 *>(a.lin_kv) +
+                                        (((int64_t)h * nq + n) * a.lin_dx + D) * D, D * 2, &S.k1_full);
+            }
+            if (lf) {
+                const int row0 = (int)(((int64_t)h * nq + n) * a.lin_dx);
+                ptx::mbar_arrive_expect_tx(&S.lin_full, 2 * 16384);
+                ptx::tma_load_2d(lin_b, &tm_kv, 0, row0, &S.lin_full);
+                ptx::tma_load_2d(lin_b + 16384, &tm_kv, 64, row0, &S.lin_full);
+            }
         }
         __syncwarp();
+        if (lf) ptx::mbar_wait_sleep(&S.lin_done, 0);   // the linear MMA has released the rings
         for (int j = 0; j < count; j++) {
             const int b = __ldg(sel + j);
-            const int ks = j % KSTAGES, vs = j % VSTAGES;
+            const int ks = j % KSTAGES;
             ptx::mbar_wait_sleep(&S.k_empty[ks], (uint32_t)(((j / KSTAGES) & 1) ^ 1));
             if (lane == 0) TB_TRACE(j, 10);
             if (ptx::elect_one()) {
@@ -214,22 +314,29 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
                 ptx::tma_load_3d(S.k[ks], &tm_k, 0, b * BN, h, &S.k_full[ks]);
             }
             __syncwarp();
-            ptx::mbar_wait_sleep(&S.v_empty[vs], (uint32_t)(((j / VSTAGES) & 1) ^ 1));
-            if (lane == 0) TB_TRACE(j, 11);
-            if (ptx::elect_one()) {
-                ptx::mbar_arrive_expect_tx(&S.v_full[vs], V_BYTES);
-                ptx::tma_load_3d(S.v[vs], &tm_v, 0, b * BN, h, &S.v_full[vs]);
-                ptx::tma_load_3d(S.v[vs] + V_BYTES / 2, &tm_v, 64, b * BN, h, &S.v_full[vs]);
-            }
-            __syncwarp();
         }
-        if (fused) {
+        if (fused_end) {
             ptx::mbar_wait_sleep(&S.o_final, 0);        // every MMA reading the rings is done
             const int row0 = (int)(((int64_t)h * nq + n) * a.lin_dx);
             if (ptx::elect_one()) {
                 ptx::mbar_arrive_expect_tx(&S.lin_full, 2 * 16384);
                 ptx::tma_load_2d(lin_b, &tm_kv, 0, row0, &S.lin_full);
                 ptx::tma_load_2d(lin_b + 16384, &tm_kv, 64, row0, &S.lin_full);
+            }
+            __syncwarp();
+        }
+    } else if (warp == 6) {
+        // ---------------------------------------------------- TMA producer (V)
+        if (lf) ptx::mbar_wait_sleep(&S.lin_done, 0);
+        for (int j = 0; j < count; j++) {
+            const int b = __ldg(sel + j);
+            const int vs = j % VSTAGES;
+            ptx::mbar_wait_sleep(&S.v_empty[vs], (uint32_t)(((j / VSTAGES) & 1) ^ 1));
+            if (lane == 0) TB_TRACE(j, 11);
+            if (ptx::elect_one()) {
+                ptx::mbar_arrive_expect_tx(&S.v_full[vs], V_BYTES);
+                ptx::tma_load_3d(S.v[vs], &tm_v, 0, b * BN, h, &S.v_full[vs]);
+                ptx::tma_load_3d(S.v[vs] + V_BYTES / 2, &tm_v, 64, b * BN, h, &S.v_full[vs]);
             }
             __syncwarp();
         }
@@ -244,11 +351,31 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
         // no-swizzle K-major 8x16 bf16 tiles; SBO = 0 makes every 8-row group alias the same rows
         const uint64_t bias_a = ptx::sdesc_noswz_alias(ptx::smem_u32(S.bias_a));
         const uint64_t bias_b = ptx::sdesc_noswz_alias(ptx::smem_u32(S.bias_b));
-        ptx::mbar_wait_sleep(&S.q_full, 0);
+        auto lin_mma = [&](uint32_t dst) {
+            // numL = phi(Q) . KV_sel  (M128 N128 K128, bf16)
+            MMA_WAIT(&S.phiq_full, 0);
+            MMA_WAIT(&S.lin_full, 0);
+            ptx::tc_fence_after();
+            if (ptx::elect_one()) {
+#pragma unroll
+                for (int ks = 0; ks < D / 16; ks++) {
+                    const int sub = ks >> 2, w = ks & 3;
+                    const uint64_t ad = ptx::sdesc_sw128(ptx::smem_u32(lin_a + sub * 16384)) + 2 * w;
+                    const uint64_t bd = ptx::sdesc_sw128(ptx::smem_u32(lin_b + sub * 16384)) + 2 * w;
+                    ptx::mma_f16(dst, ad, bd, ID_PV, ks > 0 ? 1u : 0u);
+                }
+                ptx::mma_commit(&S.lin_done);
+            }
+            __syncwarp();
+        };
+        if (lf) lin_mma(TM_O);                          // O starts as numL
+        MMA_WAIT(&S.q_full, 0);
         auto pv = [&](int i) {
             const int pb = i & 1, vs = i % VSTAGES;
-            ptx::mbar_wait_sleep(&S.v_full[vs], (uint32_t)((i / VSTAGES) & 1));
-            ptx::mbar_wait_sleep(&S.p_full[pb], (uint32_t)((i >> 1) & 1));
+            if (lane == 0) TB_TRACE(i, 13);
+            MMA_WAIT(&S.v_full[vs], (uint32_t)((i / VSTAGES) & 1));
+            if (lane == 0) TB_TRACE(i, 14);
+            MMA_WAIT(&S.p_full[pb], (uint32_t)((i >> 1) & 1));
             ptx::tc_fence_after();
             if (lane == 0) TB_TRACE(i, 9);
             // V [tokens][channels]: channel-contiguous = MN-major B; atoms 64 ch x 8 tokens
@@ -256,7 +383,7 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             if (ptx::elect_one()) {
 #pragma unroll
                 for (int k = 0; k < BN / 16; k++)   // K=16 bf16 per MMA: 8 TMEM cols of P, 16 token rows of V
-                    ptx::mma_f16_ts(TM_O, tmem + pb * BN + 8 * k, vd + 128 * k, ID_PV_MN, (i > 0 || k > 0) ? 1u : 0u);
+                    ptx::mma_f16_ts(TM_O, tmem + pb * BN + 8 * k, vd + 128 * k, ID_PV_MN, (lf || i > 0 || k > 0) ? 1u : 0u);
                 ptx::mma_commit(&S.pv_done[pb]);
                 ptx::mma_commit(&S.v_empty[vs]);
             }
@@ -264,7 +391,8 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
         };
         auto qk = [&](int j) {
             const int ks = j % KSTAGES, sb = j & 1;
-            ptx::mbar_wait_sleep(&S.k_full[ks], (uint32_t)((j / KSTAGES) & 1));
+            if (lane == 0) TB_TRACE(j, 15);
+            MMA_WAIT(&S.k_full[ks], (uint32_t)((j / KSTAGES) & 1));
             ptx::tc_fence_after();
             if (lane == 0) TB_TRACE(j, 8);
             const uint64_t kd = ptx::sdesc_sw128(ptx::smem_u32(S.k[ks]));
@@ -289,23 +417,7 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
         }
         if (ptx::elect_one()) ptx::mma_commit(&S.o_final);
         __syncwarp();
-        if (fused) {
-            // numL = phi(Q) . KV_sel  (M128 N128 K128, bf16) into the free S/P columns 0..127
-            ptx::mbar_wait_sleep(&S.phiq_full, 0);
-            ptx::mbar_wait_sleep(&S.lin_full, 0);
-            ptx::tc_fence_after();
-            if (ptx::elect_one()) {
-#pragma unroll
-                for (int ks = 0; ks < D / 16; ks++) {
-                    const int sub = ks >> 2, w = ks & 3;
-                    const uint64_t ad = ptx::sdesc_sw128(ptx::smem_u32(lin_a + sub * 16384)) + 2 * w;
-                    const uint64_t bd = ptx::sdesc_sw128(ptx::smem_u32(lin_b + sub * 16384)) + 2 * w;
-                    ptx::mma_f16(tmem, ad, bd, ID_PV, ks > 0 ? 1u : 0u);
-                }
-                ptx::mma_commit(&S.lin_done);
-            }
-            __syncwarp();
-        }
+        if (fused_end) lin_mma(tmem);                  // into the free S/P columns 0..127
     } else {
         // ------------------------------------------------ softmax + epilogue
         const int r = warp * 32 + lane;             // row in tile == TMEM lane
@@ -313,20 +425,134 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
         const bool row_ok = row < L;
         const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
         const float scale2 = a.scale * LOG2E;
-        // corr = q_row . k_mean (unquantized q, f32)
-        float corr = 0.0f;
-        if (row_ok) {
-            const T *qr = reinterpret_cast<const T *>(a.q) + ((int64_t)h * L + row) * D;
-            const float *km = a.k_mean + (int64_t)h * D;
-#pragma unroll 4
-            for (int c = 0; c < D; c += 8) {
-                float x[8];
-                load8(qr + c, x);
+        // phi(q_row) -> bf16 A operand of the linear MMA (128B-swizzled K halves
+        // in lin_a); returns den_L = phi(q) . sum phi(K_b) over the complement.
+        // wq: the row already in registers (bf16), else it is (re)loaded.
+        const T *qrow = reinterpret_cast<const T *>(a.q) + ((int64_t)h * L + (row_ok ? row : 0)) * D;
+        auto stage_phi = [&](const uint4 *wq) {
+            if (threadIdx.x == 0) TB_TRACE_X(70, 2);
+            ptx::mbar_wait_sleep(&S.k1_full, 0);
+            if (threadIdx.x == 0) TB_TRACE_X(70, 3);
+            const __nv_bfloat16 *k1 = S.k1;
+            float dl = 0.0f;
 #pragma unroll
-                for (int i = 0; i < 8; i++) corr = fmaf(x[i], __ldg(km + c + i), corr);
+            for (int kc = 0; kc < D / 8; kc++) {
+                uint32_t pk[4];
+                float xq[8];
+                if (sizeof(T) == 2 && wq != nullptr) {
+                    const __nv_bfloat162 *b2 = reinterpret_cast<const __nv_bfloat162 *>(&wq[kc]);
+#pragma unroll
+                    for (int i = 0; i < 4; i++) { const float2 f = __bfloat1622float2(b2[i]); xq[2 * i] = f.x; xq[2 * i + 1] = f.y; }
+                } else {
+                    load8(qrow + kc * 8, xq);
+                    if (!row_ok) {
+#pragma unroll
+                        for (int i = 0; i < 8; i++) xq[i] = 0.0f;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    // branch-free phi (attention.py:287-290); padding rows read
+                    // q = 0 and are never stored
+                    const float x0 = xq[2 * u], x1 = xq[2 * u + 1];
+                    const float f0 = x0 >= 0.0f ? x0 + 1.0f : ex2(x0 * LOG2E);
+                    const float f1 = x1 >= 0.0f ? x1 + 1.0f : ex2(x1 * LOG2E);
+                    dl = fmaf(f0, __bfloat162float(k1[kc * 8 + 2 * u]), dl);
+                    dl = fmaf(f1, __bfloat162float(k1[kc * 8 + 2 * u + 1]), dl);
+                    __nv_bfloat162 pp = __floats2bfloat162_rn(f0, f1);
+                    pk[u] = *reinterpret_cast<uint32_t *>(&pp);
+                }
+                uint8_t *dst = lin_a + (kc >> 3) * 16384 + r * 128 + (((kc & 7) ^ (r & 7)) * 16);
+                *reinterpret_cast<uint4 *>(dst) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            }
+            if (threadIdx.x == 0) TB_TRACE_X(70, 4);
+            ptx::fence_async_smem();
+            ptx::mbar_arrive(&S.phiq_full);
+            if (threadIdx.x == 0) TB_TRACE_X(70, 5);
+            return dl;
+        };
+        // Prologue, warp-cooperative and coalesced: each warp walks its 32 rows
+        // two at a time (lanes 0-15 row 2i, 16-31 row 2i+1, 16 B of the row per
+        // lane), so every load instruction reads 512 contiguous bytes.  Per row:
+        // corr = q . k_mean (unquantized q, f32; a tolerance-level quantity whose
+        // reference order is an sgemm's) and, in lf mode, phi(q) -> the bf16 A
+        // operand of the linear MMA (128B-swizzled K halves in lin_a) and
+        // den_L = phi(q) . sum phi(K_b) over the complement; 16-lane shuffle
+        // reductions, results through smem (read after the barrier below).
+        {
+            const int half = lane >> 4, cl = lane & 15;
+            float km[8], kk[8];
+            {
+                const float4 *km4 = reinterpret_cast<const float4 *>(a.k_mean + (int64_t)h * D + cl * 8);
+                const float4 ka = __ldg(km4), kb = __ldg(km4 + 1);
+                km[0] = ka.x; km[1] = ka.y; km[2] = ka.z; km[3] = ka.w;
+                km[4] = kb.x; km[5] = kb.y; km[6] = kb.z; km[7] = kb.w;
+            }
+            const T *qbase = reinterpret_cast<const T *>(a.q) + (int64_t)h * L * D + cl * 8;
+            const int rbase = warp * 32 + half;
+            uint4 qv[sizeof(T) == 2 ? 16 : 1];
+            if constexpr (sizeof(T) == 2) {
+#pragma unroll
+                for (int it = 0; it < 16; it++) {
+                    const int rowi = n * BM + rbase + 2 * it;
+                    qv[it] = rowi < L ? __ldg(reinterpret_cast<const uint4 *>(qbase + (int64_t)rowi * D))
+                                      : make_uint4(0, 0, 0, 0);
+                }
+            }
+            if (lf) {
+                ptx::mbar_wait_sleep(&S.k1_full, 0);
+                const uint4 kw = *reinterpret_cast<const uint4 *>(S.k1 + cl * 8);
+                const __nv_bfloat162 *k2 = reinterpret_cast<const __nv_bfloat162 *>(&kw);
+#pragma unroll
+                for (int i = 0; i < 4; i++) { const float2 f = __bfloat1622float2(k2[i]); kk[2 * i] = f.x; kk[2 * i + 1] = f.y; }
+            }
+#pragma unroll
+            for (int it = 0; it < 16; it++) {
+                const int rr = rbase + 2 * it;
+                float x[8];
+                if constexpr (sizeof(T) == 2) {
+                    const __nv_bfloat162 *b2 = reinterpret_cast<const __nv_bfloat162 *>(&qv[it]);
+#pragma unroll
+                    for (int i = 0; i < 4; i++) { const float2 f = __bfloat1622float2(b2[i]); x[2 * i] = f.x; x[2 * i + 1] = f.y; }
+                } else {
+                    const int rowi = n * BM + rr;
+                    if (rowi < L) {
+                        load8(qbase + (int64_t)rowi * D, x);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 8; i++) x[i] = 0.0f;
+                    }
+                }
+                float cp = 0.0f, dp = 0.0f;
+#pragma unroll
+                for (int i = 0; i < 8; i++) cp = fmaf(x[i], km[i], cp);
+                if (lf) {
+                    uint32_t pk[4];
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const float x0 = x[2 * u], x1 = x[2 * u + 1];
+                        const float f0 = x0 >= 0.0f ? x0 + 1.0f : ex2(x0 * LOG2E);
+                        const float f1 = x1 >= 0.0f ? x1 + 1.0f : ex2(x1 * LOG2E);
+                        dp = fmaf(f0, kk[2 * u], fmaf(f1, kk[2 * u + 1], dp));
+                        __nv_bfloat162 pp = __floats2bfloat162_rn(f0, f1);
+                        pk[u] = *reinterpret_cast<uint32_t *>(&pp);
+                    }
+                    uint8_t *dst = lin_a + (cl >> 3) * 16384 + rr * 128 + (((cl & 7) ^ (rr & 7)) * 16);
+                    *reinterpret_cast<uint4 *>(dst) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                }
+#pragma unroll
+                for (int o = 8; o > 0; o >>= 1) {
+                    cp += __shfl_xor_sync(0xffffffffu, cp, o);
+                    dp += __shfl_xor_sync(0xffffffffu, dp, o);
+                }
+                if (cl == 0) { S.corr_s[rr] = cp; S.den_s[rr] = dp; }
+            }
+            if (lf) {
+                ptx::fence_async_smem();
+                ptx::mbar_arrive(&S.phiq_full);
             }
         }
-        const float c0 = corr * scale2;
+        if (threadIdx.x == 0) TB_TRACE_X(70, 6);
         const float sq = __ldg(a.q_scales + (int64_t)h * nq + n);
         const float *ksc = a.k_scales + (int64_t)h * nkv;
         const int last_blk = nkv - 1;
@@ -348,15 +574,25 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             S.c1[j] = sq * __ldg(ksc + b) * scale2;
             S.rag[j] = (b == last_blk) && last_ext < BN;
         }
+        if (threadIdx.x == 0) TB_TRACE_X(70, 7);
         ptx::named_bar_sync(1, BM);
-        float m_ref = -INFINITY, m_true = -INFINITY, l = 0.0f;
+        TB_PH(ph_t1 = clock64());
+        if (threadIdx.x == 0) TB_TRACE_X(70, 8);
+        const float c0 = (row_ok ? S.corr_s[r] : 0.0f) * scale2;
+        const float den_l = S.den_s[r];
+        // lf: O already holds numL at the reference log2(linear_mix), l = den_L.
+        // (Warp-uniform start: the rebase below is warp-collective.  A row with
+        // l == 0 -- phi(q) underflowed, or a padding row -- whose exponentials
+        // all underflow is caught by the l + psum > 0 test and rebased down.)
+        float m_ref = lf ? __log2f(a.linear_mix) : -INFINITY, m_true = -INFINITY;
+        float l = lf ? den_l : 0.0f;
         for (int j = 0; j < count; j++) {
             const int sb = j & 1;
             const float c1 = S.c1[j];
             // s32 scores as the floats M + s (M = 1.5*2^23, exact): fold -M*c1 into the offset
             const float c0m = fmaf(-12582912.0f, c1, c0);
             if (threadIdx.x == 0) TB_TRACE(j, 0);
-            ptx::mbar_wait_sleep(&S.s_full[sb], (uint32_t)((j >> 1) & 1));
+            SM_WAIT(&S.s_full[sb], (uint32_t)((j >> 1) & 1));
             ptx::tc_fence_after();
             if (threadIdx.x == 0) TB_TRACE(j, 1);
             uint32_t s[4][16];
@@ -418,7 +654,7 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             bool slow = EXACT;
             if (!EXACT) {
                 psum = run_p(c0m - m_ref);
-                slow = __any_sync(0xffffffffu, !(psum <= 0x1p60f));
+                slow = __any_sync(0xffffffffu, !(psum <= 0x1p60f) || !(l + psum > 0.0f));
             }
             if (slow) {
                 if (!EXACT) load_s();         // S is intact in TMEM until P is stored
@@ -460,11 +696,12 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
                     // lazy rebase of O when a row's max outgrows its reference by
                     // > 8 (p <= 256).  tcgen05.ld/st are warp-collective, so the
                     // decision is made per warp; rows that do not need it use 1.
-                    const bool need = mx > m_ref + 8.0f;
+                    const bool need = mx > m_ref + 8.0f || (l == 0.0f && mx < m_ref - 8.0f);
                     if (__any_sync(0xffffffffu, need)) {
-                        ptx::mbar_wait_sleep(&S.pv_done[(j - 1) & 1], (uint32_t)(((j - 1) >> 1) & 1));
+                        if (j > 0) ptx::mbar_wait_sleep(&S.pv_done[(j - 1) & 1], (uint32_t)(((j - 1) >> 1) & 1));
+                        else ptx::mbar_wait_sleep(&S.lin_done, 0);   // lf: O = numL
                         ptx::tc_fence_after();
-                        const float alpha = need ? ex2(m_ref - mx) : 1.0f;
+                        const float alpha = need ? (l == 0.0f ? 0.0f : ex2(m_ref - mx)) : 1.0f;   // l == 0: O == 0
 #pragma unroll 1
                         for (int c = 0; c < D; c += 16) {
                             uint32_t o[16];
@@ -492,57 +729,36 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             if (threadIdx.x == 0) TB_TRACE(j, 3);
             if (threadIdx.x == 96) TB_TRACE(j, 12);
         }
+        TB_PH(ph_t2 = clock64());
         if (!EXACT) m_true = m_ref;                  // combine against the reference (exact in math)
         // ------------------------------------------------------- epilogue
+        if (threadIdx.x == 0) TB_TRACE_X(71, 0);
         ptx::mbar_wait_sleep(&S.o_final, 0);
         ptx::tc_fence_after();
+        if (threadIdx.x == 0) TB_TRACE_X(71, 1);
         float den_fused = 0.0f;
-        if (fused) {
-            // phi(q_row) -> bf16 A operand (128B-swizzled K halves); den = phi(q) . sum phi(K_b)
-            const __nv_bfloat16 *k1 = reinterpret_cast<const __nv_bfloat16 *>(a.lin_kv) +
-                                      (((int64_t)h * nq + n) * a.lin_dx + D) * D;
-            const T *qr = reinterpret_cast<const T *>(a.q) + ((int64_t)h * L + (row_ok ? row : 0)) * D;
-#pragma unroll 2
-            for (int kc = 0; kc < D / 8; kc++) {
-                uint32_t pk[4];
-                float xq[8];
-                load8(qr + kc * 8, xq);
-#pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    float f0 = 0.0f, f1 = 0.0f;
-                    if (row_ok) {
-                        const float x0 = xq[2 * u], x1 = xq[2 * u + 1];
-                        f0 = x0 >= 0.0f ? x0 + 1.0f : __expf(x0);
-                        f1 = x1 >= 0.0f ? x1 + 1.0f : __expf(x1);
-                    }
-                    den_fused = fmaf(f0, __bfloat162float(k1[kc * 8 + 2 * u]), den_fused);
-                    den_fused = fmaf(f1, __bfloat162float(k1[kc * 8 + 2 * u + 1]), den_fused);
-                    __nv_bfloat162 pp = __floats2bfloat162_rn(f0, f1);
-                    pk[u] = *reinterpret_cast<uint32_t *>(&pp);
-                }
-                uint8_t *dst = lin_a + (kc >> 3) * 16384 + r * 128 + (((kc & 7) ^ (r & 7)) * 16);
-                *reinterpret_cast<uint4 *>(dst) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-            }
-            ptx::fence_async_smem();
-            ptx::mbar_arrive(&S.phiq_full);
+        if (fused_end) {
+            den_fused = stage_phi(nullptr);
+            if (threadIdx.x == 0) TB_TRACE_X(71, 2);
             ptx::mbar_wait_sleep(&S.lin_done, 0);
             ptx::tc_fence_after();
+            if (threadIdx.x == 0) TB_TRACE_X(71, 3);
         }
         // rebase to the true row max (natural-log units for the combine)
         const float f = ex2(m_ref - m_true);
         const float m_nat = m_true * LN2;           // log2-domain max -> natural units
         const float l_true = l * f;
-        const bool lin = fused || (a.num_l != nullptr && a.linear_mix != 0.0f);
+        const bool lin = fused_end || (!lf && a.num_l != nullptr && a.linear_mix != 0.0f);
         const int64_t lin_ld = a.lin_ld ? a.lin_ld : D;
         const int64_t lin_hs = a.lin_hs ? a.lin_hs : (int64_t)L * lin_ld;
-        const float *nl_row = (lin && !fused) ? a.num_l + (int64_t)h * lin_hs + (int64_t)row * lin_ld : nullptr;
-        const float *dl_ptr = (lin && !fused) ? (a.lin_ld ? nl_row + D : a.den_l + (int64_t)h * L + row) : nullptr;
+        const float *nl_row = (lin && !fused_end) ? a.num_l + (int64_t)h * lin_hs + (int64_t)row * lin_ld : nullptr;
+        const float *dl_ptr = (lin && !fused_end) ? (a.lin_ld ? nl_row + D : a.den_l + (int64_t)h * L + row) : nullptr;
         float ss = f, shrink = 0.0f, den = l_true;
         if (lin && row_ok) {
             const float ref = fmaxf(m_nat, 0.0f);
             const float e_ss = expf(m_nat - ref);
             shrink = expf(-ref) * a.linear_mix;
-            den = l_true * e_ss + shrink * (fused ? den_fused : *dl_ptr);
+            den = l_true * e_ss + shrink * (fused_end ? den_fused : *dl_ptr);
             ss = f * e_ss;
         }
         const float inv = 1.0f / den;
@@ -554,12 +770,12 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
         for (int c = 0; c < D; c += 16) {
             uint32_t o[16], nlt[16];
             ptx::tmem_ld16(TM_O + lane_base + c, o);
-            if (fused) ptx::tmem_ld16(tmem + lane_base + c, nlt);
+            if (fused_end) ptx::tmem_ld16(tmem + lane_base + c, nlt);
             ptx::tmem_wait_ld();
             if (!row_ok) continue;
             float v[16];
             const int64_t off = ((int64_t)h * L + row) * D + c;
-            if (fused) {
+            if (fused_end) {
 #pragma unroll
                 for (int i = 0; i < 16; i++)
                     v[i] = (__uint_as_float(o[i]) * ss + shrink * __uint_as_float(nlt[i])) * inv;
@@ -593,6 +809,8 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             }
         }
     }
+    if (threadIdx.x == 0) TB_TRACE_X(71, 4);
+    TB_PH(if (threadIdx.x == 0) tb_phase_done(ph_t0, ph_g0, ph_t1, ph_t2));
     ptx::tc_fence_before();
     __syncthreads();
     if (warp == 5) ptx::tmem_dealloc<256>(tmem);
@@ -1130,5 +1348,18 @@ extern "C" int tb_sla_attention(const tb_sla_args *a, void *stream) {
 #ifdef TB_SLA_TRACE
 extern "C" int tb_sla_trace_read(unsigned long long *host) {
     return cudaMemcpyFromSymbol(host, tb_sla_trace, sizeof(tb_sla_trace)) == cudaSuccess ? 0 : -2;
+}
+// phase[4] then sm[160][4]; reset = 1 re-arms the accumulators
+extern "C" int tb_sla_phase_read(unsigned long long *host, int reset) {
+    if (cudaMemcpyFromSymbol(host, tb_sla_phase, sizeof(tb_sla_phase)) != cudaSuccess) return -2;
+    if (cudaMemcpyFromSymbol(host + 4, tb_sla_sm, sizeof(tb_sla_sm)) != cudaSuccess) return -2;
+    if (reset) {
+        static unsigned long long init[160][4];
+        for (int i = 0; i < 160; i++) { init[i][0] = ~0ull; init[i][1] = 0; init[i][2] = ~0ull; init[i][3] = 0; }
+        unsigned long long z[4] = {0, 0, 0, 0};
+        if (cudaMemcpyToSymbol(tb_sla_phase, z, sizeof(z)) != cudaSuccess) return -2;
+        if (cudaMemcpyToSymbol(tb_sla_sm, init, sizeof(init)) != cudaSuccess) return -2;
+    }
+    return 0;
 }
 #endif
