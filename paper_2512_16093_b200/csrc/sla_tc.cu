@@ -310,8 +310,12 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             ptx::mbar_wait_sleep(&S.k_empty[ks], (uint32_t)(((j / KSTAGES) & 1) ^ 1));
             if (lane == 0) TB_TRACE(j, 10);
             if (ptx::elect_one()) {
+#ifdef TB_X_NOLOAD
+                ptx::mbar_arrive(&S.k_full[ks]);
+#else
                 ptx::mbar_arrive_expect_tx(&S.k_full[ks], K_BYTES);
                 ptx::tma_load_3d(S.k[ks], &tm_k, 0, b * BN, h, &S.k_full[ks]);
+#endif
             }
             __syncwarp();
         }
@@ -334,9 +338,13 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             ptx::mbar_wait_sleep(&S.v_empty[vs], (uint32_t)(((j / VSTAGES) & 1) ^ 1));
             if (lane == 0) TB_TRACE(j, 11);
             if (ptx::elect_one()) {
+#ifdef TB_X_NOLOAD
+                ptx::mbar_arrive(&S.v_full[vs]);
+#else
                 ptx::mbar_arrive_expect_tx(&S.v_full[vs], V_BYTES);
                 ptx::tma_load_3d(S.v[vs], &tm_v, 0, b * BN, h, &S.v_full[vs]);
                 ptx::tma_load_3d(S.v[vs] + V_BYTES / 2, &tm_v, 64, b * BN, h, &S.v_full[vs]);
+#endif
             }
             __syncwarp();
         }
@@ -381,8 +389,11 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             // V [tokens][channels]: channel-contiguous = MN-major B; atoms 64 ch x 8 tokens
             const uint64_t vd = ptx::sdesc_sw128_mn(ptx::smem_u32(S.v[vs]), V_BYTES / 2, 1024);
             if (ptx::elect_one()) {
+#ifndef TB_X_PVN
+#define TB_X_PVN (BN / 16)
+#endif
 #pragma unroll
-                for (int k = 0; k < BN / 16; k++)   // K=16 bf16 per MMA: 8 TMEM cols of P, 16 token rows of V
+                for (int k = 0; k < TB_X_PVN; k++)  // K=16 bf16 per MMA: 8 TMEM cols of P, 16 token rows of V
                     ptx::mma_f16_ts(TM_O, tmem + pb * BN + 8 * k, vd + 128 * k, ID_PV_MN, (lf || i > 0 || k > 0) ? 1u : 0u);
                 ptx::mma_commit(&S.pv_done[pb]);
                 ptx::mma_commit(&S.v_empty[vs]);
@@ -400,8 +411,11 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             if (ptx::elect_one()) {
                 // D = 1 x 6291456 + 1 x 6291456 = 1.5*2^23 (bf16 operands, f32 bits) in every cell
                 if (TB_SLA_BIAS) ptx::mma_f16(tmem + sb * BN, bias_a, bias_b, ID_BIAS, 0u);
+#ifndef TB_X_QKN
+#define TB_X_QKN (D / 32)
+#endif
 #pragma unroll
-                for (int k = 0; k < D / 32; k++)    // K=32 int8 = 32 B per MMA
+                for (int k = 0; k < TB_X_QKN; k++)  // K=32 int8 = 32 B per MMA
                     ptx::mma_i8(tmem + sb * BN, qd + 2 * k, kd + 2 * k, ID_QK, (TB_SLA_BIAS || k > 0) ? 1u : 0u);
                 ptx::mma_commit(&S.s_full[sb]);
                 ptx::mma_commit(&S.k_empty[ks]);

@@ -25,6 +25,19 @@ __global__ void __launch_bounds__(1024, 1) k(int iters, unsigned long long *out,
             if (OP == 4) asm volatile("{.reg .b32 t; cvt.rn.bf16x2.f32 t, %0, %1; mov.b32 %0, t;}" : "+r"(r[i]) : "r"(r[(i + 1) & 7]));
             if (OP == 5) asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+r"(r[i]));
             if (OP == 6) asm volatile("mad.lo.u32 %0, %0, 0x800000, %1;" : "+r"(r[i]) : "r"(r[(i + 1) & 7]));
+            if (OP == 8) asm volatile("cvt.rn.f32.s32 %0, %0;" : "+r"(r[i]));
+            if (OP == 9) {  // FADD2 on a register pair
+                unsigned long long v = ((unsigned long long)r[i] << 32) | r[(i + 1) & 7];
+                asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(v) : "l"(c));
+                r[i] = (uint32_t)v;
+            }
+            if (OP == 10) {  // W8A8 epilogue pair: 2 x I2F + FFMA2
+                asm volatile("cvt.rn.f32.s32 %0, %0;" : "+r"(r[i]));
+                asm volatile("cvt.rn.f32.s32 %0, %0;" : "+r"(r[(i + 1) & 7]));
+                unsigned long long v = ((unsigned long long)r[(i + 2) & 7] << 32) | r[(i + 3) & 7];
+                asm volatile("fma.rn.f32x2 %0, %0, %1, %0;" : "+l"(v) : "l"(c));
+                r[(i + 2) & 7] = (uint32_t)v;
+            }
             if (OP == 7) {  // mix: 1 ex2 + 2 ffma2 + 1 add + 1 f2fp per "element pair"
                 unsigned long long v = ((unsigned long long)r[i] << 32) | r[(i + 1) & 7];
                 asm volatile("fma.rn.f32x2 %0, %0, %1, %0;" : "+l"(v) : "l"(c));
@@ -68,6 +81,9 @@ int main() {
         run<5>("MUFU.EX2", nt, 8);
         run<6>("IMAD", nt, 8);
         run<7>("mix (ffma2,fadd2,ex2,iadd,f2fp)", nt, 40);
+        run<8>("I2F (cvt.rn.f32.s32)", nt, 8);
+        run<9>("FADD2", nt, 8);
+        run<10>("2 I2F + FFMA2", nt, 24);
     }
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
 }
