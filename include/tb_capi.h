@@ -206,6 +206,11 @@ int tb_linear_kv_part(const void *k, const void *v, int64_t H, int64_t L, int64_
 int tb_add_norm(const float *x, const float *y, const float *emb, float alpha, const float *gain, const float *offset,
                 int64_t rows, int64_t cols, float eps, int layer_norm, float *sum_out, void *norm_out, void *stream);
 
+/* Delta merge step (replaces the loop body of merge.apply_deltas,
+ * merge.py:63-70): acc[i] = acc[i] + fl(c * x[i]) with two RN roundings, the
+ * numpy order bit-for-bit; called once per delta in list order. */
+int tb_axpy_rn(float *acc, const float *x, float c, int64_t n, void *stream);
+
 /* quantize_blockwise (block 128) of a logical [rows, cols] matrix stored as
  * cols/128 planes [rows, 128] (a head-major attention output [H, L, 128]);
  * codes [rows, cols] row-major, scales [ceil(rows/128), cols/128]. */

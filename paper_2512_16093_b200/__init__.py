@@ -13,6 +13,6 @@ __version__ = "0.1.0"
 def __getattr__(name):
     # lazy submodule import keeps `import paper_2512_16093_b200` cheap
     import importlib
-    if name in ("attention", "blockquant", "sampler", "ops", "ulysses", "tensor_store"):
+    if name in ("attention", "blockquant", "sampler", "ops", "ulysses", "tensor_store", "merge"):
         return importlib.import_module(f".{name}", __name__)
     raise AttributeError(name)

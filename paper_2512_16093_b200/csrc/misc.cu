@@ -377,3 +377,30 @@ extern "C" int tb_add_norm(const float *x, const float *y, const float *emb, flo
                                                           (__nv_bfloat16 *)norm_out);
     return check_launch("add_norm");
 }
+
+// ------------------------------------------------------------ delta merging
+// merge.py apply_deltas (merge.py:55-71): merged = merged + f32(c) * delta in
+// list order, numpy's two roundings (RN multiply, then RN add; no FMA).
+__global__ void axpy_rn_kernel(float *__restrict__ acc, const float *__restrict__ x, float c, int64_t n) {
+    const int64_t n4 = n >> 2;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+        float4 a = reinterpret_cast<float4 *>(acc)[i];
+        const float4 d = __ldg(reinterpret_cast<const float4 *>(x) + i);
+        a.x = __fadd_rn(a.x, __fmul_rn(c, d.x));
+        a.y = __fadd_rn(a.y, __fmul_rn(c, d.y));
+        a.z = __fadd_rn(a.z, __fmul_rn(c, d.z));
+        a.w = __fadd_rn(a.w, __fmul_rn(c, d.w));
+        reinterpret_cast<float4 *>(acc)[i] = a;
+    }
+    for (int64_t i = 4 * n4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        acc[i] = __fadd_rn(acc[i], __fmul_rn(c, x[i]));
+}
+
+extern "C" int tb_axpy_rn(float *acc, const float *x, float c, int64_t n, void *stream) {
+    TB_REQUIRE(((uintptr_t)acc & 15) == 0 && ((uintptr_t)x & 15) == 0, "acc and x must be 16-byte aligned");
+    if (n == 0) return TB_OK;
+    const int64_t blocks = imin64(cdiv(cdiv(n, 4), 256), 148 * 8);
+    axpy_rn_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(acc, x, c, n);
+    return check_launch("axpy_rn");
+}

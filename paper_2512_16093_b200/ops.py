@@ -539,6 +539,13 @@ def add_norm(x, y=None, emb=None, alpha: float = 0.0, gain=None, offset=None, la
     return (sum_out if write_sum else None), norm
 
 
+def axpy_rn(acc: torch.Tensor, x: torch.Tensor, c: float) -> torch.Tensor:
+    """acc += fl(c * x) in place (f32, two RN roundings; merge.py:68)."""
+    assert acc.dtype == torch.float32 and x.dtype == torch.float32 and acc.is_contiguous()
+    call("tb_axpy_rn", ptr(acc), ptr(x.contiguous()), float(c), acc.numel(), stream_ptr())
+    return acc
+
+
 def gelu(x):
     x = x.float().contiguous()
     out = torch.empty_like(x)
