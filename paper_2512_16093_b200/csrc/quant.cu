@@ -351,6 +351,7 @@ __global__ void __launch_bounds__(256) pool_quant_tile_kernel(
             if ((tid & 31) == 0) red[blk][(tid >> 5) & 1] = am;
         }
     }
+    if (codes == nullptr) return;                            // pooling only (uniform)
     __syncthreads();
     if (tid < NBLK && tid * BLOCK < et) {
         const float am = fmaxf(red[tid][0], red[tid][1]);
@@ -596,7 +597,7 @@ static int pool_quant_launch(const void *x, int dtype, const float *center, int6
     TB_REQUIRE(H < 65536, "too many heads");
     dim3 grid((unsigned)nb, (unsigned)H);
     cudaStream_t st = as_stream(stream);
-    const bool fast = d == 128 && codes != nullptr && (block == 64 || block == 128);
+    const bool fast = d == 128 && (codes != nullptr || pooled != nullptr) && (block == 64 || block == 128);
     if (fast && dtype == TB_BF16 && ((uintptr_t)x % 16) == 0 && ((uintptr_t)codes % 16) == 0 &&
         (pooled == nullptr || ((uintptr_t)pooled % 8) == 0) && (center == nullptr || ((uintptr_t)center % 8) == 0)) {
         dim3 tgrid((unsigned)cdiv(L, 128), (unsigned)H);

@@ -163,6 +163,20 @@ def pool_quant_tokens_t(x: torch.Tensor, block: int, center: torch.Tensor | None
     return codes, scales, pooled, pooled_t
 
 
+def pool_tokens_t(x: torch.Tensor, block: int):
+    """pool_block_means (attention.py:256-266) of raw x, plus the transposed
+    [H, d, ldt] copy for the coalesced top-k kernel -> (pooled, pooled_t)."""
+    x = _dev_tensor(x, "x")
+    H, L, d = x.shape
+    nb = cdiv(L, block)
+    ldt = -(-nb // 4) * 4
+    pooled = _empty((H, nb, d), torch.float32, x)
+    pooled_t = _empty((H, d, ldt), torch.float32, x)
+    call("tb_pool_quant_tokens_t", ptr(x), dtype_code(x), None, H, L, d, block, None, None,
+         ptr(pooled), ptr(pooled_t), ldt, stream_ptr())
+    return pooled, pooled_t
+
+
 def topk_count(ratio: float, nkv: int) -> int:
     """attention.py:279."""
     return math.ceil(ratio * nkv)
@@ -392,37 +406,56 @@ def sla_attention(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: fl
     # under the Q / K passes and the (issue-bound) top-k selection.
     side = _side_stream()
     side.wait_stream(main)
-    kv_part = None
-    with torch.cuda.stream(side):
-        km = kmean(k) if quantized else None
-        ev = _KM_EVENT.setdefault(torch.cuda.current_device(), torch.cuda.Event())
-        ev.record(side)
-        if lin and tc:
+    kv_part = lin_pack = lin_kv = cov = None
+    if fast_lin:
+        # Three streams.  The top-k selection needs only the pooled raw K
+        # (attention.py:404-406), so the main stream runs Q pass -> K pooling ->
+        # top-k -> coverage GEMM without waiting for k_mean; k_mean (a
+        # sequential chain) and the K codes that need it run on the side
+        # stream, kv_part (HBM-bound, needs only k and v) on a third from t=0.
+        third = _aux_stream("kvpart")
+        third.wait_stream(main)
+        with torch.cuda.stream(third):
             kv_part = linear_kv_part(kb, vb, kv_block)
-    if quantized:
+        with torch.cuda.stream(side):
+            km = kmean(k)
+            kc, ks, _ = pool_quant_tokens(k, kv_block, km, pool=False)
         qc, qs, qp = pool_quant_tokens(q, q_block, None, pool=True)
-    else:
-        qc = qs = kc = ks = None
-        qp, kp = pool_block_means(q, q_block), pool_block_means(k, kv_block)
-    if quantized:
-        main.wait_stream(side) if not (lin and tc) else main.wait_event(_km_event(side))
-        km.record_stream(main)
-        if fast_lin:
-            kc, ks, kp, kpt = pool_quant_tokens_t(k, kv_block, km)
-        else:
-            kc, ks, kp = pool_quant_tokens(k, kv_block, km, pool=True)
-    lin_pack = lin_kv = None
-    cov = None
-    if lin and tc:
+        kp, kpt = pool_tokens_t(k, kv_block)
         idx, comp, cov = topk_blocks_cov(qp, kp, count, want_comp=return_parts, kpt=kpt)
-        main.wait_stream(side)
+        main.wait_stream(third)
         kv_part.record_stream(main)
         lin_kv = linear_kv_sel(kv_part, cov, nkv)
+        main.wait_stream(side)
+        for t in (km, kc, ks):
+            t.record_stream(main)
     else:
-        idx, comp, _ = topk_blocks(qp, kp, count, want_comp=lin or return_parts)
-        if lin:
-            fast = (H * L * d >= (1 << 22)) if linear_fast is None else linear_fast
-            lin_pack = linear_branch(q, k, v, comp, q_block, kv_block, fast=fast)
+        # Side stream: k_mean (a latency-bound sequential chain) and, for the
+        # tensor-core path, the linear branch's per-block operand kv_part
+        with torch.cuda.stream(side):
+            km = kmean(k) if quantized else None
+            ev = _KM_EVENT.setdefault(torch.cuda.current_device(), torch.cuda.Event())
+            ev.record(side)
+            if lin and tc:
+                kv_part = linear_kv_part(kb, vb, kv_block)
+        if quantized:
+            qc, qs, qp = pool_quant_tokens(q, q_block, None, pool=True)
+            main.wait_stream(side) if not (lin and tc) else main.wait_event(_km_event(side))
+            km.record_stream(main)
+            kc, ks, kp = pool_quant_tokens(k, kv_block, km, pool=True)
+        else:
+            qc = qs = kc = ks = None
+            qp, kp = pool_block_means(q, q_block), pool_block_means(k, kv_block)
+        if lin and tc:
+            idx, comp, cov = topk_blocks_cov(qp, kp, count, want_comp=return_parts, kpt=None)
+            main.wait_stream(side)
+            kv_part.record_stream(main)
+            lin_kv = linear_kv_sel(kv_part, cov, nkv)
+        else:
+            idx, comp, _ = topk_blocks(qp, kp, count, want_comp=lin or return_parts)
+            if lin:
+                fast = (H * L * d >= (1 << 22)) if linear_fast is None else linear_fast
+                lin_pack = linear_branch(q, k, v, comp, q_block, kv_block, fast=fast)
     out = torch.empty((H, L, d), dtype=out_dtype, device=q.device)
     row_max = torch.empty((H, L), dtype=torch.float32, device=q.device) if return_parts else None
     den = torch.empty((H, L), dtype=torch.float32, device=q.device) if return_parts else None
