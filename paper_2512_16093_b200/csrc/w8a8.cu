@@ -264,7 +264,12 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) w8a8_tc_kernel(
 namespace gemm2 {
 constexpr int BM = 128, BN = 256, BK = 128, STAGES = 5;
 constexpr int EPI_WARPS = 8;
-constexpr int THREADS = 64 + EPI_WARPS * 32;
+// warpgroup 0: TMA warp, MMA warp, two idle warps; warpgroups 1-2: the 8
+// epilogue warps.  setmaxnreg moves the control warpgroup's registers to the
+// epilogue (each role's code sits inside the branch that resized it, so ptxas
+// allocates the epilogue against the larger budget)
+constexpr int THREADS = 128 + EPI_WARPS * 32;
+constexpr int CTRL_REGS = 56, EPI_REGS = 224;     // 128*56 + 256*224 <= 64K
 struct Smem {
     uint8_t a[STAGES][BM * BK];
     uint8_t b[STAGES][(BN / 2) * BK];
@@ -281,7 +286,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
     const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
     const __grid_constant__ CUtensorMap tma_out,
     const float *__restrict__ sa, const float *__restrict__ sb, const float *__restrict__ bias,
-    int M, int N, int K) {
+    int M, int N, int K, int plane, int act) {
     using namespace gemm2;
     constexpr int CW = BN / 2;
     constexpr uint32_t TMEM_COLS = 2 * BN;
@@ -307,6 +312,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
     ptx::tc_fence_after();
     const uint32_t tmem = S.tmem_base;
 
+    if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" :: "n"(CTRL_REGS));
     if (warp == 0) {
         if (ptx::elect_one()) {
             int stage = 0;
@@ -350,8 +357,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
                 }
             }
         }
+    }
     } else {
-        const int ew = warp - 2;
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" :: "n"(EPI_REGS));
+        const int ew = warp - 4;
         const int quarter = warp & 3;
         const int half = ew >> 2;
         const uint32_t seg_empty0 = ptx::mapa(ptx::smem_u32(&S.seg_empty[0]), 0);
@@ -385,15 +394,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
                 continue;
 #endif
                 const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + buf * BN + half * CW;
-                uint32_t rb[2][16];
-                ptx::tmem_ld16(taddr, rb[0]);
+                // 32-column groups, double-buffered: tcgen05.wait::ld covers every
+                // outstanding load, so the next group's two loads are issued before
+                // this group's math
+                constexpr int G = 32, NG = CW / G;
+                uint32_t rb[2][G];
+                ptx::tmem_ld16(taddr, *reinterpret_cast<uint32_t (*)[16]>(&rb[0][0]));
+                ptx::tmem_ld16(taddr + 16, *reinterpret_cast<uint32_t (*)[16]>(&rb[0][16]));
                 ptx::tmem_wait_ld();
 #pragma unroll
-                for (int c = 0; c < CW / 16; c++) {
-                    if (c + 1 < CW / 16) ptx::tmem_ld16(taddr + (c + 1) * 16, rb[(c + 1) & 1]);
-                    const uint32_t (&r)[16] = rb[c & 1];
+                for (int g = 0; g < NG; g++) {
+                    if (g + 1 < NG) {
+                        ptx::tmem_ld16(taddr + (g + 1) * G, *reinterpret_cast<uint32_t (*)[16]>(&rb[(g + 1) & 1][0]));
+                        ptx::tmem_ld16(taddr + (g + 1) * G + 16, *reinterpret_cast<uint32_t (*)[16]>(&rb[(g + 1) & 1][16]));
+                    }
+                    const uint32_t (&r)[G] = rb[g & 1];
 #pragma unroll
-                    for (int i = 0; i < 16; i += 2) {
+                    for (int i = 0; i < G; i += 2) {
                         float2 x;
                         if (!EXACT && (i & 6) == 6) {
                             const float2 m = make_float2(__int_as_float((int)r[i] + 0x4B400000),
@@ -402,7 +419,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
                         } else {
                             x = make_float2(__int2float_rn((int)r[i]), __int2float_rn((int)r[i + 1]));
                         }
-                        float2 &o = acc2[(c * 16 + i) >> 1];
+                        float2 &o = acc2[(g * G + i) >> 1];
                         if constexpr (EXACT) {
                             o.x = __fadd_rn(o.x, __fmul_rn(__fmul_rn(x.x, sa2.x), sb2.x));
                             o.y = __fadd_rn(o.y, __fmul_rn(__fmul_rn(x.y, sa2.y), sb2.y));
@@ -410,7 +427,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
                             o = ptx::ffma2(x, sab2, o);
                         }
                     }
-                    ptx::tmem_wait_ld();
+                    if (g + 1 < NG) ptx::tmem_wait_ld();
                 }
                 ptx::tc_fence_before();
                 __syncwarp();
@@ -424,6 +441,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
                     acc2[i].x = __fadd_rn(acc2[i].x, __ldg(bias + col0 + 2 * i));
                     acc2[i].y = __fadd_rn(acc2[i].y, __ldg(bias + col0 + 2 * i + 1));
                 }
+            }
+            if (act == 1) {
+#pragma unroll
+                for (int i = 0; i < CW / 2; i++) { acc2[i].x = gelu_tanh(acc2[i].x); acc2[i].y = gelu_tanh(acc2[i].y); }
             }
             constexpr int CPC = OUT_BF16 ? 64 : 32;
             const uint32_t stg_s = ptx::smem_u32(S.stage_out[ew]);
@@ -455,7 +476,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
                 ptx::fence_async_smem();
                 __syncwarp();
                 if (lane == 0) {
-                    ptx::tma_store_2d(&tma_out, S.stage_out[ew], col0 + ch * CPC, row0);
+                    const int c = col0 + ch * CPC;
+                    if (plane) ptx::tma_store_3d(&tma_out, S.stage_out[ew], c % plane, row0, c / plane);
+                    else ptx::tma_store_2d(&tma_out, S.stage_out[ew], c, row0);
                     ptx::bulk_commit();
                 }
             }
@@ -564,16 +587,21 @@ int w8a8_dispatch(const int8_t *a, const float *sa, const int8_t *bt, const floa
     if (M == 0 || N == 0) return TB_OK;
     const bool tc = block == 128 && K % 128 == 0 && N % 128 == 0 && K > 0 && M < (1ll << 31) &&
                     ((uintptr_t)a % 16) == 0 && ((uintptr_t)bt % 16) == 0 && ((uintptr_t)out % 16) == 0;
-    // the 2-SM kernel measures at parity with the 1-SM one (both epilogue-bound); opt-in
-    static const bool use2sm = [] { const char *e = getenv("TB_W8A8_2SM"); return e && atoi(e) != 0; }();
-    if (tc && use2sm && N % 256 == 0 && M >= 256 && plane == 0 && act == 0) {
+    // 2-SM kernel (CTA pairs, 256x256 tiles, register-rebalanced epilogue) by
+    // default where the shape allows; TB_W8A8_2SM=0 forces the 1-SM kernel
+    static const bool use2sm = [] { const char *e = getenv("TB_W8A8_2SM"); return !e || atoi(e) != 0; }();
+    if (tc && use2sm && N % 256 == 0 && M >= 256) {
         CUtensorMap ta, tbm, tout;
         const bool obf = out_dtype == TB_BF16;
-        if (!make_tmap_2d(&ta, a, CU_TENSOR_MAP_DATA_TYPE_UINT8, K, M, K, 128, 128) ||
-            !make_tmap_2d(&tbm, bt, CU_TENSOR_MAP_DATA_TYPE_UINT8, K, N, K, 128, 128) ||
-            !make_tmap_2d(&tout, out, obf ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, N, M,
-                          N * (obf ? 2 : 4), obf ? 64 : 32, 32))
-            return fail(TB_ECUDA, "cuTensorMapEncodeTiled failed");
+        bool okm = make_tmap_2d(&ta, a, CU_TENSOR_MAP_DATA_TYPE_UINT8, K, M, K, 128, 128) &&
+                   make_tmap_2d(&tbm, bt, CU_TENSOR_MAP_DATA_TYPE_UINT8, K, N, K, 128, 128);
+        if (plane)       // planes [N/plane][M][plane] (bf16), box 64 columns x 32 rows
+            okm = okm && make_tmap_3d(&tout, out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, plane, M, N / plane, plane * 2,
+                                      M * plane * 2, 64, 32, 1);
+        else
+            okm = okm && make_tmap_2d(&tout, out, obf ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                      N, M, N * (obf ? 2 : 4), obf ? 64 : 32, 32);
+        if (!okm) return fail(TB_ECUDA, "cuTensorMapEncodeTiled failed");
         const int ntiles = (int)(cdiv(M, 256) * (N / 256));
         int clusters = num_sms() / 2;
         if (ntiles < clusters) clusters = ntiles;
@@ -582,7 +610,8 @@ int w8a8_dispatch(const int8_t *a, const float *sa, const int8_t *bt, const floa
     {                                                                                                      \
         auto kern = w8a8_2sm_kernel<E, B>;                                                                 \
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm2::SMEM_BYTES);   \
-        kern<<<grid, gemm2::THREADS, gemm2::SMEM_BYTES, st>>>(ta, tbm, tout, sa, sb, bias, (int)M, (int)N, (int)K); \
+        kern<<<grid, gemm2::THREADS, gemm2::SMEM_BYTES, st>>>(ta, tbm, tout, sa, sb, bias, (int)M, (int)N, (int)K, \
+                                                              (int)plane, act);                                  \
     }
         if (exact && !obf) TB_GEMM2(true, false)
         else if (exact) TB_GEMM2(true, true)
