@@ -338,7 +338,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
             constexpr uint32_t idesc = ptx::idesc_i8(2 * BM, BN);
             for (int tile = cluster; tile < ntiles; tile += nclusters) {
                 for (int kb = 0; kb < nkb; kb++) {
-                    ptx::mbar_wait_sleep(&S.seg_empty[buf], bphase ^ 1);
+                    // segment buffer drained (and, fast mode, re-seeded) by both CTAs'
+                    // epilogues; their initial arrive completes phase 0 before first use
+                    ptx::mbar_wait_sleep(&S.seg_empty[buf], bphase);
                     ptx::mbar_wait_sleep(&S.full[stage], phase);
                     ptx::tc_fence_after();
                     const uint64_t ad = ptx::sdesc_sw128(ptx::smem_u32(S.a[stage]));
@@ -346,7 +348,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
                     if (ptx::elect_one()) {
 #pragma unroll
                         for (int k = 0; k < BK / 32; k++)
-                            ptx::mma_i8_pair(tmem + buf * BN, ad + 2 * k, bd + 2 * k, idesc, k > 0 ? 1u : 0u);
+                            ptx::mma_i8_pair(tmem + buf * BN, ad + 2 * k, bd + 2 * k, idesc, (!EXACT || k > 0) ? 1u : 0u);
                         ptx::mma_commit_pair(&S.empty[stage], 0x3);
                         ptx::mma_commit_pair(&S.seg_full[buf], 0x3);
                     }
@@ -367,6 +369,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
         const uint32_t seg_empty1 = ptx::mapa(ptx::smem_u32(&S.seg_empty[1]), 0);
         int buf = 0;
         uint32_t bphase = 0;
+        // fast mode seeds each segment buffer before the MMA accumulates into it:
+        // odd 16-column chunks with the f32 bits of M = 1.5*2^23 (the integer MMA
+        // adds on top, the chunk reads back as the float M + seg and one FADD2 on
+        // the FMA pipe converts a pair), even chunks with 0 (I2FP on the ALU
+        // pipe) -- the conversion load split between the two pipes.
+        // |seg| <= 128*127^2 < 2^22 keeps M + seg exact.
+        auto seed = [&](uint32_t taddr) {
+            uint32_t mbits[16], zero[16];
+#pragma unroll
+            for (int i = 0; i < 16; i++) { mbits[i] = 0x4B400000u; zero[i] = 0u; }
+#pragma unroll
+            for (int c = 0; c < CW / 16; c++) ptx::tmem_st16(taddr + c * 16, (c & 1) ? mbits : zero);
+            ptx::tmem_wait_st();
+        };
+#pragma unroll
+        for (int b = 0; b < 2; b++) {
+            if (!EXACT) seed(tmem + ((uint32_t)(quarter * 32) << 16) + b * BN + half * CW);
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive_cluster(b ? seg_empty1 : seg_empty0);
+        }
         for (int tile = cluster; tile < ntiles; tile += nclusters) {
             const int mp = tile / nnt, nt = tile % nnt;
             const int col0 = nt * BN + half * CW;
@@ -412,10 +435,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
 #pragma unroll
                     for (int i = 0; i < G; i += 2) {
                         float2 x;
-                        if (!EXACT && (i & 6) == 6) {
-                            const float2 m = make_float2(__int_as_float((int)r[i] + 0x4B400000),
-                                                         __int_as_float((int)r[i + 1] + 0x4B400000));
-                            x = ptx::fadd2(m, make_float2(-12582912.0f, -12582912.0f));
+                        if (!EXACT && (((g * G + i) >> 4) & 1)) {        // seeded chunk: M + seg
+                            x = ptx::fadd2(make_float2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])),
+                                           make_float2(-12582912.0f, -12582912.0f));
                         } else {
                             x = make_float2(__int2float_rn((int)r[i]), __int2float_rn((int)r[i + 1]));
                         }
@@ -429,6 +451,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
                     }
                     if (g + 1 < NG) ptx::tmem_wait_ld();
                 }
+                if (!EXACT) seed(taddr);
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive_cluster(buf ? seg_empty1 : seg_empty0);   // the leader's barrier
