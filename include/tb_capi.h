@@ -225,6 +225,16 @@ int tb_w8a8_gemm_fast_ex(const int8_t *a, const float *sa, const int8_t *bt, con
                          int64_t M, int64_t N, int64_t K, int64_t block, void *out, int out_dtype, int64_t plane,
                          int act, void *stream);
 
+/* tb_w8a8_gemm_fast_ex (+ optional GELU) whose epilogue block-quantizes the
+ * bf16-rounded result for the next projection (sampler.py:180-185:
+ * mlp_in -> GELU -> quantize -> mlp_out): codes q_out [M, N] int8 and scales
+ * [ceil(M/128), N/128], bit-identical to tb_quantize_blockwise of the bf16
+ * tb_w8a8_gemm_fast_ex output.  Needs block 128, N % 256 == 0, M >= 256
+ * (TB_EUNSUPPORTED otherwise: the caller runs the two-kernel path). */
+int tb_w8a8_gemm_quant(const int8_t *a, const float *sa, const int8_t *bt, const float *sb, const float *bias,
+                       int64_t M, int64_t N, int64_t K, int64_t block, int act, int8_t *q_out, float *scales_out,
+                       void *stream);
+
 /* Fast-mode W8A8: identical operands, the two block scales folded into one
  * FMA per element (tolerance-level, not bit-exact); used by the DiT step. */
 int tb_w8a8_gemm_fast(const int8_t *a, const float *sa, const int8_t *bt, const float *sb,

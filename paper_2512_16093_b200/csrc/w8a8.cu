@@ -276,18 +276,23 @@ struct Smem {
     uint64_t full[STAGES], empty[STAGES];
     uint64_t seg_full[2], seg_empty[2];
     uint32_t tmem_base;
+    float qred[2][4];                          // OUTM 2: per (column half, row quarter) absmax
     alignas(1024) uint8_t stage_out[EPI_WARPS][32 * 128];
 };
 constexpr size_t SMEM_BYTES = sizeof(Smem) + 1024;
 }  // namespace gemm2
 
-template <bool EXACT, bool OUT_BF16>
+// OUTM: 0 f32, 1 bf16, 2 block-quantized INT8 (the next projection's A
+// operand: the bf16-rounded result quantized per 128x128 block exactly like
+// quantize_blockwise, codes TMA-stored, one f32 scale per block to qscales).
+template <bool EXACT, int OUTM>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w8a8_2sm_kernel(
     const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
     const __grid_constant__ CUtensorMap tma_out,
     const float *__restrict__ sa, const float *__restrict__ sb, const float *__restrict__ bias,
-    int M, int N, int K, int plane, int act) {
+    int M, int N, int K, int plane, int act, float *__restrict__ qscales) {
     using namespace gemm2;
+    constexpr bool OUT_BF16 = OUTM == 1;
     constexpr int CW = BN / 2;
     constexpr uint32_t TMEM_COLS = 2 * BN;
     extern __shared__ uint8_t smem_raw[];
@@ -469,9 +474,54 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
 #pragma unroll
                 for (int i = 0; i < CW / 2; i++) { acc2[i].x = gelu_tanh(acc2[i].x); acc2[i].y = gelu_tanh(acc2[i].y); }
             }
-            constexpr int CPC = OUT_BF16 ? 64 : 32;
             const uint32_t stg_s = ptx::smem_u32(S.stage_out[ew]);
             const int row0 = mp * 2 * BM + (int)rank * BM + quarter * 32;
+            if constexpr (OUTM == 2) {
+                // block absmax of the bf16-rounded values (rows >= M excluded) over
+                // the 4 row-quarter warps of this column half (named barrier per half)
+                const bool rok = row0 + lane < M;
+                float am = 0.0f;
+#pragma unroll
+                for (int i = 0; i < CW / 2; i++) {
+                    acc2[i].x = __bfloat162float(__float2bfloat16_rn(acc2[i].x));
+                    acc2[i].y = __bfloat162float(__float2bfloat16_rn(acc2[i].y));
+                    am = fmaxf(am, fmaxf(fabsf(acc2[i].x), fabsf(acc2[i].y)));
+                }
+                am = warp_max<32>(rok ? am : 0.0f);
+                if (lane == 0) S.qred[half][quarter] = am;
+                ptx::named_bar_sync(1 + half, 128);
+                am = fmaxf(fmaxf(S.qred[half][0], S.qred[half][1]), fmaxf(S.qred[half][2], S.qred[half][3]));
+                ptx::named_bar_sync(1 + half, 128);            // qred reusable
+                const float sc = quant_scale(am);
+                if (quarter == 0 && lane == 0 && mb < nmb) qscales[(int64_t)mb * nnb + nb] = sc;
+                const float safe = (sc == 0.0f) ? 1.0f : sc;
+                const float inv = __frcp_rn(safe);
+                const bool exq = !(safe >= 1.17549435e-38f && inv <= 3.0e38f);   // subnormal scale: exact division
+                if (lane == 0) ptx::bulk_wait_read0();
+                __syncwarp();
+#pragma unroll
+                for (int u = 0; u < 8; u++) {                  // 16 codes (one 16-B unit) per step
+                    uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+                    for (int j = 0; j < 16; j++) {
+                        const float2 pr = acc2[(16 * u + j) >> 1];
+                        const float v = (j & 1) ? pr.y : pr.x;
+                        const uint32_t c8 = exq ? (uint32_t)(uint8_t)quant_code(v, safe) : quant_code_fast(v, safe, inv);
+                        w[j >> 2] |= c8 << ((j & 3) * 8);
+                    }
+                    const uint32_t dst = stg_s + lane * 128 + ((u ^ (lane & 7)) * 16);
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" :: "r"(dst), "r"(w[0]), "r"(w[1]),
+                                 "r"(w[2]), "r"(w[3]) : "memory");
+                }
+                ptx::fence_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    ptx::tma_store_2d(&tma_out, S.stage_out[ew], col0, row0);
+                    ptx::bulk_commit();
+                }
+                continue;
+            }
+            constexpr int CPC = OUT_BF16 ? 64 : 32;
 #pragma unroll
             for (int ch = 0; ch < CW / CPC; ch++) {
                 if (lane == 0) ptx::bulk_wait_read0();
@@ -631,10 +681,10 @@ int w8a8_dispatch(const int8_t *a, const float *sa, const int8_t *bt, const floa
         const int grid = 2 * clusters;
 #define TB_GEMM2(E, B)                                                                                     \
     {                                                                                                      \
-        auto kern = w8a8_2sm_kernel<E, B>;                                                                 \
+        auto kern = w8a8_2sm_kernel<E, (B) ? 1 : 0>;                                                       \
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm2::SMEM_BYTES);   \
         kern<<<grid, gemm2::THREADS, gemm2::SMEM_BYTES, st>>>(ta, tbm, tout, sa, sb, bias, (int)M, (int)N, (int)K, \
-                                                              (int)plane, act);                                  \
+                                                              (int)plane, act, nullptr);                         \
     }
         if (exact && !obf) TB_GEMM2(true, false)
         else if (exact) TB_GEMM2(true, true)
@@ -709,4 +759,32 @@ extern "C" int tb_w8a8_gemm_fast_ex(const int8_t *a, const float *sa, const int8
                                     const float *bias, int64_t M, int64_t N, int64_t K, int64_t block, void *out,
                                     int out_dtype, int64_t plane, int act, void *stream) {
     return w8a8_dispatch(a, sa, bt, sb, bias, M, N, K, block, out, out_dtype, 0, as_stream(stream), plane, act);
+}
+
+// Fast-mode GEMM whose epilogue block-quantizes its (bf16-rounded, optionally
+// GELU'd) result for the next projection: codes [M, N] int8 row-major and
+// scales [ceil(M/128), N/128] f32, bit-identical to tb_quantize_blockwise of
+// the bf16 output of tb_w8a8_gemm_fast_ex.  2-SM kernel shapes only
+// (N % 256 == 0, M >= 256, K % 128 == 0); TB_EUNSUPPORTED otherwise.
+extern "C" int tb_w8a8_gemm_quant(const int8_t *a, const float *sa, const int8_t *bt, const float *sb,
+                                  const float *bias, int64_t M, int64_t N, int64_t K, int64_t block, int act,
+                                  int8_t *q_out, float *scales_out, void *stream) {
+    TB_REQUIRE(act == 0 || act == 1, "act must be 0 (none) or 1 (gelu-tanh)");
+    if (M == 0 || N == 0) return TB_OK;
+    const bool ok = block == 128 && K % 128 == 0 && K > 0 && N % 256 == 0 && M >= 256 && M < (1ll << 31) &&
+                    ((uintptr_t)a % 16) == 0 && ((uintptr_t)bt % 16) == 0 && ((uintptr_t)q_out % 16) == 0;
+    if (!ok) return fail(TB_EUNSUPPORTED, "quantizing epilogue needs block 128, N % 256 == 0, M >= 256");
+    CUtensorMap ta, tbm, tout;
+    if (!make_tmap_2d(&ta, a, CU_TENSOR_MAP_DATA_TYPE_UINT8, K, M, K, 128, 128) ||
+        !make_tmap_2d(&tbm, bt, CU_TENSOR_MAP_DATA_TYPE_UINT8, K, N, K, 128, 128) ||
+        !make_tmap_2d(&tout, q_out, CU_TENSOR_MAP_DATA_TYPE_UINT8, N, M, N, 128, 32))
+        return fail(TB_ECUDA, "cuTensorMapEncodeTiled failed");
+    const int ntiles = (int)(cdiv(M, 256) * (N / 256));
+    int clusters = num_sms() / 2;
+    if (ntiles < clusters) clusters = ntiles;
+    auto kern = w8a8_2sm_kernel<false, 2>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm2::SMEM_BYTES);
+    kern<<<2 * clusters, gemm2::THREADS, gemm2::SMEM_BYTES, as_stream(stream)>>>(
+        ta, tbm, tout, sa, sb, bias, (int)M, (int)N, (int)K, 0, act, scales_out);
+    return check_launch("w8a8_gemm_quant");
 }

@@ -123,8 +123,8 @@ def block_forward(x: torch.Tensor, sigma: float, w: DeviceLayer, heads: int, sla
     # x2 = x1 + po and b = LayerNorm(x2), one pass (x2 overwrites x1)
     x2, b = ops.add_norm(x1, po, None, 0.0, w.ln_gain, w.ln_offset, layer_norm=True, sum_out=x1)
     bq, bsc = ops.quantize_blockwise(b, 128, check_finite=False)
-    h1 = ops.w8a8_gemm_ex(bq, bsc, w.mlp_in.bt, w.mlp_in.scales, 128, None, torch.bfloat16, act=1)  # GELU fused
-    hq, hsc = ops.quantize_blockwise(h1, 128, check_finite=False)
+    # mlp_in -> GELU -> block quantization for mlp_out, all in the GEMM epilogue
+    hq, hsc = ops.w8a8_gemm_quant(bq, bsc, w.mlp_in.bt, w.mlp_in.scales, 128, None, act=1)
     p2 = ops.w8a8_gemm(hq, hsc, w.mlp_out.bt, w.mlp_out.scales, 128, None, torch.float32, exact=False)
     return x2, p2
 

@@ -107,6 +107,26 @@ def w8a8_gemm_ex(a_q, a_s, bt_q, b_s, block: int = 128, bias=None, out_dtype=tor
     return out
 
 
+def w8a8_gemm_quant(a_q, a_s, bt_q, b_s, block: int = 128, bias=None, act: int = 0):
+    """Fast-mode W8A8 (+ GELU when act=1) whose result is block-quantized for the
+    next projection -> (codes int8 [M, N], scales [ceil(M/128), N/128]); equal to
+    quantize_blockwise(w8a8_gemm_ex(..., bf16, act=act)).  One kernel (the
+    quantization in the GEMM epilogue) where the 2-SM kernel applies."""
+    M, K = a_q.shape
+    N = bt_q.shape[0]
+    if bt_q.shape[1] != K:
+        raise ValueError(f"inner dims differ: {K} vs {bt_q.shape[1]}")
+    if not (block == 128 and K % 128 == 0 and N % 256 == 0 and M >= 256):
+        h = w8a8_gemm_ex(a_q, a_s, bt_q, b_s, block, bias, torch.bfloat16, act=act)
+        return quantize_blockwise(h, block, check_finite=False)
+    q = _empty((M, N), torch.int8, a_q)
+    sc = _empty((cdiv(M, 128), N // 128), torch.float32, a_q)
+    call("tb_w8a8_gemm_quant", ptr(a_q.contiguous()), ptr(a_s.contiguous()), ptr(bt_q.contiguous()),
+         ptr(b_s.contiguous()), ptr(None if bias is None else bias.float().contiguous()), M, N, K, block, act,
+         ptr(q), ptr(sc), stream_ptr())
+    return q, sc
+
+
 def quantized_linear(x, bt_q, b_s, block: int = 128, bias=None, out_dtype=torch.float32, exact: bool = True,
                      check_finite: bool = False):
     """quantized_linear_forward (blockquant.py:164-182): activation quant + W8A8."""

@@ -305,6 +305,26 @@ def test_w8a8_planar_output_and_gelu_epilogue(tb):
     assert torch.allclose(gel, want, rtol=2e-2, atol=2e-2)
 
 
+@pytest.mark.parametrize("M,act,bias", [(640, 1, False), (300, 0, True), (1000, 1, True)])
+def test_w8a8_gemm_quant_epilogue_matches_two_kernel_path(tb, M, act, bias):
+    """tb_w8a8_gemm_quant: the GEMM epilogue's block quantization of the
+    bf16-rounded (GELU'd) result is bit-identical to quantize_blockwise of the
+    bf16 GEMM output -- ragged last row block (rows >= M excluded from the
+    absmax) and bias included."""
+    K, N = 512, 768
+    g = torch.Generator(device="cuda").manual_seed(7 + M)
+    xq = torch.randint(-127, 128, (M, K), dtype=torch.int8, device="cuda", generator=g)
+    xs = torch.rand((-(-M // 128), K // 128), device="cuda", generator=g) * 0.01
+    bt = torch.randint(-127, 128, (N, K), dtype=torch.int8, device="cuda", generator=g)
+    bs = torch.rand((K // 128, N // 128), device="cuda", generator=g) * 0.01
+    b = torch.randn(N, device="cuda", generator=g) if bias else None
+    q, s = tb.w8a8_gemm_quant(xq, xs, bt, bs, 128, b, act=act)
+    h = tb.w8a8_gemm_ex(xq, xs, bt, bs, 128, b, torch.bfloat16, act=act)
+    q2, s2 = tb.quantize_blockwise(h, 128, check_finite=False)
+    assert torch.equal(s, s2)
+    assert torch.equal(q, q2)
+
+
 def test_quantize_blockwise_planar_matches_row_major(tb):
     H, L = 6, 1000
     g = torch.Generator(device="cuda").manual_seed(6)
