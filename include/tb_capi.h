@@ -153,6 +153,12 @@ typedef struct tb_sla_args {
     float *out;                        /* [H,L,d] f32 (or bf16 when out_dtype) */
     int out_dtype;
     float *row_max, *den;              /* optional [H,L] sparse-branch stats */
+    /* out_dtype == TB_I8 (tensor-core path, no row_max / den): out holds the
+     * block-quantized bf16-rounded output as the out-projection's A operand --
+     * int8 codes [L, H*d] row-major (token, head*d + channel) -- and
+     * out_scales [ceil(L/128), H] its 128 x 128 block scales (one per
+     * (q-block, head) tile; quantize_blockwise_planar semantics) */
+    float *out_scales;
 } tb_sla_args;
 
 /* _sparse_branch + combine (attention.py:347-389, 392-421).  d==128,

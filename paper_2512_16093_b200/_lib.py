@@ -78,6 +78,7 @@ class SlaArgs(ctypes.Structure):
         ("out", _P),
         ("out_dtype", _i),
         ("row_max", _P), ("den", _P),
+        ("out_scales", _P),
     ]
 
 

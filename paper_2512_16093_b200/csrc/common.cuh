@@ -50,6 +50,42 @@ __device__ __forceinline__ uint32_t quant_code_fast(float x, float safe, float i
     return (uint32_t)__float_as_int(u) & 0xFFu;
 }
 
+// quant_code_fast for N (multiple of 4) values packed into N/4 words
+// (little-endian bytes), branch-free on the common path: the rare near-tie
+// elements (|dlt| within 2^-15 of 0.5) are collected in a mask and redone with
+// the exact division afterwards, so the unrolled loop carries no per-element
+// branch.
+template <int N>
+__device__ __forceinline__ void quant_fast_n(const float (&x)[N], float safe, float inv, bool exact_all,
+                                             uint32_t (&w)[N / 4]) {
+    uint32_t need = 0u;
+#pragma unroll
+    for (int k = 0; k < N / 4; k++) w[k] = 0u;
+#pragma unroll
+    for (int i = 0; i < N; i++) {
+        const float u = __fmaf_rn(x[i], inv, 12582912.0f);
+        const float t = __fsub_rn(u, 12582912.0f);
+        const float dlt = __fmaf_rn(x[i], inv, -t);
+        need |= (uint32_t)(fabsf(dlt) > 0.5f - 0x1p-15f) << i;
+        w[i >> 2] |= ((uint32_t)__float_as_int(u) & 0xFFu) << ((i & 3) * 8);
+    }
+    if (exact_all) need = ~0u;
+    if (need) {
+#pragma unroll
+        for (int i = 0; i < N; i++) {             // static indices keep x[] in registers
+            if ((need >> i) & 1u) {
+                const uint32_t c8 = (uint32_t)(uint8_t)quant_code(x[i], safe);
+                const int sh = (i & 3) * 8;
+                w[i >> 2] = (w[i >> 2] & ~(0xFFu << sh)) | (c8 << sh);
+            }
+        }
+    }
+}
+__device__ __forceinline__ void quant16_fast(const float (&x)[16], float safe, float inv, bool exact_all,
+                                             uint32_t (&w)[4]) {
+    quant_fast_n<16>(x, safe, inv, exact_all, w);
+}
+
 template <int N>
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll

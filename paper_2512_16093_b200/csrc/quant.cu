@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(256) quantize_blockwise_kernel(
 // output [H, L, head_dim]); codes and scales are written for the logical
 // [rows, cols] matrix (the out-projection's A operand).
 template <typename T, bool PLANAR = false>
-__global__ void __launch_bounds__(256) quantize_blockwise128_kernel(
+__global__ void __launch_bounds__(256, sizeof(T) == 2 ? 3 : 2) quantize_blockwise128_kernel(
     const T *__restrict__ x, int64_t rows, int64_t cols, int64_t nbc,
     int8_t *__restrict__ q, float *__restrict__ scales, int32_t *__restrict__ nonfinite) {
     __shared__ float red[32];
@@ -60,20 +60,43 @@ __global__ void __launch_bounds__(256) quantize_blockwise128_kernel(
     const int lane16 = threadIdx.x & 15;           // column group (8 cols each)
     const int rsub = threadIdx.x >> 4;             // 16 rows per pass
     const bool col_ok = lane16 * 8 < nc;
-    float v[8][8];
+    // bf16 input stays packed in registers (32 instead of 64), so 4 CTAs fit
+    // per SM and 128 KB of loads are in flight per SM; unpacked on use
+    constexpr bool PACKED = sizeof(T) == 2;
+    float v[PACKED ? 1 : 8][8];
+    uint4 raw[PACKED ? 8 : 1];
+    auto unpack = [&](int p, float (&f)[8]) {
+        const __nv_bfloat162 *b = reinterpret_cast<const __nv_bfloat162 *>(&raw[PACKED ? p : 0]);
+#pragma unroll
+        for (int j = 0; j < 4; j++) { const float2 t = __bfloat1622float2(b[j]); f[2 * j] = t.x; f[2 * j + 1] = t.y; }
+    };
     float am = 0.0f;
     bool bad = false;
+#pragma unroll
+    for (int p = 0; p < 8; p++) {
+        int r = rsub + p * 16;
+        if constexpr (PACKED) raw[p] = make_uint4(0u, 0u, 0u, 0u);
+        if (col_ok && r < nr) {
+            const T *src = PLANAR ? x + (c0 / 128) * rows * 128 + (r0 + r) * 128 + lane16 * 8
+                                  : x + (r0 + r) * cols + c0 + lane16 * 8;
+            if constexpr (PACKED) raw[p] = __ldg(reinterpret_cast<const uint4 *>(src));
+        }
+    }
 #pragma unroll
     for (int p = 0; p < 8; p++) {
         int r = rsub + p * 16;
         if (col_ok && r < nr) {
             const T *src = PLANAR ? x + (c0 / 128) * rows * 128 + (r0 + r) * 128 + lane16 * 8
                                   : x + (r0 + r) * cols + c0 + lane16 * 8;
-            if constexpr (sizeof(T) == 2) {
-                uint4 raw = *reinterpret_cast<const uint4 *>(src);
-                const __nv_bfloat16 *b = reinterpret_cast<const __nv_bfloat16 *>(&raw);
+            float vv[8];
+            if constexpr (PACKED) {
+                unpack(p, vv);
 #pragma unroll
-                for (int j = 0; j < 8; j++) v[p][j] = __bfloat162float(b[j]);
+                for (int j = 0; j < 8; j++) {
+                    bad |= !isfinite(vv[j]);
+                    am = fmaxf(am, fabsf(vv[j]));
+                }
+                continue;
             } else {
                 float4 a = *reinterpret_cast<const float4 *>(src);
                 float4 b = *reinterpret_cast<const float4 *>(src + 4);
@@ -98,13 +121,16 @@ __global__ void __launch_bounds__(256) quantize_blockwise128_kernel(
     for (int p = 0; p < 8; p++) {
         int r = rsub + p * 16;
         if (col_ok && r < nr) {
-            uint32_t w[2] = {0, 0};
+            // branch-free fast codes (bit-identical; near-ties redone exactly)
+            float vq[8];
+            if constexpr (PACKED) {
+                unpack(p, vq);
+            } else {
 #pragma unroll
-            for (int j = 0; j < 8; j++) {
-                const uint32_t c8 = exact ? (uint32_t)(uint8_t)quant_code(v[p][j], safe)
-                                          : quant_code_fast(v[p][j], safe, inv);    // bit-identical
-                w[j >> 2] |= c8 << ((j & 3) * 8);
+                for (int j = 0; j < 8; j++) vq[j] = v[p][j];
             }
+            uint32_t w[2];
+            quant_fast_n<8>(vq, safe, inv, exact, w);
             *reinterpret_cast<uint2 *>(q + (r0 + r) * cols + c0 + lane16 * 8) = make_uint2(w[0], w[1]);
         }
     }
@@ -377,15 +403,16 @@ __global__ void __launch_bounds__(256) pool_quant_tile_kernel(
         uint32_t wv[8];
         *reinterpret_cast<uint4 *>(&wv[0]) = src[0];
         *reinterpret_cast<uint4 *>(&wv[4]) = src[1];
-        uint32_t out[4] = {0u, 0u, 0u, 0u};
+        float xv[16];
 #pragma unroll
         for (int i = 0; i < 16; i++) {
             const uint32_t w = wv[i >> 1];
             float v = __uint_as_float((i & 1) ? (w & 0xFFFF0000u) : (w << 16));
             if (center) v = __fsub_rn(v, cg[i]);
-            const uint32_t c8 = exact ? (uint32_t)(uint8_t)quant_code(v, safe) : quant_code_fast(v, safe, inv);
-            out[i >> 2] |= c8 << ((i & 3) * 8);
+            xv[i] = v;
         }
+        uint32_t out[4];
+        quant16_fast(xv, safe, inv, exact, out);
         *reinterpret_cast<uint4 *>(codes + (h * L + lo + t) * 128 + 16 * g) = make_uint4(out[0], out[1], out[2], out[3]);
     }
 }

@@ -780,15 +780,13 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             if (a.row_max) a.row_max[(int64_t)h * L + row] = m_nat;
             if (a.den) a.den[(int64_t)h * L + row] = l_true;
         }
-#pragma unroll 1
-        for (int c = 0; c < D; c += 16) {
+        // final values of 16 output channels from TMEM (O, and the end-of-kernel
+        // linear numerator when fused_end) and the combine factors above
+        auto out16 = [&](int c, float (&v)[16]) {
             uint32_t o[16], nlt[16];
             ptx::tmem_ld16(TM_O + lane_base + c, o);
             if (fused_end) ptx::tmem_ld16(tmem + lane_base + c, nlt);
             ptx::tmem_wait_ld();
-            if (!row_ok) continue;
-            float v[16];
-            const int64_t off = ((int64_t)h * L + row) * D + c;
             if (fused_end) {
 #pragma unroll
                 for (int i = 0; i < 16; i++)
@@ -796,7 +794,7 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             } else if (lin) {
 #pragma unroll
                 for (int i = 0; i < 16; i += 4) {
-                    const float4 nl = *reinterpret_cast<const float4 *>(nl_row + c + i);
+                    const float4 nl = row_ok ? *reinterpret_cast<const float4 *>(nl_row + c + i) : make_float4(0.f, 0.f, 0.f, 0.f);
                     v[i] = (__uint_as_float(o[i]) * ss + shrink * nl.x) * inv;
                     v[i + 1] = (__uint_as_float(o[i + 1]) * ss + shrink * nl.y) * inv;
                     v[i + 2] = (__uint_as_float(o[i + 2]) * ss + shrink * nl.z) * inv;
@@ -806,20 +804,64 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
 #pragma unroll
                 for (int i = 0; i < 16; i++) v[i] = __uint_as_float(o[i]) * f * inv;
             }
-            if (a.out_dtype == TB_BF16) {
-                __nv_bfloat16 *dst = reinterpret_cast<__nv_bfloat16 *>(a.out) + off;
+        };
+        if (a.out_dtype == TB_I8) {
+            // The out-projection's A operand straight from the epilogue: the
+            // bf16-rounded tile (what a bf16 output would hold) quantized as one
+            // 128 x 128 block -- absmax over the tile's valid rows (4 warps,
+            // named barrier), then the codes in a second TMEM pass
+            // (quantize_blockwise semantics, blockquant.py:91-110)
+            float am = 0.0f;
+#pragma unroll 1
+            for (int c = 0; c < D; c += 16) {
+                float v[16];
+                out16(c, v);
 #pragma unroll
-                for (int i = 0; i < 16; i += 8) {
-                    uint4 w;
-                    __nv_bfloat162 *p = reinterpret_cast<__nv_bfloat162 *>(&w);
+                for (int i = 0; i < 16; i++) am = fmaxf(am, fabsf(__bfloat162float(__float2bfloat16_rn(v[i]))));
+            }
+            am = warp_max<32>(row_ok ? am : 0.0f);
+            if (lane == 0) S.corr_s[warp] = am;       // the prologue's scratch, long since consumed
+            ptx::named_bar_sync(1, BM);
+            am = fmaxf(fmaxf(S.corr_s[0], S.corr_s[1]), fmaxf(S.corr_s[2], S.corr_s[3]));
+            const float sc = quant_scale(am);
+            if (threadIdx.x == 0) a.out_scales[(int64_t)n * a.H + h] = sc;
+            const float safe = (sc == 0.0f) ? 1.0f : sc;
+            const float rq = __frcp_rn(safe);
+            const bool exq = !(safe >= 1.17549435e-38f && rq <= 3.0e38f);   // subnormal scale: exact division
+            int8_t *dst = reinterpret_cast<int8_t *>(a.out) + (int64_t)row * (a.H * D) + (int64_t)h * D;
+#pragma unroll 1
+            for (int c = 0; c < D; c += 16) {
+                float v[16];
+                out16(c, v);
 #pragma unroll
-                    for (int u = 0; u < 4; u++) p[u] = __floats2bfloat162_rn(v[i + 2 * u], v[i + 2 * u + 1]);
-                    *reinterpret_cast<uint4 *>(dst + i) = w;
+                for (int i = 0; i < 16; i++) v[i] = __bfloat162float(__float2bfloat16_rn(v[i]));
+                uint32_t w[4];
+                quant16_fast(v, safe, rq, exq, w);
+                if (row_ok) *reinterpret_cast<uint4 *>(dst + c) = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+        } else {
+#pragma unroll 1
+            for (int c = 0; c < D; c += 16) {
+                float v[16];
+                out16(c, v);
+                if (!row_ok) continue;
+                const int64_t off = ((int64_t)h * L + row) * D + c;
+                if (a.out_dtype == TB_BF16) {
+                    __nv_bfloat16 *dst = reinterpret_cast<__nv_bfloat16 *>(a.out) + off;
+#pragma unroll
+                    for (int i = 0; i < 16; i += 8) {
+                        uint4 w;
+                        __nv_bfloat162 *p = reinterpret_cast<__nv_bfloat162 *>(&w);
+#pragma unroll
+                        for (int u = 0; u < 4; u++) p[u] = __floats2bfloat162_rn(v[i + 2 * u], v[i + 2 * u + 1]);
+                        *reinterpret_cast<uint4 *>(dst + i) = w;
+                    }
+                } else {
+                    float *dst = a.out + off;
+#pragma unroll
+                    for (int i = 0; i < 16; i += 4)
+                        *reinterpret_cast<float4 *>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
                 }
-            } else {
-                float *dst = a.out + off;
-#pragma unroll
-                for (int i = 0; i < 16; i += 4) *reinterpret_cast<float4 *>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
             }
         }
     }
@@ -1285,6 +1327,11 @@ __global__ void __launch_bounds__(sla2::THREADS, 1) sla_tc2_kernel(
 
 int sla_simt(const tb_sla_args *a, cudaStream_t st);
 
+int tb_sla_kernel_variant() {
+    static const int variant = [] { const char *e = getenv("TB_SLA_KERNEL"); return e ? atoi(e) : 1; }();
+    return variant;
+}
+
 bool sla_tc_supported(const tb_sla_args *a) {
     static_assert(sla2::MAX_SEL == sla::MAX_SEL, "table sizes");
     return a->quantized && a->d == 128 && a->q_block == 128 && a->kv_block == 64 &&
@@ -1308,7 +1355,7 @@ int sla_tc(const tb_sla_args *a, cudaStream_t st) {
     if (!ok) return fail(TB_ECUDA, "cuTensorMapEncodeTiled failed (sla)");
     // the exact-max variant only when the caller asks for the sparse-branch stats
     const bool exact = a->row_max != nullptr || a->den != nullptr;
-    static const int variant = [] { const char *e = getenv("TB_SLA_KERNEL"); return e ? atoi(e) : 1; }();   // 2: two-tile kernel (measured slower, kept for study)
+    const int variant = a->out_dtype == TB_I8 ? 1 : tb_sla_kernel_variant();   // 2: two-tile kernel (measured slower, kept for study)
     if (variant == 2) {
         dim3 grid2((unsigned)cdiv(nq, 2), (unsigned)a->H);
         auto launch2 = [&](auto kern) {
@@ -1354,6 +1401,8 @@ extern "C" int tb_sla_attention(const tb_sla_args *a, void *stream) {
                "quantized branch needs codes, scales and k_mean");
     if (a->H == 0) return TB_OK;
     cudaStream_t st = as_stream(stream);
+    TB_REQUIRE(a->out_dtype != TB_I8 || (a->out_scales != nullptr && sla_tc_supported(a)),
+               "int8 output needs the tensor-core kernel and out_scales");
     if (sla_tc_supported(a)) return sla_tc(a, st);
     TB_REQUIRE(a->lin_kv == nullptr, "fused linear epilogue needs the tensor-core envelope");
     return sla_simt(a, st);

@@ -501,14 +501,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
                 __syncwarp();
 #pragma unroll
                 for (int u = 0; u < 8; u++) {                  // 16 codes (one 16-B unit) per step
-                    uint32_t w[4] = {0u, 0u, 0u, 0u};
+                    float xv[16];
 #pragma unroll
-                    for (int j = 0; j < 16; j++) {
-                        const float2 pr = acc2[(16 * u + j) >> 1];
-                        const float v = (j & 1) ? pr.y : pr.x;
-                        const uint32_t c8 = exq ? (uint32_t)(uint8_t)quant_code(v, safe) : quant_code_fast(v, safe, inv);
-                        w[j >> 2] |= c8 << ((j & 3) * 8);
-                    }
+                    for (int j = 0; j < 8; j++) { xv[2 * j] = acc2[8 * u + j].x; xv[2 * j + 1] = acc2[8 * u + j].y; }
+                    uint32_t w[4];
+                    quant16_fast(xv, safe, inv, exq, w);
                     const uint32_t dst = stg_s + lane * 128 + ((u ^ (lane & 7)) * 16);
                     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" :: "r"(dst), "r"(w[0]), "r"(w[1]),
                                  "r"(w[2]), "r"(w[3]) : "memory");

@@ -117,8 +117,15 @@ def block_forward(x: torch.Tensor, sigma: float, w: DeviceLayer, heads: int, sla
         # qkv lands head-major [3H, L, hd] straight from the GEMM epilogue (no permute);
         # the out-projection quantizes the head-major attention output in place
         qkv = ops.w8a8_gemm_ex(aq, asc, w.qkv.bt, w.qkv.scales, 128, None, torch.bfloat16, plane=hd)
-        o = attn(qkv[:heads], qkv[heads:2 * heads], qkv[2 * heads:])           # [H, L, hd]
-        oq, osc = ops.quantize_blockwise_planar(o)
+        if hd == 128 and Lp >= 128:
+            # the attention epilogue emits the out-projection's block-quantized
+            # A operand (codes [L, H*hd] + scales) directly
+            oq, osc = ops.sla_attention(qkv[:heads], qkv[heads:2 * heads], qkv[2 * heads:], sla["q_block"],
+                                        sla["kv_block"], sla["topk_ratio"], sla.get("linear_mix", 1.0), True,
+                                        out_dtype=torch.int8)
+        else:
+            o = attn(qkv[:heads], qkv[heads:2 * heads], qkv[2 * heads:])           # [H, L, hd]
+            oq, osc = ops.quantize_blockwise_planar(o)
     po = ops.w8a8_gemm(oq, osc, w.out_proj.bt, w.out_proj.scales, 128, None, torch.float32, exact=False)
     # x2 = x1 + po and b = LayerNorm(x2), one pass (x2 overwrites x1)
     x2, b = ops.add_norm(x1, po, None, 0.0, w.ln_gain, w.ln_offset, layer_norm=True, sum_out=x1)

@@ -14,7 +14,7 @@ import math
 import torch
 
 from . import _lib
-from ._lib import TB_BF16, TB_F32, call, dtype_code, ptr, stream_ptr
+from ._lib import TB_BF16, TB_F32, TB_I8, call, dtype_code, ptr, stream_ptr
 
 
 def cdiv(a: int, b: int) -> int:
@@ -476,7 +476,14 @@ def sla_attention(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: fl
             if lin:
                 fast = (H * L * d >= (1 << 22)) if linear_fast is None else linear_fast
                 lin_pack = linear_branch(q, k, v, comp, q_block, kv_block, fast=fast)
-    out = torch.empty((H, L, d), dtype=out_dtype, device=q.device)
+    q8 = out_dtype == torch.int8
+    if q8 and not (tc and not return_parts):
+        raise ValueError("int8 output (quantized out-projection operand) needs the tensor-core path")
+    # int8: codes [L, H*d] + scales [nq, H] of the bf16-rounded output (the
+    # out-projection's block-quantized A operand, written by the epilogue)
+    out = (torch.empty((L, H * d), dtype=torch.int8, device=q.device) if q8
+           else torch.empty((H, L, d), dtype=out_dtype, device=q.device))
+    out_scales = torch.empty((nq, H), dtype=torch.float32, device=q.device) if q8 else None
     row_max = torch.empty((H, L), dtype=torch.float32, device=q.device) if return_parts else None
     den = torch.empty((H, L), dtype=torch.float32, device=q.device) if return_parts else None
     args = sla_args(q=ptr(q), k=ptr(k), v=ptr(v), dtype=dtype_code(q), H=H, L=L, d=d, q_block=q_block,
@@ -487,15 +494,15 @@ def sla_attention(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: fl
                     lin_ld=0 if lin_pack is None else lin_pack.shape[2],
                     lin_hs=0 if lin_pack is None else lin_pack.shape[1] * lin_pack.shape[2],
                     lin_kv=ptr(lin_kv), lin_dx=0 if lin_kv is None else lin_kv.shape[2], out=ptr(out),
-                    out_dtype=TB_BF16 if out_dtype == torch.bfloat16 else TB_F32,
-                    row_max=ptr(row_max), den=ptr(den))
+                    out_dtype=TB_I8 if q8 else (TB_BF16 if out_dtype == torch.bfloat16 else TB_F32),
+                    row_max=ptr(row_max), den=ptr(den), out_scales=ptr(out_scales))
     lib = _lib.load(require_device=True)
     _lib.check(lib.tb_sla_attention(__import__("ctypes").byref(args), stream_ptr()), "tb_sla_attention")
     if return_parts:
         parts = dict(qp=qp, kp=kp, idx=idx, comp=comp, q_codes=qc, q_scales=qs, k_codes=kc, k_scales=ks,
                      k_mean=km, lin_pack=lin_pack, lin_kv=lin_kv, row_max=row_max, den=den, count=count)
         return out, parts
-    return out
+    return (out, out_scales) if q8 else out
 
 
 _AUX = {}

@@ -325,6 +325,20 @@ def test_w8a8_gemm_quant_epilogue_matches_two_kernel_path(tb, M, act, bias):
     assert torch.equal(q, q2)
 
 
+@pytest.mark.parametrize("L", [1000, 1024])
+def test_sla_int8_output_matches_bf16_then_planar_quant(tb, L):
+    """out_dtype=int8: the fused kernel's epilogue quantization of its output
+    tile equals quantize_blockwise_planar of the bf16 output (ragged last
+    q-block included)."""
+    q, k, v = gen.gaussian_qkv(43, 3, L, 128, bf16=True)
+    qd, kd, vd = (torch.from_numpy(x).to(torch.bfloat16).cuda() for x in (q, k, v))
+    o = tb.sla_attention(qd, kd, vd, 128, 64, 0.1, 1.0, out_dtype=torch.bfloat16)
+    want_q, want_s = tb.quantize_blockwise_planar(o)
+    got_q, got_s = tb.sla_attention(qd, kd, vd, 128, 64, 0.1, 1.0, out_dtype=torch.int8)
+    assert torch.equal(got_s, want_s)
+    assert torch.equal(got_q, want_q)
+
+
 def test_quantize_blockwise_planar_matches_row_major(tb):
     H, L = 6, 1000
     g = torch.Generator(device="cuda").manual_seed(6)
