@@ -282,6 +282,22 @@ struct Smem {
 constexpr size_t SMEM_BYTES = sizeof(Smem) + 1024;
 }  // namespace gemm2
 
+// Tile raster of the 2-SM kernel: groups of W8_GROUP_M row-pair bands, row
+// band fastest inside a group, so the ~74 co-running clusters share a few A
+// bands and a few B column tiles (both L2-resident) instead of streaming every
+// B tile once per A band.
+#ifndef W8_GROUP_M
+#define W8_GROUP_M 8
+#endif
+__device__ __forceinline__ void tile_coords(int tile, int nmp, int nnt, int &mp, int &nt) {
+    const int per = W8_GROUP_M * nnt;
+    const int g = tile / per, w = tile - g * per;
+    const int m0 = g * W8_GROUP_M;
+    const int gs = min(W8_GROUP_M, nmp - m0);
+    mp = m0 + w % gs;
+    nt = w / gs;
+}
+
 // OUTM: 0 f32, 1 bf16, 2 block-quantized INT8 (the next projection's A
 // operand: the bf16-rounded result quantized per 128x128 block exactly like
 // quantize_blockwise, codes TMA-stored, one f32 scale per block to qscales).
@@ -324,7 +340,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = cluster; tile < ntiles; tile += nclusters) {
-                const int mp = tile / nnt, nt = tile % nnt;
+                int mp, nt;
+                tile_coords(tile, nmp, nnt, mp, nt);
                 for (int kb = 0; kb < nkb; kb++) {
                     ptx::mbar_wait_sleep(&S.empty[stage], phase ^ 1);
                     const uint32_t fullc = ptx::mapa(ptx::smem_u32(&S.full[stage]), 0);
@@ -396,7 +413,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
             if (lane == 0) ptx::mbar_arrive_cluster(b ? seg_empty1 : seg_empty0);
         }
         for (int tile = cluster; tile < ntiles; tile += nclusters) {
-            const int mp = tile / nnt, nt = tile % nnt;
+            int mp, nt;
+            tile_coords(tile, nmp, nnt, mp, nt);
             const int col0 = nt * BN + half * CW;
             const int nb = col0 / 128;
             const int mb = 2 * mp + (int)rank;                    // this CTA's 128-row scale block
