@@ -178,10 +178,12 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) w8a8_tc_kernel(
                         }
                         float2 &o = acc2[(c * 16 + i) >> 1];
                         if constexpr (EXACT) {
-                            // scalar RN ops: the reference rounding sequence bit-for-bit (the
-                            // packed f32x2 forms differ in the last bits on sm_100a)
-                            o.x = __fadd_rn(o.x, __fmul_rn(__fmul_rn(x.x, sa2.x), sb2.x));
-                            o.y = __fadd_rn(o.y, __fmul_rn(__fmul_rn(x.y, sa2.y), sb2.y));
+                            // the reference sequence bit-for-bit: packed RN ops round each
+                            // lane like the scalar op, but ptxas contracts a packed multiply
+                            // feeding a packed add into FFMA2 (tools/ubench_f32x2.cu), so the
+                            // product that feeds the add is formed with scalar RN multiplies
+                            const float2 p = ptx::fmul2(x, sa2);
+                            o = ptx::fadd2(o, make_float2(__fmul_rn(p.x, sb2.x), __fmul_rn(p.y, sb2.y)));
                         } else {
                             o = ptx::ffma2(x, sab2, o);
                         }
@@ -466,8 +468,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
                         }
                         float2 &o = acc2[(g * G + i) >> 1];
                         if constexpr (EXACT) {
-                            o.x = __fadd_rn(o.x, __fmul_rn(__fmul_rn(x.x, sa2.x), sb2.x));
-                            o.y = __fadd_rn(o.y, __fmul_rn(__fmul_rn(x.y, sa2.y), sb2.y));
+                            // the reference sequence bit-for-bit: packed RN ops round each
+                            // lane like the scalar op, but ptxas contracts a packed multiply
+                            // feeding a packed add into FFMA2 (tools/ubench_f32x2.cu), so the
+                            // product that feeds the add is formed with scalar RN multiplies
+                            const float2 p = ptx::fmul2(x, sa2);
+                            o = ptx::fadd2(o, make_float2(__fmul_rn(p.x, sb2.x), __fmul_rn(p.y, sb2.y)));
                         } else {
                             o = ptx::ffma2(x, sab2, o);
                         }
