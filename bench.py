@@ -232,7 +232,7 @@ def bench_dit(world, rank, num_layers):
     from paper_2512_16093_b200 import dit, ulysses
     torch.cuda.empty_cache()
     layers = dit.random_layers(DIT_DIM, DIT_FFN, num_layers, seed=0)
-    lo, hi = ulysses.token_bounds(L_, world, rank)
+    lo, hi = ulysses.token_bounds(L_, world, rank, dit.TOKEN_ALIGN)
     g = torch.Generator(device="cuda").manual_seed(77 + rank)
     x_init = torch.randn((hi - lo, DIT_DIM), generator=g, device="cuda")
     noises = [torch.randn((hi - lo, DIT_DIM), generator=g, device="cuda") for _ in range(DIT_STEPS - 1)]

@@ -46,6 +46,11 @@ class DeviceLayer:
     mlp_out: DeviceLinear
 
 
+
+# token-shard alignment of the sequence-parallel DiT (ulysses.token_bounds align):
+# the 128-token quantization blocks of the attention output never straddle ranks
+TOKEN_ALIGN = 128
+
 def quantize_device_weight(w: torch.Tensor, block: int = 128) -> DeviceLinear:
     """blockquant.quantize_blockwise on device (bit-exact codes), stored transposed."""
     q, s = ops.quantize_blockwise(w, block, check_finite=False)
@@ -109,10 +114,19 @@ def block_forward(x: torch.Tensor, sigma: float, w: DeviceLayer, heads: int, sla
 
     aq, asc = ops.quantize_blockwise(a, 128, check_finite=False)
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        # token shards are TOKEN_ALIGN-aligned (token_bounds(L, P, rank, TOKEN_ALIGN)),
+        # so every 128x128 quantization block of the attention output is rank-local
         qkv = ops.w8a8_gemm(aq, asc, w.qkv.bt, w.qkv.scales, 128, None, torch.bfloat16, exact=False)
-        q, k, v = (t.view(Lp, heads, hd) for t in qkv.split(dim, dim=1))
-        o = ulysses.ulysses_sla_attention(q.contiguous(), k.contiguous(), v.contiguous(), L_global, attn, group)
-        oq, osc = ops.quantize_blockwise(o.reshape(Lp, dim).contiguous(), 128, check_finite=False)
+        q, k, v = (t.view(Lp, heads, hd).contiguous() for t in qkv.split(dim, dim=1))
+        if hd == 128:
+            def attn_q8(qh, kh, vh):
+                return ops.sla_attention(qh, kh, vh, sla["q_block"], sla["kv_block"], sla["topk_ratio"],
+                                         sla.get("linear_mix", 1.0), True, out_dtype=torch.int8)
+            # int8 codes + scales cross the reverse all-to-all (half the bytes of bf16)
+            oq, osc = ulysses.ulysses_sla_attention_q8(q, k, v, L_global, attn_q8, group, TOKEN_ALIGN)
+        else:
+            o = ulysses.ulysses_sla_attention(q, k, v, L_global, attn, group, TOKEN_ALIGN)
+            oq, osc = ops.quantize_blockwise(o.reshape(Lp, dim).contiguous(), 128, check_finite=False)
     else:
         # qkv lands head-major [3H, L, hd] straight from the GEMM epilogue (no permute);
         # the out-projection quantizes the head-major attention output in place

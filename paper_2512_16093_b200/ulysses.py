@@ -11,7 +11,16 @@ parallel outside attention; the boundary is one all-to-all each way:
 
 over NCCL (torch.distributed, backend "nccl"; "gloo" for CPU tests of the
 index math).  Token shards may be uneven (L % P != 0): shard p owns tokens
-[p*ceil(L/P), ...).  Heads must divide evenly (40 / {1,2,4,8}).
+[p*per, ...) with per = ceil(L/P) rounded up to a multiple of `align`.  Heads
+must divide evenly (40 / {1,2,4,8}).
+
+Quantized return path: with 128-aligned token shards every
+128-token x 128-channel block of the attention output lives on one rank, so
+the head-shard attention can emit the out-projection's block-quantized INT8
+operand directly (codes + one scale per (128-token block, head)) and the
+reverse all-to-all moves int8 codes instead of bf16 -- half the bytes, and no
+quantization pass on the receiver.  Bit-identical to quantizing the gathered
+bf16 output (per-block quantization commutes with the exchange).
 """
 from __future__ import annotations
 
@@ -19,8 +28,13 @@ import torch
 import torch.distributed as dist
 
 
-def token_bounds(L: int, P: int, rank: int) -> tuple[int, int]:
+def shard_size(L: int, P: int, align: int = 1) -> int:
     per = -(-L // P)
+    return -(-per // align) * align
+
+
+def token_bounds(L: int, P: int, rank: int, align: int = 1) -> tuple[int, int]:
+    per = shard_size(L, P, align)
     lo = min(rank * per, L)
     return lo, min(lo + per, L)
 
@@ -31,7 +45,7 @@ def _world():
     return 1, 0
 
 
-def seq_to_heads(x: torch.Tensor, L: int, group=None) -> torch.Tensor:
+def seq_to_heads(x: torch.Tensor, L: int, group=None, align: int = 1) -> torch.Tensor:
     """[L_p, H, d] token shard -> [H/P, L, d] head shard (one all-to-all)."""
     P, rank = (dist.get_world_size(group), dist.get_rank(group)) if dist.is_initialized() else (1, 0)
     Lp, H, d = x.shape
@@ -40,7 +54,7 @@ def seq_to_heads(x: torch.Tensor, L: int, group=None) -> torch.Tensor:
     hp = H // P
     if P == 1:
         return x.permute(1, 0, 2).contiguous()
-    per = -(-L // P)
+    per = shard_size(L, P, align)
     # send buffer [P, per, hp, d]: chunk j = my tokens for head group j (padded to `per` rows)
     send = x.new_zeros((P, per, hp, d))
     send[:, :Lp] = x.view(Lp, P, hp, d).permute(1, 0, 2, 3)
@@ -49,33 +63,73 @@ def seq_to_heads(x: torch.Tensor, L: int, group=None) -> torch.Tensor:
     # recv chunk i = tokens of rank i for my head group
     out = x.new_empty((hp, L, d))
     for i in range(P):
-        lo, hi = token_bounds(L, P, i)
+        lo, hi = token_bounds(L, P, i, align)
         out[:, lo:hi] = recv[i, :hi - lo].permute(1, 0, 2)
     return out
 
 
-def heads_to_seq(o: torch.Tensor, L: int, group=None) -> torch.Tensor:
+def heads_to_seq(o: torch.Tensor, L: int, group=None, align: int = 1) -> torch.Tensor:
     """[H/P, L, d] head shard -> [L_p, H, d] token shard (inverse all-to-all)."""
     P, rank = (dist.get_world_size(group), dist.get_rank(group)) if dist.is_initialized() else (1, 0)
     hp, _, d = o.shape
     if P == 1:
         return o.permute(1, 0, 2).contiguous()
-    per = -(-L // P)
+    per = shard_size(L, P, align)
     send = o.new_zeros((P, per, hp, d))
     for i in range(P):
-        lo, hi = token_bounds(L, P, i)
+        lo, hi = token_bounds(L, P, i, align)
         send[i, :hi - lo] = o[:, lo:hi].permute(1, 0, 2)
     recv = torch.empty_like(send)
     dist.all_to_all_single(recv, send, group=group)
-    lo, hi = token_bounds(L, P, rank)
+    lo, hi = token_bounds(L, P, rank, align)
     # recv chunk j = my tokens for head group j
     return recv[:, :hi - lo].permute(1, 0, 2, 3).reshape(hi - lo, P * hp, d).contiguous()
 
 
-def ulysses_sla_attention(q_shard, k_shard, v_shard, L: int, attn_fn, group=None):
+def ulysses_sla_attention(q_shard, k_shard, v_shard, L: int, attn_fn, group=None, align: int = 1):
     """Token-sharded q/k/v [L_p, H, d] -> attention on a head shard -> token-sharded o."""
-    qh = seq_to_heads(q_shard, L, group)
-    kh = seq_to_heads(k_shard, L, group)
-    vh = seq_to_heads(v_shard, L, group)
+    qh = seq_to_heads(q_shard, L, group, align)
+    kh = seq_to_heads(k_shard, L, group, align)
+    vh = seq_to_heads(v_shard, L, group, align)
     oh = attn_fn(qh, kh, vh)
-    return heads_to_seq(oh.to(q_shard.dtype), L, group)
+    return heads_to_seq(oh.to(q_shard.dtype), L, group, align)
+
+
+def heads_to_seq_q8(codes: torch.Tensor, scales: torch.Tensor, L: int, group=None, block: int = 128):
+    """Head-shard block-quantized output -> token shard (quantized return path).
+
+    codes [L, hp*d] int8 (token, local head*d + channel) and scales
+    [ceil(L/block), hp] of this rank's heads -> codes [L_p, H*d] and scales
+    [ceil(L_p/block), H] of this rank's 128-aligned token shard, all heads."""
+    P, rank = (dist.get_world_size(group), dist.get_rank(group)) if dist.is_initialized() else (1, 0)
+    if P == 1:
+        return codes, scales
+    hpd, hp = codes.shape[1], scales.shape[1]
+    per = shard_size(L, P, block)
+    nbp = per // block
+    send = codes.new_zeros((P, per, hpd))
+    send_s = scales.new_zeros((P, nbp, hp))
+    for i in range(P):
+        lo, hi = token_bounds(L, P, i, block)
+        send[i, :hi - lo] = codes[lo:hi]
+        b0, b1 = lo // block, -(-hi // block)
+        send_s[i, :b1 - b0] = scales[b0:b1]
+    recv, recv_s = torch.empty_like(send), torch.empty_like(send_s)
+    dist.all_to_all_single(recv, send, group=group)
+    dist.all_to_all_single(recv_s, send_s, group=group)
+    lo, hi = token_bounds(L, P, rank, block)
+    nb = -(-(hi - lo) // block)
+    # chunk j = my tokens of head group j -> columns j*hp*d.. of the full row
+    out = recv[:, :hi - lo].permute(1, 0, 2).reshape(hi - lo, P * hpd).contiguous()
+    out_s = recv_s[:, :nb].permute(1, 0, 2).reshape(nb, P * hp).contiguous()
+    return out, out_s
+
+
+def ulysses_sla_attention_q8(q_shard, k_shard, v_shard, L: int, attn_q8_fn, group=None, block: int = 128):
+    """Token-sharded q/k/v (128-aligned shards) -> head-shard attention emitting
+    int8 codes + block scales -> token-shard out-projection operand."""
+    qh = seq_to_heads(q_shard, L, group, block)
+    kh = seq_to_heads(k_shard, L, group, block)
+    vh = seq_to_heads(v_shard, L, group, block)
+    codes, scales = attn_q8_fn(qh, kh, vh)
+    return heads_to_seq_q8(codes, scales, L, group, block)

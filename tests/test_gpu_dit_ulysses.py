@@ -1,0 +1,71 @@
+"""Sequence-parallel DiT block on one GPU with two ranks: the Ulysses exchange
+(gloo, CUDA tensors staged through the host) around the real kernels, with the
+quantized return path (int8 attention output codes + block scales crossing the
+reverse all-to-all).  Every kernel is row- or head-local and the token shards
+are 128-aligned, so the two-rank block output equals the one-rank output
+bit-for-bit."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+L, DIM, HEADS, FFN = 700, 256, 2, 512
+SLA = dict(q_block=128, kv_block=64, topk_ratio=0.25, linear_mix=1.0)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _staged_all_to_all(out, inp, group=None, **kw):
+    # gloo has no CUDA all_to_all: stage through host memory
+    h_out = torch.empty(out.shape, dtype=out.dtype)
+    _orig_a2a(h_out, inp.cpu(), group=group)
+    out.copy_(h_out)
+
+
+_orig_a2a = dist.all_to_all_single
+
+
+def _block(world, rank):
+    from paper_2512_16093_b200 import dit, ulysses
+    layer = dit.random_layers(DIM, FFN, 1, seed=3)[0]
+    g = torch.Generator(device="cuda").manual_seed(9)
+    x = torch.randn((L, DIM), generator=g, device="cuda")
+    lo, hi = ulysses.token_bounds(L, world, rank, dit.TOKEN_ALIGN)
+    x2, p2 = dit.block_forward(x[lo:hi].contiguous(), 0.7, layer, HEADS, SLA, L)
+    return (x2 + p2).cpu(), lo, hi
+
+
+def _worker(rank, world, port, ref_path, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dist.all_to_all_single = _staged_all_to_all
+    torch.cuda.set_device(0)
+    out, lo, hi = _block(world, rank)
+    ref = torch.load(ref_path)
+    out_q.put((rank, torch.equal(out, ref[lo:hi]), (out - ref[lo:hi]).abs().max().item()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_dit_block_two_ranks_equals_one_rank(tmp_path):
+    ref, _, _ = _block(1, 0)
+    ref_path = str(tmp_path / "ref.pt")
+    torch.save(ref, ref_path)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, ref_path, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, same, err in res:
+        assert same, (rank, err)
