@@ -38,8 +38,8 @@ def _block(world, rank):
     g = torch.Generator(device="cuda").manual_seed(9)
     x = torch.randn((L, DIM), generator=g, device="cuda")
     lo, hi = ulysses.token_bounds(L, world, rank, dit.TOKEN_ALIGN)
-    x2, p2 = dit.block_forward(x[lo:hi].contiguous(), 0.7, layer, HEADS, SLA, L)
-    return (x2 + p2).cpu(), lo, hi
+    xo, pend = dit.block_forward(x[lo:hi].contiguous(), 0.7, layer, HEADS, SLA, L)
+    return (xo if pend is None else xo + pend).cpu(), lo, hi
 
 
 def _worker(rank, world, port, ref_path, out_q):
