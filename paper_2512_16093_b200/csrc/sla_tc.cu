@@ -653,7 +653,11 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
                         if (i >= lim) p0 = 0.0f;
                         if (i + 1 >= lim) p1 = 0.0f;
                     }
+#ifdef TB_X_NOSUM
+                    if (i == 0) psum2[0] = make_float2(p0, p1);
+#else
                     psum2[(i >> 1) & 3] = ptx::fadd2(psum2[(i >> 1) & 3], make_float2(p0, p1));
+#endif
                     __nv_bfloat162 pp = __floats2bfloat162_rn(p0, p1);
                     pk[i >> 5][(i >> 1) & 15] = *reinterpret_cast<uint32_t *>(&pp);
                 }
