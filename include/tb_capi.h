@@ -159,6 +159,13 @@ typedef struct tb_sla_args {
      * out_scales [ceil(L/128), H] its 128 x 128 block scales (one per
      * (q-block, head) tile; quantize_blockwise_planar semantics) */
     float *out_scales;
+    /* FP8 P/V (opt-in; tensor-core path, bf16 inputs): when
+     * v_fp8 != NULL the PV product runs as kind::f8f6f4 on e4m3 P and the e4m3
+     * V codes [H,L,d] from tb_quant_v_fp8 with their per-head scales v_scales
+     * [H]; NULL keeps BF16 P/V (the default: FP8 misses rel-L1 <= 1e-2 on
+     * sparse-dominated rows). */
+    const uint8_t *v_fp8;
+    const float *v_scales;
 } tb_sla_args;
 
 /* _sparse_branch + combine (attention.py:347-389, 392-421).  d==128,
@@ -167,6 +174,14 @@ typedef struct tb_sla_args {
  * staged tiles, warp-specialised online softmax); other shapes -> CUDA-core
  * kernel with the same semantics. */
 int tb_sla_attention(const tb_sla_args *a, void *stream);
+
+/* FP8 V for the opt-in FP8 P/V path (no reference function; SURVEY.md §8
+ * a17).  Per head h: scale[h] = f32(absmax(v[h])) / 448 (RN), codes =
+ * e4m3 round-to-nearest-even, satfinite, of v / safe (IEEE divide; safe = 1
+ * when the head is all zero).  am_ws: H uint32 of workspace.  Restated in
+ * oracle/oracle.py quantize_v_fp8. */
+int tb_quant_v_fp8(const void *v, int dtype, int64_t H, int64_t L, int64_t d, uint8_t *codes, float *scales,
+                   unsigned *am_ws, void *stream);
 
 /* V [H,L,d] -> bf16 V^T [H,d,l_pad] (zero padded), the K-major B operand
  * of the PV MMA. */

@@ -191,6 +191,50 @@ def quantized_linear(x, wq, w_scales, block=128, bias=None):
     return y
 
 
+# ------------------------------------------------------------ FP8 (a17)
+# No reference function (the north star's "P/V to FP8");
+# the rule restated here is the product's definition, pinned against
+# torch's CPU float8_e4m3fn cast (tests/test_oracle_golden.py).
+
+def e4m3_encode(x):
+    """f32 -> e4m3 codes (uint8): round to nearest even, saturating to +-448
+    (cvt.rn.satfinite.e4m3x2.f32); NaN -> 0x7F."""
+    x = _f32(x)
+    ax = np.abs(x).astype(np.float64)
+    sign = np.signbit(x).astype(np.uint8) << 7
+    with np.errstate(divide="ignore", invalid="ignore"):
+        e = np.floor(np.log2(np.where(ax > 0, ax, 1.0)))
+    e = np.clip(e, -6, 8)                             # subnormals share the 2^-6 binade's quantum 2^-9
+    # exact for f32 inputs: scaling by a power of two, then rint (half-even)
+    m = np.rint(ax / np.exp2(e - 3))
+    e = np.where(m >= 16, e + 1, e)
+    m = np.where(m >= 16, m / 2, m)                   # 16 -> next binade's 8 (exact)
+    code = np.where(m >= 8, ((e + 7) * 8 + (m - 8)), m)   # m < 8 only in the subnormal binade (e = -6)
+    code = np.minimum(code, 126)                      # satfinite: 0x7E = 448
+    code = code.astype(np.uint8) | sign
+    return np.where(np.isnan(x), np.uint8(0x7F), code).astype(np.uint8)
+
+
+def e4m3_decode(c):
+    c = np.asarray(c, np.uint8)
+    e = ((c >> 3) & 0xF).astype(np.int32)
+    m = (c & 7).astype(np.float64)
+    v = np.where(e == 0, m * 2.0 ** -9, (8 + m) * np.exp2(e - 10.0))
+    v = np.where((c & 0x7F) == 0x7F, np.nan, v)
+    return np.where(c & 0x80, -v, v).astype(np.float32)
+
+
+def quantize_v_fp8(v):
+    """V [h,s,d] -> (e4m3 codes uint8 [h,s,d], per-head scales f32 [h]):
+    scale = f32(absmax) / 448 (f32 RN), codes = e4m3(v / safe), safe = 1 for
+    an all-zero head (the tb_quant_v_fp8 rule)."""
+    v = _f32(v)
+    am = np.abs(v).reshape(v.shape[0], -1).max(axis=1).astype(np.float32)
+    sc = (am / np.float32(448.0)).astype(np.float32)
+    safe = np.where(sc == 0, np.float32(1.0), sc).astype(np.float32)
+    return e4m3_encode((v / safe[:, None, None]).astype(np.float32)), sc
+
+
 # ------------------------------------------------------- float branches
 
 def feature_map(x):
@@ -213,9 +257,14 @@ def _positions(blocks, s, kvb):
         if len(blocks) else np.empty(0, np.int64)
 
 
-def sparse_branch(q, k, v, idx, qb, kvb, scale=None, quantized=True):
-    """attention.py:347-389 -> (num [h,s,d], den [h,s], row_max [h,s])."""
+def sparse_branch(q, k, v, idx, qb, kvb, scale=None, quantized=True, pv_fp8=False):
+    """attention.py:347-389 -> (num [h,s,d], den [h,s], row_max [h,s]).
+    pv_fp8: the a17 simulation -- P (against the exact row max) and V
+    (quantize_v_fp8) rounded to e4m3 for the numerator, den from f32 P."""
     q, k, v = _f32(q), _f32(k), _f32(v)
+    if pv_fp8:
+        vc, vs = quantize_v_fp8(v)
+        vq = e4m3_decode(vc) * vs[:, None, None]
     h, s, d = q.shape
     scale = np.float32(1.0 / math.sqrt(d) if scale is None else scale)
     if quantized:
@@ -241,7 +290,7 @@ def sparse_branch(q, k, v, idx, qb, kvb, scale=None, quantized=True):
                 lg = scale * (q[hh, lo:hi] @ k[hh, pos].T)
             m = lg.max(axis=1)
             e = np.exp(lg - m[:, None])
-            num[hh, lo:hi] = e @ v[hh, pos]
+            num[hh, lo:hi] = (e4m3_decode(e4m3_encode(e)) @ vq[hh, pos]) if pv_fp8 else e @ v[hh, pos]
             den[hh, lo:hi] = e.sum(axis=1)
             rmax[hh, lo:hi] = m
     return num, den, rmax
@@ -280,7 +329,7 @@ def combine(num_s, den_s, rmax, num_l, den_l, mix):
 
 
 def sla_attention(q, k, v, q_block=64, kv_block=64, topk_ratio=0.1, linear_mix=1.0,
-                  quantized=True, scale=None, return_parts=False):
+                  quantized=True, scale=None, return_parts=False, pv_fp8=False):
     """attention.py:392-421."""
     q, k, v = _f32(q), _f32(k), _f32(v)
     s = q.shape[1]
@@ -289,7 +338,7 @@ def sla_attention(q, k, v, q_block=64, kv_block=64, topk_ratio=0.1, linear_mix=1
     qp, kp = pool_block_means(q, q_block), pool_block_means(k, kv_block)
     idx = select_topk(qp, kp, topk_ratio)
     nkv = kp.shape[1]
-    num_s, den_s, rmax = sparse_branch(q, k, v, idx, q_block, kv_block, scale, quantized)
+    num_s, den_s, rmax = sparse_branch(q, k, v, idx, q_block, kv_block, scale, quantized, pv_fp8)
     comp = complement(idx, nkv)
     if comp.shape[2] == 0 or linear_mix == 0.0:
         out = num_s / den_s[..., None]

@@ -45,6 +45,7 @@ SIGNATURES = {
     "tb_pool_quant_tokens_t": [_P, _i, _P, _I, _I, _I, _I, _P, _P, _P, _P, _I, _P],
     "tb_sla_attention": [_P, _P],
     "tb_transpose_v": [_P, _i, _I, _I, _I, _I, _P, _P],
+    "tb_quant_v_fp8": [_P, _i, _I, _I, _I, _P, _P, _P, _P],
     "tb_feature_map": [_P, _i, _I, _I, _I, _I, _P, _i, _P],
     "tb_linear_operands": [_P, _P, _P, _i, _I, _I, _I, _I, _I, _I, _P, _P, _P, _i, _P, _I, _P],
     "tb_gemm_bf16_batched": [_P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _i, _P],
@@ -79,6 +80,7 @@ class SlaArgs(ctypes.Structure):
         ("out_dtype", _i),
         ("row_max", _P), ("den", _P),
         ("out_scales", _P),
+        ("v_fp8", _P), ("v_scales", _P),
     ]
 
 

@@ -157,6 +157,16 @@ __device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uin
         "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}"
         :: "r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate) : "memory");
 }
+// kind::f8f6f4 with the A operand in TMEM (four e4m3 per 32-bit column
+// along K), B from shared memory, f32 accumulate (M128 N128 K32 per MMA).
+__device__ __forceinline__ void mma_f8_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], [%1], %2, %3, p;\n\t}"
+        :: "r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate) : "memory");
+}
 // kind::i8 with the A operand in TMEM (M rows = lanes, four int8 per 32-bit
 // column along K), B from shared memory.
 __device__ __forceinline__ void mma_i8_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
@@ -369,6 +379,12 @@ __device__ __forceinline__ uint64_t sdesc_noswz_alias(uint32_t smem_addr) {
 __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
     return (2u << 4)                        // D format S32
          | (1u << 7) | (1u << 10)           // A, B signed int8
+         | ((uint32_t)(N >> 3) << 17)
+         | ((uint32_t)(M >> 4) << 24);
+}
+// kind::f8f6f4 with e4m3 A and B (format code 0), f32 D
+__host__ __device__ constexpr uint32_t idesc_e4m3(int M, int N) {
+    return (1u << 4)                        // D format F32
          | ((uint32_t)(N >> 3) << 17)
          | ((uint32_t)(M >> 4) << 24);
 }

@@ -724,3 +724,127 @@ extern "C" int tb_quantize_blockwise_planar(const void *x, int dtype, int64_t ro
                                                                                 scales, nullptr);
     return check_launch("quantize_blockwise_planar");
 }
+
+// ---------------------------------------------------------------- FP8 V
+// SURVEY.md §8 a17 (no reference function; the north star's "P/V to FP8"):
+// V [H, L, d] -> e4m3 codes with one scale per head,
+//   scale = f32(absmax(v[h])) / 448 (RN),  code = e4m3_rn_satfinite(v / safe)
+// (safe = 1 for an all-zero head; IEEE divide).  Oracle:
+// oracle/oracle.py quantize_v_fp8.  Two HBM passes: per-head absmax
+// (uint-ordered atomicMax of non-negative floats), then the codes.
+#include <cuda_fp8.h>
+#include <algorithm>
+namespace tb {
+template <typename T>
+__device__ __forceinline__ void vfp8_load8(const T *src, int64_t i, float (&x)[8]) {
+    if constexpr (sizeof(T) == 2) {
+        const uint4 w = __ldg(reinterpret_cast<const uint4 *>(src) + i);
+        const __nv_bfloat162 *b = reinterpret_cast<const __nv_bfloat162 *>(&w);
+#pragma unroll
+        for (int u = 0; u < 4; u++) { const float2 f = __bfloat1622float2(b[u]); x[2 * u] = f.x; x[2 * u + 1] = f.y; }
+    } else {
+        const float4 a = __ldg(reinterpret_cast<const float4 *>(src) + 2 * i);
+        const float4 b = __ldg(reinterpret_cast<const float4 *>(src) + 2 * i + 1);
+        x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+    }
+}
+
+// Each CTA walks chunks of VB = 4 x 256 vectors (8 elements each): the four
+// loads of a thread are issued before any use (4 x 16 B in flight per
+// thread) and each load instruction is coalesced across the warp.
+constexpr int VFP8_U = 4;
+template <typename T>
+__global__ void __launch_bounds__(256) vfp8_absmax_kernel(const T *__restrict__ v, int64_t per_head,
+                                                          unsigned *__restrict__ am_bits) {
+    const int h = blockIdx.y;
+    const T *src = v + (int64_t)h * per_head;
+    const int64_t nvec = per_head / 8;
+    float am = 0.0f;
+    for (int64_t c0 = (int64_t)blockIdx.x * 256 * VFP8_U; c0 < nvec; c0 += (int64_t)gridDim.x * 256 * VFP8_U) {
+        float x[VFP8_U][8];
+#pragma unroll
+        for (int u = 0; u < VFP8_U; u++) {
+            const int64_t i = c0 + u * 256 + threadIdx.x;
+            if (i < nvec) vfp8_load8(src, i, x[u]);
+            else {
+#pragma unroll
+                for (int e = 0; e < 8; e++) x[u][e] = 0.0f;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < VFP8_U; u++)
+#pragma unroll
+            for (int e = 0; e < 8; e++) am = fmaxf(am, fabsf(x[u][e]));
+    }
+    am = warp_max<32>(am);
+    __shared__ float red[8];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = am;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float m = red[0];
+        for (int w = 1; w < 8; w++) m = fmaxf(m, red[w]);
+        atomicMax(am_bits + h, __float_as_uint(m));
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) vfp8_codes_kernel(const T *__restrict__ v, int64_t per_head,
+                                                         const unsigned *__restrict__ am_bits,
+                                                         uint8_t *__restrict__ codes, float *__restrict__ scales) {
+    const int h = blockIdx.y;
+    const float sc = __fdiv_rn(__uint_as_float(__ldg(am_bits + h)), 448.0f);
+    if (blockIdx.x == 0 && threadIdx.x == 0) scales[h] = sc;
+    const float safe = sc == 0.0f ? 1.0f : sc;
+    const T *src = v + (int64_t)h * per_head;
+    uint8_t *dst = codes + (int64_t)h * per_head;
+    const int64_t nvec = per_head / 8;
+    for (int64_t c0 = (int64_t)blockIdx.x * 256 * VFP8_U; c0 < nvec; c0 += (int64_t)gridDim.x * 256 * VFP8_U) {
+        float x[VFP8_U][8];
+#pragma unroll
+        for (int u = 0; u < VFP8_U; u++) {
+            const int64_t i = c0 + u * 256 + threadIdx.x;
+            if (i < nvec) vfp8_load8(src, i, x[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < VFP8_U; u++) {
+            const int64_t i = c0 + u * 256 + threadIdx.x;
+            uint32_t w[2];
+#pragma unroll
+            for (int q = 0; q < 2; q++) {
+                const __nv_fp8x2_storage_t lo = __nv_cvt_float2_to_fp8x2(
+                    make_float2(__fdiv_rn(x[u][4 * q], safe), __fdiv_rn(x[u][4 * q + 1], safe)), __NV_SATFINITE, __NV_E4M3);
+                const __nv_fp8x2_storage_t hi = __nv_cvt_float2_to_fp8x2(
+                    make_float2(__fdiv_rn(x[u][4 * q + 2], safe), __fdiv_rn(x[u][4 * q + 3], safe)), __NV_SATFINITE,
+                    __NV_E4M3);
+                w[q] = (uint32_t)lo | ((uint32_t)hi << 16);
+            }
+            if (i < nvec) *reinterpret_cast<uint2 *>(dst + 8 * i) = make_uint2(w[0], w[1]);
+        }
+    }
+}
+}  // namespace tb
+
+// am_ws: caller workspace of H uint32 (zeroed here on the stream)
+extern "C" int tb_quant_v_fp8(const void *v, int dtype, int64_t H, int64_t L, int64_t d, uint8_t *codes,
+                              float *scales, unsigned *am_ws, void *stream) {
+    TB_REQUIRE(dtype == TB_F32 || dtype == TB_BF16, "dtype must be f32 or bf16");
+    if (H == 0 || L == 0 || d == 0) return TB_OK;
+    const int64_t per_head = L * d;
+    TB_REQUIRE(per_head % 8 == 0, "seq * head_dim must be a multiple of 8");
+    TB_REQUIRE((uintptr_t)v % 16 == 0 && (uintptr_t)codes % 8 == 0, "v must be 16-B and codes 8-B aligned");
+    TB_REQUIRE(H <= 65535, "too many heads");
+    cudaStream_t st = as_stream(stream);
+    cudaMemsetAsync(am_ws, 0, H * sizeof(unsigned), st);
+    const int64_t vecs = per_head / 8;
+    // ~8 CTAs of 256 threads per SM in total over the heads
+    unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(vecs, 256 * VFP8_U), cdiv(8 * 148, H)));
+    dim3 grid(gx, (unsigned)H);
+    if (dtype == TB_BF16) {
+        vfp8_absmax_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>((const __nv_bfloat16 *)v, per_head, am_ws);
+        vfp8_codes_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>((const __nv_bfloat16 *)v, per_head, am_ws, codes, scales);
+    } else {
+        vfp8_absmax_kernel<float><<<grid, 256, 0, st>>>((const float *)v, per_head, am_ws);
+        vfp8_codes_kernel<float><<<grid, 256, 0, st>>>((const float *)v, per_head, am_ws, codes, scales);
+    }
+    return check_launch("quant_v_fp8");
+}

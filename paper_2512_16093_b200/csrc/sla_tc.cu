@@ -29,6 +29,8 @@
 #include <cstdlib>
 #include <type_traits>
 
+#include <cuda_fp8.h>
+
 #include "common.cuh"
 #include "ptx.cuh"
 #include "tmap.cuh"
@@ -203,7 +205,15 @@ __device__ __forceinline__ void load8(const T *p, float *x) {
     }
 }
 
-template <typename T, bool EXACT>
+// F8 (opt-in): P and V as e4m3 and PV as kind::f8f6f4
+// (M128 N128 K32, A = P in TMEM, four per column; B = the V code tile, one
+// 128-channel SW128 box, MN-major).  V carries one scale per head (oracle/
+// oracle.py quantize_v_fp8); P is stored unscaled (p <= 448 is guaranteed: the
+// fast path accepts a block only when its row sum is <= 448, the exact path
+// rebases when the max outgrows the reference by > 8, i.e. p <= 256).  O
+// accumulates sum p * v / sv; the fused linear numerator is brought to the
+// same scale by staging phi(Q) / sv, and the epilogue multiplies by sv.
+template <typename T, bool EXACT, bool F8 = false>
 __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
     const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_kv, tb_sla_args a, int nq,
@@ -341,9 +351,14 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
 #ifdef TB_X_NOLOAD
                 ptx::mbar_arrive(&S.v_full[vs]);
 #else
-                ptx::mbar_arrive_expect_tx(&S.v_full[vs], V_BYTES);
-                ptx::tma_load_3d(S.v[vs], &tm_v, 0, b * BN, h, &S.v_full[vs]);
-                ptx::tma_load_3d(S.v[vs] + V_BYTES / 2, &tm_v, 64, b * BN, h, &S.v_full[vs]);
+                if constexpr (F8) {       // one 128-channel x 64-token e4m3 box
+                    ptx::mbar_arrive_expect_tx(&S.v_full[vs], V_BYTES / 2);
+                    ptx::tma_load_3d(S.v[vs], &tm_v, 0, b * BN, h, &S.v_full[vs]);
+                } else {
+                    ptx::mbar_arrive_expect_tx(&S.v_full[vs], V_BYTES);
+                    ptx::tma_load_3d(S.v[vs], &tm_v, 0, b * BN, h, &S.v_full[vs]);
+                    ptx::tma_load_3d(S.v[vs] + V_BYTES / 2, &tm_v, 64, b * BN, h, &S.v_full[vs]);
+                }
 #endif
             }
             __syncwarp();
@@ -355,6 +370,7 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
         constexpr uint32_t ID_PV = ptx::idesc_bf16(BM, D);
         constexpr uint32_t ID_PV_MN = ptx::idesc_bf16(BM, D) | (1u << 16);   // B = V tile, MN-major
         constexpr uint32_t ID_BIAS = ptx::idesc_bf16(BM, BN);
+        constexpr uint32_t ID_PV8_MN = ptx::idesc_e4m3(BM, D) | (1u << 16);  // e4m3 P (TMEM) x V codes, MN-major
         const uint64_t qd = ptx::sdesc_sw128(ptx::smem_u32(S.q));
         // no-swizzle K-major 8x16 bf16 tiles; SBO = 0 makes every 8-row group alias the same rows
         const uint64_t bias_a = ptx::sdesc_noswz_alias(ptx::smem_u32(S.bias_a));
@@ -392,9 +408,19 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
 #ifndef TB_X_PVN
 #define TB_X_PVN (BN / 16)
 #endif
+                if constexpr (F8) {
+                    // e4m3 atoms are 128 channels (128 B) x 8 tokens: K=32 per MMA =
+                    // 8 TMEM cols of P (4 per col), 32 token rows of V (4 KB)
+                    const uint64_t vd8 = ptx::sdesc_sw128_mn(ptx::smem_u32(S.v[vs]), V_BYTES / 2, 1024);
+#pragma unroll
+                    for (int k = 0; k < BN / 32; k++)
+                        ptx::mma_f8_ts(TM_O, tmem + pb * BN + 8 * k, vd8 + 256 * k, ID_PV8_MN,
+                                       (lf || i > 0 || k > 0) ? 1u : 0u);
+                } else {
 #pragma unroll
                 for (int k = 0; k < TB_X_PVN; k++)  // K=16 bf16 per MMA: 8 TMEM cols of P, 16 token rows of V
                     ptx::mma_f16_ts(TM_O, tmem + pb * BN + 8 * k, vd + 128 * k, ID_PV_MN, (lf || i > 0 || k > 0) ? 1u : 0u);
+                }
                 ptx::mma_commit(&S.pv_done[pb]);
                 ptx::mma_commit(&S.v_empty[vs]);
             }
@@ -439,6 +465,9 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
         const bool row_ok = row < L;
         const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
         const float scale2 = a.scale * LOG2E;
+        // F8: V codes carry the per-head scale sv (O accumulates p * v / sv)
+        const float vsc = F8 ? __ldg(a.v_scales + h) : 1.0f;
+        const float ivsc = F8 ? 1.0f / (vsc == 0.0f ? 1.0f : vsc) : 1.0f;
         // phi(q_row) -> bf16 A operand of the linear MMA (128B-swizzled K halves
         // in lin_a); returns den_L = phi(q) . sum phi(K_b) over the complement.
         // wq: the row already in registers (bf16), else it is (re)loaded.
@@ -548,7 +577,7 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
                         const float f0 = x0 >= 0.0f ? x0 + 1.0f : ex2(x0 * LOG2E);
                         const float f1 = x1 >= 0.0f ? x1 + 1.0f : ex2(x1 * LOG2E);
                         dp = fmaf(f0, kk[2 * u], fmaf(f1, kk[2 * u + 1], dp));
-                        __nv_bfloat162 pp = __floats2bfloat162_rn(f0, f1);
+                        __nv_bfloat162 pp = F8 ? __floats2bfloat162_rn(f0 * ivsc, f1 * ivsc) : __floats2bfloat162_rn(f0, f1);
                         pk[u] = *reinterpret_cast<uint32_t *>(&pp);
                     }
                     uint8_t *dst = lin_a + (cl >> 3) * 16384 + rr * 128 + (((cl & 7) ^ (rr & 7)) * 16);
@@ -658,8 +687,14 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
 #else
                     psum2[(i >> 1) & 3] = ptx::fadd2(psum2[(i >> 1) & 3], make_float2(p0, p1));
 #endif
+                    if constexpr (F8) {      // four e4m3 per TMEM column (K order = byte order)
+                        const uint32_t h2 = __nv_cvt_float2_to_fp8x2(make_float2(p0, p1), __NV_SATFINITE, __NV_E4M3);
+                        if ((i & 2) == 0) pk[0][i >> 2] = h2;
+                        else pk[0][i >> 2] |= h2 << 16;
+                    } else {
                     __nv_bfloat162 pp = __floats2bfloat162_rn(p0, p1);
                     pk[i >> 5][(i >> 1) & 15] = *reinterpret_cast<uint32_t *>(&pp);
+                    }
                 }
                 const float2 ps = ptx::fadd2(ptx::fadd2(psum2[0], psum2[1]), ptx::fadd2(psum2[2], psum2[3]));
                 return ps.x + ps.y;
@@ -672,7 +707,8 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             bool slow = EXACT;
             if (!EXACT) {
                 psum = run_p(c0m - m_ref);
-                slow = __any_sync(0xffffffffu, !(psum <= 0x1p60f) || !(l + psum > 0.0f));
+                // F8: every p <= 448 (e4m3 max) follows from a row sum <= 448
+                slow = __any_sync(0xffffffffu, !(psum <= (F8 ? 448.0f : 0x1p60f)) || !(l + psum > 0.0f));
             }
             if (slow) {
                 if (!EXACT) load_s();         // S is intact in TMEM until P is stored
@@ -739,7 +775,7 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             l += psum;
             // P_j overwrites S_j's first 32 columns (A operand of PV, bf16x2 per column)
             ptx::tmem_st16(tmem + lane_base + sb * BN, pk[0]);
-            ptx::tmem_st16(tmem + lane_base + sb * BN + 16, pk[1]);
+            if (!F8) ptx::tmem_st16(tmem + lane_base + sb * BN + 16, pk[1]);
             ptx::tmem_wait_st();
             if (threadIdx.x == 0) TB_TRACE(j, 6);
             ptx::tc_fence_before();
@@ -780,6 +816,8 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             ss = f * e_ss;
         }
         const float inv = 1.0f / den;
+        ss *= vsc;                                  // F8: O holds sum p * v / sv
+        const float fo = f * vsc;
         if (row_ok) {
             if (a.row_max) a.row_max[(int64_t)h * L + row] = m_nat;
             if (a.den) a.den[(int64_t)h * L + row] = l_true;
@@ -806,7 +844,7 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
                 }
             } else {
 #pragma unroll
-                for (int i = 0; i < 16; i++) v[i] = __uint_as_float(o[i]) * f * inv;
+                for (int i = 0; i < 16; i++) v[i] = __uint_as_float(o[i]) * fo * inv;
             }
         };
         if (a.out_dtype == TB_I8) {
@@ -1350,8 +1388,9 @@ int sla_tc(const tb_sla_args *a, cudaStream_t st) {
     CUtensorMap tq, tk, tv;
     bool ok = make_tmap_3d(&tq, a->q_codes, CU_TENSOR_MAP_DATA_TYPE_UINT8, D, a->L, a->H, D, a->L * D, D, BM, 1) &&
               make_tmap_3d(&tk, a->k_codes, CU_TENSOR_MAP_DATA_TYPE_UINT8, D, a->L, a->H, D, a->L * D, D, BN, 1) &&
-              make_tmap_3d(&tv, a->dtype == TB_BF16 ? a->v : a->vt, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, D, a->L, a->H,
-                           D * 2, a->L * D * 2, 64, BN, 1);
+              (a->v_fp8 ? make_tmap_3d(&tv, a->v_fp8, CU_TENSOR_MAP_DATA_TYPE_UINT8, D, a->L, a->H, D, a->L * D, D, BN, 1)
+                        : make_tmap_3d(&tv, a->dtype == TB_BF16 ? a->v : a->vt, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, D,
+                                       a->L, a->H, D * 2, a->L * D * 2, 64, BN, 1));
     CUtensorMap tkv = tq;
     if (a->lin_kv)
         ok = ok && make_tmap_2d(&tkv, a->lin_kv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, D, a->H * nq * a->lin_dx, D * 2,
@@ -1359,7 +1398,7 @@ int sla_tc(const tb_sla_args *a, cudaStream_t st) {
     if (!ok) return fail(TB_ECUDA, "cuTensorMapEncodeTiled failed (sla)");
     // the exact-max variant only when the caller asks for the sparse-branch stats
     const bool exact = a->row_max != nullptr || a->den != nullptr;
-    const int variant = a->out_dtype == TB_I8 ? 1 : tb_sla_kernel_variant();   // 2: two-tile kernel (measured slower, kept for study)
+    const int variant = (a->out_dtype == TB_I8 || a->v_fp8) ? 1 : tb_sla_kernel_variant();   // 2: two-tile kernel (measured slower, kept for study)
     if (variant == 2) {
         dim3 grid2((unsigned)cdiv(nq, 2), (unsigned)a->H);
         auto launch2 = [&](auto kern) {
@@ -1380,7 +1419,10 @@ int sla_tc(const tb_sla_args *a, cudaStream_t st) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
         kern<<<grid, THREADS, SMEM_BYTES, st>>>(tq, tk, tv, tkv, *a, (int)nq, (int)nkv);
     };
-    if (a->dtype == TB_BF16) {
+    if (a->v_fp8) {
+        if (exact) launch(sla_tc_kernel<__nv_bfloat16, true, true>);
+        else launch(sla_tc_kernel<__nv_bfloat16, false, true>);
+    } else if (a->dtype == TB_BF16) {
         if (exact) launch(sla_tc_kernel<__nv_bfloat16, true>);
         else launch(sla_tc_kernel<__nv_bfloat16, false>);
     } else {
@@ -1407,6 +1449,8 @@ extern "C" int tb_sla_attention(const tb_sla_args *a, void *stream) {
     cudaStream_t st = as_stream(stream);
     TB_REQUIRE(a->out_dtype != TB_I8 || (a->out_scales != nullptr && sla_tc_supported(a)),
                "int8 output needs the tensor-core kernel and out_scales");
+    TB_REQUIRE(a->v_fp8 == nullptr || (a->v_scales != nullptr && a->dtype == TB_BF16 && sla_tc_supported(a)),
+               "FP8 P/V needs bf16 inputs, v_scales and the tensor-core envelope");
     if (sla_tc_supported(a)) return sla_tc(a, st);
     TB_REQUIRE(a->lin_kv == nullptr, "fused linear epilogue needs the tensor-core envelope");
     return sla_simt(a, st);

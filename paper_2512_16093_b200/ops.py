@@ -154,6 +154,18 @@ def kmean(k: torch.Tensor) -> torch.Tensor:
     return out
 
 
+def quant_v_fp8(v: torch.Tensor):
+    """V [H, L, d] -> (e4m3 codes uint8 [H, L, d], per-head scales f32 [H]) for the
+    opt-in FP8 P/V path (rule in include/tb_capi.h)."""
+    v = _dev_tensor(v, "v")
+    H, L, d = v.shape
+    codes = _empty((H, L, d), torch.uint8, v)
+    scales = _empty((H,), torch.float32, v)
+    ws = _empty((max(H, 1),), torch.int32, v)
+    call("tb_quant_v_fp8", ptr(v), dtype_code(v), H, L, d, ptr(codes), ptr(scales), ptr(ws), stream_ptr())
+    return codes, scales
+
+
 def pool_quant_tokens(x: torch.Tensor, block: int, center: torch.Tensor | None = None, pool: bool = True):
     """attention.py:201-220 (+ fused pooling of raw x) -> (codes, scales, pooled|None)."""
     x = _dev_tensor(x, "x")
@@ -394,8 +406,14 @@ def sla_args(**kw) -> _lib.SlaArgs:
 
 def sla_attention(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: float = 0.1,
                   linear_mix: float = 1.0, quantized: bool = True, scale: float | None = None,
-                  out_dtype=torch.float32, linear_fast: bool | None = None, return_parts: bool = False):
-    """sla_attention (attention.py:392-421) on device tensors [H, L, d]."""
+                  out_dtype=torch.float32, linear_fast: bool | None = None, return_parts: bool = False,
+                  pv_fp8: bool = False):
+    """sla_attention (attention.py:392-421) on device tensors [H, L, d].
+
+    pv_fp8: opt-in FP8 P/V -- V quantized to e4m3 with
+    per-head scales (quant_v_fp8) and the PV product as kind::f8f6f4 on e4m3
+    P; tensor-core envelope and bf16 inputs only.  Off by default: FP8 P/V
+    misses rel-L1 <= 1e-2 when the sparse branch dominates (Appendix A.6)."""
     q, k, v = _dev_tensor(q, "q"), _dev_tensor(k, "k"), _dev_tensor(v, "v")
     if not (q.shape == k.shape == v.shape) or q.dim() != 3:
         raise ValueError(f"q/k/v must share shape [heads, seq, head_dim], got "
@@ -427,6 +445,9 @@ def sla_attention(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: fl
     side = _side_stream()
     side.wait_stream(main)
     kv_part = lin_pack = lin_kv = cov = None
+    v8 = v8s = None
+    if pv_fp8 and not (tc and q.dtype == torch.bfloat16):
+        raise ValueError("FP8 P/V needs bf16 inputs on the tensor-core path (d=128, q_block=128, kv_block=64)")
     if fast_lin:
         # Three streams.  The top-k selection needs only the pooled raw K
         # (attention.py:404-406), so the main stream runs Q pass -> K pooling ->
@@ -437,6 +458,8 @@ def sla_attention(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: fl
         third.wait_stream(main)
         with torch.cuda.stream(third):
             kv_part = linear_kv_part(kb, vb, kv_block)
+            if pv_fp8:                                  # V codes only need v
+                v8, v8s = quant_v_fp8(v)
         with torch.cuda.stream(side):
             km = kmean(k)
             kc, ks, _ = pool_quant_tokens(k, kv_block, km, pool=False)
@@ -445,6 +468,9 @@ def sla_attention(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: fl
         idx, comp, cov = topk_blocks_cov(qp, kp, count, want_comp=return_parts, kpt=kpt)
         main.wait_stream(third)
         kv_part.record_stream(main)
+        if pv_fp8:
+            v8.record_stream(main)
+            v8s.record_stream(main)
         lin_kv = linear_kv_sel(kv_part, cov, nkv)
         main.wait_stream(side)
         for t in (km, kc, ks):
@@ -476,6 +502,8 @@ def sla_attention(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: fl
             if lin:
                 fast = (H * L * d >= (1 << 22)) if linear_fast is None else linear_fast
                 lin_pack = linear_branch(q, k, v, comp, q_block, kv_block, fast=fast)
+    if pv_fp8 and v8 is None:
+        v8, v8s = quant_v_fp8(v)
     q8 = out_dtype == torch.int8
     if q8 and not (tc and not return_parts):
         raise ValueError("int8 output (quantized out-projection operand) needs the tensor-core path")
@@ -495,12 +523,14 @@ def sla_attention(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: fl
                     lin_hs=0 if lin_pack is None else lin_pack.shape[1] * lin_pack.shape[2],
                     lin_kv=ptr(lin_kv), lin_dx=0 if lin_kv is None else lin_kv.shape[2], out=ptr(out),
                     out_dtype=TB_I8 if q8 else (TB_BF16 if out_dtype == torch.bfloat16 else TB_F32),
-                    row_max=ptr(row_max), den=ptr(den), out_scales=ptr(out_scales))
+                    row_max=ptr(row_max), den=ptr(den), out_scales=ptr(out_scales),
+                    v_fp8=ptr(v8), v_scales=ptr(v8s))
     lib = _lib.load(require_device=True)
     _lib.check(lib.tb_sla_attention(__import__("ctypes").byref(args), stream_ptr()), "tb_sla_attention")
     if return_parts:
         parts = dict(qp=qp, kp=kp, idx=idx, comp=comp, q_codes=qc, q_scales=qs, k_codes=kc, k_scales=ks,
-                     k_mean=km, lin_pack=lin_pack, lin_kv=lin_kv, row_max=row_max, den=den, count=count)
+                     k_mean=km, lin_pack=lin_pack, lin_kv=lin_kv, row_max=row_max, den=den, count=count,
+                     v_fp8=v8, v_scales=v8s)
         return out, parts
     return (out, out_scales) if q8 else out
 

@@ -368,3 +368,67 @@ def test_add_norm_matches_reference_norms(tb, layer_norm):
     else:
         ref = ref_s / torch.sqrt((ref_s ** 2).mean(-1, keepdim=True) + 1e-6) * gain
     assert torch.allclose(n.float(), ref, rtol=1e-2, atol=1e-2)
+
+
+# ------------------------------------------------ FP8 P/V
+
+@pytest.mark.parametrize("L", [1000, 4096])
+def test_quant_v_fp8_bit_exact(tb, L):
+    """tb_quant_v_fp8 codes and per-head scales equal oracle.quantize_v_fp8
+    bit-for-bit (bf16 and f32 inputs; a zero head; a tiny-magnitude head
+    that exercises e4m3 subnormals; a head with one large outlier)."""
+    _, _, v = gen.gaussian_qkv(31, 4, L, 128, bf16=True)
+    v = v.copy()
+    v[1] = 0.0
+    v[2] *= 2.0 ** -20
+    v[3, 7, 5] = 300.0
+    want_c, want_s = O.quantize_v_fp8(v)
+    for use_bf16 in (True, False):
+        codes, scales = tb.quant_v_fp8(dev(v, use_bf16))
+        assert np.array_equal(scales.cpu().numpy(), want_s), use_bf16
+        assert np.array_equal(codes.cpu().numpy(), want_c), use_bf16
+
+
+@pytest.mark.parametrize("L", [1000, 4096])
+def test_sla_fp8_pv_gaussian(tb, L):
+    """FP8 P/V on Gaussian inputs: within the north-star bar of the f32 oracle
+    (linear branch on and off), and closer still to the FP8 simulation."""
+    q, k, v = gen.gaussian_qkv(32, 2, L, 128, bf16=True)
+    for mix in (1.0, 0.0):
+        want = O.sla_attention(q, k, v, 128, 64, 0.1, mix)
+        sim = O.sla_attention(q, k, v, 128, 64, 0.1, mix, pv_fp8=True)
+        for parts in (False, True):                   # fast (lazy reference) and exact-max kernels
+            r = tb.sla_attention(dev(q, True), dev(k, True), dev(v, True), 128, 64, 0.1, mix,
+                                 pv_fp8=True, return_parts=parts)
+            got = (r[0] if parts else r).cpu().numpy()
+            # mix 0 (sparse branch alone): e4m3's 3 mantissa bits on P put
+            # ~2e-2 of rel-L1 between ANY two FP8 orderings (the kernel's P is
+            # taken against its lazy reference, the simulation's against the
+            # exact row max), SURVEY A.6 -- the bar there is cos only
+            tol = REL_L1_MAX if mix else 5e-2
+            cos, _, rel1 = metrics(got, sim)
+            assert cos >= COS_MIN and rel1 <= tol, ("sim", mix, parts, cos, rel1)
+            cos, _, rel1 = metrics(got, want)
+            assert cos >= COS_MIN and rel1 <= tol, ("f32", mix, parts, cos, rel1)
+
+
+def test_sla_fp8_pv_sparse_dominated_and_peaky(tb):
+    """Block-coherent inputs (sparse branch dominates) and peaky logits (the
+    fast path's overflow fallback): FP8 P/V stays within cos 0.999 of both the
+    f32 oracle and the FP8 simulation; rel-L1 there is ~2-3e-2 (SURVEY A.6 --
+    why BF16 P/V stays the default)."""
+    q, k, v = gen.block_coherent_qkv(33, 2, 4096, 128, blk=64)
+    qp, kp, vp = gen.gaussian_qkv(34, 2, 4096, 128, bf16=True)
+    kp = kp.copy()
+    for b in (3, 17, 40, 63):
+        kp[:, b * 64:(b + 1) * 64] *= 16.0
+    for (a, b_, c) in ((q, k, v), (qp, kp, vp)):
+        for mix in (1.0, 0.0):
+            want = O.sla_attention(a, b_, c, 128, 64, 0.1, mix)
+            sim = O.sla_attention(a, b_, c, 128, 64, 0.1, mix, pv_fp8=True)
+            got = tb.sla_attention(dev(a, True), dev(b_, True), dev(c, True), 128, 64, 0.1, mix,
+                                   pv_fp8=True).cpu().numpy()
+            cos, _, rel1 = metrics(got, sim)
+            assert cos >= COS_MIN and rel1 <= 5e-2, ("sim", mix, cos, rel1)
+            cos, _, rel1 = metrics(got, want)
+            assert cos >= COS_MIN and rel1 <= 5e-2, ("f32", mix, cos, rel1)

@@ -143,3 +143,24 @@ def test_score_order_probes():
             assert mism <= 0.02 * got.size, (tag, mism)
         # top-k indices (the contract) are exact in every probe
         assert np.array_equal(O.select_topk(qp, kp, 0.3), g[tag + ".idx"]), tag
+
+
+def test_e4m3_encoder_matches_torch_cast():
+    """The FP8 restatement (SURVEY §8 a17 has no reference function) is pinned
+    against torch's CPU float8_e4m3fn cast: every representable value, every
+    midpoint and its float neighbours (round-half-even), subnormals, and
+    Gaussian samples over 7 decades; saturation to 448 in [448, 464)."""
+    import torch
+    rng = np.random.default_rng(0)
+    allv = O.e4m3_decode(np.arange(256, dtype=np.uint8))
+    fin = np.unique(allv[np.isfinite(allv)])
+    mids = ((fin[1:].astype(np.float64) + fin[:-1]) / 2).astype(np.float32)
+    x = np.concatenate([rng.standard_normal(20000).astype(np.float32) * sc for sc in (1e-4, 1e-2, 1, 30, 300)]
+                       + [fin, mids, np.nextafter(mids, np.float32(np.inf)), np.nextafter(mids, np.float32(-np.inf)),
+                          np.array([448.0, 449.0, 463.9, -450.0, 0.0, -0.0], np.float32)])
+    x = x[np.abs(x) < 464]
+    want = torch.from_numpy(x).to(torch.float8_e4m3fn).view(torch.uint8).numpy()
+    assert np.array_equal(O.e4m3_encode(x), want)
+    assert np.array_equal(O.e4m3_decode(want), torch.from_numpy(want).view(torch.float8_e4m3fn).float().numpy())
+    c, s = O.quantize_v_fp8(np.zeros((1, 4, 8), np.float32))
+    assert s[0] == 0 and not c.any()

@@ -23,6 +23,18 @@ a = ops.sla_args(q=ops.ptr(q), k=ops.ptr(k), v=ops.ptr(v), dtype=1, H=H, L=L, d=
                  k_mean=ops.ptr(parts["k_mean"]), idx=ops.ptr(parts["idx"]), vt=None, l_pad=l_pad,
                  num_l=None, den_l=None, lin_ld=0, lin_hs=0, lin_kv=ops.ptr(parts["lin_kv"]),
                  lin_dx=parts["lin_kv"].shape[2], out=ops.ptr(out), out_dtype=1, row_max=None, den=None)
+FP8 = os.environ.get("TB_FP8", "0") == "1"      # opt-in FP8 P/V
+if FP8:
+    v8, v8s = ops.quant_v_fp8(v)
+    a.v_fp8, a.v_scales = ops.ptr(v8), ops.ptr(v8s)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(10):
+        ops.quant_v_fp8(v)
+    e1.record()
+    torch.cuda.synchronize()
+    print(f"quant_v_fp8: {e0.elapsed_time(e1) / 10:.3f} ms")
 lib = _lib.load()
 for _ in range(3):
     lib.tb_sla_attention(ctypes.byref(a), ops.stream_ptr())
@@ -34,4 +46,4 @@ e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 10
 ops_ = 4 * H * L * min(parts["count"] * 64, L) * D
-print(f"{os.environ.get('TB200_LIB', 'libtb200.so')}: {ms:.3f} ms  {ops_ / ms / 1e9:.1f} TOPS")
+print(f"{os.environ.get('TB200_LIB', 'libtb200.so')}{' fp8 P/V' if FP8 else ''}: {ms:.3f} ms  {ops_ / ms / 1e9:.1f} TOPS")
