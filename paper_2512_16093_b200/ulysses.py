@@ -45,27 +45,38 @@ def _world():
     return 1, 0
 
 
+def _pack_seq(x: torch.Tensor, P: int, per: int) -> torch.Tensor:
+    """[L_p, H, d] token shard -> send buffer [P, per, H/P, d]: chunk j = my
+    tokens of head group j (rows past L_p are never read by the receiver, so
+    they stay unwritten)."""
+    Lp, H, d = x.shape
+    hp = H // P
+    send = x.new_empty((P, per, hp, d))
+    send[:, :Lp] = x.view(Lp, P, hp, d).permute(1, 0, 2, 3)
+    return send
+
+
+def _unpack_heads(recv: torch.Tensor, L: int) -> torch.Tensor:
+    """recv [P, per, hp, d] (chunk i = rank i's tokens [i*per, ...)) -> [hp, L, d].
+    token_bounds puts rank i's tokens at global [i*per, min((i+1)*per, L)), so
+    the received buffer read as [P*per, hp, d] is the global token order (the
+    last rank's padding lands past L): one copy."""
+    P, per, hp, d = recv.shape
+    return recv.view(P * per, hp, d)[:L].permute(1, 0, 2).contiguous()
+
+
 def seq_to_heads(x: torch.Tensor, L: int, group=None, align: int = 1) -> torch.Tensor:
     """[L_p, H, d] token shard -> [H/P, L, d] head shard (one all-to-all)."""
-    P, rank = (dist.get_world_size(group), dist.get_rank(group)) if dist.is_initialized() else (1, 0)
-    Lp, H, d = x.shape
+    P = dist.get_world_size(group) if dist.is_initialized() else 1
+    H = x.shape[1]
     if H % P:
         raise ValueError(f"heads {H} not divisible by world size {P}")
-    hp = H // P
     if P == 1:
         return x.permute(1, 0, 2).contiguous()
-    per = shard_size(L, P, align)
-    # send buffer [P, per, hp, d]: chunk j = my tokens for head group j (padded to `per` rows)
-    send = x.new_zeros((P, per, hp, d))
-    send[:, :Lp] = x.view(Lp, P, hp, d).permute(1, 0, 2, 3)
+    send = _pack_seq(x, P, shard_size(L, P, align))
     recv = torch.empty_like(send)
     dist.all_to_all_single(recv, send, group=group)
-    # recv chunk i = tokens of rank i for my head group
-    out = x.new_empty((hp, L, d))
-    for i in range(P):
-        lo, hi = token_bounds(L, P, i, align)
-        out[:, lo:hi] = recv[i, :hi - lo].permute(1, 0, 2)
-    return out
+    return _unpack_heads(recv, L)
 
 
 def heads_to_seq(o: torch.Tensor, L: int, group=None, align: int = 1) -> torch.Tensor:
@@ -75,10 +86,8 @@ def heads_to_seq(o: torch.Tensor, L: int, group=None, align: int = 1) -> torch.T
     if P == 1:
         return o.permute(1, 0, 2).contiguous()
     per = shard_size(L, P, align)
-    send = o.new_zeros((P, per, hp, d))
-    for i in range(P):
-        lo, hi = token_bounds(L, P, i, align)
-        send[i, :hi - lo] = o[:, lo:hi].permute(1, 0, 2)
+    send = o.new_empty((P, per, hp, d))
+    send.view(P * per, hp, d)[:L] = o.permute(1, 0, 2)        # chunk i = rank i's tokens (one copy)
     recv = torch.empty_like(send)
     dist.all_to_all_single(recv, send, group=group)
     lo, hi = token_bounds(L, P, rank, align)
@@ -86,11 +95,32 @@ def heads_to_seq(o: torch.Tensor, L: int, group=None, align: int = 1) -> torch.T
     return recv[:, :hi - lo].permute(1, 0, 2, 3).reshape(hi - lo, P * hp, d).contiguous()
 
 
+def seq_to_heads_qkv(q, k, v, L: int, group=None, align: int = 1):
+    """seq_to_heads of q, k and v with the three all-to-alls issued at once
+    (async): each tensor's unpack copy runs while the next exchange is still
+    on the wire."""
+    P = dist.get_world_size(group) if dist.is_initialized() else 1
+    H = q.shape[1]
+    if H % P:
+        raise ValueError(f"heads {H} not divisible by world size {P}")
+    if P == 1:
+        return tuple(t.permute(1, 0, 2).contiguous() for t in (q, k, v))
+    per = shard_size(L, P, align)
+    bufs = []
+    for t in (q, k, v):
+        send = _pack_seq(t, P, per)
+        recv = torch.empty_like(send)
+        bufs.append((send, recv, dist.all_to_all_single(recv, send, group=group, async_op=True)))
+    out = []
+    for send, recv, work in bufs:
+        work.wait()
+        out.append(_unpack_heads(recv, L))
+    return tuple(out)
+
+
 def ulysses_sla_attention(q_shard, k_shard, v_shard, L: int, attn_fn, group=None, align: int = 1):
     """Token-sharded q/k/v [L_p, H, d] -> attention on a head shard -> token-sharded o."""
-    qh = seq_to_heads(q_shard, L, group, align)
-    kh = seq_to_heads(k_shard, L, group, align)
-    vh = seq_to_heads(v_shard, L, group, align)
+    qh, kh, vh = seq_to_heads_qkv(q_shard, k_shard, v_shard, L, group, align)
     oh = attn_fn(qh, kh, vh)
     return heads_to_seq(oh.to(q_shard.dtype), L, group, align)
 
@@ -128,8 +158,6 @@ def heads_to_seq_q8(codes: torch.Tensor, scales: torch.Tensor, L: int, group=Non
 def ulysses_sla_attention_q8(q_shard, k_shard, v_shard, L: int, attn_q8_fn, group=None, block: int = 128):
     """Token-sharded q/k/v (128-aligned shards) -> head-shard attention emitting
     int8 codes + block scales -> token-shard out-projection operand."""
-    qh = seq_to_heads(q_shard, L, group, block)
-    kh = seq_to_heads(k_shard, L, group, block)
-    vh = seq_to_heads(v_shard, L, group, block)
+    qh, kh, vh = seq_to_heads_qkv(q_shard, k_shard, v_shard, L, group, block)
     codes, scales = attn_q8_fn(qh, kh, vh)
     return heads_to_seq_q8(codes, scales, L, group, block)
