@@ -121,7 +121,8 @@ def block_forward(x: torch.Tensor, sigma: float, w: DeviceLayer, heads: int, sla
         if hd == 128:
             def attn_q8(qh, kh, vh):
                 return ops.sla_attention(qh, kh, vh, sla["q_block"], sla["kv_block"], sla["topk_ratio"],
-                                         sla.get("linear_mix", 1.0), True, out_dtype=torch.int8)
+                                         sla.get("linear_mix", 1.0), True, out_dtype=torch.int8,
+                                         pv_fp8=sla.get("pv_fp8", False))
             # int8 codes + scales cross the reverse all-to-all (half the bytes of bf16)
             oq, osc = ulysses.ulysses_sla_attention_q8(q, k, v, L_global, attn_q8, group, TOKEN_ALIGN)
         else:
@@ -136,7 +137,7 @@ def block_forward(x: torch.Tensor, sigma: float, w: DeviceLayer, heads: int, sla
             # A operand (codes [L, H*hd] + scales) directly
             oq, osc = ops.sla_attention(qkv[:heads], qkv[heads:2 * heads], qkv[2 * heads:], sla["q_block"],
                                         sla["kv_block"], sla["topk_ratio"], sla.get("linear_mix", 1.0), True,
-                                        out_dtype=torch.int8)
+                                        out_dtype=torch.int8, pv_fp8=sla.get("pv_fp8", False))
         else:
             o = attn(qkv[:heads], qkv[heads:2 * heads], qkv[2 * heads:])           # [H, L, hd]
             oq, osc = ops.quantize_blockwise_planar(o)

@@ -22,11 +22,18 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _staged_all_to_all(out, inp, group=None, **kw):
-    # gloo has no CUDA all_to_all: stage through host memory
+class _Done:
+    def wait(self):
+        return True
+
+
+def _staged_all_to_all(out, inp, group=None, async_op=False, **kw):
+    # gloo has no CUDA all_to_all: stage through host memory (synchronously;
+    # an async caller gets an already-completed work handle)
     h_out = torch.empty(out.shape, dtype=out.dtype)
     _orig_a2a(h_out, inp.cpu(), group=group)
     out.copy_(h_out)
+    return _Done() if async_op else None
 
 
 _orig_a2a = dist.all_to_all_single

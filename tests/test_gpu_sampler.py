@@ -94,3 +94,7 @@ def test_fast_dit_tensor_core_envelope_matches_oracle(S):
     nz = [torch.from_numpy(n).cuda() for n in noises[1:]]
     got = dit.rcm_sample(dl, heads, sla, x_init, nz, sig).cpu().numpy()
     close(got, want)
+    # opt-in FP8 P/V attention inside the same DiT: the
+    # sample stays within the sampler bar of the f32-PV oracle
+    got8 = dit.rcm_sample(dl, heads, dict(sla, pv_fp8=True), x_init, nz, sig).cpu().numpy()
+    close(got8, want)
