@@ -286,8 +286,28 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("TB_BENCH_GLOO_CHECK") == "1":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 and os.environ.get("TB_BENCH_GLOO_CHECK") == "1":
+        # FUNCTIONAL CHECK ONLY (never a measurement): exercises the N>1 code path
+        # (token shards, Ulysses exchanges, max-over-ranks) on a one-GPU box --
+        # NCCL refuses two ranks on one device, so gloo with the exchange
+        # staged through host memory (tests/test_gpu_dit_ulysses.py's shim)
+        dist.init_process_group("gloo")
+        _a2a = dist.all_to_all_single
+
+        class _Done:
+            def wait(self):
+                return True
+
+        def _staged(out, inp, group=None, async_op=False, **kw):
+            h = torch.empty(out.shape, dtype=out.dtype)
+            _a2a(h, inp.cpu(), group=group)
+            out.copy_(h)
+            return _Done() if async_op else None
+        dist.all_to_all_single = _staged
+    elif world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2512_16093_b200 import _lib, ops, ulysses
     from paper_2512_16093_b200.attention import attention_flop_report, SLAConfig
@@ -419,6 +439,37 @@ def main():
         ems = e0.elapsed_time(e1) / n_e2e
         e2e = {"value": total_ops / (ems * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": ems,
                "h2d_bytes_per_step": sum(t.numel() * 2 for t in hq), "d2h_bytes_per_step": hout.numel() * 2}
+    else:
+        # N > 1: each rank's token shard of q/k/v from pinned host memory, the
+        # Ulysses attention (exchange, head-shard attention, exchange back), and
+        # the token-shard output back to pinned host memory; max over ranks.
+        # Bytes are per rank (every rank moves its own shard).
+        hq = [t.cpu().pin_memory() for t in shard]
+        hout = torch.empty(shard[0].shape, dtype=torch.bfloat16).pin_memory()
+        dq = [torch.empty_like(t) for t in shard]
+
+        def e2e_step():
+            for d_, h_ in zip(dq, hq):
+                d_.copy_(h_, non_blocking=True)
+            o = ulysses.ulysses_sla_attention(dq[0], dq[1], dq[2], L_, attn)
+            hout.copy_(o, non_blocking=True)
+        e2e_step()
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n_e2e = max(2, min(args.steps, 5))
+        e0.record()
+        for _ in range(n_e2e):
+            e2e_step()
+        e1.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / n_e2e], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ems = float(t.item())
+        e2e = {"value": total_ops / (ems * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": ems,
+               "h2d_bytes_per_step": sum(t_.numel() * 2 for t_ in hq), "d2h_bytes_per_step": hout.numel() * 2,
+               "bytes_note": "per rank"}
+        del hq, hout, dq
 
     # ---- W8A8 GEMM sweep (configs[1]), tensor-core exact + fast promotion
     w8 = None
