@@ -432,3 +432,26 @@ def test_sla_fp8_pv_sparse_dominated_and_peaky(tb):
             assert cos >= COS_MIN and rel1 <= 5e-2, ("sim", mix, cos, rel1)
             cos, _, rel1 = metrics(got, want)
             assert cos >= COS_MIN and rel1 <= 5e-2, ("f32", mix, cos, rel1)
+
+
+@pytest.mark.parametrize("L", [128, 200, 1100])
+def test_sla_fp8_pv_edges_and_int8_output(tb, L):
+    """FP8 P/V at the smallest tensor-core sequence (one q-block), ragged last
+    kv blocks, and with the out-projection's int8 output: codes and scales
+    equal quantize_blockwise_planar of the bf16 FP8-P/V output."""
+    q, k, v = gen.gaussian_qkv(35, 2, L, 128, bf16=True)
+    dq, dk, dv = dev(q, True), dev(k, True), dev(v, True)
+    want = O.sla_attention(q, k, v, 128, 64, 0.1, 1.0)
+    got = tb.sla_attention(dq, dk, dv, 128, 64, 0.1, 1.0, pv_fp8=True).cpu().numpy()
+    cos, _, rel1 = metrics(got, want)
+    assert cos >= COS_MIN and rel1 <= REL_L1_MAX, (cos, rel1)
+    o16 = tb.sla_attention(dq, dk, dv, 128, 64, 0.1, 1.0, out_dtype=torch.bfloat16, pv_fp8=True)
+    codes, scales = tb.sla_attention(dq, dk, dv, 128, 64, 0.1, 1.0, out_dtype=torch.int8, pv_fp8=True)
+    wq, ws = tb.quantize_blockwise_planar(o16)
+    assert torch.equal(codes, wq) and torch.equal(scales, ws)
+
+
+def test_quant_v_fp8_rejects_misaligned(tb):
+    v = torch.zeros((1, 129, 8), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(ValueError):
+        tb.quant_v_fp8(v.view(-1)[1:1 + 128 * 8].view(1, 128, 8))     # 2-B offset: not 16-B aligned
