@@ -166,6 +166,19 @@ typedef struct tb_sla_args {
      * sparse-dominated rows). */
     const uint8_t *v_fp8;
     const float *v_scales;
+    /* Fused Ulysses return path (out_dtype TB_I8 only):
+     * when out_peers != NULL the epilogue stores each 128-token tile's int8
+     * codes and block scale straight into the buffers of the rank that owns
+     * those tokens (NVLink peer memory, e.g. torch symmetric memory), instead
+     * of a local buffer followed by an all-to-all.  out_peers / scale_peers
+     * are DEVICE arrays of P pointers; owner = row / peer_rows (peer_rows %
+     * 128 == 0); codes land at out_peers[owner] + (row - owner*peer_rows) *
+     * out_heads*d + (head0 + h)*d and the scale at scale_peers[owner]
+     * [((row - owner*peer_rows)/128) * out_heads + head0 + h].  out and
+     * out_scales are ignored. */
+    void *const *out_peers;
+    float *const *scale_peers;
+    int64_t peer_rows, head0, out_heads;
 } tb_sla_args;
 
 /* _sparse_branch + combine (attention.py:347-389, 392-421).  d==128,

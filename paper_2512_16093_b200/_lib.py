@@ -81,6 +81,8 @@ class SlaArgs(ctypes.Structure):
         ("row_max", _P), ("den", _P),
         ("out_scales", _P),
         ("v_fp8", _P), ("v_scales", _P),
+        ("out_peers", _P), ("scale_peers", _P),
+        ("peer_rows", _I), ("head0", _I), ("out_heads", _I),
     ]
 
 

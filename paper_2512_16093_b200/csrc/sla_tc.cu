@@ -866,11 +866,25 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             ptx::named_bar_sync(1, BM);
             am = fmaxf(fmaxf(S.corr_s[0], S.corr_s[1]), fmaxf(S.corr_s[2], S.corr_s[3]));
             const float sc = quant_scale(am);
-            if (threadIdx.x == 0) a.out_scales[(int64_t)n * a.H + h] = sc;
+            // destination: this rank's buffers, or (fused Ulysses return) the
+            // token owner's buffers in peer memory -- a 128-row tile never
+            // straddles two owners (peer_rows % 128 == 0)
+            int8_t *obase = reinterpret_cast<int8_t *>(a.out);
+            float *sbase = a.out_scales;
+            int64_t orow0 = (int64_t)n * BM, ocols = a.H * D, ohead = h;
+            if (a.out_peers) {
+                const int64_t owner = orow0 / a.peer_rows;
+                obase = reinterpret_cast<int8_t *>(a.out_peers[owner]);
+                sbase = a.scale_peers[owner];
+                orow0 -= owner * a.peer_rows;
+                ocols = a.out_heads * D;
+                ohead = a.head0 + h;
+            }
+            if (threadIdx.x == 0) sbase[(orow0 / BM) * (ocols / D) + ohead] = sc;
             const float safe = (sc == 0.0f) ? 1.0f : sc;
             const float rq = __frcp_rn(safe);
             const bool exq = !(safe >= 1.17549435e-38f && rq <= 3.0e38f);   // subnormal scale: exact division
-            int8_t *dst = reinterpret_cast<int8_t *>(a.out) + (int64_t)row * (a.H * D) + (int64_t)h * D;
+            int8_t *dst = obase + (orow0 + r) * ocols + ohead * D;
 #pragma unroll 1
             for (int c = 0; c < D; c += 16) {
                 float v[16];
@@ -1447,8 +1461,12 @@ extern "C" int tb_sla_attention(const tb_sla_args *a, void *stream) {
                "quantized branch needs codes, scales and k_mean");
     if (a->H == 0) return TB_OK;
     cudaStream_t st = as_stream(stream);
-    TB_REQUIRE(a->out_dtype != TB_I8 || (a->out_scales != nullptr && sla_tc_supported(a)),
+    TB_REQUIRE(a->out_dtype != TB_I8 || ((a->out_scales != nullptr || a->out_peers != nullptr) && sla_tc_supported(a)),
                "int8 output needs the tensor-core kernel and out_scales");
+    TB_REQUIRE(a->out_peers == nullptr ||
+                   (a->out_dtype == TB_I8 && a->scale_peers != nullptr && a->peer_rows > 0 && a->peer_rows % 128 == 0 &&
+                    a->head0 >= 0 && a->head0 + a->H <= a->out_heads),
+               "peer output needs int8 output, scale_peers, peer_rows % 128 == 0 and head0 + H <= out_heads");
     TB_REQUIRE(a->v_fp8 == nullptr || (a->v_scales != nullptr && a->dtype == TB_BF16 && sla_tc_supported(a)),
                "FP8 P/V needs bf16 inputs, v_scales and the tensor-core envelope");
     if (sla_tc_supported(a)) return sla_tc(a, st);

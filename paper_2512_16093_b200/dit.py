@@ -16,6 +16,7 @@ attention exchanges q/k/v/o with one all-to-all each way (ulysses.py).
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import torch
@@ -123,8 +124,16 @@ def block_forward(x: torch.Tensor, sigma: float, w: DeviceLayer, heads: int, sla
                 return ops.sla_attention(qh, kh, vh, sla["q_block"], sla["kv_block"], sla["topk_ratio"],
                                          sla.get("linear_mix", 1.0), True, out_dtype=torch.int8,
                                          pv_fp8=sla.get("pv_fp8", False))
-            # int8 codes + scales cross the reverse all-to-all (half the bytes of bf16)
-            oq, osc = ulysses.ulysses_sla_attention_q8(q, k, v, L_global, attn_q8, group, TOKEN_ALIGN)
+            if os.environ.get("TB_ULYSSES_P2P") == "1":
+                # reverse exchange fused into the attention epilogue (peer-memory stores)
+                def attn_peer(qh, kh, vh, peer_out):
+                    return ops.sla_attention(qh, kh, vh, sla["q_block"], sla["kv_block"], sla["topk_ratio"],
+                                             sla.get("linear_mix", 1.0), True, out_dtype=torch.int8,
+                                             pv_fp8=sla.get("pv_fp8", False), peer_out=peer_out)
+                oq, osc = ulysses.ulysses_sla_attention_q8_p2p(q, k, v, L_global, attn_peer, group, TOKEN_ALIGN)
+            else:
+                # int8 codes + scales cross the reverse all-to-all (half the bytes of bf16)
+                oq, osc = ulysses.ulysses_sla_attention_q8(q, k, v, L_global, attn_q8, group, TOKEN_ALIGN)
         else:
             o = ulysses.ulysses_sla_attention(q, k, v, L_global, attn, group, TOKEN_ALIGN)
             oq, osc = ops.quantize_blockwise(o.reshape(Lp, dim).contiguous(), 128, check_finite=False)

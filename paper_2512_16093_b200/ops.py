@@ -407,13 +407,19 @@ def sla_args(**kw) -> _lib.SlaArgs:
 def sla_attention(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: float = 0.1,
                   linear_mix: float = 1.0, quantized: bool = True, scale: float | None = None,
                   out_dtype=torch.float32, linear_fast: bool | None = None, return_parts: bool = False,
-                  pv_fp8: bool = False):
+                  pv_fp8: bool = False, peer_out: dict | None = None):
     """sla_attention (attention.py:392-421) on device tensors [H, L, d].
 
     pv_fp8: opt-in FP8 P/V -- V quantized to e4m3 with
     per-head scales (quant_v_fp8) and the PV product as kind::f8f6f4 on e4m3
     P; tensor-core envelope and bf16 inputs only.  Off by default: FP8 P/V
-    misses rel-L1 <= 1e-2 when the sparse branch dominates (Appendix A.6)."""
+    misses rel-L1 <= 1e-2 when the sparse branch dominates (Appendix A.6).
+
+    peer_out (out_dtype int8 only): the fused Ulysses return path -- dict with
+    ``codes`` / ``scales``: int64 device tensors [P] of the owners' buffer
+    addresses (peer memory), ``rows`` (token-shard rows, multiple of 128),
+    ``head0`` (global index of this shard's first head), ``heads`` (global H).
+    The epilogue stores every tile in its token owner's buffers; returns None."""
     q, k, v = _dev_tensor(q, "q"), _dev_tensor(k, "k"), _dev_tensor(v, "v")
     if not (q.shape == k.shape == v.shape) or q.dim() != 3:
         raise ValueError(f"q/k/v must share shape [heads, seq, head_dim], got "
@@ -507,11 +513,16 @@ def sla_attention(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: fl
     q8 = out_dtype == torch.int8
     if q8 and not (tc and not return_parts):
         raise ValueError("int8 output (quantized out-projection operand) needs the tensor-core path")
+    if peer_out is not None and not q8:
+        raise ValueError("peer output needs out_dtype int8")
     # int8: codes [L, H*d] + scales [nq, H] of the bf16-rounded output (the
     # out-projection's block-quantized A operand, written by the epilogue)
-    out = (torch.empty((L, H * d), dtype=torch.int8, device=q.device) if q8
-           else torch.empty((H, L, d), dtype=out_dtype, device=q.device))
-    out_scales = torch.empty((nq, H), dtype=torch.float32, device=q.device) if q8 else None
+    if peer_out is not None:
+        out = out_scales = None
+    else:
+        out = (torch.empty((L, H * d), dtype=torch.int8, device=q.device) if q8
+               else torch.empty((H, L, d), dtype=out_dtype, device=q.device))
+        out_scales = torch.empty((nq, H), dtype=torch.float32, device=q.device) if q8 else None
     row_max = torch.empty((H, L), dtype=torch.float32, device=q.device) if return_parts else None
     den = torch.empty((H, L), dtype=torch.float32, device=q.device) if return_parts else None
     args = sla_args(q=ptr(q), k=ptr(k), v=ptr(v), dtype=dtype_code(q), H=H, L=L, d=d, q_block=q_block,
@@ -525,6 +536,9 @@ def sla_attention(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: fl
                     out_dtype=TB_I8 if q8 else (TB_BF16 if out_dtype == torch.bfloat16 else TB_F32),
                     row_max=ptr(row_max), den=ptr(den), out_scales=ptr(out_scales),
                     v_fp8=ptr(v8), v_scales=ptr(v8s))
+    if peer_out is not None:
+        args.out_peers, args.scale_peers = ptr(peer_out["codes"]), ptr(peer_out["scales"])
+        args.peer_rows, args.head0, args.out_heads = int(peer_out["rows"]), int(peer_out["head0"]), int(peer_out["heads"])
     lib = _lib.load(require_device=True)
     _lib.check(lib.tb_sla_attention(__import__("ctypes").byref(args), stream_ptr()), "tb_sla_attention")
     if return_parts:
@@ -532,6 +546,8 @@ def sla_attention(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: fl
                      k_mean=km, lin_pack=lin_pack, lin_kv=lin_kv, row_max=row_max, den=den, count=count,
                      v_fp8=v8, v_scales=v8s)
         return out, parts
+    if peer_out is not None:
+        return None
     return (out, out_scales) if q8 else out
 
 

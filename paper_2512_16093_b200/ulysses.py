@@ -161,3 +161,52 @@ def ulysses_sla_attention_q8(q_shard, k_shard, v_shard, L: int, attn_q8_fn, grou
     qh, kh, vh = seq_to_heads_qkv(q_shard, k_shard, v_shard, L, group, block)
     codes, scales = attn_q8_fn(qh, kh, vh)
     return heads_to_seq_q8(codes, scales, L, group, block)
+
+
+# ------------------------------------------------- fused return path (P2P)
+# The head-shard attention's epilogue stores each 128-token tile's int8 codes
+# and block scale straight into the token owner's buffers over NVLink (torch
+# symmetric memory gives every rank the peers' buffer addresses), so the
+# reverse exchange is part of the attention kernel: no send buffer, no
+# all-to-all launch, and the transfer overlaps the attention tile by tile.
+# A device-side barrier then makes every peer's stores visible before the
+# out-projection reads them.  Reuse of the buffers by the next layer is
+# ordered by that layer's forward all-to-all (a rank cannot start writing
+# into a peer before the peer has joined it, which it does only after its
+# out-projection in stream order).
+_P2P = {}
+
+
+def _p2p_buffers(per: int, H: int, d: int, group, device, block: int = 128):
+    import torch.distributed._symmetric_memory as symm_mem
+    g = group if group is not None else dist.group.WORLD
+    key = (per, H, d, g.group_name, device.index)
+    if key not in _P2P:
+        codes = symm_mem.empty((per, H * d), dtype=torch.int8, device=device)
+        scales = symm_mem.empty((per // block, H), dtype=torch.float32, device=device)
+        hc = symm_mem.rendezvous(codes, g.group_name)
+        hs = symm_mem.rendezvous(scales, g.group_name)
+        cp = torch.tensor([int(x) for x in hc.buffer_ptrs], dtype=torch.int64, device=device)
+        sp = torch.tensor([int(x) for x in hs.buffer_ptrs], dtype=torch.int64, device=device)
+        _P2P[key] = (codes, scales, hc, cp, sp)
+    return _P2P[key]
+
+
+def ulysses_sla_attention_q8_p2p(q_shard, k_shard, v_shard, L: int, attn_peer_fn, group=None, block: int = 128):
+    """ulysses_sla_attention_q8 with the reverse exchange fused into the
+    attention epilogue (peer-memory stores).  attn_peer_fn(qh, kh, vh,
+    peer_out) runs the head-shard attention with ops.sla_attention(...,
+    out_dtype=torch.int8, peer_out=peer_out).  Returns this rank's codes
+    [L_p, H*d] and scales [ceil(L_p/128), H] (views of its symmetric buffers,
+    valid until the next call)."""
+    P, rank = dist.get_world_size(group), dist.get_rank(group)
+    Lp, H, d = q_shard.shape
+    if H % P:
+        raise ValueError(f"heads {H} not divisible by world size {P}")
+    per = shard_size(L, P, block)
+    codes, scales, hc, cp, sp = _p2p_buffers(per, H, d, group, q_shard.device, block)
+    qh, kh, vh = seq_to_heads_qkv(q_shard, k_shard, v_shard, L, group, block)
+    attn_peer_fn(qh, kh, vh, dict(codes=cp, scales=sp, rows=per, head0=rank * (H // P), heads=H))
+    hc.barrier()                    # all peers' tile stores into this rank's buffers are done
+    lo, hi = token_bounds(L, P, rank, block)
+    return codes[:hi - lo], scales[:-(-(hi - lo) // block)]
