@@ -269,6 +269,18 @@ int tb_w8a8_gemm_quant(const int8_t *a, const float *sa, const int8_t *bt, const
                        int64_t M, int64_t N, int64_t K, int64_t block, int act, int8_t *q_out, float *scales_out,
                        void *stream);
 
+/* Fused Ulysses forward exchange (new, multi-GPU; replaces the q/k/v
+ * all-to-all after the qkv projection of toy_block_forward, sampler.py:
+ * 161-170): fast-mode W8A8 of this rank's token shard (sequence rows [row0,
+ * row0 + M)) whose epilogue TMA-stores every output box straight into the
+ * head owner's buffer.  peers: HOST array of P (<= 8) device pointers (peer
+ * memory, e.g. torch symmetric memory), each bf16 [3*(H/P), L, 128] = the q,
+ * k, v planes of that rank's heads over all L tokens.  N = 3*H*128; 2-SM
+ * kernel shapes only (block 128, M >= 256), TB_EUNSUPPORTED otherwise. */
+int tb_w8a8_gemm_qkv_peers(const int8_t *a, const float *sa, const int8_t *bt, const float *sb, const float *bias,
+                           int64_t M, int64_t N, int64_t K, int64_t block, void *const *peers, int64_t P,
+                           int64_t H, int64_t row0, int64_t L, void *stream);
+
 /* Fast-mode W8A8: identical operands, the two block scales folded into one
  * FMA per element (tolerance-level, not bit-exact); used by the DiT step. */
 int tb_w8a8_gemm_fast(const int8_t *a, const float *sa, const int8_t *bt, const float *sb,

@@ -35,6 +35,7 @@ SIGNATURES = {
     "tb_w8a8_gemm": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _i, _P],
     "tb_w8a8_gemm_fast": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _i, _P],
     "tb_w8a8_gemm_quant": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _i, _P, _P, _P],
+    "tb_w8a8_gemm_qkv_peers": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _I, _I, _I, _I, _P],
     "tb_w8a8_gemm_fast_ex": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _i, _I, _i, _P],
     "tb_quantized_linear": [_P, _i, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _i, _P],
     "tb_pool_block_means": [_P, _i, _I, _I, _I, _I, _P, _P],

@@ -16,6 +16,8 @@
 // fast mode folds the two scales into one FMA (tolerance-level).
 #include <cstdlib>
 
+#include <cstring>
+
 #include "common.cuh"
 #include "ptx.cuh"
 #include "tmap.cuh"
@@ -300,6 +302,18 @@ __device__ __forceinline__ void tile_coords(int tile, int nmp, int nnt, int &mp,
     nt = w / gs;
 }
 
+// Fused Ulysses forward exchange (planar bf16 output only): one tensor map per
+// destination rank over that rank's head-shard buffer [3*hp, L, plane] (q, k, v
+// planes of its hp heads, all L tokens).  Output plane c/plane = w*H + head
+// (w = q/k/v) goes to rank head/hp, plane w*hp + head%hp, at global token row
+// row0 + local row -- the GEMM's epilogue stores each tile straight into the
+// head owner's buffer over peer memory, replacing the q/k/v all-to-all.
+constexpr int MAX_PEERS = 8;
+struct alignas(64) PeerMaps {
+    CUtensorMap m[MAX_PEERS];
+    int32_t n, hp, H, row0;
+};
+
 // OUTM: 0 f32, 1 bf16, 2 block-quantized INT8 (the next projection's A
 // operand: the bf16-rounded result quantized per 128x128 block exactly like
 // quantize_blockwise, codes TMA-stored, one f32 scale per block to qscales).
@@ -308,7 +322,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
     const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
     const __grid_constant__ CUtensorMap tma_out,
     const float *__restrict__ sa, const float *__restrict__ sb, const float *__restrict__ bias,
-    int M, int N, int K, int plane, int act, float *__restrict__ qscales) {
+    int M, int N, int K, int plane, int act, float *__restrict__ qscales, const __grid_constant__ PeerMaps pm) {
     using namespace gemm2;
     constexpr bool OUT_BF16 = OUTM == 1;
     constexpr int CW = BN / 2;
@@ -571,8 +585,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
                 __syncwarp();
                 if (lane == 0) {
                     const int c = col0 + ch * CPC;
-                    if (plane) ptx::tma_store_3d(&tma_out, S.stage_out[ew], c % plane, row0, c / plane);
-                    else ptx::tma_store_2d(&tma_out, S.stage_out[ew], c, row0);
+                    if (pm.n) {
+                        // the head owner's buffer; boxes past this rank's rows are
+                        // skipped (they would land in the next rank's token rows)
+                        const int pl = c / plane, w = pl / pm.H, hd = pl - w * pm.H, owner = hd / pm.hp;
+                        if (row0 < M)
+                            ptx::tma_store_3d(&pm.m[owner], S.stage_out[ew], c % plane, pm.row0 + row0,
+                                              w * pm.hp + (hd - owner * pm.hp));
+                    } else if (plane) {
+                        ptx::tma_store_3d(&tma_out, S.stage_out[ew], c % plane, row0, c / plane);
+                    } else {
+                        ptx::tma_store_2d(&tma_out, S.stage_out[ew], c, row0);
+                    }
                     ptx::bulk_commit();
                 }
             }
@@ -700,12 +724,14 @@ int w8a8_dispatch(const int8_t *a, const float *sa, const int8_t *bt, const floa
         int clusters = num_sms() / 2;
         if (ntiles < clusters) clusters = ntiles;
         const int grid = 2 * clusters;
+        PeerMaps no_peers;
+        memset(&no_peers, 0, sizeof(no_peers));
 #define TB_GEMM2(E, B)                                                                                     \
     {                                                                                                      \
         auto kern = w8a8_2sm_kernel<E, (B) ? 1 : 0>;                                                       \
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm2::SMEM_BYTES);   \
         kern<<<grid, gemm2::THREADS, gemm2::SMEM_BYTES, st>>>(ta, tbm, tout, sa, sb, bias, (int)M, (int)N, (int)K, \
-                                                              (int)plane, act, nullptr);                         \
+                                                              (int)plane, act, nullptr, no_peers);               \
     }
         if (exact && !obf) TB_GEMM2(true, false)
         else if (exact) TB_GEMM2(true, true)
@@ -805,7 +831,48 @@ extern "C" int tb_w8a8_gemm_quant(const int8_t *a, const float *sa, const int8_t
     if (ntiles < clusters) clusters = ntiles;
     auto kern = w8a8_2sm_kernel<false, 2>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm2::SMEM_BYTES);
+    PeerMaps no_peers;
+    memset(&no_peers, 0, sizeof(no_peers));
     kern<<<2 * clusters, gemm2::THREADS, gemm2::SMEM_BYTES, as_stream(stream)>>>(
-        ta, tbm, tout, sa, sb, bias, (int)M, (int)N, (int)K, 0, act, scales_out);
+        ta, tbm, tout, sa, sb, bias, (int)M, (int)N, (int)K, 0, act, scales_out, no_peers);
     return check_launch("w8a8_gemm_quant");
+}
+
+// Fused Ulysses forward exchange: the qkv projection of this rank's token shard
+// (rows [row0, row0 + M) of the sequence) with every 64-column x 32-row output
+// box TMA-stored into the head owner's buffer.  peers: HOST array of P device
+// pointers (peer memory), each bf16 [3*hp, L, 128] (q, k, v planes of that
+// rank's hp = H/P heads); N = 3*H*128; 2-SM kernel shapes (M >= 256).
+extern "C" int tb_w8a8_gemm_qkv_peers(const int8_t *a, const float *sa, const int8_t *bt, const float *sb,
+                                      const float *bias, int64_t M, int64_t N, int64_t K, int64_t block,
+                                      void *const *peers, int64_t P, int64_t H, int64_t row0, int64_t L,
+                                      void *stream) {
+    TB_REQUIRE(peers != nullptr && P >= 1 && P <= MAX_PEERS && H % P == 0, "1 <= P <= 8 peers, H % P == 0");
+    TB_REQUIRE(N == 3 * H * 128, "N must be 3 * H * 128 (q, k, v planes of 128)");
+    TB_REQUIRE(row0 >= 0 && row0 + M <= L, "token rows out of range");
+    if (M == 0) return TB_OK;
+    const bool ok = block == 128 && K % 128 == 0 && K > 0 && N % 256 == 0 && M >= 256 && M < (1ll << 31) &&
+                    ((uintptr_t)a % 16) == 0 && ((uintptr_t)bt % 16) == 0;
+    if (!ok) return fail(TB_EUNSUPPORTED, "peer qkv epilogue needs the 2-SM kernel shape (block 128, M >= 256)");
+    const int64_t hp = H / P;
+    CUtensorMap ta, tbm;
+    PeerMaps pm;
+    memset(&pm, 0, sizeof(pm));
+    bool okm = make_tmap_2d(&ta, a, CU_TENSOR_MAP_DATA_TYPE_UINT8, K, M, K, 128, 128) &&
+               make_tmap_2d(&tbm, bt, CU_TENSOR_MAP_DATA_TYPE_UINT8, K, N, K, 128, 128);
+    for (int64_t r = 0; r < P; r++) {
+        TB_REQUIRE(peers[r] != nullptr && (uintptr_t)peers[r] % 16 == 0, "peer buffers must be 16-B aligned");
+        okm = okm && make_tmap_3d(&pm.m[r], peers[r], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 128, L, 3 * hp, 256,
+                                  L * 256, 64, 32, 1);
+    }
+    if (!okm) return fail(TB_ECUDA, "cuTensorMapEncodeTiled failed (peers)");
+    pm.n = (int)P; pm.hp = (int)hp; pm.H = (int)H; pm.row0 = (int)row0;
+    const int ntiles = (int)(cdiv(M, 256) * (N / 256));
+    int clusters = num_sms() / 2;
+    if (ntiles < clusters) clusters = ntiles;
+    auto kern = w8a8_2sm_kernel<false, 1>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm2::SMEM_BYTES);
+    kern<<<2 * clusters, gemm2::THREADS, gemm2::SMEM_BYTES, as_stream(stream)>>>(
+        ta, tbm, ta, sa, sb, bias, (int)M, (int)N, (int)K, 128, 0, nullptr, pm);
+    return check_launch("w8a8_gemm_qkv_peers");
 }

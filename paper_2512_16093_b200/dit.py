@@ -114,7 +114,19 @@ def block_forward(x: torch.Tensor, sigma: float, w: DeviceLayer, heads: int, sla
                                  sla.get("linear_mix", 1.0), True, out_dtype=torch.bfloat16)
 
     aq, asc = ops.quantize_blockwise(a, 128, check_finite=False)
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+    multi = dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1
+    if multi and hd == 128 and os.environ.get("TB_ULYSSES_P2P") == "1":
+        # both exchanges fused into their producers over peer memory: the qkv
+        # GEMM epilogue stores into the head owners' buffers, the attention
+        # epilogue stores the int8 out-projection operand into the token owners'
+        qh, kh, vh = ulysses.qkv_to_heads_p2p(aq, asc, w.qkv.bt, w.qkv.scales, L_global, heads, group, TOKEN_ALIGN)
+
+        def attn_peer(qh_, kh_, vh_, peer_out):
+            return ops.sla_attention(qh_, kh_, vh_, sla["q_block"], sla["kv_block"], sla["topk_ratio"],
+                                     sla.get("linear_mix", 1.0), True, out_dtype=torch.int8,
+                                     pv_fp8=sla.get("pv_fp8", False), peer_out=peer_out)
+        oq, osc = ulysses.attn_return_p2p(qh, kh, vh, L_global, attn_peer, group, TOKEN_ALIGN)
+    elif multi:
         # token shards are TOKEN_ALIGN-aligned (token_bounds(L, P, rank, TOKEN_ALIGN)),
         # so every 128x128 quantization block of the attention output is rank-local
         qkv = ops.w8a8_gemm(aq, asc, w.qkv.bt, w.qkv.scales, 128, None, torch.bfloat16, exact=False)
@@ -124,16 +136,8 @@ def block_forward(x: torch.Tensor, sigma: float, w: DeviceLayer, heads: int, sla
                 return ops.sla_attention(qh, kh, vh, sla["q_block"], sla["kv_block"], sla["topk_ratio"],
                                          sla.get("linear_mix", 1.0), True, out_dtype=torch.int8,
                                          pv_fp8=sla.get("pv_fp8", False))
-            if os.environ.get("TB_ULYSSES_P2P") == "1":
-                # reverse exchange fused into the attention epilogue (peer-memory stores)
-                def attn_peer(qh, kh, vh, peer_out):
-                    return ops.sla_attention(qh, kh, vh, sla["q_block"], sla["kv_block"], sla["topk_ratio"],
-                                             sla.get("linear_mix", 1.0), True, out_dtype=torch.int8,
-                                             pv_fp8=sla.get("pv_fp8", False), peer_out=peer_out)
-                oq, osc = ulysses.ulysses_sla_attention_q8_p2p(q, k, v, L_global, attn_peer, group, TOKEN_ALIGN)
-            else:
-                # int8 codes + scales cross the reverse all-to-all (half the bytes of bf16)
-                oq, osc = ulysses.ulysses_sla_attention_q8(q, k, v, L_global, attn_q8, group, TOKEN_ALIGN)
+            # int8 codes + scales cross the reverse all-to-all (half the bytes of bf16)
+            oq, osc = ulysses.ulysses_sla_attention_q8(q, k, v, L_global, attn_q8, group, TOKEN_ALIGN)
         else:
             o = ulysses.ulysses_sla_attention(q, k, v, L_global, attn, group, TOKEN_ALIGN)
             oq, osc = ops.quantize_blockwise(o.reshape(Lp, dim).contiguous(), 128, check_finite=False)

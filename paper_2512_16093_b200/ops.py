@@ -107,6 +107,22 @@ def w8a8_gemm_ex(a_q, a_s, bt_q, b_s, block: int = 128, bias=None, out_dtype=tor
     return out
 
 
+def w8a8_gemm_qkv_peers(a_q, a_s, bt_q, b_s, peers, heads: int, row0: int, L: int, block: int = 128, bias=None):
+    """Fused Ulysses forward exchange: the qkv projection of this rank's token
+    rows [row0, row0 + M) stored straight into the head owners' buffers
+    (``peers``: P device addresses of bf16 [3*H/P, L, 128] buffers, peer memory
+    on a multi-GPU box)."""
+    import ctypes
+    M, K = a_q.shape
+    N = bt_q.shape[0]
+    if bt_q.shape[1] != K:
+        raise ValueError(f"inner dims differ: {K} vs {bt_q.shape[1]}")
+    arr = (ctypes.c_void_p * len(peers))(*[int(p) for p in peers])
+    call("tb_w8a8_gemm_qkv_peers", ptr(a_q.contiguous()), ptr(a_s.contiguous()), ptr(bt_q.contiguous()),
+         ptr(b_s.contiguous()), ptr(None if bias is None else bias.float().contiguous()), M, N, K, block,
+         ctypes.cast(arr, ctypes.c_void_p), len(peers), heads, row0, L, stream_ptr())
+
+
 def w8a8_gemm_quant(a_q, a_s, bt_q, b_s, block: int = 128, bias=None, act: int = 0):
     """Fast-mode W8A8 (+ GELU when act=1) whose result is block-quantized for the
     next projection -> (codes int8 [M, N], scales [ceil(M/128), N/128]); equal to

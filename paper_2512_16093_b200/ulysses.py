@@ -192,21 +192,67 @@ def _p2p_buffers(per: int, H: int, d: int, group, device, block: int = 128):
     return _P2P[key]
 
 
+def attn_return_p2p(qh, kh, vh, L: int, attn_peer_fn, group=None, block: int = 128):
+    """Head-shard attention whose int8 epilogue stores every tile into the
+    token owner's symmetric-memory buffers, then the device barrier.  Returns
+    this rank's codes [L_p, H*d] and scales [ceil(L_p/128), H] (views of its
+    symmetric buffers, valid until the next call)."""
+    P, rank = dist.get_world_size(group), dist.get_rank(group)
+    hp, _, d = qh.shape
+    H = hp * P
+    per = shard_size(L, P, block)
+    codes, scales, hc, cp, sp = _p2p_buffers(per, H, d, group, qh.device, block)
+    attn_peer_fn(qh, kh, vh, dict(codes=cp, scales=sp, rows=per, head0=rank * hp, heads=H))
+    hc.barrier()                    # all peers' tile stores into this rank's buffers are done
+    lo, hi = token_bounds(L, P, rank, block)
+    return codes[:hi - lo], scales[:-(-(hi - lo) // block)]
+
+
+_QKV = {}
+
+
+def qkv_to_heads_p2p(a_q, a_s, w_bt, w_scales, L: int, heads: int, group=None, block: int = 128):
+    """Fused forward exchange: the qkv projection of this rank's (128-aligned)
+    token shard with its epilogue storing every tile into the head owner's
+    symmetric-memory buffer [3*hp, L, 128] (tb_w8a8_gemm_qkv_peers), then the
+    device barrier.  Returns this rank's head-major q, k, v [hp, L, 128]
+    (views of its buffer, valid until the next call)."""
+    import torch.distributed._symmetric_memory as symm_mem
+    from . import ops
+    P, rank = dist.get_world_size(group), dist.get_rank(group)
+    if heads % P:
+        raise ValueError(f"heads {heads} not divisible by world size {P}")
+    hp = heads // P
+    g = group if group is not None else dist.group.WORLD
+    dev = a_q.device
+    key = (L, heads, g.group_name, dev.index)
+    if key not in _QKV:
+        buf = symm_mem.empty((3 * hp, L, 128), dtype=torch.bfloat16, device=dev)
+        hdl = symm_mem.rendezvous(buf, g.group_name)
+        _QKV[key] = (buf, hdl, [int(x) for x in hdl.buffer_ptrs])
+    buf, hdl, ptrs = _QKV[key]
+    lo, hi = token_bounds(L, P, rank, block)
+    if hi - lo >= 256:
+        ops.w8a8_gemm_qkv_peers(a_q, a_s, w_bt, w_scales, ptrs, heads, lo, L, block)
+    elif hi > lo:
+        # shard below the 2-SM kernel's 256 rows: local planes, then copies
+        # into the owners' buffers through their symmetric-memory views
+        planes = ops.w8a8_gemm_ex(a_q, a_s, w_bt, w_scales, block, None, torch.bfloat16, plane=128)
+        for o in range(P):
+            view = hdl.get_buffer(o, (3 * hp, L, 128), torch.bfloat16)
+            for w in range(3):
+                view[w * hp:(w + 1) * hp, lo:hi] = planes[w * heads + o * hp:w * heads + (o + 1) * hp]
+    hdl.barrier()                   # every rank's q/k/v tiles are in place
+    return buf[:hp], buf[hp:2 * hp], buf[2 * hp:]
+
+
 def ulysses_sla_attention_q8_p2p(q_shard, k_shard, v_shard, L: int, attn_peer_fn, group=None, block: int = 128):
     """ulysses_sla_attention_q8 with the reverse exchange fused into the
     attention epilogue (peer-memory stores).  attn_peer_fn(qh, kh, vh,
     peer_out) runs the head-shard attention with ops.sla_attention(...,
-    out_dtype=torch.int8, peer_out=peer_out).  Returns this rank's codes
-    [L_p, H*d] and scales [ceil(L_p/128), H] (views of its symmetric buffers,
-    valid until the next call)."""
-    P, rank = dist.get_world_size(group), dist.get_rank(group)
-    Lp, H, d = q_shard.shape
-    if H % P:
-        raise ValueError(f"heads {H} not divisible by world size {P}")
-    per = shard_size(L, P, block)
-    codes, scales, hc, cp, sp = _p2p_buffers(per, H, d, group, q_shard.device, block)
+    out_dtype=torch.int8, peer_out=peer_out)."""
+    P = dist.get_world_size(group)
+    if q_shard.shape[1] % P:
+        raise ValueError(f"heads {q_shard.shape[1]} not divisible by world size {P}")
     qh, kh, vh = seq_to_heads_qkv(q_shard, k_shard, v_shard, L, group, block)
-    attn_peer_fn(qh, kh, vh, dict(codes=cp, scales=sp, rows=per, head0=rank * (H // P), heads=H))
-    hc.barrier()                    # all peers' tile stores into this rank's buffers are done
-    lo, hi = token_bounds(L, P, rank, block)
-    return codes[:hi - lo], scales[:-(-(hi - lo) // block)]
+    return attn_return_p2p(qh, kh, vh, L, attn_peer_fn, group, block)

@@ -74,15 +74,28 @@ def _p2p_world1(port, out_q):
             return o.sla_attention(qh, kh, vh, 128, 64, 0.1, 1.0, out_dtype=torch.int8, peer_out=peer_out)
         c, s = ulysses.ulysses_sla_attention_q8_p2p(shard[0], shard[1], shard[2], L, attn_peer)
         torch.cuda.synchronize()
-        out_q.put((bool(torch.equal(c, want_c)), bool(torch.equal(s, want_s)), ""))
+        ok = torch.equal(c, want_c) and torch.equal(s, want_s)
+        # the fused forward exchange through symmetric memory (qkv GEMM epilogue)
+        dim = H * d
+        g = torch.Generator(device="cuda").manual_seed(6)
+        x = torch.randn((L, dim), generator=g, device="cuda").to(torch.bfloat16)
+        wq, ws = o.quantize_blockwise(torch.randn((dim, 3 * dim), generator=g, device="cuda") / dim ** 0.5, 128)
+        bt = o.transpose_codes(wq)
+        aq, asc = o.quantize_blockwise(x, 128, check_finite=False)
+        planes = o.w8a8_gemm_ex(aq, asc, bt, ws, 128, None, torch.bfloat16, plane=128)
+        qh, kh, vh = ulysses.qkv_to_heads_p2p(aq, asc, bt, ws, L, H)
+        torch.cuda.synchronize()
+        ok_qkv = torch.equal(torch.cat([qh, kh, vh]), planes)
+        out_q.put((bool(ok), bool(ok_qkv), ""))
         dist.destroy_process_group()
     except Exception as e:                              # report instead of hanging the parent
         out_q.put((False, False, repr(e)))
 
 
 def test_symmetric_memory_path_world1():
-    """The real path (torch symmetric memory rendezvous, peer pointer table,
-    device barrier) at world size 1 on the one GPU: equals the plain output."""
+    """The real paths (torch symmetric memory rendezvous, peer pointer tables,
+    device barriers) at world size 1 on the one GPU: the attention return and
+    the qkv forward exchange equal the plain outputs."""
     import socket
     import torch.multiprocessing as mp
     if not torch.cuda.is_available():
@@ -94,6 +107,35 @@ def test_symmetric_memory_path_world1():
     qq = ctx.Queue()
     p = ctx.Process(target=_p2p_world1, args=(port, qq))
     p.start()
-    ok_c, ok_s, err = qq.get(timeout=240)
+    ok_attn, ok_qkv, err = qq.get(timeout=240)
     p.join(timeout=60)
-    assert ok_c and ok_s, err
+    assert ok_attn and ok_qkv, (ok_attn, ok_qkv, err)
+
+
+@pytest.mark.parametrize("P,L", [(2, 1000), (4, 2400)])
+def test_qkv_peer_epilogue_matches_planar_gemm(ops, P, L):
+    """tb_w8a8_gemm_qkv_peers: every emulated rank's qkv projection of its
+    128-aligned token rows, stored into the head owners' [3*hp, L, 128]
+    buffers, reassembles the unsharded head-major planes bit-for-bit."""
+    H, d = 4, 128
+    dim = H * d
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.randn((L, dim), generator=g, device="cuda").to(torch.bfloat16)
+    w = torch.randn((dim, 3 * dim), generator=g, device="cuda") / dim ** 0.5
+    wq, ws = ops.quantize_blockwise(w, 128)
+    bt = ops.transpose_codes(wq)
+    aq, asc = ops.quantize_blockwise(x, 128, check_finite=False)
+    planes = ops.w8a8_gemm_ex(aq, asc, bt, ws, 128, None, torch.bfloat16, plane=128)     # [3H, L, 128]
+    hp = H // P
+    bufs = [torch.full((3 * hp, L, 128), float("nan"), dtype=torch.bfloat16, device="cuda") for _ in range(P)]
+    ptrs = [b.data_ptr() for b in bufs]
+    for rank in range(P):
+        lo, hi = ulysses.token_bounds(L, P, rank, 128)
+        assert hi - lo >= 256
+        ops.w8a8_gemm_qkv_peers(aq[lo:hi].contiguous(), asc[lo // 128:-(-hi // 128)].contiguous(), bt, ws, ptrs,
+                                H, lo, L)
+    torch.cuda.synchronize()
+    for o in range(P):
+        for wi in range(3):
+            want = planes[wi * H + o * hp:wi * H + (o + 1) * hp]
+            assert torch.equal(bufs[o][wi * hp:(wi + 1) * hp], want), (o, wi)
