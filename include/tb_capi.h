@@ -188,6 +188,23 @@ typedef struct tb_sla_args {
  * kernel with the same semantics. */
 int tb_sla_attention(const tb_sla_args *a, void *stream);
 
+/* ---------------------------------------------- NVLink peer memory
+ * (new, multi-GPU: the fused Ulysses exchanges store into peers' buffers).
+ * tb_peer_alloc: a dedicated cudaMalloc (zeroed) that CUDA IPC can export;
+ * tb_peer_export writes its 64-byte cudaIpcMemHandle_t, tb_peer_import maps
+ * a peer's handle into this process (cudaIpcMemLazyEnablePeerAccess).
+ * tb_peer_barrier: stream-ordered device barrier of a group of P ranks over
+ * per-rank flag blocks (P uint32 each, in peer memory; flags = DEVICE array
+ * of the P block pointers): barrier number `epoch` (monotonic, starting at
+ * 1) makes every peer's stores issued before its barrier visible to the
+ * work after this rank's. */
+int tb_peer_alloc(int64_t bytes, void **ptr);
+int tb_peer_free(void *ptr);
+int tb_peer_export(void *ptr, void *handle);
+int tb_peer_import(const void *handle, void **ptr);
+int tb_peer_close(void *ptr);
+int tb_peer_barrier(uint32_t *const *flags, int64_t P, int64_t rank, uint32_t epoch, void *stream);
+
 /* FP8 V for the opt-in FP8 P/V path (no reference function; SURVEY.md §8
  * a17).  Per head h: scale[h] = f32(absmax(v[h])) / 448 (RN), codes =
  * e4m3 round-to-nearest-even, satfinite, of v / safe (IEEE divide; safe = 1

@@ -47,6 +47,12 @@ SIGNATURES = {
     "tb_sla_attention": [_P, _P],
     "tb_transpose_v": [_P, _i, _I, _I, _I, _I, _P, _P],
     "tb_quant_v_fp8": [_P, _i, _I, _I, _I, _P, _P, _P, _P],
+    "tb_peer_alloc": [_I, _P],
+    "tb_peer_free": [_P],
+    "tb_peer_export": [_P, _P],
+    "tb_peer_import": [_P, _P],
+    "tb_peer_close": [_P],
+    "tb_peer_barrier": [_P, _I, _I, ctypes.c_uint32, _P],
     "tb_feature_map": [_P, _i, _I, _I, _I, _I, _P, _i, _P],
     "tb_linear_operands": [_P, _P, _P, _i, _I, _I, _I, _I, _I, _I, _P, _P, _P, _i, _P, _I, _P],
     "tb_gemm_bf16_batched": [_P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _i, _P],

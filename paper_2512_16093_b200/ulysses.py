@@ -163,47 +163,119 @@ def ulysses_sla_attention_q8(q_shard, k_shard, v_shard, L: int, attn_q8_fn, grou
     return heads_to_seq_q8(codes, scales, L, group, block)
 
 
-# ------------------------------------------------- fused return path (P2P)
-# The head-shard attention's epilogue stores each 128-token tile's int8 codes
-# and block scale straight into the token owner's buffers over NVLink (torch
-# symmetric memory gives every rank the peers' buffer addresses), so the
-# reverse exchange is part of the attention kernel: no send buffer, no
-# all-to-all launch, and the transfer overlaps the attention tile by tile.
-# A device-side barrier then makes every peer's stores visible before the
-# out-projection reads them.  Reuse of the buffers by the next layer is
-# ordered by that layer's forward all-to-all (a rank cannot start writing
-# into a peer before the peer has joined it, which it does only after its
-# out-projection in stream order).
+# ------------------------------------------------- fused exchanges (P2P)
+# Both exchanges can ride NVLink inside their producers: the qkv projection's
+# epilogue stores every tile into the HEAD owner's buffer, and the attention's
+# int8 epilogue stores every tile into the TOKEN owner's buffer, so a DiT layer
+# needs no send buffers, no all-to-all launches and no unpack copies, and the
+# transfers overlap the producing kernels tile by tile.  The buffers are
+# dedicated allocations mapped into every rank's process with CUDA IPC
+# (csrc/peer.cu; valid for one process per GPU over NVLink, and for several
+# processes sharing a GPU, which is how the multi-rank path is tested here), and
+# a stream-ordered device barrier over flag blocks in the same memory makes the
+# peers' stores visible before the consumer runs.  Buffer reuse across layers is
+# ordered by those barriers.
+
+
+def _tensor_at(addr: int, shape, dtype, device) -> torch.Tensor:
+    """Zero-copy torch view of device memory at `addr` (own or peer-mapped)."""
+    elt = {torch.int8: ("|i1", 1), torch.uint8: ("|u1", 1), torch.float32: ("<f4", 4),
+           torch.bfloat16: ("<i2", 2), torch.int32: ("<i4", 4)}[dtype]
+
+    class _CAI:
+        __cuda_array_interface__ = {"shape": tuple(shape), "typestr": elt[0], "data": (int(addr), False),
+                                    "version": 3, "strides": None}
+    t = torch.as_tensor(_CAI(), device=device)
+    return t.view(torch.bfloat16) if dtype == torch.bfloat16 else t
+
+
+class PeerGroup:
+    """Per-process-group peer memory: allocations every rank can store into,
+    and the group's device barrier."""
+
+    def __init__(self, group=None):
+        import ctypes
+        from . import _lib
+        self.ctypes, self.lib = ctypes, _lib.load(require_device=True)
+        self.group = group
+        self.P, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        self.epoch = 0
+        flags = self.alloc(4 * self.P)
+        self.flag_table = torch.tensor(flags, dtype=torch.int64, device=self.device)
+
+    def alloc(self, nbytes: int) -> list[int]:
+        """A zeroed allocation of nbytes on every rank -> the P addresses, as
+        seen from this process (own pointer at index rank)."""
+        c = self.ctypes
+        p = c.c_void_p()
+        _check(self.lib.tb_peer_alloc(nbytes, c.byref(p)), "tb_peer_alloc")
+        h = c.create_string_buffer(64)
+        _check(self.lib.tb_peer_export(p, h), "tb_peer_export")
+        handles = [None] * self.P
+        dist.all_gather_object(handles, bytes(h.raw), group=self.group)
+        ptrs = []
+        for r, hr in enumerate(handles):
+            if r == self.rank:
+                ptrs.append(int(p.value))
+            else:
+                q = c.c_void_p()
+                _check(self.lib.tb_peer_import(c.create_string_buffer(hr, 64), c.byref(q)), "tb_peer_import")
+                ptrs.append(int(q.value))
+        return ptrs
+
+    def barrier(self):
+        from .ops import stream_ptr
+        self.epoch += 1
+        _check(self.lib.tb_peer_barrier(self.ctypes.c_void_p(self.flag_table.data_ptr()), self.P, self.rank,
+                                        self.epoch, stream_ptr()), "tb_peer_barrier")
+
+
+def _check(rc: int, what: str):
+    from . import _lib
+    _lib.check(rc, what)
+
+
+_GROUPS = {}
+
+
+def peer_group(group=None) -> PeerGroup:
+    g = group if group is not None else dist.group.WORLD
+    key = (g.group_name, torch.cuda.current_device())
+    if key not in _GROUPS:
+        _GROUPS[key] = PeerGroup(group)
+    return _GROUPS[key]
+
+
 _P2P = {}
 
 
 def _p2p_buffers(per: int, H: int, d: int, group, device, block: int = 128):
-    import torch.distributed._symmetric_memory as symm_mem
-    g = group if group is not None else dist.group.WORLD
-    key = (per, H, d, g.group_name, device.index)
+    pg = peer_group(group)
+    key = (per, H, d, id(pg))
     if key not in _P2P:
-        codes = symm_mem.empty((per, H * d), dtype=torch.int8, device=device)
-        scales = symm_mem.empty((per // block, H), dtype=torch.float32, device=device)
-        hc = symm_mem.rendezvous(codes, g.group_name)
-        hs = symm_mem.rendezvous(scales, g.group_name)
-        cp = torch.tensor([int(x) for x in hc.buffer_ptrs], dtype=torch.int64, device=device)
-        sp = torch.tensor([int(x) for x in hs.buffer_ptrs], dtype=torch.int64, device=device)
-        _P2P[key] = (codes, scales, hc, cp, sp)
+        cptrs = pg.alloc(per * H * d)
+        sptrs = pg.alloc(4 * (per // block) * H)
+        codes = _tensor_at(cptrs[pg.rank], (per, H * d), torch.int8, device)
+        scales = _tensor_at(sptrs[pg.rank], (per // block, H), torch.float32, device)
+        cp = torch.tensor(cptrs, dtype=torch.int64, device=device)
+        sp = torch.tensor(sptrs, dtype=torch.int64, device=device)
+        _P2P[key] = (codes, scales, pg, cp, sp)
     return _P2P[key]
 
 
 def attn_return_p2p(qh, kh, vh, L: int, attn_peer_fn, group=None, block: int = 128):
     """Head-shard attention whose int8 epilogue stores every tile into the
-    token owner's symmetric-memory buffers, then the device barrier.  Returns
+    token owner's peer buffers, then the device barrier.  Returns
     this rank's codes [L_p, H*d] and scales [ceil(L_p/128), H] (views of its
-    symmetric buffers, valid until the next call)."""
+    peer buffers, valid until the next call)."""
     P, rank = dist.get_world_size(group), dist.get_rank(group)
     hp, _, d = qh.shape
     H = hp * P
     per = shard_size(L, P, block)
-    codes, scales, hc, cp, sp = _p2p_buffers(per, H, d, group, qh.device, block)
+    codes, scales, pg, cp, sp = _p2p_buffers(per, H, d, group, qh.device, block)
     attn_peer_fn(qh, kh, vh, dict(codes=cp, scales=sp, rows=per, head0=rank * hp, heads=H))
-    hc.barrier()                    # all peers' tile stores into this rank's buffers are done
+    pg.barrier()                    # all peers' tile stores into this rank's buffers are done
     lo, hi = token_bounds(L, P, rank, block)
     return codes[:hi - lo], scales[:-(-(hi - lo) // block)]
 
@@ -214,35 +286,33 @@ _QKV = {}
 def qkv_to_heads_p2p(a_q, a_s, w_bt, w_scales, L: int, heads: int, group=None, block: int = 128):
     """Fused forward exchange: the qkv projection of this rank's (128-aligned)
     token shard with its epilogue storing every tile into the head owner's
-    symmetric-memory buffer [3*hp, L, 128] (tb_w8a8_gemm_qkv_peers), then the
-    device barrier.  Returns this rank's head-major q, k, v [hp, L, 128]
-    (views of its buffer, valid until the next call)."""
-    import torch.distributed._symmetric_memory as symm_mem
+    peer buffer [3*hp, L, 128] (tb_w8a8_gemm_qkv_peers), then the device
+    barrier.  Returns this rank's head-major q, k, v [hp, L, 128] (views of
+    its buffer, valid until the next call)."""
     from . import ops
     P, rank = dist.get_world_size(group), dist.get_rank(group)
     if heads % P:
         raise ValueError(f"heads {heads} not divisible by world size {P}")
     hp = heads // P
-    g = group if group is not None else dist.group.WORLD
+    pg = peer_group(group)
     dev = a_q.device
-    key = (L, heads, g.group_name, dev.index)
+    key = (L, heads, id(pg))
     if key not in _QKV:
-        buf = symm_mem.empty((3 * hp, L, 128), dtype=torch.bfloat16, device=dev)
-        hdl = symm_mem.rendezvous(buf, g.group_name)
-        _QKV[key] = (buf, hdl, [int(x) for x in hdl.buffer_ptrs])
-    buf, hdl, ptrs = _QKV[key]
+        ptrs = pg.alloc(3 * hp * L * 128 * 2)
+        _QKV[key] = (_tensor_at(ptrs[pg.rank], (3 * hp, L, 128), torch.bfloat16, dev), ptrs)
+    buf, ptrs = _QKV[key]
     lo, hi = token_bounds(L, P, rank, block)
     if hi - lo >= 256:
         ops.w8a8_gemm_qkv_peers(a_q, a_s, w_bt, w_scales, ptrs, heads, lo, L, block)
     elif hi > lo:
         # shard below the 2-SM kernel's 256 rows: local planes, then copies
-        # into the owners' buffers through their symmetric-memory views
+        # into the owners' buffers through their peer-mapped views
         planes = ops.w8a8_gemm_ex(a_q, a_s, w_bt, w_scales, block, None, torch.bfloat16, plane=128)
         for o in range(P):
-            view = hdl.get_buffer(o, (3 * hp, L, 128), torch.bfloat16)
+            view = _tensor_at(ptrs[o], (3 * hp, L, 128), torch.bfloat16, dev)
             for w in range(3):
                 view[w * hp:(w + 1) * hp, lo:hi] = planes[w * heads + o * hp:w * heads + (o + 1) * hp]
-    hdl.barrier()                   # every rank's q/k/v tiles are in place
+    pg.barrier()                    # every rank's q/k/v tiles are in place
     return buf[:hp], buf[hp:2 * hp], buf[2 * hp:]
 
 

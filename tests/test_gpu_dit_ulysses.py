@@ -49,26 +49,36 @@ def _block(world, rank):
     return (xo if pend is None else xo + pend).cpu(), lo, hi
 
 
-def _worker(rank, world, port, ref_path, out_q):
+def _worker(rank, world, port, ref_path, out_q, p2p=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    dist.all_to_all_single = _staged_all_to_all
-    torch.cuda.set_device(0)
-    out, lo, hi = _block(world, rank)
-    ref = torch.load(ref_path)
-    out_q.put((rank, torch.equal(out, ref[lo:hi]), (out - ref[lo:hi]).abs().max().item()))
-    dist.destroy_process_group()
+    if p2p:
+        os.environ["TB_ULYSSES_P2P"] = "1"
+    try:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        dist.all_to_all_single = _staged_all_to_all
+        torch.cuda.set_device(0)
+        out, lo, hi = _block(world, rank)
+        ref = torch.load(ref_path)
+        out_q.put((rank, torch.equal(out, ref[lo:hi]), (out - ref[lo:hi]).abs().max().item()))
+        dist.destroy_process_group()
+    except Exception as e:                      # report instead of leaving the parent waiting
+        out_q.put((rank, False, repr(e)))
 
 
 @pytest.mark.gpu
-def test_dit_block_two_ranks_equals_one_rank(tmp_path):
+@pytest.mark.parametrize("p2p", [False, True], ids=["nccl-path", "p2p"])
+def test_dit_block_two_ranks_equals_one_rank(tmp_path, p2p):
+    """p2p: both exchanges fused into their producers over peer memory
+    (TB_ULYSSES_P2P=1) -- two processes on the one GPU, so the IPC handle
+    exchange, the cross-process peer stores and the device barriers are the
+    real multi-rank ones."""
     ref, _, _ = _block(1, 0)
     ref_path = str(tmp_path / "ref.pt")
     torch.save(ref, ref_path)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, ref_path, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, ref_path, q, p2p), daemon=True) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(2)]

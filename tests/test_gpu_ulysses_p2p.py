@@ -92,10 +92,10 @@ def _p2p_world1(port, out_q):
         out_q.put((False, False, repr(e)))
 
 
-def test_symmetric_memory_path_world1():
-    """The real paths (torch symmetric memory rendezvous, peer pointer tables,
-    device barriers) at world size 1 on the one GPU: the attention return and
-    the qkv forward exchange equal the plain outputs."""
+def test_peer_memory_path_world1():
+    """The real paths (IPC peer allocations, pointer tables, device barriers)
+    at world size 1 on the one GPU: the attention return and the qkv forward
+    exchange equal the plain outputs."""
     import socket
     import torch.multiprocessing as mp
     if not torch.cuda.is_available():
