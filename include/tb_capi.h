@@ -169,7 +169,7 @@ typedef struct tb_sla_args {
     /* Fused Ulysses return path (out_dtype TB_I8 only):
      * when out_peers != NULL the epilogue stores each 128-token tile's int8
      * codes and block scale straight into the buffers of the rank that owns
-     * those tokens (NVLink peer memory, e.g. torch symmetric memory), instead
+     * those tokens (NVLink peer memory from tb_peer_alloc / tb_peer_import), instead
      * of a local buffer followed by an all-to-all.  out_peers / scale_peers
      * are DEVICE arrays of P pointers; owner = row / peer_rows (peer_rows %
      * 128 == 0); codes land at out_peers[owner] + (row - owner*peer_rows) *
@@ -291,7 +291,7 @@ int tb_w8a8_gemm_quant(const int8_t *a, const float *sa, const int8_t *bt, const
  * 161-170): fast-mode W8A8 of this rank's token shard (sequence rows [row0,
  * row0 + M)) whose epilogue TMA-stores every output box straight into the
  * head owner's buffer.  peers: HOST array of P (<= 8) device pointers (peer
- * memory, e.g. torch symmetric memory), each bf16 [3*(H/P), L, 128] = the q,
+ * memory from tb_peer_alloc / tb_peer_import), each bf16 [3*(H/P), L, 128] = the q,
  * k, v planes of that rank's heads over all L tokens.  N = 3*H*128; 2-SM
  * kernel shapes only (block 128, M >= 256), TB_EUNSUPPORTED otherwise. */
 int tb_w8a8_gemm_qkv_peers(const int8_t *a, const float *sa, const int8_t *bt, const float *sb, const float *bias,
