@@ -455,3 +455,30 @@ def test_quant_v_fp8_rejects_misaligned(tb):
     v = torch.zeros((1, 129, 8), dtype=torch.bfloat16, device="cuda")
     with pytest.raises(ValueError):
         tb.quant_v_fp8(v.view(-1)[1:1 + 128 * 8].view(1, 128, 8))     # 2-B offset: not 16-B aligned
+
+
+@pytest.mark.parametrize("tb_,smooth,s", [(64, True, 1000), (64, False, 512), (128, True, 700)])
+def test_quantized_attention_drop_in_matches_oracle(tb, tb_, smooth, s):
+    """attention.quantized_attention (a10: dense INT8 Sage attention, every kv
+    block selected, no linear branch) against the oracle's restatement of
+    attention.py:230-253."""
+    from paper_2512_16093_b200.attention import AttnInputs, QuantAttnConfig, quantized_attention
+    q, k, v = gen.gaussian_qkv(51, 2, s, 64, bf16=False)
+    got = quantized_attention(AttnInputs(q, k, v), QuantAttnConfig(tb_, smooth))
+    want = O.quantized_attention(q, k, v, tb_, smooth)
+    cos, _, rel1 = metrics(got, want)
+    assert cos >= COS_MIN and rel1 <= REL_L1_MAX, (cos, rel1)
+
+
+@pytest.mark.parametrize("d,qb", [(128, 128), (64, 64)])
+def test_sla_topk_one_is_mix_independent_bit_exact(tb, d, qb):
+    """topk_ratio 1.0 leaves the complement empty: the output must not depend
+    on linear_mix at all, bit for bit (test_attention.py:278-284), on the
+    tensor-core (d 128, q_block 128) and CUDA-core paths."""
+    q, k, v = gen.gaussian_qkv(52, 2, 640, d, bf16=True)
+    dq, dk, dv = dev(q, True), dev(k, True), dev(v, True)
+    outs = [tb.sla_attention(dq, dk, dv, qb, 64, 1.0, mix).cpu() for mix in (1.0, 0.0, 3.5)]
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+    want = O.sla_attention(q, k, v, qb, 64, 1.0, 1.0)
+    cos, _, rel1 = metrics(outs[0].numpy(), want)
+    assert cos >= COS_MIN and rel1 <= REL_L1_MAX, (cos, rel1)
