@@ -224,7 +224,7 @@ def dit_ops_per_layer(L=L_, dim=DIT_DIM, ffn=DIT_FFN, heads=H_):
     return 2 * L * (dim * 3 * dim + dim * dim + 2 * dim * ffn) + sparse_ops(H=heads, L=L)
 
 
-def bench_dit(world, rank, num_layers):
+def bench_dit(world, rank, num_layers, pv_fp8=False):
     """cfg5 latency: one full rCM sample (4 steps x num_layers layers), seq-parallel
     linears + Ulysses attention across ranks; max over ranks of CUDA-event time."""
     import torch
@@ -237,7 +237,7 @@ def bench_dit(world, rank, num_layers):
     x_init = torch.randn((hi - lo, DIT_DIM), generator=g, device="cuda")
     noises = [torch.randn((hi - lo, DIT_DIM), generator=g, device="cuda") for _ in range(DIT_STEPS - 1)]
     sig = [80.0 * (0.5 / 80.0) ** (i / (DIT_STEPS - 1)) for i in range(DIT_STEPS)] + [0.0]   # make_schedule(4)
-    sla = dict(q_block=QB, kv_block=KVB, topk_ratio=RATIO, linear_mix=1.0)
+    sla = dict(q_block=QB, kv_block=KVB, topk_ratio=RATIO, linear_mix=1.0, pv_fp8=pv_fp8)
     dit.block_forward(x_init, sig[0], layers[0], H_, sla, L_)          # warm-up (one block)
     torch.cuda.synchronize()
     if world > 1:
@@ -275,6 +275,7 @@ def main():
     ap.add_argument("--no-fp8", action="store_true", help="skip the opt-in FP8 P/V measurement")
     ap.add_argument("--no-graph", action="store_true", help="eager launches in the timed region")
     ap.add_argument("--dit-layers", type=int, default=40)
+    ap.add_argument("--dit-pv-fp8", action="store_true", help="DiT attention with the opt-in FP8 P/V (not the default)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -501,7 +502,9 @@ def main():
     if not args.no_dit:
         del shard
         head_major = None if world > 1 else head_major
-        dit_res = bench_dit(world, rank, args.dit_layers)
+        dit_res = bench_dit(world, rank, args.dit_layers, args.dit_pv_fp8)
+        if args.dit_pv_fp8:
+            dit_res["workload"] += " (opt-in FP8 P/V)"
 
     # ---- opt-in FP8 P/V: the same step and the fused kernel
     # alone with e4m3 P and V (kind::f8f6f4 PV), after the DiT sample so the
