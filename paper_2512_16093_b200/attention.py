@@ -291,7 +291,7 @@ def quantized_attention(inputs: AttnInputs, cfg: QuantAttnConfig | None = None):
     cfg = cfg or QuantAttnConfig()
     q, k, v = _dev(inputs.q), _dev(inputs.k), _dev(inputs.v)
     h, s, d = q.shape
-    tb = cfg.token_block
+    tb = min(cfg.token_block, s)        # a block longer than the sequence is one block of s tokens
     nb = -(-s // tb)
     qc, qs, _ = ops.pool_quant_tokens(q, tb, None, pool=False)
     km = ops.kmean(k) if cfg.smooth_k else torch.zeros((h, d), device=q.device)

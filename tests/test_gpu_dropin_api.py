@@ -1,0 +1,230 @@
+"""The drop-in modules (paper_2512_16093_b200.attention / .blockquant) against
+the behaviours the reference's own suites pin (pkg/tests/test_attention.py,
+test_blockquant.py; restated here, numpy in -> numpy out, on the GPU path):
+exactness properties, known answers, tie rules, error texts and the pinned
+fidelity thresholds."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def A():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2512_16093_b200 import _lib, attention
+    _lib.load(require_device=True)
+    return attention
+
+
+@pytest.fixture(scope="module")
+def B():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2512_16093_b200 import blockquant
+    return blockquant
+
+
+def gauss(A, seed, h, s, d):
+    rng = np.random.default_rng(seed)
+    return A.AttnInputs(*(rng.standard_normal((h, s, d), dtype=np.float32) for _ in range(3)))
+
+
+def f64_attention(x):
+    q, k, v = (t.astype(np.float64) for t in (x.q, x.k, x.v))
+    lg = x.scale * q @ k.transpose(0, 2, 1)
+    p = np.exp(lg - lg.max(-1, keepdims=True))
+    return (p / p.sum(-1, keepdims=True)) @ v
+
+
+# ------------------------------------------------------------ dense / smoothing
+
+def test_reference_attention_properties(A):
+    x = gauss(A, 0, 2, 1, 8)
+    assert np.array_equal(A.reference_attention(x), x.v)                  # one key: output = v
+    x = gauss(A, 3, 2, 128, 32)
+    assert A.error_metrics(A.reference_attention(x), f64_attention(x).astype(np.float32))[1] <= 1e-6
+    _, p = A.reference_attention(gauss(A, 5, 3, 64, 16), return_probs=True)
+    assert np.abs(p.sum(-1) - 1).max() <= 1e-6
+    rng = np.random.default_rng(1)
+    k = np.repeat(rng.standard_normal((2, 1, 8)).astype(np.float32), 16, axis=1)
+    q, v = (rng.standard_normal((2, 16, 8)).astype(np.float32) for _ in range(2))
+    out = A.reference_attention(A.AttnInputs(q, k, v))                     # equal keys: column mean
+    assert np.allclose(out, np.broadcast_to(v.mean(1, keepdims=True), out.shape), atol=1e-6)
+
+
+def test_smooth_keys_properties(A):
+    kc, km = A.smooth_keys(np.full((2, 16, 4), 3.25, np.float32))
+    assert np.array_equal(kc, np.zeros((2, 16, 4), np.float32)) and np.allclose(km, 3.25)
+    rng = np.random.default_rng(4)
+    q = rng.standard_normal((2, 48, 16)).astype(np.float32)
+    k = rng.standard_normal((2, 48, 16)).astype(np.float32) + 0.7
+    kc, km = A.smooth_keys(k)
+    rebuilt = q @ kc.transpose(0, 2, 1) + q @ km[:, :, None]
+    assert A.error_metrics(rebuilt, q @ k.transpose(0, 2, 1))[1] <= 1e-5
+
+
+# ----------------------------------------------------------- quantized attention
+
+def test_quantized_attention_properties(A):
+    x = gauss(A, 6, 4, 1, 16)
+    assert np.array_equal(A.quantized_attention(x), x.v)
+    rng = np.random.default_rng(7)
+    k, v = (rng.standard_normal((2, 32, 8)).astype(np.float32) for _ in range(2))
+    out = A.quantized_attention(A.AttnInputs(np.zeros((2, 32, 8), np.float32), k, v))
+    assert np.allclose(out, np.broadcast_to(v.mean(1, keepdims=True), out.shape), atol=1e-6)
+
+
+def test_quantized_attention_fidelity(A):
+    worst_cos, worst_rel = 1.0, 0.0
+    for seed in range(5, 15):
+        x = gauss(A, seed, 4, 256, 64)
+        cos, rel = A.error_metrics(A.quantized_attention(x), A.reference_attention(x))
+        worst_cos, worst_rel = min(worst_cos, cos), max(worst_rel, rel)
+    assert worst_cos >= 0.999 and worst_rel <= 5e-2
+    x = gauss(A, 5, 4, 256, 64)
+    assert A.error_metrics(A.quantized_attention(x, A.QuantAttnConfig(smooth_k=False)),
+                           A.reference_attention(x))[0] >= 0.99
+
+
+# -------------------------------------------------------------- pooling / top-k
+
+def test_pool_block_means_known_answers(A):
+    x = np.random.default_rng(8).standard_normal((2, 10, 4)).astype(np.float32)
+    p = A.pool_block_means(x, 10)
+    assert p.shape == (2, 1, 4) and np.allclose(p[:, 0], x.mean(1), atol=1e-6)
+    x = np.random.default_rng(9).standard_normal((2, 7, 3)).astype(np.float32)
+    assert np.array_equal(A.pool_block_means(x, 1), x)
+    x = np.arange(5, dtype=np.float32).reshape(1, 5, 1)                   # blocks of 2, 2, 1
+    assert np.array_equal(A.pool_block_means(x, 2), np.array([[[0.5], [2.5], [4.0]]], np.float32))
+
+
+def test_select_topk_known_answers(A):
+    rng = np.random.default_rng(10)
+    m = A.select_topk_blocks(rng.standard_normal((2, 3, 4)).astype(np.float32),
+                             rng.standard_normal((2, 5, 4)).astype(np.float32), A.SLAConfig(topk_ratio=1.0))
+    assert np.array_equal(m.indices, np.broadcast_to(np.arange(5), (2, 3, 5)))
+    scores = np.array([[[3, 1, 2, 0], [0, 0, 1, 5]]], np.float32)         # identity kp: scores = qp
+    m = A.select_topk_blocks(scores, np.eye(4, dtype=np.float32)[None], A.SLAConfig(topk_ratio=0.5))
+    assert m.indices[0].tolist() == [[0, 2], [2, 3]]
+    m = A.select_topk_blocks(np.zeros((1, 1, 4), np.float32), np.ones((1, 8, 4), np.float32),
+                             A.SLAConfig(topk_ratio=0.25))
+    assert m.indices[0, 0].tolist() == [0, 1]                             # ties -> lower index
+
+
+def test_select_topk_power_of_two_scale_invariance_and_complement(A):
+    rng = np.random.default_rng(11)
+    qp = rng.standard_normal((2, 6, 8)).astype(np.float32)
+    kp = rng.standard_normal((2, 9, 8)).astype(np.float32)
+    cfg = A.SLAConfig(topk_ratio=0.34)
+    base = A.select_topk_blocks(qp, kp, cfg).indices
+    for cq, ck in ((2.0, 1.0), (1.0, 0.25), (8.0, 4.0)):
+        assert np.array_equal(A.select_topk_blocks(np.float32(cq) * qp, np.float32(ck) * kp, cfg).indices, base)
+    m = A.select_topk_blocks(rng.standard_normal((2, 4, 8)).astype(np.float32),
+                             rng.standard_normal((2, 10, 8)).astype(np.float32), A.SLAConfig(topk_ratio=0.3))
+    c = m.complement()
+    assert c.count == 10 - m.count
+    both = np.sort(np.concatenate([m.indices, c.indices], -1), -1)
+    assert np.array_equal(both, np.broadcast_to(np.arange(10), both.shape))
+
+
+# --------------------------------------------------------------- linear branch
+
+def test_linear_attention_properties(A):
+    x = gauss(A, 13, 2, 32, 8)
+    empty = A.BlockMask(16, 16, 2, np.empty((2, 2, 0), np.int64))
+    num, den = A.linear_attention(x, empty)
+    assert not num.any() and not den.any()
+    x = gauss(A, 14, 3, 1, 8)
+    num, den = A.linear_attention(x)
+    assert np.allclose(num / den[..., None], x.v, atol=1e-6)
+    x = gauss(A, 15, 2, 128, 16)
+    _, den = A.linear_attention(x, A.BlockMask(32, 32, 4, np.full((2, 4, 1), 2, np.int64)))
+    assert den.min() > 0
+
+
+def test_linear_attention_masked_vs_f64(A):
+    x = gauss(A, 16, 2, 40, 8)                                             # last kv block partial (16+16+8)
+    mask = A.BlockMask(20, 16, 3, np.array([[[0, 2], [1, 2]], [[0, 1], [0, 2]]], np.int64))
+    num, den = A.linear_attention(x, mask)
+    phi = lambda t: np.where(t >= 0, t + 1.0, np.exp(np.minimum(t, 0.0)))
+    for h in range(2):
+        for n in range(2):
+            rows = slice(20 * n, min(20 * n + 20, 40))
+            pos = np.concatenate([np.arange(16 * b, min(16 * b + 16, 40)) for b in mask.indices[h, n]])
+            pk, pq = phi(x.k[h, pos].astype(np.float64)), phi(x.q[h, rows].astype(np.float64))
+            assert np.allclose(num[h, rows], pq @ (pk.T @ x.v[h, pos]), rtol=1e-5, atol=1e-5)
+            assert np.allclose(den[h, rows], pq @ pk.sum(0), rtol=1e-5, atol=1e-5)
+
+
+# ---------------------------------------------------------------- sla attention
+
+@pytest.mark.parametrize("h,s,d,mix", [(2, 128, 16, 1.0), (1, 96, 8, 0.0), (3, 64, 32, 2.5), (2, 100, 16, 1.0),
+                                       (2, 90, 8, 1.0)])
+def test_sla_full_selection_equals_dense(A, h, s, d, mix):
+    x = gauss(A, 20 + h + s, h, s, d)
+    cfg = A.SLAConfig(q_block=32, kv_block=32, topk_ratio=1.0, linear_mix=mix, quantized_sparse_branch=False)
+    assert A.error_metrics(A.sla_attention(x, cfg), A.reference_attention(x))[1] <= 1e-5
+
+
+def test_sla_full_selection_ignores_mix_and_rejects_big_blocks(A):
+    x = gauss(A, 21, 2, 64, 16)
+    outs = [A.sla_attention(x, A.SLAConfig(32, 32, 1.0, m, False)) for m in (0.0, 1.0, 123.0)]
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[1], outs[2])
+    with pytest.raises(ValueError):
+        A.sla_attention(gauss(A, 22, 1, 16, 8), A.SLAConfig(q_block=64, kv_block=64))
+    for bad in (dict(topk_ratio=0.0), dict(topk_ratio=1.5), dict(q_block=0), dict(linear_mix=-1.0)):
+        with pytest.raises(ValueError):
+            A.SLAConfig(**bad)
+
+
+def test_sla_fidelity_gaussian_and_block_coherent(A):
+    x = gauss(A, 9, 4, 512, 64)
+    assert A.error_metrics(A.sla_attention(x, A.SLAConfig(topk_ratio=0.1)), A.reference_attention(x))[0] >= 0.58
+    rng = np.random.default_rng(9)
+    h, s, d, blk = 4, 512, 64, 64
+    nb = s // blk
+    centres = (3.0 * rng.standard_normal((h, nb, d))).astype(np.float32)
+    k = np.repeat(centres, blk, axis=1) + 0.3 * rng.standard_normal((h, s, d)).astype(np.float32)
+    tgt = np.repeat(rng.integers(0, nb, (h, nb)), blk, axis=1)
+    q = centres[np.arange(h)[:, None], tgt] + 0.3 * rng.standard_normal((h, s, d)).astype(np.float32)
+    v = rng.standard_normal((h, s, d)).astype(np.float32)
+    x = A.AttnInputs(q, k, v)
+    ref = A.reference_attention(x)
+    assert A.error_metrics(A.sla_attention(x, A.SLAConfig(topk_ratio=0.1, quantized_sparse_branch=False)),
+                           ref)[0] >= 0.9999
+    assert A.error_metrics(A.sla_attention(x, A.SLAConfig(topk_ratio=0.1)), ref)[0] >= 0.99
+
+
+# -------------------------------------------------------- flop report / metrics
+
+def test_flop_report_and_instrumented_macs(A):
+    assert A.attention_flop_report(4096, 64, 1).to_dict() == {"dense_flops": 4 * 4096 * 4096 * 64}
+    r = A.attention_flop_report(4096, 64, 1, A.SLAConfig(topk_ratio=1.0))
+    assert r.sparse_softmax_flops == r.dense_flops
+    r = A.attention_flop_report(2560, 64, 1, A.SLAConfig(topk_ratio=0.1))
+    assert r.sparse_softmax_flops * 10 == r.dense_flops and r.dense_to_sparse_ratio == 10.0
+    cfg = A.SLAConfig(q_block=64, kv_block=64, topk_ratio=0.1)
+    r = A.attention_flop_report(640, 32, 2, cfg)
+    assert r.linear_branch_flops == 4 * 2 * 640 * 32 * 32
+    assert r.selection_overhead_flops == 2 * 2 * 10 * 10 * 32 and r.sparse_softmax_flops <= r.dense_flops
+    macs = A.instrumented_sparse_macs(gauss(A, 24, 2, 640, 32), cfg)
+    assert macs["total_macs"] * 10 == macs["dense_macs"] and 2 * macs["total_macs"] == r.sparse_softmax_flops
+
+
+def test_error_metrics_semantics(A):
+    a = np.random.default_rng(0).standard_normal((3, 4)).astype(np.float32)
+    assert A.error_metrics(a, a) == (1.0, 0.0)
+    a = np.random.default_rng(1).standard_normal(16).astype(np.float32)
+    cos, rel = A.error_metrics(-a, a)
+    assert abs(cos + 1) < 1e-7 and abs(rel - 2) < 1e-7
+    b = np.zeros(4, np.float32)
+    b[0] = 1.0
+    a = b.copy()
+    a[1] = 0.1
+    assert abs(A.error_metrics(a, b)[1] - 0.1) < 1e-7
+    for x, y in ((np.zeros(4, np.float32), np.ones(4, np.float32)), (np.ones(4, np.float32), np.zeros(4, np.float32))):
+        with pytest.raises(ValueError):
+            A.error_metrics(x, y)
