@@ -228,3 +228,133 @@ def test_error_metrics_semantics(A):
     for x, y in ((np.zeros(4, np.float32), np.ones(4, np.float32)), (np.ones(4, np.float32), np.zeros(4, np.float32))):
         with pytest.raises(ValueError):
             A.error_metrics(x, y)
+
+
+# ------------------------------------------------------------------ blockquant
+
+def _dequant_loop(bq):
+    out = np.empty((bq.rows, bq.cols), np.float32)
+    b = bq.block
+    for i in range(bq.scales.shape[0]):
+        for j in range(bq.scales.shape[1]):
+            out[i * b:(i + 1) * b, j * b:(j + 1) * b] = np.asarray(bq.q)[i * b:(i + 1) * b, j * b:(j + 1) * b] \
+                .astype(np.float32) * np.asarray(bq.scales)[i, j]
+    return out
+
+
+def test_blockquant_known_answers(B):
+    z = B.quantize_blockwise(np.zeros((128, 128), np.float32))
+    assert not np.asarray(z.q).any() and not np.asarray(z.scales).any()
+    assert not np.asarray(B.dequantize_blockwise(z)).any()
+    c = np.float32(0.731)
+    m = np.full((128, 128), 127 * c, np.float32)
+    bq = B.quantize_blockwise(m)                                          # constant block: a fixed point
+    assert (np.asarray(bq.q) == 127).all() and np.asarray(bq.scales).shape == (1, 1)
+    assert np.allclose(np.asarray(bq.scales)[0, 0], c, rtol=1e-6)
+    assert np.array_equal(np.asarray(B.dequantize_blockwise(bq)), m)
+    s = np.float32(0.01)
+    ext = B.BlockQuantized(rows=2, cols=2, block=128, q=np.array([[127, -127], [127, -127]], np.int8),
+                           scales=np.array([[s]], np.float32))
+    assert np.array_equal(np.asarray(B.dequantize_blockwise(ext)), np.array([[127 * s, -127 * s]] * 2, np.float32))
+
+
+def test_blockquant_roundtrip_bound_and_brute_force_dequant(B):
+    m = np.random.default_rng(7).standard_normal((256, 256), dtype=np.float32)
+    bq = B.quantize_blockwise(m)
+    err = np.abs(m - np.asarray(B.dequantize_blockwise(bq)))
+    assert (err <= B._expand_scales(np.asarray(bq.scales), 128, 256, 256) / 2 + np.spacing(np.abs(m))).all()
+    m = np.random.default_rng(8).standard_normal((300, 200), dtype=np.float32)     # edge blocks
+    bq = B.quantize_blockwise(m)
+    assert np.array_equal(np.asarray(B.dequantize_blockwise(bq)), _dequant_loop(bq))
+
+
+@pytest.mark.parametrize("seed", [0, 17, 4242, 9999])
+def test_blockquant_requantize_idempotent(B, seed):
+    rng = np.random.default_rng(seed)
+    m = (rng.standard_normal((64, 96)) * rng.uniform(1e-3, 1e3)).astype(np.float32)
+    cfg = B.BlockQuantConfig(block=32)
+    first = B.quantize_blockwise(m, cfg)
+    again = B.quantize_blockwise(np.asarray(B.dequantize_blockwise(first)), cfg)
+    assert np.array_equal(np.asarray(first.q), np.asarray(again.q))
+    assert np.array_equal(np.asarray(first.scales), np.asarray(again.scales))
+
+
+@pytest.mark.parametrize("c", [2.0, 0.5, 8.0, 0.0625])
+def test_blockquant_power_of_two_scaling(B, c):
+    m = np.random.default_rng(9).standard_normal((130, 70), dtype=np.float32)
+    base, scaled = B.quantize_blockwise(m), B.quantize_blockwise(np.float32(c) * m)
+    assert np.array_equal(np.asarray(scaled.q), np.asarray(base.q))
+    assert np.array_equal(np.asarray(scaled.scales), np.float32(c) * np.asarray(base.scales))
+
+
+def test_blockquant_rejects_non_finite_and_mismatches(B):
+    m = np.zeros((4, 4), np.float32)
+    m[1, 2] = np.inf
+    with pytest.raises(ValueError):
+        B.quantize_blockwise(m)
+    rng = np.random.default_rng(4)
+    a = B.quantize_blockwise(rng.standard_normal((8, 16), dtype=np.float32))
+    with pytest.raises(ValueError, match="inner dims"):
+        B.w8a8_matmul(a, B.quantize_blockwise(rng.standard_normal((8, 8), dtype=np.float32)))
+    with pytest.raises(ValueError, match="block"):
+        B.w8a8_matmul(a, B.quantize_blockwise(rng.standard_normal((16, 8), dtype=np.float32),
+                                              B.BlockQuantConfig(block=64)))
+    w = B.quantize_blockwise(rng.standard_normal((32, 16), dtype=np.float32))
+    with pytest.raises(ValueError):
+        B.quantized_linear_forward(np.zeros((4, 8), np.float32), w)
+
+
+def test_w8a8_known_answers(B):
+    rng = np.random.default_rng(1)
+    a = B.quantize_blockwise(rng.standard_normal((64, 64), dtype=np.float32))
+    assert not np.asarray(B.w8a8_matmul(a, B.quantize_blockwise(np.zeros((64, 32), np.float32)))).any()
+    a = B.quantize_blockwise(np.eye(128, dtype=np.float32))
+    b = B.quantize_blockwise(np.random.default_rng(2).standard_normal((128, 128), dtype=np.float32))
+    want = np.asarray(B.dequantize_blockwise(a)) @ np.asarray(B.dequantize_blockwise(b))
+    assert np.allclose(np.asarray(B.w8a8_matmul(a, b)), want, atol=1e-6)
+    rng = np.random.default_rng(11)
+    a, b = (B.quantize_blockwise(rng.standard_normal((256, 256), dtype=np.float32)) for _ in range(2))
+    assert np.abs(np.asarray(B.w8a8_matmul(a, b)) - _dequant_loop(a) @ _dequant_loop(b)).max() <= 1e-3
+
+
+def test_w8a8_equals_int64_segment_order(B):
+    rng = np.random.default_rng(3)
+    cfg = B.BlockQuantConfig(block=64)
+    a = B.quantize_blockwise(rng.standard_normal((96, 192), dtype=np.float32), cfg)
+    b = B.quantize_blockwise(rng.standard_normal((192, 80), dtype=np.float32), cfg)
+    aq, bqq, sa, sb = (np.asarray(t) for t in (a.q, b.q, a.scales, b.scales))
+    out = np.zeros((96, 80), np.float32)
+    for kb in range(sa.shape[1]):
+        lo, hi = 64 * kb, min(64 * kb + 64, 192)
+        seg = (aq[:, lo:hi].astype(np.int64) @ bqq[lo:hi].astype(np.int64)).astype(np.float32)
+        seg *= np.repeat(sa[:, kb], [64, 32])[:, None]
+        seg *= np.repeat(sb[kb], [64, 16])[None, :]
+        out += seg
+    assert np.array_equal(np.asarray(B.w8a8_matmul(a, b)), out)
+
+
+def test_quantized_linear_forward_semantics(B):
+    rng = np.random.default_rng(5)
+    w = B.quantize_blockwise(rng.standard_normal((32, 16), dtype=np.float32))
+    bias = rng.standard_normal(16, dtype=np.float32)
+    assert np.array_equal(np.asarray(B.quantized_linear_forward(np.zeros((4, 32), np.float32), w, bias)),
+                          np.tile(bias, (4, 1)))
+    rng = np.random.default_rng(6)
+    x = rng.standard_normal((8, 32), dtype=np.float32)
+    w = B.quantize_blockwise(rng.standard_normal((32, 16), dtype=np.float32))
+    assert np.array_equal(np.asarray(B.quantized_linear_forward(x, w)),
+                          np.asarray(B.w8a8_matmul(B.quantize_blockwise(x), w)))
+    rng = np.random.default_rng(13)
+    x = rng.standard_normal((128, 128), dtype=np.float32)
+    wf = rng.standard_normal((128, 128), dtype=np.float32)
+    got = np.asarray(B.quantized_linear_forward(x, B.quantize_blockwise(wf)))
+    assert np.linalg.norm(got - x @ wf) / np.linalg.norm(x @ wf) <= 0.02
+
+
+def test_compression_ratio_accounting(B):
+    bq = B.quantize_blockwise(np.random.default_rng(0).standard_normal((128, 128)).astype(np.float32))
+    assert B.compression_ratio(bq, 2.0) == (128 * 128 + 4) / (2 * 128 * 128)
+    assert abs(B.compression_ratio(bq, 4.0) - 0.25006) < 1e-4
+    assert B.compression_ratio(B.quantize_blockwise(np.ones((1, 1), np.float32)), 1.0) == 5.0
+    with pytest.raises(ValueError):
+        B.compression_ratio(bq, 0.0)
