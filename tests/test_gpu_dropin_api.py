@@ -358,3 +358,144 @@ def test_compression_ratio_accounting(B):
     assert B.compression_ratio(B.quantize_blockwise(np.ones((1, 1), np.float32)), 1.0) == 5.0
     with pytest.raises(ValueError):
         B.compression_ratio(bq, 0.0)
+
+
+# --------------------------------------------------------------------- sampler
+
+@pytest.fixture(scope="module")
+def S():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2512_16093_b200 import sampler
+    return sampler
+
+
+def test_norms_known_answers_and_f64(S, A):
+    assert np.array_equal(np.asarray(S.rmsnorm(np.zeros((3, 8), np.float32), np.ones(8, np.float32))),
+                          np.zeros((3, 8), np.float32))
+    x = np.ones((1, 16), np.float32)
+    assert np.abs(np.asarray(S.rmsnorm(x, np.ones(16, np.float32), eps=1e-12)) - x).max() <= 1e-6
+    rng = np.random.default_rng(0)
+    x, g = rng.standard_normal((64, 32)).astype(np.float32), rng.standard_normal(32).astype(np.float32)
+    x64 = x.astype(np.float64)
+    want = (x64 / np.sqrt((x64 ** 2).mean(-1, keepdims=True) + 1e-6) * g).astype(np.float32)
+    assert A.error_metrics(np.asarray(S.rmsnorm(x, g)), want)[1] <= 1e-6
+    gain, off = (np.random.default_rng(i).standard_normal(8).astype(np.float32) for i in (1, 2))
+    assert np.array_equal(np.asarray(S.layernorm(np.full((4, 8), 2.5, np.float32), gain, off)), np.tile(off, (4, 1)))
+    x = np.random.default_rng(3).standard_normal((32, 64)).astype(np.float32) * 5 + 3
+    out = np.asarray(S.layernorm(x, np.ones(64, np.float32), np.zeros(64, np.float32)))
+    assert np.abs(out.mean(-1)).max() <= 1e-5 and np.abs(out.var(-1) - 1).max() <= 1e-4
+    rng = np.random.default_rng(4)
+    x, g, o = (rng.standard_normal(sh).astype(np.float32) for sh in ((64, 32), 32, 32))
+    x64 = x.astype(np.float64)
+    mu = x64.mean(-1, keepdims=True)
+    want = ((x64 - mu) / np.sqrt(((x64 - mu) ** 2).mean(-1, keepdims=True) + 1e-6) * g + o).astype(np.float32)
+    assert A.error_metrics(np.asarray(S.layernorm(x, g, o)), want)[1] <= 1e-6
+    for fn, args in ((S.rmsnorm, ()), (S.layernorm, (np.zeros(4, np.float32),))):
+        with pytest.raises(ValueError):
+            fn(np.ones((2, 4), np.float32), np.ones(4, np.float32), *args, eps=0.0)
+
+
+def _gauss_weights(S, seed, d, mult=4):
+    rng = np.random.default_rng(seed)
+    mat = lambda r, c: rng.standard_normal((r, c), dtype=np.float32) / np.float32(np.sqrt(r))
+    return S.ToyBlockWeights(rms_gain=rng.standard_normal(d, dtype=np.float32) * 0.1 + 1,
+                             ln_gain=rng.standard_normal(d, dtype=np.float32) * 0.1 + 1,
+                             ln_offset=rng.standard_normal(d, dtype=np.float32) * 0.1,
+                             qkv=mat(d, 3 * d), out_proj=mat(d, d), mlp_in=mat(d, mult * d),
+                             mlp_out=mat(mult * d, d), sigma_emb=rng.standard_normal(d, dtype=np.float32) * 0.01)
+
+
+def test_toy_block_semantics(S, A):
+    d = 32
+    zero = S.ToyBlockWeights(**{n: np.zeros(sh, np.float32) for n, sh in (
+        ("rms_gain", d), ("ln_gain", d), ("ln_offset", d), ("qkv", (d, 3 * d)), ("out_proj", (d, d)),
+        ("mlp_in", (d, 4 * d)), ("mlp_out", (4 * d, d)), ("sigma_emb", d))})
+    x = np.random.default_rng(5).standard_normal((16, d)).astype(np.float32)
+    assert np.array_equal(np.asarray(S.toy_block_forward(x, 7.0, zero, heads=4)), x)      # zero weights: identity
+    with pytest.raises(ValueError):
+        S.toy_block_forward(np.zeros((4, 30), np.float32), 1.0, S.ToyBlockWeights(
+            **{n: np.zeros(sh, np.float32) for n, sh in (("rms_gain", 30), ("ln_gain", 30), ("ln_offset", 30),
+               ("qkv", (30, 90)), ("out_proj", (30, 30)), ("mlp_in", (30, 120)), ("mlp_out", (120, 30)),
+               ("sigma_emb", 30))}), heads=4)
+    w = _gauss_weights(S, 6, 128)
+    x = np.random.default_rng(7).standard_normal((256, 128)).astype(np.float32)
+    dense = np.asarray(S.toy_block_forward(x, 1.5, w, heads=4, attn_mode="dense"))
+    sla = np.asarray(S.toy_block_forward(x, 1.5, w, heads=4, attn_mode="sla",
+                                         sla_cfg=A.SLAConfig(64, 64, 1.0, 1.0, False)))
+    assert A.error_metrics(sla, dense)[1] <= 1e-5
+    from paper_2512_16093_b200.blockquant import quantize_blockwise
+    w = _gauss_weights(S, 13, 128)
+    wq = S.ToyBlockWeights(rms_gain=w.rms_gain, ln_gain=w.ln_gain, ln_offset=w.ln_offset,
+                           qkv=quantize_blockwise(w.qkv), out_proj=quantize_blockwise(w.out_proj),
+                           mlp_in=quantize_blockwise(w.mlp_in), mlp_out=quantize_blockwise(w.mlp_out),
+                           sigma_emb=w.sigma_emb)
+    x = np.random.default_rng(13).standard_normal((256, 128)).astype(np.float32)
+    dense = np.asarray(S.toy_block_forward(x, 2.0, w, heads=4, attn_mode="dense"))
+    quant = np.asarray(S.toy_block_forward(x, 2.0, wq, heads=4, attn_mode="quantized"))
+    assert A.error_metrics(quant, dense)[0] >= 0.97
+
+
+def test_schedule_semantics(S):
+    s1 = S.make_schedule(1, sigma_max=80.0, sigma_min=0.5)
+    assert np.array_equal(s1.sigmas, np.array([80.0, 0.0], np.float32)) and s1.num_steps == 1
+    s = S.make_schedule(3, sigma_max=80.0, sigma_min=0.5).sigmas.astype(np.float64)
+    assert s[0] == 80.0 and abs(s[2] - 0.5) < 1e-6 and s[3] == 0.0
+    assert abs(s[1] / s[0] - s[2] / s[1]) < 1e-6 and abs(s[1] - np.sqrt(40.0)) < 1e-4
+    for n, smax, smin in ((100, 80.0, 0.5), (7, 500.0, 1e-3), (200, 1.0, 0.9)):
+        sc = S.make_schedule(n, smax, smin)
+        assert sc.num_steps == n and (np.diff(sc.sigmas) < 0).all() and sc.sigmas[-1] == 0.0
+    for bad in (lambda: S.make_schedule(3, sigma_max=0.5, sigma_min=0.5), lambda: S.make_schedule(0),
+                lambda: S.Schedule(np.array([1.0, 2.0, 0.0], np.float32))):
+        with pytest.raises(ValueError):
+            bad()
+
+
+def test_consistency_sample_semantics(S):
+    c = np.float32(3.75)
+    for n in (1, 2, 5):
+        out = S.consistency_sample(lambda x, s: np.full_like(x, c), S.make_schedule(n), (4, 4), seed=0)
+        assert np.array_equal(out, np.full((4, 4), c, np.float32))
+    for n in (1, 3, 4, 100):
+        calls = []
+        S.consistency_sample(lambda x, s: (calls.append(s), x * np.float32(0.9))[1], S.make_schedule(n), (2, 2), 5)
+        assert len(calls) == n
+    seen = {}
+
+    def first(x, s):
+        seen.setdefault("x", np.array(x, copy=True))
+        seen.setdefault("s", s)
+        return np.zeros_like(x)
+    S.consistency_sample(first, S.make_schedule(1, sigma_max=10.0, sigma_min=1.0), (8,), seed=3)
+    assert seen["s"] == 10.0 and np.array_equal(seen["x"], np.float32(10.0) * S.step_noise(3, 0, (8,)))
+    a = (np.random.default_rng(8).standard_normal((6, 6)) * 0.3).astype(np.float32)
+    lin = lambda x, s: (a @ x.T).T.astype(np.float32)
+    sc = S.make_schedule(3, sigma_max=4.0, sigma_min=0.25)
+    x = np.float32(sc.sigmas[0]) * S.step_noise(11, 0, (2, 6))
+    for i in (1, 2):
+        x = lin(x, None) + np.float32(sc.sigmas[i]) * S.step_noise(11, i, (2, 6))
+    assert np.allclose(S.consistency_sample(lin, sc, (2, 6), 11), lin(x, None), atol=1e-6)
+    tanh = lambda x, s: np.tanh(x)
+    assert np.array_equal(S.consistency_sample(tanh, S.make_schedule(4), (16, 8), 9),
+                          S.consistency_sample(tanh, S.make_schedule(4), (16, 8), 9))
+    with pytest.raises(ValueError):
+        S.consistency_sample(lambda x, s: np.zeros((1,), np.float32), S.make_schedule(2), (4,), seed=0)
+
+
+def test_two_expert_semantics(S):
+    sc = S.make_schedule(3, 80.0, 0.5)
+    hi_, lo_ = (lambda x, s: np.full_like(x, np.float32(2.0))), (lambda x, s: np.full_like(x, np.float32(-1.0)))
+    mid = float(np.sqrt(sc.sigmas[1] * sc.sigmas[2]))
+    for boundary, want_sw, want in ((1000.0, 0, -1.0), (0.01, 0, 2.0), (mid, 1, -1.0)):
+        out, sw = S.two_expert_sample(S.TwoExpertConfig(boundary, hi_, lo_), sc, (4,), seed=0)
+        assert sw == want_sw and np.array_equal(out, np.full((4,), want, np.float32))
+    with pytest.raises(ValueError):
+        S.TwoExpertConfig(0.0, hi_, lo_)
+
+
+def test_quantized_weights_take_the_w8a8_path(S, A):
+    layers = S.make_random_weights(64, num_layers=1, seed=4)
+    x = np.random.default_rng(1).standard_normal((16, 64)).astype(np.float32)
+    dense = np.asarray(S.ToyModel(layers=layers, heads=2)(x, 0.5))
+    quant = np.asarray(S.ToyModel(layers=S.quantize_weights(layers), heads=2)(x, 0.5))
+    assert A.error_metrics(quant, dense)[0] >= 0.97 and not np.array_equal(quant, dense)
