@@ -494,8 +494,10 @@ def main():
                 e1.record()
                 torch.cuda.synchronize()
                 gms = e0.elapsed_time(e1) / 10
-                res[mode] = {"ms": gms, "TOPS": 2 * M * K * N / (gms * 1e-3) / 1e12}
+                tops = 2 * M * K * N / (gms * 1e-3) / 1e12
+                res[mode] = {"ms": gms, "TOPS": tops, "frac_int8_peak": tops / (2.0 * bf16_peak)}
             w8[f"{K}x{N}"] = res
+        w8["peak_note"] = f"INT8 dense peak taken as 2 x the {peak_kind} bf16 burst {bf16_peak} TFLOP/s"
 
     # ---- cfg5: full rCM 4-step sampling of the Wan2.1-14B-720P-shaped toy DiT
     dit_res = None
