@@ -265,6 +265,9 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) w8a8_tc_kernel(
 // the operand-full and segment-free barriers and issues the MMAs; commits are
 // multicast to both CTAs; both CTAs' epilogues drain their own TMEM rows with
 // the same promotion as the single-SM kernel and TMA-store their rows.
+#ifndef TB_W8_STG2
+#define TB_W8_STG2 1
+#endif
 namespace gemm2 {
 constexpr int BM = 128, BN = 256, BK = 128, STAGES = 5;
 constexpr int EPI_WARPS = 8;
@@ -282,8 +285,15 @@ struct Smem {
     uint32_t tmem_base;
     float qred[2][4];                          // OUTM 2: per (column half, row quarter) absmax
     alignas(1024) uint8_t stage_out[EPI_WARPS][32 * 128];
+#if TB_W8_STG2
+    // second staging buffer per warp: the TMA store of chunk c drains while
+    // chunk c+1 is staged (the tile-end store no longer serialises on each
+    // store's shared-memory read)
+    alignas(1024) uint8_t stage_out2[EPI_WARPS][32 * 128];
+#endif
 };
 constexpr size_t SMEM_BYTES = sizeof(Smem) + 1024;
+static_assert(SMEM_BYTES <= 232448, "2-SM W8A8 shared memory over the 227 KB opt-in limit");
 }  // namespace gemm2
 
 // Tile raster of the 2-SM kernel: groups of W8_GROUP_M row-pair bands, row
@@ -557,9 +567,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
                 continue;
             }
             constexpr int CPC = OUT_BF16 ? 64 : 32;
+            static_assert(!TB_W8_STG2 || (CW / CPC) % 2 == 0, "chunk count per tile must be even");
 #pragma unroll
             for (int ch = 0; ch < CW / CPC; ch++) {
+#if TB_W8_STG2
+                uint8_t *stg = (ch & 1) ? S.stage_out2[ew] : S.stage_out[ew];
+                const uint32_t stg_s = ptx::smem_u32(stg);
+                if (lane == 0) ptx::bulk_wait_read1();         // the store that last used this buffer has read it
+#else
+                uint8_t *stg = S.stage_out[ew];
                 if (lane == 0) ptx::bulk_wait_read0();
+#endif
                 __syncwarp();
 #pragma unroll
                 for (int u = 0; u < 8; u++) {
@@ -590,12 +608,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
                         // skipped (they would land in the next rank's token rows)
                         const int pl = c / plane, w = pl / pm.H, hd = pl - w * pm.H, owner = hd / pm.hp;
                         if (row0 < M)
-                            ptx::tma_store_3d(&pm.m[owner], S.stage_out[ew], c % plane, pm.row0 + row0,
+                            ptx::tma_store_3d(&pm.m[owner], stg, c % plane, pm.row0 + row0,
                                               w * pm.hp + (hd - owner * pm.hp));
                     } else if (plane) {
-                        ptx::tma_store_3d(&tma_out, S.stage_out[ew], c % plane, row0, c / plane);
+                        ptx::tma_store_3d(&tma_out, stg, c % plane, row0, c / plane);
                     } else {
-                        ptx::tma_store_2d(&tma_out, S.stage_out[ew], c, row0);
+                        ptx::tma_store_2d(&tma_out, stg, c, row0);
                     }
                     ptx::bulk_commit();
                 }
