@@ -62,7 +62,9 @@ int tb_transpose_codes(const int8_t *src, int64_t rows, int64_t cols, int8_t *ds
  * sum over k-blocks ascending of (exact_int_segment * sa) * sb, then + bias
  * (f32 [N], may be NULL).  block==128, K%128==0, N%16==0 runs on tcgen05
  * (kind::i8, s32 TMEM accumulators); other shapes on a CUDA-core kernel with
- * the identical arithmetic. */
+ * the identical arithmetic.  Any block with block * 127^2 < 2^31: segments
+ * are exact int32 sums rounded to f32 once, which is what the reference's
+ * int64 path does above block 1040 (blockquant.py:119-129). */
 int tb_w8a8_gemm(const int8_t *a, const float *sa, const int8_t *bt, const float *sb,
                  const float *bias, int64_t M, int64_t N, int64_t K, int64_t block,
                  void *out, int out_dtype, void *stream);

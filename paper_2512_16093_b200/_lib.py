@@ -7,6 +7,7 @@ a CUDA device is missing, every op raises.
 from __future__ import annotations
 
 import ctypes
+import threading
 import os
 
 import torch
@@ -122,6 +123,7 @@ def exported_symbols():
 
 
 def check(rc: int, what: str):
+    _release()
     if rc == TB_OK:
         return
     msg = load().tb_last_error().decode(errors="replace")
@@ -135,8 +137,29 @@ def call(name: str, *args):
     check(getattr(lib, name)(*args), name)
 
 
+_KEEP = threading.local()
+
+
 def ptr(t: torch.Tensor | None):
-    return None if t is None else ctypes.c_void_p(t.data_ptr())
+    """Raw device address of ``t`` for a C-ABI argument list.  The tensor is
+    kept alive until the next ``call`` / ``check`` returns: call sites pass
+    temporaries (``ptr(x.contiguous())``), and a temporary freed before its
+    kernel is enqueued could be handed by the caching allocator to the next
+    temporary in the same argument list and overwritten before the kernel
+    reads it.  Once the kernel is enqueued, stream order makes the free safe."""
+    if t is None:
+        return None
+    keep = getattr(_KEEP, "items", None)
+    if keep is None:
+        keep = _KEEP.items = []
+    keep.append(t)
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _release():
+    keep = getattr(_KEEP, "items", None)
+    if keep:
+        keep.clear()
 
 
 def stream_ptr():

@@ -17,6 +17,10 @@ int check_launch(const char *what);
 #define TB_REQUIRE(cond, msg) \
     do { if (!(cond)) return ::tb::fail(TB_EINVAL, (msg)); } while (0)
 
+int ensure_smem(const void *fn, int bytes);
+template <typename F>
+inline void smem_attr(F *kern, int bytes) { ensure_smem(reinterpret_cast<const void *>(kern), bytes); }
+
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
 // ----------------------------------------------------------- load helpers

@@ -182,10 +182,10 @@ extern "C" int tb_gemm_bf16_batched(const void *A, const void *B, void *C, int64
     const int grid = (int)(ntiles < num_sms() ? ntiles : num_sms());
     cudaStream_t st = as_stream(stream);
     if (out_dtype == TB_F32) {
-        cudaFuncSetAttribute(gemm_bf16_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+        smem_attr(gemm_bf16_kernel<true>, (int)SMEM_BYTES);
         gemm_bf16_kernel<true><<<grid, THREADS, SMEM_BYTES, st>>>(ta, tbm, C, (int)H, (int)M, (int)N, (int)K, ldc, ldc * M);
     } else {
-        cudaFuncSetAttribute(gemm_bf16_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+        smem_attr(gemm_bf16_kernel<false>, (int)SMEM_BYTES);
         gemm_bf16_kernel<false><<<grid, THREADS, SMEM_BYTES, st>>>(ta, tbm, C, (int)H, (int)M, (int)N, (int)K, ldc, ldc * M);
     }
     return check_launch("gemm_bf16");

@@ -185,7 +185,7 @@ extern "C" int tb_linear_kv_part(const void *k, const void *v, int64_t H, int64_
         !make_tmap_2d(&to, kv_part, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, D, H * nkv * dx, D * 2, 64, 128))
         return fail(TB_ECUDA, "cuTensorMapEncodeTiled failed (kv_part)");
     cudaStream_t st = as_stream(stream);
-    cudaFuncSetAttribute(kv_part_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+    smem_attr(kv_part_kernel, (int)SMEM_BYTES);
     kv_part_kernel<<<dim3((unsigned)nkv, (unsigned)H), THREADS, SMEM_BYTES, st>>>(tk, tv, to, (int)L, (int)nkv,
                                                                                   (int)dx, (__nv_bfloat16 *)kv_part);
     return check_launch("kv_part");

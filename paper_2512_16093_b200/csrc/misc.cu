@@ -3,7 +3,10 @@
 //   rmsnorm / layernorm / gelu (sampler.py:34-58) for the DiT block,
 //   error/info plumbing of the C ABI.
 #include <cstdio>
+#include <mutex>
+#include <set>
 #include <string>
+#include <tuple>
 
 #include "common.cuh"
 
@@ -20,6 +23,21 @@ int check_launch(const char *what) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(TB_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
     return TB_OK;
+}
+
+// cudaFuncSetAttribute once per (device, kernel, bytes): the attribute is
+// sticky, so the launch path only pays a locked set lookup.
+int ensure_smem(const void *fn, int bytes) {
+    static std::mutex mu;
+    static std::set<std::tuple<int, const void *, int>> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const auto key = std::make_tuple(dev, fn, bytes);
+    std::lock_guard<std::mutex> g(mu);
+    if (done.count(key)) return 0;
+    const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.insert(key);
+    return (int)e;
 }
 
 __device__ __forceinline__ float phi(float x) { return x >= 0.0f ? x + 1.0f : expf(x); }

@@ -675,7 +675,7 @@ extern "C" int tb_kmean(const void *k, int dtype, int64_t H, int64_t L, int64_t 
                           CU_TENSOR_MAP_SWIZZLE_NONE))
             return fail(TB_ECUDA, "cuTensorMapEncodeTiled failed (kmean)");
         const int smem = KM_STAGES * KM_CH * 64;
-        cudaFuncSetAttribute(kmean_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        smem_attr(kmean_split_kernel, smem);
         kmean_split_kernel<<<dim3(4, (unsigned)H), 32, smem, st>>>(tm, L, kmean);
     } else if (aligned && d <= 128) {
         constexpr int STAGES = 6;
@@ -683,10 +683,10 @@ extern "C" int tb_kmean(const void *k, int dtype, int64_t H, int64_t L, int64_t 
         if (chunk < 8) chunk = 8;
         size_t smem = (size_t)STAGES * chunk * d * es;
         if (dtype == TB_F32) {
-            cudaFuncSetAttribute(kmean_bulk_kernel<float, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            smem_attr(kmean_bulk_kernel<float, STAGES>, (int)smem);
             kmean_bulk_kernel<float, STAGES><<<(unsigned)H, 128, smem, st>>>((const float *)k, L, (int)d, chunk, kmean);
         } else {
-            cudaFuncSetAttribute(kmean_bulk_kernel<__nv_bfloat16, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            smem_attr(kmean_bulk_kernel<__nv_bfloat16, STAGES>, (int)smem);
             kmean_bulk_kernel<__nv_bfloat16, STAGES><<<(unsigned)H, 128, smem, st>>>((const __nv_bfloat16 *)k, L, (int)d, chunk, kmean);
         }
     } else {

@@ -928,468 +928,9 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
     if (warp == 5) ptx::tmem_dealloc<256>(tmem);
 }
 
-// ---------------------------------------------------------------------------
-// Two q-tiles per CTA (one CTA per SM, all 512 TMEM columns): the Q codes of
-// both tiles live in TMEM (A operand of QK read from TMEM -- no per-block
-// shared-memory re-read of Q, and the N=64 INT8 MMA is no longer bound by the
-// shared-memory operand bandwidth), and three S buffers rotate over the
-// interleaved block sequence A0 B0 A1 B1 ...: QK(g+3) reuses the buffer PV(g)
-// just consumed, so each tile still has its next scores ready while it
-// computes the current softmax.  TMEM: Q_A 0-31, Q_B 32-63, S 64/128/192,
-// O_A 256-383, O_B 384-511.  Warps 0-3 tile A, 4-7 tile B (softmax + epilogue,
-// thread = row = TMEM lane), warp 8 TMA, warp 9 MMA.
-namespace sla2 {
-constexpr int BM = 128, BN = 64, D = 128, KSTAGES = 4, VSTAGES = 4, NSB = 3;
-constexpr int THREADS = 320, TMA_WARP = 8, MMA_WARP = 9;
-constexpr uint32_t QCOL = 0, SCOL = 64, OCOL = 256;
-constexpr uint32_t K_BYTES = BN * D, V_BYTES = D * BN * 2;
-constexpr int MAX_SEL = 2048;
-struct Smem {
-    uint8_t ring[128 * 1024];          // K ring (4 x 8 KB) + V ring (4 x 16 KB); fused epilogue: 4 x 32 KB
-    uint64_t q_full, o_final;
-    uint64_t k_full[KSTAGES], k_empty[KSTAGES];
-    uint64_t v_full[VSTAGES], v_empty[VSTAGES];
-    uint64_t s_full[NSB], p_full[NSB], pv_done[NSB];
-    uint64_t phiq_full[2], lin_full[2], lin_done[2];
-    alignas(128) uint16_t bias_a[128], bias_b[128];
-    float c1[2][MAX_SEL];
-    uint8_t rag[2][MAX_SEL];
-    uint32_t tmem_base;
-};
-constexpr size_t SMEM_BYTES = sizeof(Smem);
-}  // namespace sla2
-
-template <typename T, bool EXACT>
-__global__ void __launch_bounds__(sla2::THREADS, 1) sla_tc2_kernel(
-    const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
-    const __grid_constant__ CUtensorMap tm_kv, tb_sla_args a, int nq, int nkv) {
-    using namespace sla2;
-    using sla::LOG2E;
-    using sla::LN2;
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    Smem &S = *reinterpret_cast<Smem *>(smem_raw);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int h = blockIdx.y;
-    const int n0 = blockIdx.x * 2;
-    const int ntile = (n0 + 1 < nq) ? 2 : 1;               // last CTA may hold a single tile
-    const int count = (int)a.count;
-    const int G = ntile * count;                           // interleaved block sequence length
-    const int L = (int)a.L;
-    uint8_t *kring = S.ring;                               // 4 x 8 KB
-    uint8_t *vring = S.ring + KSTAGES * K_BYTES;           // 4 x 16 KB
-    // sequence g -> (tile, j): interleaved A0 B0 A1 B1 ... (single tile: t = 0)
-    auto tile_of = [&](int g) { return ntile == 2 ? (g & 1) : 0; };
-    auto j_of = [&](int g) { return ntile == 2 ? (g >> 1) : g; };
-    auto sel_of = [&](int t) { return a.idx + ((int64_t)h * nq + n0 + t) * count; };
-
-    if (warp == TMA_WARP && lane == 0) {
-        if (ptx::smem_u32(smem_raw) & 1023) __trap();
-        ptx::mbar_init(&S.q_full, 32 * 4 * ntile);
-        ptx::mbar_init(&S.o_final, 1);
-        for (int s = 0; s < KSTAGES; s++) { ptx::mbar_init(&S.k_full[s], 1); ptx::mbar_init(&S.k_empty[s], 1); }
-        for (int s = 0; s < VSTAGES; s++) { ptx::mbar_init(&S.v_full[s], 1); ptx::mbar_init(&S.v_empty[s], 1); }
-        for (int b = 0; b < NSB; b++) {
-            ptx::mbar_init(&S.s_full[b], 1);
-            ptx::mbar_init(&S.p_full[b], 128);
-            ptx::mbar_init(&S.pv_done[b], 1);
-        }
-        for (int t = 0; t < 2; t++) {
-            ptx::mbar_init(&S.phiq_full[t], 128);
-            ptx::mbar_init(&S.lin_full[t], 1);
-            ptx::mbar_init(&S.lin_done[t], 1);
-        }
-        for (int i = 0; i < 128; i++) {
-            S.bias_a[i] = (i % 8 == 0) ? 0x3F80 : 0;    // bf16 1.0
-            S.bias_b[i] = (i % 8 == 0) ? 0x4AC0 : 0;    // bf16 6291456 = 1.5 * 2^22
-        }
-        ptx::fence_async_smem();
-        ptx::fence_barrier_init();
-        ptx::prefetch_tmap(&tm_k);
-        ptx::prefetch_tmap(&tm_v);
-    }
-    if (warp == MMA_WARP) ptx::tmem_alloc<512>(&S.tmem_base);
-    ptx::tc_fence_before();
-    __syncthreads();
-    ptx::tc_fence_after();
-    const uint32_t tmem = S.tmem_base;
-    const bool fused = a.lin_kv != nullptr && a.linear_mix != 0.0f;
-
-    if (warp == TMA_WARP) {
-        // ------------------------------------------------------ TMA producer
-        for (int g = 0; g < G; g++) {
-            const int t = tile_of(g), j = j_of(g);
-            const int b = __ldg(sel_of(t) + j);
-            const int ks = g % KSTAGES, vs = g % VSTAGES;
-            ptx::mbar_wait_sleep(&S.k_empty[ks], (uint32_t)(((g / KSTAGES) & 1) ^ 1));
-            if (ptx::elect_one()) {
-                ptx::mbar_arrive_expect_tx(&S.k_full[ks], K_BYTES);
-                ptx::tma_load_3d(kring + ks * K_BYTES, &tm_k, 0, b * BN, h, &S.k_full[ks]);
-            }
-            __syncwarp();
-            ptx::mbar_wait_sleep(&S.v_empty[vs], (uint32_t)(((g / VSTAGES) & 1) ^ 1));
-            if (ptx::elect_one()) {
-                ptx::mbar_arrive_expect_tx(&S.v_full[vs], V_BYTES);
-                ptx::tma_load_3d(vring + vs * V_BYTES, &tm_v, 0, b * BN, h, &S.v_full[vs]);
-                ptx::tma_load_3d(vring + vs * V_BYTES + V_BYTES / 2, &tm_v, 64, b * BN, h, &S.v_full[vs]);
-            }
-            __syncwarp();
-        }
-        if (fused) {
-            ptx::mbar_wait_sleep(&S.o_final, 0);        // every MMA reading the rings is done
-            for (int t = 0; t < ntile; t++) {
-                const int row0 = (int)(((int64_t)h * nq + n0 + t) * a.lin_dx);
-                uint8_t *lb = S.ring + (2 * t + 1) * 32768;
-                if (ptx::elect_one()) {
-                    ptx::mbar_arrive_expect_tx(&S.lin_full[t], 2 * 16384);
-                    ptx::tma_load_2d(lb, &tm_kv, 0, row0, &S.lin_full[t]);
-                    ptx::tma_load_2d(lb + 16384, &tm_kv, 64, row0, &S.lin_full[t]);
-                }
-                __syncwarp();
-            }
-        }
-    } else if (warp == MMA_WARP) {
-        // ------------------------------------------------------- MMA issuer
-        constexpr uint32_t ID_QK = ptx::idesc_i8(BM, BN);
-        constexpr uint32_t ID_PV = ptx::idesc_bf16(BM, D);
-        constexpr uint32_t ID_PV_MN = ptx::idesc_bf16(BM, D) | (1u << 16);
-        constexpr uint32_t ID_BIAS = ptx::idesc_bf16(BM, BN);
-        const uint64_t bias_a = ptx::sdesc_noswz_alias(ptx::smem_u32(S.bias_a));
-        const uint64_t bias_b = ptx::sdesc_noswz_alias(ptx::smem_u32(S.bias_b));
-        ptx::mbar_wait_sleep(&S.q_full, 0);
-        ptx::tc_fence_after();
-        auto qk = [&](int g) {
-            const int ks = g % KSTAGES, sb = g % NSB, t = tile_of(g);
-            ptx::mbar_wait_sleep(&S.k_full[ks], (uint32_t)((g / KSTAGES) & 1));
-            ptx::tc_fence_after();
-            const uint64_t kd = ptx::sdesc_sw128(ptx::smem_u32(kring + ks * K_BYTES));
-            const uint32_t sd = tmem + SCOL + sb * BN;
-            if (ptx::elect_one()) {
-                ptx::mma_f16(sd, bias_a, bias_b, ID_BIAS, 0u);
-#pragma unroll
-                for (int k = 0; k < D / 32; k++)    // K=32 int8 = 8 TMEM columns of Q, 32 B of K
-                    ptx::mma_i8_ts(sd, tmem + QCOL + t * 32 + 8 * k, kd + 2 * k, ID_QK, 1u);
-                ptx::mma_commit(&S.s_full[sb]);
-                ptx::mma_commit(&S.k_empty[ks]);
-            }
-            __syncwarp();
-        };
-        auto pv = [&](int g) {
-            const int pb = g % NSB, vs = g % VSTAGES, t = tile_of(g), j = j_of(g);
-            ptx::mbar_wait_sleep(&S.v_full[vs], (uint32_t)((g / VSTAGES) & 1));
-            ptx::mbar_wait_sleep(&S.p_full[pb], (uint32_t)((g / NSB) & 1));
-            ptx::tc_fence_after();
-            const uint64_t vd = ptx::sdesc_sw128_mn(ptx::smem_u32(vring + vs * V_BYTES), V_BYTES / 2, 1024);
-            if (ptx::elect_one()) {
-#pragma unroll
-                for (int k = 0; k < BN / 16; k++)
-                    ptx::mma_f16_ts(tmem + OCOL + t * 128, tmem + SCOL + pb * BN + 8 * k, vd + 128 * k, ID_PV_MN,
-                                    (j > 0 || k > 0) ? 1u : 0u);
-                ptx::mma_commit(&S.pv_done[pb]);
-                ptx::mma_commit(&S.v_empty[vs]);
-            }
-            __syncwarp();
-        };
-        for (int g = 0; g < NSB && g < G; g++) qk(g);
-        for (int g = 0; g < G; g++) {
-            pv(g);
-            if (g + NSB < G) qk(g + NSB);          // reuses the buffer PV(g) just read (in-order pipe)
-        }
-        if (ptx::elect_one()) ptx::mma_commit(&S.o_final);
-        __syncwarp();
-        if (fused) {
-            for (int t = 0; t < ntile; t++) {
-                // numL_t = phi(Q_t) . KV_sel_t (M128 N128 K128) into free columns t*128 .. t*128+127
-                ptx::mbar_wait_sleep(&S.phiq_full[t], 0);
-                ptx::mbar_wait_sleep(&S.lin_full[t], 0);
-                ptx::tc_fence_after();
-                uint8_t *la = S.ring + (2 * t) * 32768, *lb = S.ring + (2 * t + 1) * 32768;
-                if (ptx::elect_one()) {
-#pragma unroll
-                    for (int ks = 0; ks < D / 16; ks++) {
-                        const int sub = ks >> 2, w = ks & 3;
-                        const uint64_t ad = ptx::sdesc_sw128(ptx::smem_u32(la + sub * 16384)) + 2 * w;
-                        const uint64_t bd = ptx::sdesc_sw128(ptx::smem_u32(lb + sub * 16384)) + 2 * w;
-                        ptx::mma_f16(tmem + t * 128, ad, bd, ID_PV, ks > 0 ? 1u : 0u);
-                    }
-                    ptx::mma_commit(&S.lin_done[t]);
-                }
-                __syncwarp();
-            }
-        }
-    } else {
-        // ------------------------------------------------ softmax + epilogue
-        const int t = warp >> 2;                    // q-tile
-        const int wq = warp & 3;                    // TMEM lane quarter
-        const int r = wq * 32 + lane;               // row in tile == TMEM lane
-        const int n = n0 + t;
-        const bool tile_ok = t < ntile;
-        const int row = n * BM + r;
-        const bool row_ok = tile_ok && row < L;
-        const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
-        const float scale2 = a.scale * LOG2E;
-        if (tile_ok) {
-            // Q codes of this row -> TMEM (A operand of QK), rows >= L zero
-            uint32_t qw[32];
-            const uint4 *src = reinterpret_cast<const uint4 *>(a.q_codes + ((int64_t)h * L + (row_ok ? row : 0)) * D);
-#pragma unroll
-            for (int c = 0; c < 8; c++) {
-                const uint4 w = row_ok ? __ldg(src + c) : make_uint4(0u, 0u, 0u, 0u);
-                qw[4 * c] = w.x; qw[4 * c + 1] = w.y; qw[4 * c + 2] = w.z; qw[4 * c + 3] = w.w;
-            }
-            ptx::tmem_st32(tmem + lane_base + QCOL + t * 32, qw);
-            ptx::tmem_wait_st();
-            ptx::tc_fence_before();
-            ptx::mbar_arrive(&S.q_full);
-        }
-        float corr = 0.0f;
-        if (row_ok) {
-            const T *qr = reinterpret_cast<const T *>(a.q) + ((int64_t)h * L + row) * D;
-            const float *km = a.k_mean + (int64_t)h * D;
-#pragma unroll 4
-            for (int c = 0; c < D; c += 8) {
-                float x[8];
-                load8(qr + c, x);
-#pragma unroll
-                for (int i = 0; i < 8; i++) corr = fmaf(x[i], __ldg(km + c + i), corr);
-            }
-        }
-        const float c0 = corr * scale2;
-        const float *ksc = a.k_scales + (int64_t)h * nkv;
-        const int last_blk = nkv - 1;
-        const int last_ext = L - last_blk * BN;
-        if (tile_ok) {
-            const float sq = __ldg(a.q_scales + (int64_t)h * nq + n);
-            const int32_t *sel = sel_of(t);
-            for (int j = r; j < count; j += BM) {
-                const int b = __ldg(sel + j);
-                S.c1[t][j] = sq * __ldg(ksc + b) * scale2;
-                S.rag[t][j] = (b == last_blk) && last_ext < BN;
-            }
-        }
-        ptx::named_bar_sync(1 + t, BM);
-        float m_ref = -INFINITY, m_true = -INFINITY, l = 0.0f;
-        for (int j = 0; tile_ok && j < count; j++) {
-            const int g = ntile == 2 ? 2 * j + t : j;
-            const int sb = g % NSB;
-            const uint32_t sbase = tmem + lane_base + SCOL + sb * BN;
-            const float c1 = S.c1[t][j];
-            const float c0m = fmaf(-12582912.0f, c1, c0);
-            ptx::mbar_wait_sleep(&S.s_full[sb], (uint32_t)((g / NSB) & 1));
-            ptx::tc_fence_after();
-            uint32_t s[4][16];
-            auto load_s = [&]() {
-#pragma unroll
-                for (int q4 = 0; q4 < 4; q4++) ptx::tmem_ld16(sbase + q4 * 16, s[q4]);
-                ptx::tmem_wait_ld();
-            };
-            load_s();
-            const bool ragged = S.rag[t][j] != 0;
-            const int lim = ragged ? last_ext : BN;
-            auto xm = [&](int i) { return __int_as_float((int)s[i >> 4][i & 15]); };
-            float2 psum2[4];
-            uint32_t pk[2][16];
-            auto make_p = [&](auto rg, float off) {
-                constexpr bool RG = decltype(rg)::value;
-                const float2 c12 = make_float2(c1, c1), off2 = make_float2(off, off);
-                const float2 cu = make_float2(c1 * 0.00390625f, c1 * 0.00390625f);
-                const float ou = fmaf(off, 0.00390625f, 0.48828125f);
-                const float2 ou2 = make_float2(ou, ou);
-#pragma unroll
-                for (int u = 0; u < 4; u++) psum2[u] = make_float2(0.0f, 0.0f);
-#pragma unroll
-                for (int i = 0; i < 64; i += 2) {
-                    constexpr int PP = TB_SLA_PP;
-                    float p0, p1;
-                    if ((PP >> ((i >> 1) & 7)) & 1) {
-                        const float2 e = ex2_poly2_sat(ptx::ffma2_sat(make_float2(xm(i), xm(i + 1)), cu, ou2));
-                        p0 = e.x;
-                        p1 = e.y;
-                    } else {
-                        const float2 y = ptx::ffma2(make_float2(xm(i), xm(i + 1)), c12, off2);
-                        p0 = ex2(y.x);
-                        p1 = ex2(y.y);
-                    }
-                    if (RG) {
-                        if (i >= lim) p0 = 0.0f;
-                        if (i + 1 >= lim) p1 = 0.0f;
-                    }
-                    psum2[(i >> 1) & 3] = ptx::fadd2(psum2[(i >> 1) & 3], make_float2(p0, p1));
-                    __nv_bfloat162 pp = __floats2bfloat162_rn(p0, p1);
-                    pk[i >> 5][(i >> 1) & 15] = *reinterpret_cast<uint32_t *>(&pp);
-                }
-                const float2 ps = ptx::fadd2(ptx::fadd2(psum2[0], psum2[1]), ptx::fadd2(psum2[2], psum2[3]));
-                return ps.x + ps.y;
-            };
-            auto run_p = [&](float off) {
-                return ragged ? make_p(std::integral_constant<bool, true>(), off)
-                              : make_p(std::integral_constant<bool, false>(), off);
-            };
-            float psum = 0.0f;
-            bool slow = EXACT;
-            if (!EXACT) {
-                psum = run_p(c0m - m_ref);
-                slow = __any_sync(0xffffffffu, !(psum <= 0x1p60f));
-            }
-            if (slow) {
-                if (!EXACT) load_s();
-                float sx = (c1 >= 0.0f) ? -INFINITY : INFINITY;
-#pragma unroll
-                for (int i = 0; i < 64; i++)
-                    if (!ragged || i < lim) sx = (c1 >= 0.0f) ? fmaxf(sx, xm(i)) : fminf(sx, xm(i));
-                const float mx = fmaf(sx, c1, c0m);
-                m_true = fmaxf(m_true, mx);
-                if (m_ref == -INFINITY) {
-                    m_ref = mx;
-                } else {
-                    const bool need = mx > m_ref + 8.0f;
-                    if (__any_sync(0xffffffffu, need)) {
-                        // PV of this tile's previous block is issued after QK(g): wait for it
-                        const int gp = g - ntile;
-                        ptx::mbar_wait_sleep(&S.pv_done[gp % NSB], (uint32_t)((gp / NSB) & 1));
-                        ptx::tc_fence_after();
-                        const float alpha = need ? ex2(m_ref - mx) : 1.0f;
-                        const uint32_t obase = tmem + lane_base + OCOL + t * 128;
-#pragma unroll 1
-                        for (int c = 0; c < D; c += 16) {
-                            uint32_t o[16];
-                            ptx::tmem_ld16(obase + c, o);
-                            ptx::tmem_wait_ld();
-#pragma unroll
-                            for (int i = 0; i < 16; i++) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-                            ptx::tmem_st16(obase + c, o);
-                        }
-                        l *= alpha;
-                        if (need) m_ref = mx;
-                    }
-                }
-                psum = run_p(c0m - m_ref);
-            }
-            l += psum;
-            ptx::tmem_st16(sbase, pk[0]);
-            ptx::tmem_st16(sbase + 16, pk[1]);
-            ptx::tmem_wait_st();
-            ptx::tc_fence_before();
-            ptx::mbar_arrive(&S.p_full[sb]);
-        }
-        if (!EXACT) m_true = m_ref;
-        // ------------------------------------------------------- epilogue
-        ptx::mbar_wait_sleep(&S.o_final, 0);
-        ptx::tc_fence_after();
-        if (tile_ok) {
-            float den_fused = 0.0f;
-            if (fused) {
-                uint8_t *la = S.ring + (2 * t) * 32768;
-                const __nv_bfloat16 *k1 = reinterpret_cast<const __nv_bfloat16 *>(a.lin_kv) +
-                                          (((int64_t)h * nq + n) * a.lin_dx + D) * D;
-                const T *qr = reinterpret_cast<const T *>(a.q) + ((int64_t)h * L + (row_ok ? row : 0)) * D;
-#pragma unroll 2
-                for (int kc = 0; kc < D / 8; kc++) {
-                    uint32_t pq[4];
-                    float xq[8];
-                    load8(qr + kc * 8, xq);
-#pragma unroll
-                    for (int u = 0; u < 4; u++) {
-                        float f0 = 0.0f, f1 = 0.0f;
-                        if (row_ok) {
-                            const float x0 = xq[2 * u], x1 = xq[2 * u + 1];
-                            f0 = x0 >= 0.0f ? x0 + 1.0f : __expf(x0);
-                            f1 = x1 >= 0.0f ? x1 + 1.0f : __expf(x1);
-                        }
-                        den_fused = fmaf(f0, __bfloat162float(k1[kc * 8 + 2 * u]), den_fused);
-                        den_fused = fmaf(f1, __bfloat162float(k1[kc * 8 + 2 * u + 1]), den_fused);
-                        __nv_bfloat162 pp = __floats2bfloat162_rn(f0, f1);
-                        pq[u] = *reinterpret_cast<uint32_t *>(&pp);
-                    }
-                    uint8_t *dst = la + (kc >> 3) * 16384 + r * 128 + (((kc & 7) ^ (r & 7)) * 16);
-                    *reinterpret_cast<uint4 *>(dst) = make_uint4(pq[0], pq[1], pq[2], pq[3]);
-                }
-                ptx::fence_async_smem();
-                ptx::mbar_arrive(&S.phiq_full[t]);
-                ptx::mbar_wait_sleep(&S.lin_done[t], 0);
-                ptx::tc_fence_after();
-            }
-            const float f = ex2(m_ref - m_true);
-            const float m_nat = m_true * LN2;
-            const float l_true = l * f;
-            const bool lin = fused || (a.num_l != nullptr && a.linear_mix != 0.0f);
-            const int64_t lin_ld = a.lin_ld ? a.lin_ld : D;
-            const int64_t lin_hs = a.lin_hs ? a.lin_hs : (int64_t)L * lin_ld;
-            const float *nl_row = (lin && !fused) ? a.num_l + (int64_t)h * lin_hs + (int64_t)row * lin_ld : nullptr;
-            const float *dl_ptr = (lin && !fused) ? (a.lin_ld ? nl_row + D : a.den_l + (int64_t)h * L + row) : nullptr;
-            float ss = f, shrink = 0.0f, den = l_true;
-            if (lin && row_ok) {
-                const float ref = fmaxf(m_nat, 0.0f);
-                const float e_ss = expf(m_nat - ref);
-                shrink = expf(-ref) * a.linear_mix;
-                den = l_true * e_ss + shrink * (fused ? den_fused : *dl_ptr);
-                ss = f * e_ss;
-            }
-            const float inv = 1.0f / den;
-            if (row_ok) {
-                if (a.row_max) a.row_max[(int64_t)h * L + row] = m_nat;
-                if (a.den) a.den[(int64_t)h * L + row] = l_true;
-            }
-            const uint32_t obase = tmem + lane_base + OCOL + t * 128;
-            const uint32_t nbase = tmem + lane_base + t * 128;
-#pragma unroll 1
-            for (int c = 0; c < D; c += 16) {
-                uint32_t o[16], nlt[16];
-                ptx::tmem_ld16(obase + c, o);
-                if (fused) ptx::tmem_ld16(nbase + c, nlt);
-                ptx::tmem_wait_ld();
-                if (!row_ok) continue;
-                float v[16];
-                const int64_t off = ((int64_t)h * L + row) * D + c;
-                if (fused) {
-#pragma unroll
-                    for (int i = 0; i < 16; i++)
-                        v[i] = (__uint_as_float(o[i]) * ss + shrink * __uint_as_float(nlt[i])) * inv;
-                } else if (lin) {
-#pragma unroll
-                    for (int i = 0; i < 16; i += 4) {
-                        const float4 nl = *reinterpret_cast<const float4 *>(nl_row + c + i);
-                        v[i] = (__uint_as_float(o[i]) * ss + shrink * nl.x) * inv;
-                        v[i + 1] = (__uint_as_float(o[i + 1]) * ss + shrink * nl.y) * inv;
-                        v[i + 2] = (__uint_as_float(o[i + 2]) * ss + shrink * nl.z) * inv;
-                        v[i + 3] = (__uint_as_float(o[i + 3]) * ss + shrink * nl.w) * inv;
-                    }
-                } else {
-#pragma unroll
-                    for (int i = 0; i < 16; i++) v[i] = __uint_as_float(o[i]) * f * inv;
-                }
-                if (a.out_dtype == TB_BF16) {
-                    __nv_bfloat16 *dst = reinterpret_cast<__nv_bfloat16 *>(a.out) + off;
-#pragma unroll
-                    for (int i = 0; i < 16; i += 8) {
-                        uint4 w;
-                        __nv_bfloat162 *p = reinterpret_cast<__nv_bfloat162 *>(&w);
-#pragma unroll
-                        for (int u = 0; u < 4; u++) p[u] = __floats2bfloat162_rn(v[i + 2 * u], v[i + 2 * u + 1]);
-                        *reinterpret_cast<uint4 *>(dst + i) = w;
-                    }
-                } else {
-                    float *dst = a.out + off;
-#pragma unroll
-                    for (int i = 0; i < 16; i += 4)
-                        *reinterpret_cast<float4 *>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-                }
-            }
-        }
-    }
-    ptx::tc_fence_before();
-    __syncthreads();
-    if (warp == MMA_WARP) ptx::tmem_dealloc<512>(tmem);
-}
-
 int sla_simt(const tb_sla_args *a, cudaStream_t st);
 
-int tb_sla_kernel_variant() {
-    static const int variant = [] { const char *e = getenv("TB_SLA_KERNEL"); return e ? atoi(e) : 1; }();
-    return variant;
-}
-
 bool sla_tc_supported(const tb_sla_args *a) {
-    static_assert(sla2::MAX_SEL == sla::MAX_SEL, "table sizes");
     return a->quantized && a->d == 128 && a->q_block == 128 && a->kv_block == 64 &&
            (a->dtype == TB_BF16 || a->vt != nullptr) && a->L >= 128 &&
            (a->dtype == TB_BF16 || a->dtype == TB_F32) && a->count >= 1 && a->count <= sla::MAX_SEL &&
@@ -1412,25 +953,9 @@ int sla_tc(const tb_sla_args *a, cudaStream_t st) {
     if (!ok) return fail(TB_ECUDA, "cuTensorMapEncodeTiled failed (sla)");
     // the exact-max variant only when the caller asks for the sparse-branch stats
     const bool exact = a->row_max != nullptr || a->den != nullptr;
-    const int variant = (a->out_dtype == TB_I8 || a->v_fp8) ? 1 : tb_sla_kernel_variant();   // 2: two-tile kernel (measured slower, kept for study)
-    if (variant == 2) {
-        dim3 grid2((unsigned)cdiv(nq, 2), (unsigned)a->H);
-        auto launch2 = [&](auto kern) {
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sla2::SMEM_BYTES);
-            kern<<<grid2, sla2::THREADS, sla2::SMEM_BYTES, st>>>(tk, tv, tkv, *a, (int)nq, (int)nkv);
-        };
-        if (a->dtype == TB_BF16) {
-            if (exact) launch2(sla_tc2_kernel<__nv_bfloat16, true>);
-            else launch2(sla_tc2_kernel<__nv_bfloat16, false>);
-        } else {
-            if (exact) launch2(sla_tc2_kernel<float, true>);
-            else launch2(sla_tc2_kernel<float, false>);
-        }
-        return check_launch("sla_tc2");
-    }
     dim3 grid((unsigned)nq, (unsigned)a->H);
     auto launch = [&](auto kern) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+        smem_attr(kern, (int)SMEM_BYTES);
         kern<<<grid, THREADS, SMEM_BYTES, st>>>(tq, tk, tv, tkv, *a, (int)nq, (int)nkv);
     };
     if (a->v_fp8) {

@@ -341,7 +341,7 @@ static int topk_launch(const float *qp, const float *kp, const float *kpt, int64
         constexpr int R = TB_TOPK_ROWS;              // q rows per CTA (8: two CTAs per SM)
         const size_t smem = (((size_t)R * nkv * 4 + 15) & ~(size_t)15) + (size_t)d * R * 4 + 10 * 256 * 4;
         dim3 grid((unsigned)cdiv(nq, R), (unsigned)H);
-        cudaFuncSetAttribute(topk16_kernel<JT, R, R == 16 ? 1 : (R == 8 ? 2 : 3)>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        smem_attr(topk16_kernel<JT, R, R == 16 ? 1 : (R == 8 ? 2 : 3)>, (int)smem);
         topk16_kernel<JT, R, R == 16 ? 1 : (R == 8 ? 2 : 3)><<<grid, 320, smem, st>>>(qp, kpt, ldk, (int)nq, (int)nkv, (int)d, (int)count, idx, comp,
                                                   scores_out, cov, cov_ld);
         return check_launch("topk16");
@@ -349,7 +349,7 @@ static int topk_launch(const float *qp, const float *kp, const float *kpt, int64
 #define TB_TOPK(R)                                                                                 \
     {                                                                                              \
         size_t smem = (((size_t)(R) * nkv * 4 + 15) & ~(size_t)15) + (size_t)(R) * d * 4;          \
-        cudaFuncSetAttribute(topk_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        smem_attr(topk_kernel<R>, (int)smem); \
         dim3 grid((unsigned)cdiv(nq, R), (unsigned)H);                                             \
         topk_kernel<R><<<grid, 256, smem, st>>>(qp, kp, (int)nq, (int)nkv, (int)d, (int)count, small, \
                                                 idx, comp, scores_out, cov, cov_ld);               \

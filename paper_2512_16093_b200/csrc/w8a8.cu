@@ -718,7 +718,11 @@ int w8a8_dispatch(const int8_t *a, const float *sa, const int8_t *bt, const floa
                "plane must divide 128 and N, be >= 64, with bf16 output");
     TB_REQUIRE(act == 0 || act == 1, "act must be 0 (none) or 1 (gelu-tanh)");
     TB_REQUIRE(block >= 1, "block must be >= 1");
-    TB_REQUIRE(block <= 1040, "block edge > 1040 (f32-exact segment bound) unsupported");
+    // segments accumulate exactly in int32 (tensor cores: s32 TMEM; SIMT: dp4a)
+    // and are rounded to f32 once, like the reference's int64 path above its
+    // f32-exact bound of 1040 (blockquant.py:26,119-129): exact while
+    // block * 127^2 < 2^31
+    TB_REQUIRE(block * 16129 < (1ll << 31), "block edge too large for an exact int32 segment (block * 127^2 >= 2^31)");
     TB_REQUIRE(out_dtype == TB_F32 || out_dtype == TB_BF16, "out dtype must be f32 or bf16");
     if (M == 0 || N == 0) return TB_OK;
     const bool tc = block == 128 && K % 128 == 0 && N % 128 == 0 && K > 0 && M < (1ll << 31) &&
@@ -747,7 +751,7 @@ int w8a8_dispatch(const int8_t *a, const float *sa, const int8_t *bt, const floa
 #define TB_GEMM2(E, B)                                                                                     \
     {                                                                                                      \
         auto kern = w8a8_2sm_kernel<E, (B) ? 1 : 0>;                                                       \
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm2::SMEM_BYTES);   \
+        smem_attr(kern, (int)gemm2::SMEM_BYTES);   \
         kern<<<grid, gemm2::THREADS, gemm2::SMEM_BYTES, st>>>(ta, tbm, tout, sa, sb, bias, (int)M, (int)N, (int)K, \
                                                               (int)plane, act, nullptr, no_peers);               \
     }
@@ -777,7 +781,7 @@ int w8a8_dispatch(const int8_t *a, const float *sa, const int8_t *bt, const floa
 #define TB_GEMM_LAUNCH(BNV, E, B)                                                                          \
     {                                                                                                      \
         auto kern = w8a8_tc_kernel<BNV, E, B>;                                                             \
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm::smem_bytes<BNV>()); \
+        smem_attr(kern, (int)gemm::smem_bytes<BNV>()); \
         kern<<<grid, gemm::THREADS, gemm::smem_bytes<BNV>(), st>>>(ta, tbm, tout, sa, sb, bias, out, (int)M, (int)N, (int)K, \
                                                                   (int)plane, act);                                        \
     }
@@ -848,7 +852,7 @@ extern "C" int tb_w8a8_gemm_quant(const int8_t *a, const float *sa, const int8_t
     int clusters = num_sms() / 2;
     if (ntiles < clusters) clusters = ntiles;
     auto kern = w8a8_2sm_kernel<false, 2>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm2::SMEM_BYTES);
+    smem_attr(kern, (int)gemm2::SMEM_BYTES);
     PeerMaps no_peers;
     memset(&no_peers, 0, sizeof(no_peers));
     kern<<<2 * clusters, gemm2::THREADS, gemm2::SMEM_BYTES, as_stream(stream)>>>(
@@ -889,7 +893,7 @@ extern "C" int tb_w8a8_gemm_qkv_peers(const int8_t *a, const float *sa, const in
     int clusters = num_sms() / 2;
     if (ntiles < clusters) clusters = ntiles;
     auto kern = w8a8_2sm_kernel<false, 1>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm2::SMEM_BYTES);
+    smem_attr(kern, (int)gemm2::SMEM_BYTES);
     kern<<<2 * clusters, gemm2::THREADS, gemm2::SMEM_BYTES, as_stream(stream)>>>(
         ta, tbm, ta, sa, sb, bias, (int)M, (int)N, (int)K, 128, 0, nullptr, pm);
     return check_launch("w8a8_gemm_qkv_peers");

@@ -191,7 +191,11 @@ def _tensor_at(addr: int, shape, dtype, device) -> torch.Tensor:
 
 class PeerGroup:
     """Per-process-group peer memory: allocations every rank can store into,
-    and the group's device barrier."""
+    and the group's device barrier.  ``alloc`` is a collective (every rank of
+    the group must call it in the same order), so callers allocate at setup
+    (``prepare_p2p``), not lazily inside a forward pass that ranks may take
+    differently; ``close`` (also a context-manager exit) unmaps the peers'
+    allocations and frees this rank's own."""
 
     def __init__(self, group=None):
         import ctypes
@@ -201,6 +205,7 @@ class PeerGroup:
         self.P, self.rank = dist.get_world_size(group), dist.get_rank(group)
         self.device = torch.device("cuda", torch.cuda.current_device())
         self.epoch = 0
+        self._own, self._imported = [], []
         flags = self.alloc(4 * self.P)
         self.flag_table = torch.tensor(flags, dtype=torch.int64, device=self.device)
 
@@ -210,6 +215,7 @@ class PeerGroup:
         c = self.ctypes
         p = c.c_void_p()
         _check(self.lib.tb_peer_alloc(nbytes, c.byref(p)), "tb_peer_alloc")
+        self._own.append(int(p.value))
         h = c.create_string_buffer(64)
         _check(self.lib.tb_peer_export(p, h), "tb_peer_export")
         handles = [None] * self.P
@@ -221,8 +227,32 @@ class PeerGroup:
             else:
                 q = c.c_void_p()
                 _check(self.lib.tb_peer_import(c.create_string_buffer(hr, 64), c.byref(q)), "tb_peer_import")
+                self._imported.append(int(q.value))
                 ptrs.append(int(q.value))
         return ptrs
+
+    def close(self):
+        """Collective teardown: wait for this rank's work, meet the peers (no
+        rank may still be storing into memory about to be unmapped), unmap
+        the imported allocations, free the own ones."""
+        if self._own is None:
+            return
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group=self.group)
+        c = self.ctypes
+        for q in self._imported:
+            _check(self.lib.tb_peer_close(c.c_void_p(q)), "tb_peer_close")
+        dist.barrier(group=self.group)      # every peer has unmapped before the owners free
+        for p in self._own:
+            _check(self.lib.tb_peer_free(c.c_void_p(p)), "tb_peer_free")
+        self._own = self._imported = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+        return False
 
     def barrier(self):
         from .ops import stream_ptr
@@ -245,6 +275,29 @@ def peer_group(group=None) -> PeerGroup:
     if key not in _GROUPS:
         _GROUPS[key] = PeerGroup(group)
     return _GROUPS[key]
+
+
+def close_peer_groups():
+    """Release every peer group and the exchange buffers cached on them
+    (collective over each group)."""
+    for key in list(_P2P):
+        del _P2P[key]
+    for key in list(_QKV):
+        del _QKV[key]
+    for key, pg in list(_GROUPS.items()):
+        pg.close()
+        del _GROUPS[key]
+
+
+def prepare_p2p(L: int, heads: int, d: int = 128, group=None, block: int = 128):
+    """Allocate (collectively, at setup) both fused-exchange buffer sets of a
+    DiT with L tokens and `heads` heads, so the forward pass never runs the
+    allocation collective."""
+    P = dist.get_world_size(group)
+    per = shard_size(L, P, block)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    _p2p_buffers(per, heads, d, group, dev, block)
+    _qkv_buffers(L, heads, group, dev)
 
 
 _P2P = {}
@@ -283,6 +336,16 @@ def attn_return_p2p(qh, kh, vh, L: int, attn_peer_fn, group=None, block: int = 1
 _QKV = {}
 
 
+def _qkv_buffers(L: int, heads: int, group, device):
+    pg = peer_group(group)
+    hp = heads // pg.P
+    key = (L, heads, id(pg))
+    if key not in _QKV:
+        ptrs = pg.alloc(3 * hp * L * 128 * 2)
+        _QKV[key] = (_tensor_at(ptrs[pg.rank], (3 * hp, L, 128), torch.bfloat16, device), ptrs, pg)
+    return _QKV[key]
+
+
 def qkv_to_heads_p2p(a_q, a_s, w_bt, w_scales, L: int, heads: int, group=None, block: int = 128):
     """Fused forward exchange: the qkv projection of this rank's (128-aligned)
     token shard with its epilogue storing every tile into the head owner's
@@ -294,13 +357,8 @@ def qkv_to_heads_p2p(a_q, a_s, w_bt, w_scales, L: int, heads: int, group=None, b
     if heads % P:
         raise ValueError(f"heads {heads} not divisible by world size {P}")
     hp = heads // P
-    pg = peer_group(group)
     dev = a_q.device
-    key = (L, heads, id(pg))
-    if key not in _QKV:
-        ptrs = pg.alloc(3 * hp * L * 128 * 2)
-        _QKV[key] = (_tensor_at(ptrs[pg.rank], (3 * hp, L, 128), torch.bfloat16, dev), ptrs)
-    buf, ptrs = _QKV[key]
+    buf, ptrs, pg = _qkv_buffers(L, heads, group, dev)
     lo, hi = token_bounds(L, P, rank, block)
     if hi - lo >= 256:
         ops.w8a8_gemm_qkv_peers(a_q, a_s, w_bt, w_scales, ptrs, heads, lo, L, block)

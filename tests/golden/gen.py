@@ -72,6 +72,22 @@ ATTN_CASES = [
     ("coherent_d128", "B", 7, 2, 2048, 128, 128, 64, 0.1),
 ]
 
+# Headline-shape output goldens (one head, full length; tests/golden/headline.npz):
+# (name, generator, seed, heads, seq, head_dim, q_block, kv_block, topk_ratio, linear_mix values)
+HEADLINE_CASES = [
+    ("cfg4_h1", "G", 2, 1, 75600, 128, 128, 64, 0.1, (1.0, 0.0)),
+    ("cfg4_B_h1", "B", 13, 1, 75600, 128, 128, 64, 0.1, (1.0, 0.0)),
+    ("cfg3_h1_q128", "G", 1, 1, 32760, 128, 128, 64, 0.1, (1.0, 0.0)),
+    ("cfg3_h1_q64", "G", 1, 1, 32760, 128, 64, 64, 0.1, (1.0, 0.0)),
+]
+
+
+def headline_rows(s: int) -> np.ndarray:
+    """Row subsample stored for the headline goldens: every 127th row plus the
+    last 80 (cfg4's ragged last q-block of 128 has 80 rows)."""
+    return np.unique(np.r_[np.arange(0, s, 127), np.arange(max(0, s - 80), s)]).astype(np.int64)
+
+
 # (name, seed, rows, cols, scale, block)
 QUANT_CASES = [
     ("q300x200", 8, 300, 200, 1.0, 128),

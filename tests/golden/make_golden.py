@@ -138,8 +138,29 @@ def score_probes():
     print("scores done", flush=True)
 
 
+def headline_cases():
+    """Reference outputs at the headline shapes (one head each, full length):
+    a deterministic row subsample (every 127th row + the ragged last 80) is
+    stored verbatim, so the GPU tests check the fused kernel's OUTPUT at cfg4 /
+    cfg3 against the reference itself, not only against the oracle."""
+    st: dict = {}
+    for (name, g, seed, h, s, d, qb, kvb, ratio, mixes) in gen.HEADLINE_CASES:
+        q, k, v = gen.make_inputs(g, seed, h, s, d)
+        rows = gen.headline_rows(s)
+        st[name + ".rows_idx"] = rows
+        for mix in mixes:
+            cfg = A.SLAConfig(q_block=qb, kv_block=kvb, topk_ratio=ratio, linear_mix=mix)
+            out = A.sla_attention(A.AttnInputs(q, k, v), cfg)
+            st[f"{name}.mix{mix:g}.rows"] = np.ascontiguousarray(out[:, rows, :])
+            st[f"{name}.mix{mix:g}.sha"] = np.array(sha(out))
+            print("headline", name, mix, flush=True)
+    np.savez_compressed(os.path.join(HERE, "headline.npz"), **st)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["attn", "quant", "sampler", "scores"]
+    which = sys.argv[1:] or ["attn", "quant", "sampler", "scores", "headline"]
+    if "headline" in which:
+        headline_cases()
     if "scores" in which:
         score_probes()
     if "quant" in which:

@@ -164,3 +164,21 @@ def test_e4m3_encoder_matches_torch_cast():
     assert np.array_equal(O.e4m3_decode(want), torch.from_numpy(want).view(torch.float8_e4m3fn).float().numpy())
     c, s = O.quantize_v_fp8(np.zeros((1, 4, 8), np.float32))
     assert s[0] == 0 and not c.any()
+
+
+@pytest.mark.parametrize("case", gen.HEADLINE_CASES, ids=lambda c: c[0])
+def test_oracle_headline_outputs_match_reference(case):
+    """The oracle's full sla_attention at the headline shapes (one head of
+    cfg4 / cfg3, Gaussian and block-coherent, q_block 128 and 64, mix 1 and
+    0) against row subsamples of the reference's own output: the checker the
+    GPU headline tests use is itself pinned here (float branches: f32 numpy
+    restatement, so agreement is to rounding)."""
+    name, g_, seed, h, s, d, qb, kvb, ratio, mixes = case
+    gold = load_golden("headline")
+    rows = gold[name + ".rows_idx"]
+    assert np.array_equal(rows, gen.headline_rows(s))
+    q, k, v = gen.make_inputs(g_, seed, h, s, d)
+    for mix in mixes:
+        got = O.sla_attention(q, k, v, qb, kvb, ratio, mix)[:, rows]
+        cos, _, rel1 = O.error_metrics(got, gold[f"{name}.mix{mix:g}.rows"])
+        assert cos >= 0.999999 and rel1 <= 1e-5, (name, mix, cos, rel1)
