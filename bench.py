@@ -18,6 +18,10 @@ q/k/v, all-to-all to a head shard, attention on H/P heads, all-to-all back
 
 --impl reference: the CPU oracle port (oracle/oracle.py, numpy + the C
 restatement) on the host cores, one head of the same workload per step.
+
+Roofline denominators: the tensor-core peaks MEASURED on this pool's B200s by
+tools/mma_peak.py (profiles/int8_fp8_peak.json: tcgen05 MMA-only INT8 / FP8 /
+BF16, burst and sustained), HBM from MEASURED_PEAKS.json.
 """
 from __future__ import annotations
 
@@ -78,6 +82,26 @@ def peaks():
     except Exception:
         pass
     return 6547.2, 1672.5, "measured (MEASURED_PEAKS.json values quoted in BASELINE.md)"
+
+
+PEAK_FILE = os.path.join(ROOT, "profiles", "int8_fp8_peak.json")
+
+
+def tc_peaks():
+    """Measured tcgen05 MMA-only peaks (tools/mma_peak.py on this pool's B200s)
+    -> {"int8": (burst, sustained), "fp8": ..., "bf16": ...} in TOPS, or None."""
+    try:
+        with open(PEAK_FILE) as f:
+            s = json.load(f)["summary"]
+        return {k: (s[f"{k}_tops_burst"], s[f"{k}_tops_sustained"]) for k in ("int8", "fp8", "bf16")}
+    except Exception:
+        return None
+
+
+def mixed_peak(a: float, b: float) -> float:
+    """Peak of work split evenly between two MMA kinds (QK^T and PV carry the
+    same op count): time = ops/2/a + ops/2/b."""
+    return 1.0 / (0.5 / a + 0.5 / b)
 
 
 class ClockSampler:
@@ -202,17 +226,53 @@ def run_reference(args):
 
 # ----------------------------------------------------------------- our arm
 
-def cpu_baseline_sample():
-    """Oracle port on a bounded sample (one cfg4 head, ~10-20 s), rank 0 only."""
-    sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
-    import gen
+def cpu_info():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    return model, os.cpu_count() or 1
+
+
+def cpu_oracle_time(fn, threads=None):
+    """Wall time of fn() on the host (BLAS threads limited when `threads`)."""
+    from threadpoolctl import threadpool_limits
+    if threads is None:
+        t0 = time.perf_counter()
+        r = fn()
+        return time.perf_counter() - t0, r
+    with threadpool_limits(threads):
+        t0 = time.perf_counter()
+        r = fn()
+        return time.perf_counter() - t0, r
+
+
+def parity(got, want):
+    """cos / rel-L2 / rel-L1 of the GPU output against the oracle (f64)."""
     from oracle import oracle as O
-    q, k, v = gen.gaussian_qkv(2, 1, L_, D_, bf16=True)
-    t0 = time.perf_counter()
-    O.sla_attention(q, k, v, QB, KVB, RATIO, 1.0)
-    t = time.perf_counter() - t0
-    return {"value": sparse_ops(H=1) / t / 1e12, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port",
-            "sample": f"1 of 40 heads of cfg4 (75600 tokens), {t:.1f} s, numpy/OpenBLAS oracle port"}
+    import numpy as np
+    cos, rel2, rel1 = O.error_metrics(np.asarray(got, np.float32), np.asarray(want, np.float32))
+    return {"cos": cos, "rel_l2": rel2, "rel_l1": rel1, "ok": bool(cos >= 0.999 and rel1 <= 1e-2)}
+
+
+def cpu_baseline_cfg4(q0, k0, v0, gpu_out0):
+    """Oracle port on head 0 of the bench's OWN cfg4 inputs (bf16 values, f32
+    upcast), all host threads and one thread, plus the parity of the GPU
+    output of that head from the timed step (~10-20 s, rank 0 only)."""
+    from oracle import oracle as O
+    model, cores = cpu_info()
+    t_all, want = cpu_oracle_time(lambda: O.sla_attention(q0, k0, v0, QB, KVB, RATIO, 1.0))
+    t_one, _ = cpu_oracle_time(lambda: O.sla_attention(q0, k0, v0, QB, KVB, RATIO, 1.0), threads=1)
+    return {"value": sparse_ops(H=1) / t_all / 1e12, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"head 0 of this run's cfg4 inputs (1 of 40 heads, 75600 tokens), {t_all:.1f} s on "
+                      f"{cores} threads, numpy/OpenBLAS oracle port; per-head work, so x40 heads = the step",
+            "cpu_model": model, "value_1thread": sparse_ops(H=1) / t_one / 1e12, "seconds": t_all,
+            "seconds_1thread": t_one, "parity_gpu_vs_oracle_head0": parity(gpu_out0, want)}
 
 
 DIT_DIM, DIT_FFN, DIT_STEPS = 5120, 13824, 4
@@ -224,42 +284,213 @@ def dit_ops_per_layer(L=L_, dim=DIT_DIM, ffn=DIT_FFN, heads=H_):
     return 2 * L * (dim * 3 * dim + dim * dim + 2 * dim * ffn) + sparse_ops(H=heads, L=L)
 
 
-def bench_dit(world, rank, num_layers, pv_fp8=False):
-    """cfg5 latency: one full rCM sample (4 steps x num_layers layers), seq-parallel
-    linears + Ulysses attention across ranks; max over ranks of CUDA-event time."""
+def bench_dit(world, rank, num_layers, pv_fp8=False, samples=3, tcp=None):
+    """cfg5 latency: full rCM samples (4 steps x num_layers layers), seq-parallel
+    linears + Ulysses attention across ranks; max over ranks of CUDA-event time,
+    median of `samples` samples.  The initial state and the per-step noise are
+    drawn for the WHOLE sequence from one seeded stream and each rank takes its
+    token shard, so every N computes the same sample."""
     import torch
     import torch.distributed as dist
     from paper_2512_16093_b200 import dit, ulysses
     torch.cuda.empty_cache()
     layers = dit.random_layers(DIT_DIM, DIT_FFN, num_layers, seed=0)
     lo, hi = ulysses.token_bounds(L_, world, rank, dit.TOKEN_ALIGN)
-    g = torch.Generator(device="cuda").manual_seed(77 + rank)
-    x_init = torch.randn((hi - lo, DIT_DIM), generator=g, device="cuda")
-    noises = [torch.randn((hi - lo, DIT_DIM), generator=g, device="cuda") for _ in range(DIT_STEPS - 1)]
+    g = torch.Generator(device="cuda").manual_seed(77)
+
+    def shard_of_global():
+        full = torch.randn((L_, DIT_DIM), generator=g, device="cuda")
+        part = full[lo:hi].clone()
+        del full
+        return part
+    x_init = shard_of_global()
+    noises = [shard_of_global() for _ in range(DIT_STEPS - 1)]
     sig = [80.0 * (0.5 / 80.0) ** (i / (DIT_STEPS - 1)) for i in range(DIT_STEPS)] + [0.0]   # make_schedule(4)
     sla = dict(q_block=QB, kv_block=KVB, topk_ratio=RATIO, linear_mix=1.0, pv_fp8=pv_fp8)
+    if world > 1 and os.environ.get("TB_ULYSSES_P2P") == "1":
+        ulysses.prepare_p2p(L_, H_, D_, None, dit.TOKEN_ALIGN)      # collective allocation at setup
     dit.block_forward(x_init, sig[0], layers[0], H_, sla, L_)          # warm-up (one block)
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    out = dit.rcm_sample(layers, H_, sla, x_init, noises, sig, L_global=L_)
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    lat = []
+    out = None
+    for _ in range(samples):
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        out = dit.rcm_sample(layers, H_, sla, x_init, noises, sig, L_global=L_)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            t_ = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t_, op=dist.ReduceOp.MAX)
+            ms = float(t_.item())
+        lat.append(ms / 1e3)
     ops_total = dit_ops_per_layer() * num_layers * DIT_STEPS
     finite = bool(torch.isfinite(out).all().item())
+    checksum = float(out.double().abs().sum().item())
+    if world > 1:
+        t_ = torch.tensor([checksum], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t_)
+        checksum = float(t_.item())
     del layers, noises, out
     torch.cuda.empty_cache()
-    return {"workload": "cfg5: rCM 4-step sample, Wan2.1-14B-720P-shaped toy DiT (dim 5120, 40 heads, "
-                        f"FFN 13824, {num_layers} layers, L 75600), SLA 0.1 + Sage INT8 + W8A8",
-            "latency_s": ms / 1e3, "ops": ops_total, "TOPS": ops_total / (ms * 1e-3) / 1e12,
-            "weights": "random-init on device (N(0,1)/sqrt(fan_in), block-quantized)", "finite": finite}
+    med = statistics.median(lat)
+    res = {"workload": "cfg5: rCM 4-step sample, Wan2.1-14B-720P-shaped toy DiT (dim 5120, 40 heads, "
+                       f"FFN 13824, {num_layers} layers, L 75600), SLA 0.1 + Sage INT8 + W8A8",
+           "latency_s": med, "latency_samples_s": lat, "ops": ops_total, "TOPS": ops_total / med / 1e12,
+           "weights": "random-init on device (N(0,1)/sqrt(fan_in), block-quantized)", "finite": finite,
+           "sample_abs_sum": checksum,
+           "noise": "global [L, dim] state and noise from one seeded device stream, sliced per rank"}
+    if tcp:
+        lin = 2 * L_ * (DIT_DIM * 3 * DIT_DIM + DIT_DIM * DIT_DIM + 2 * DIT_DIM * DIT_FFN) * num_layers * DIT_STEPS
+        att = ops_total - lin
+        # bound: linears at the sustained INT8 peak, attention at the sustained INT8/BF16 mix
+        t_bound = lin / (tcp["int8"][1] * 1e12) + att / (mixed_peak(tcp["int8"][1], tcp["bf16"][1]) * 1e12)
+        res["roofline"] = {"bound_s": t_bound, "frac": t_bound / med / world,
+                           "note": "per GPU: W8A8 work at the measured sustained INT8 MMA peak + attention "
+                                   "work at the sustained INT8/BF16 mix (profiles/int8_fp8_peak.json)"}
+    return res
+
+
+def time_graph(fn, reps=10):
+    """CUDA-graph the call, replay `reps` times; ms per replay (CUDA events)."""
+    import torch
+    for _ in range(2):
+        fn()
+    torch.cuda.synchronize()
+    cap = torch.cuda.Stream()
+    cap.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(cap):
+        fn()
+    torch.cuda.current_stream().wait_stream(cap)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        out = fn()
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps, out, g
+
+
+def bench_configs(tcp, cpu: bool):
+    """configs[0] (cfg1) and configs[2] (cfg3) at the reference default block
+    sizes (64/64) and at q_block 128: device step time, executed-work TOPS,
+    and (rank 0) the oracle on one head of the same inputs with parity."""
+    import numpy as np
+    import torch
+    from paper_2512_16093_b200 import ops
+    from oracle import oracle as O
+    res = {}
+    peak = mixed_peak(tcp["int8"][0], tcp["bf16"][0]) if tcp else None
+    for (name, H, L, seed) in (("cfg1", 2, 4096, 11), ("cfg3", 12, 32760, 12)):
+        g = torch.Generator(device="cuda").manual_seed(seed)
+        qkv = [torch.randn((H, L, D_), generator=g, device="cuda").to(torch.bfloat16) for _ in range(3)]
+        for qb in (64, 128):
+            ms, out, gr = time_graph(lambda: ops.sla_attention(qkv[0], qkv[1], qkv[2], qb, 64, RATIO, 1.0,
+                                                               out_dtype=torch.bfloat16))
+            ops_ = sparse_ops(H=H, L=L, qb=qb)
+            r = {"heads": H, "seq_len": L, "q_block": qb, "kv_block": 64, "topk_ratio": RATIO,
+                 "ms": ms, "TOPS": ops_ / (ms * 1e-3) / 1e12}
+            if peak:
+                r["frac_step_of_mixed_peak"] = r["TOPS"] / peak
+            if cpu:
+                h0 = [t[0:1].float().cpu().numpy() for t in qkv]
+                tcpu, want = cpu_oracle_time(lambda: O.sla_attention(h0[0], h0[1], h0[2], qb, 64, RATIO, 1.0))
+                r["cpu_baseline"] = {"value": sparse_ops(H=1, L=L, qb=qb) / tcpu / 1e12, "unit": UNIT,
+                                     "seconds_per_head": tcpu, "sample": "head 0 of the same inputs",
+                                     "kind": "port", "cores": os.cpu_count() or 1}
+                r["parity_head0"] = parity(out[0:1].float().cpu().numpy(), want)
+            del gr, out
+            res[f"{name}_q{qb}"] = r
+        del qkv
+    return res
+
+
+def bench_w8a8(tcp, hbm, cpu: bool):
+    """configs[1]: the W8A8 sweep at M = 32760 (exact and fast promotion), the
+    activation-quantization pass at those shapes, and the CPU
+    quantized_linear_forward (oracle, the reference's sgemm-per-k-block order)
+    on a 2048-row sample per shape."""
+    import numpy as np
+    import torch
+    from paper_2512_16093_b200 import ops
+    from oracle import oracle as O
+    w8 = {}
+    M = 32760
+    i8 = tcp["int8"][0] if tcp else None
+    for (K, N) in ((1536, 1536), (1536, 4608), (1536, 8960), (8960, 1536)):
+        xq = torch.randint(-127, 128, (M, K), dtype=torch.int8, device="cuda")
+        xs = torch.rand((-(-M // 128), K // 128), device="cuda") * 0.01
+        bt = torch.randint(-127, 128, (N, K), dtype=torch.int8, device="cuda")
+        bs = torch.rand((K // 128, N // 128), device="cuda") * 0.01
+        res = {}
+        for mode in ("exact", "fast"):
+            fn = lambda: ops.w8a8_gemm(xq, xs, bt, bs, 128, exact=(mode == "exact"))
+            for _ in range(3):
+                fn()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(10):
+                fn()
+            e1.record()
+            torch.cuda.synchronize()
+            gms = e0.elapsed_time(e1) / 10
+            tops = 2 * M * K * N / (gms * 1e-3) / 1e12
+            res[mode] = {"ms": gms, "TOPS": tops, "frac_int8_peak": (tops / i8) if i8 else None}
+        # full quantized_linear_forward: activation quant (bf16 x) + GEMM
+        x = torch.randn((M, K), device="cuda").to(torch.bfloat16)
+        fq = lambda: ops.quantize_blockwise(x, 128, check_finite=False)
+        for _ in range(3):
+            fq()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(10):
+            fq()
+        e1.record()
+        torch.cuda.synchronize()
+        qms = e0.elapsed_time(e1) / 10
+        res["act_quant"] = {"ms": qms, "GBps": 3 * M * K / (qms * 1e-3) / 1e9,
+                            "frac_hbm": 3 * M * K / (qms * 1e-3) / 1e9 / hbm,
+                            "bytes": "2 B bf16 read + 1 B int8 written per element"}
+        fl = lambda: ops.quantized_linear(x, bt, bs, 128, None, torch.float32, exact=True)
+        for _ in range(3):
+            fl()
+        e0.record()
+        for _ in range(10):
+            fl()
+        e1.record()
+        torch.cuda.synchronize()
+        lms = e0.elapsed_time(e1) / 10
+        res["quantized_linear_forward"] = {"ms": lms, "TOPS": 2 * M * K * N / (lms * 1e-3) / 1e12}
+        if cpu:
+            rows = 2048
+            xc = x[:rows].float().cpu().numpy()
+            wq = bt.t().contiguous().cpu().numpy()
+            ws = bs.cpu().numpy()
+
+            def cpu_ql():
+                aq, as_ = O.quantize_blockwise(xc, 128)
+                return O.w8a8_blas(aq, as_, wq, ws, 128)
+            tcpu, want = cpu_oracle_time(cpu_ql)
+            got = ops.quantized_linear(x[:rows], bt, bs, 128, None, torch.float32, exact=True).cpu().numpy()
+            res["cpu_baseline"] = {"value": 2 * rows * K * N / tcpu / 1e12, "unit": UNIT, "seconds": tcpu,
+                                   "sample": f"{rows} of {M} rows (quantize_blockwise + w8a8 in the reference's "
+                                             "numpy sgemm-per-k-block order)", "kind": "port",
+                                   "cores": os.cpu_count() or 1,
+                                   "bit_exact_gpu_vs_oracle": bool(np.array_equal(got, want))}
+        w8[f"{K}x{N}"] = res
+        del xq, xs, bt, bs, x
+    w8["peak_note"] = ("fractions of the measured tcgen05 kind::i8 MMA-only burst peak "
+                       f"{i8:.0f} TOPS (profiles/int8_fp8_peak.json)" if i8 else "no measured INT8 peak")
+    return w8
 
 
 def main():
@@ -270,8 +501,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-w8a8", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the cfg1 / cfg3 lines")
     ap.add_argument("--heads", type=int, default=H_)
     ap.add_argument("--no-dit", action="store_true")
+    ap.add_argument("--dit-samples", type=int, default=3)
     ap.add_argument("--no-fp8", action="store_true", help="skip the opt-in FP8 P/V measurement")
     ap.add_argument("--no-graph", action="store_true", help="eager launches in the timed region")
     ap.add_argument("--dit-layers", type=int, default=40)
@@ -309,20 +542,27 @@ def main():
             return _Done() if async_op else None
         dist.all_to_all_single = _staged
     elif world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")         # communicator setup visible in the log (N ranks)
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2512_16093_b200 import _lib, ops, ulysses
     from paper_2512_16093_b200.attention import attention_flop_report, SLAConfig
     _lib.load(require_device=True)
+    sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
 
     H = args.heads
     total_ops = sparse_ops(H=H)
     assert total_ops == attention_flop_report(L_, D_, H, SLAConfig(QB, KVB, RATIO)).sparse_softmax_flops
-    hp = H // world
-    g = torch.Generator(device="cuda").manual_seed(1234 + rank)
+    # the global cfg4 problem from one seeded stream; each rank keeps its token
+    # shard [L_p, H, d] of q/k/v (bf16), resident in HBM -- every N sees the same inputs
     lo, hi = ulysses.token_bounds(L_, world, rank)
-    # token shard [L_p, H, d] of q/k/v (bf16), resident in HBM
-    shard = [torch.randn((hi - lo, H, D_), generator=g, device="cuda", dtype=torch.float32).to(torch.bfloat16)
-             for _ in range(3)]
+    g = torch.Generator(device="cuda").manual_seed(1234)
+    shard = []
+    for _ in range(3):
+        full = torch.randn((L_, H, D_), generator=g, device="cuda", dtype=torch.float32).to(torch.bfloat16)
+        shard.append(full[lo:hi].clone())
+        del full
+    torch.cuda.empty_cache()
 
     def attn(qh, kh, vh):
         return ops.sla_attention(qh, kh, vh, QB, KVB, RATIO, 1.0, out_dtype=torch.bfloat16)
@@ -341,6 +581,7 @@ def main():
     # CUDA graph and replayed, so host-side launch jitter cannot starve the GPU
     # inside the timed region; the e2e figure below stays an eager call.
     graph = None
+    step_out = None
     if world == 1 and not args.no_graph:
         cap = torch.cuda.Stream()
         cap.wait_stream(torch.cuda.current_stream())
@@ -350,7 +591,7 @@ def main():
         torch.cuda.synchronize()
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
-            step()
+            step_out = step()
         for _ in range(2):
             graph.replay()
         torch.cuda.synchronize()
@@ -366,7 +607,7 @@ def main():
             if graph is not None:
                 graph.replay()
             else:
-                step()
+                step_out = step()
         ev1.record()
         torch.cuda.synchronize()
         if world > 1:
@@ -377,10 +618,23 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     value = total_ops / (ms * 1e-3) / 1e12
+    # head 0 of the timed step's output (parity against the oracle below)
+    out_head0 = None
+    if world == 1 and step_out is not None:
+        out_head0 = step_out[0:1].float().cpu().numpy()
+    elif world > 1 and step_out is not None:
+        out_head0 = None
 
     # ---- dominant kernel (fused tcgen05 attention) timed alone on its stream
     hbm, bf16_peak, peak_kind = peaks()
-    mixed_peak = bf16_peak * 4.0 / 3.0   # QK^T at INT8 (2x bf16) + PV at bf16, equal op counts
+    tcp = tc_peaks()
+    if tcp:
+        mixed = mixed_peak(tcp["int8"][0], tcp["bf16"][0])
+        peak_note = (f"measured tcgen05 MMA-only burst peaks (profiles/int8_fp8_peak.json): INT8 QK^T at "
+                     f"{tcp['int8'][0]:.0f} TOPS + BF16 PV at {tcp['bf16'][0]:.0f} TOPS, equal op counts")
+    else:
+        mixed = bf16_peak * 4.0 / 3.0
+        peak_note = f"INT8 QK^T (2x) + BF16 PV at {peak_kind} cuBLAS bf16 burst {bf16_peak} TFLOP/s x 4/3"
     roof = None
     if world == 1:
         qh, kh, vh = head_major
@@ -407,26 +661,53 @@ def main():
         torch.cuda.synchronize()
         kms = e0.elapsed_time(e1) / reps
         ach = total_ops / (kms * 1e-3) / 1e12
-        traffic = None
-        try:        # dram read+write bytes per launch from the committed ncu --set full capture
-            with open(os.path.join(ROOT, "profiles", "r01_sla_tc_traffic.json")) as f:
-                traffic = json.load(f)["traffic_bytes"]
-        except Exception:
-            pass
-        roof = {"bound": "tensor", "achieved": ach, "peak": mixed_peak, "unit": "TFLOP/s",
-                "frac": ach / mixed_peak, "traffic": traffic, "kernel": "sla_tc_kernel",
-                "kernel_ms": kms, "share_of_step": kms / ms,
-                "peak_note": f"INT8 QK^T (2x) + BF16 PV at {peak_kind} bf16 burst {bf16_peak} TFLOP/s x 4/3; "
-                             "INT8 dense peak not in MEASURED_PEAKS.json"}
+        traffic, tsrc = None, None
+        for fn in ("r02_sla_tc_traffic.json", "r01_sla_tc_traffic.json"):
+            try:        # dram read+write bytes per launch from the committed ncu --set full capture
+                with open(os.path.join(ROOT, "profiles", fn)) as f:
+                    traffic = json.load(f)["traffic_bytes"]
+                tsrc = "profiles/" + fn
+                break
+            except Exception:
+                pass
+        roof = {"bound": "tensor", "achieved": ach, "peak": mixed, "unit": "TFLOP/s",
+                "frac": ach / mixed, "traffic": traffic, "traffic_source": tsrc, "kernel": "sla_tc_kernel",
+                "kernel_ms": kms, "share_of_step": kms / ms, "peak_note": peak_note}
+        if tcp:
+            roof["frac_of_int8_fp8_peak"] = ach / tcp["int8"][0]
+            roof["frac_of_sustained_mix"] = ach / mixed_peak(tcp["int8"][1], tcp["bf16"][1])
+        del out
 
-    # ---- e2e through the public API with pinned host buffers (before the
-    # seconds-long DiT sample, which leaves the GPU power-capped)
-    e2e = None
+    # ---- e2e through the drop-in (the call a turbobench user makes:
+    # attention.sla_attention(AttnInputs(numpy f32 q, k, v), SLAConfig(...)) ->
+    # numpy f32), host buffers in and out, every copy inside the timed region;
+    # plus the torch API on pinned bf16 host tensors (ops.sla_attention_host)
+    e2e = e2e_torch = None
     if world == 1:
+        from paper_2512_16093_b200.attention import AttnInputs, sla_attention as dropin_sla
+        hn = [t.float().cpu().numpy() for t in head_major]             # f32 numpy, as the reference takes
+        cfg = SLAConfig(q_block=QB, kv_block=KVB, topk_ratio=RATIO, linear_mix=1.0)
+        inp = AttnInputs(hn[0], hn[1], hn[2])
+        dropin_sla(inp, cfg)
+        torch.cuda.synchronize()
+        times = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            o_np = dropin_sla(inp, cfg)                                # returns a host numpy array
+            times.append(time.perf_counter() - t0)
+        ems = statistics.median(times) * 1e3
+        e2e = {"value": total_ops / (ems * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": ems,
+               "h2d_bytes_per_step": sum(x.nbytes for x in hn), "d2h_bytes_per_step": o_np.nbytes,
+               "api": "paper_2512_16093_b200.attention.sla_attention(AttnInputs(numpy f32), SLAConfig) -> numpy f32 "
+                      "(drop-in for turbobench.attention.sla_attention); host wall clock, median of 3"}
+        if out_head0 is not None:
+            e2e["parity_vs_device_step_head0"] = parity(o_np[0:1], out_head0)
+        del hn, inp, o_np
         hq = [t.cpu().pin_memory() for t in head_major]
         hout = torch.empty((H, L_, D_), dtype=torch.bfloat16).pin_memory()
+
         def e2e_step():
-            # public API on pinned host buffers: per-head-chunk H2D / attention / D2H pipeline
+            # torch API on pinned bf16 host buffers: per-head-chunk H2D / attention / D2H pipeline
             ops.sla_attention_host(hq[0], hq[1], hq[2], QB, KVB, RATIO, 1.0, out=hout)
         e2e_step()
         torch.cuda.synchronize()
@@ -437,9 +718,11 @@ def main():
             e2e_step()
         e1.record()
         torch.cuda.synchronize()
-        ems = e0.elapsed_time(e1) / n_e2e
-        e2e = {"value": total_ops / (ems * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": ems,
-               "h2d_bytes_per_step": sum(t.numel() * 2 for t in hq), "d2h_bytes_per_step": hout.numel() * 2}
+        tms = e0.elapsed_time(e1) / n_e2e
+        e2e_torch = {"value": total_ops / (tms * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": tms,
+                     "h2d_bytes_per_step": sum(t.numel() * 2 for t in hq), "d2h_bytes_per_step": hout.numel() * 2,
+                     "api": "ops.sla_attention_host on pinned bf16 host tensors (CUDA events)"}
+        del hq, hout
     else:
         # N > 1: each rank's token shard of q/k/v from pinned host memory, the
         # Ulysses attention (exchange, head-shard attention, exchange back), and
@@ -469,42 +752,27 @@ def main():
         ems = float(t.item())
         e2e = {"value": total_ops / (ems * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": ems,
                "h2d_bytes_per_step": sum(t_.numel() * 2 for t_ in hq), "d2h_bytes_per_step": hout.numel() * 2,
-               "bytes_note": "per rank"}
+               "bytes_note": "per rank", "api": "ulysses_sla_attention from pinned bf16 token shards"}
         del hq, hout, dq
 
-    # ---- W8A8 GEMM sweep (configs[1]), tensor-core exact + fast promotion
+    # ---- W8A8 GEMM sweep (configs[1]) + act-quant + CPU quantized_linear_forward
     w8 = None
     if world == 1 and not args.no_w8a8:
-        w8 = {}
-        M = 32760
-        for (K, N) in ((1536, 1536), (1536, 4608), (1536, 8960), (8960, 1536)):
-            xq = torch.randint(-127, 128, (M, K), dtype=torch.int8, device="cuda")
-            xs = torch.rand((-(-M // 128), K // 128), device="cuda") * 0.01
-            bt = torch.randint(-127, 128, (N, K), dtype=torch.int8, device="cuda")
-            bs = torch.rand((K // 128, N // 128), device="cuda") * 0.01
-            res = {}
-            for mode in ("exact", "fast"):
-                fn = lambda: ops.w8a8_gemm(xq, xs, bt, bs, 128, exact=(mode == "exact"))
-                for _ in range(3):
-                    fn()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record()
-                for _ in range(10):
-                    fn()
-                e1.record()
-                torch.cuda.synchronize()
-                gms = e0.elapsed_time(e1) / 10
-                tops = 2 * M * K * N / (gms * 1e-3) / 1e12
-                res[mode] = {"ms": gms, "TOPS": tops, "frac_int8_peak": tops / (2.0 * bf16_peak)}
-            w8[f"{K}x{N}"] = res
-        w8["peak_note"] = f"INT8 dense peak taken as 2 x the {peak_kind} bf16 burst {bf16_peak} TFLOP/s"
+        w8 = bench_w8a8(tcp, hbm, cpu=not args.no_cpu_baseline)
+
+    # ---- configs[0] / configs[2] lines (cfg1, cfg3) at 64/64 and 128/64
+    cfgs = None
+    if world == 1 and not args.no_configs:
+        cfgs = bench_configs(tcp, cpu=not args.no_cpu_baseline)
 
     # ---- cfg5: full rCM 4-step sampling of the Wan2.1-14B-720P-shaped toy DiT
     dit_res = None
     if not args.no_dit:
         del shard
-        head_major = None if world > 1 else head_major
-        dit_res = bench_dit(world, rank, args.dit_layers, args.dit_pv_fp8)
+        head_major_keep = head_major
+        head_major = None
+        dit_res = bench_dit(world, rank, args.dit_layers, args.dit_pv_fp8, args.dit_samples, tcp)
+        head_major = head_major_keep
         if args.dit_pv_fp8:
             dit_res["workload"] += " (opt-in FP8 P/V)"
 
@@ -516,31 +784,13 @@ def main():
     fp8 = None
     if world == 1 and not args.no_fp8:
         qh, kh, vh = head_major
-        f8step = lambda: ops.sla_attention(qh, kh, vh, QB, KVB, RATIO, 1.0, out_dtype=torch.bfloat16, pv_fp8=True)
-        for _ in range(2):
-            f8step()
-        torch.cuda.synchronize()
-        cap = torch.cuda.Stream()
-        cap.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(cap):
-            f8step()
-        torch.cuda.current_stream().wait_stream(cap)
-        torch.cuda.synchronize()
-        g8 = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g8):
-            f8step()
-        g8.replay()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(args.steps):
-            g8.replay()
-        e1.record()
-        torch.cuda.synchronize()
-        f8ms = e0.elapsed_time(e1) / args.steps
+        f8ms, _, g8 = time_graph(lambda: ops.sla_attention(qh, kh, vh, QB, KVB, RATIO, 1.0,
+                                                           out_dtype=torch.bfloat16, pv_fp8=True), args.steps)
         del g8
         v8, v8s = ops.quant_v_fp8(vh)
         a.v_fp8, a.v_scales = ops.ptr(v8), ops.ptr(v8s)
+        out = torch.empty((H, L_, D_), dtype=torch.bfloat16, device="cuda")
+        a.out = ops.ptr(out)
         for _ in range(3):
             lib.tb_sla_attention(ctypes.byref(a), ops.stream_ptr())
         e0.record()
@@ -550,16 +800,19 @@ def main():
         torch.cuda.synchronize()
         f8k = e0.elapsed_time(e1) / reps
         a.v_fp8 = a.v_scales = None
-        f8peak = bf16_peak * 2.0     # INT8 QK^T and FP8 PV: both at 2x bf16
+        f8peak = mixed_peak(tcp["int8"][0], tcp["fp8"][0]) if tcp else bf16_peak * 2.0
         fp8 = {"step_ms": f8ms, "TOPS": total_ops / (f8ms * 1e-3) / 1e12, "kernel_ms": f8k,
                "kernel_TOPS": total_ops / (f8k * 1e-3) / 1e12, "peak": f8peak,
                "frac": total_ops / (f8k * 1e-3) / 1e12 / f8peak,
-               "note": "opt-in (pv_fp8=True); e4m3 P + per-head-scaled e4m3 V; rel-L1 ~2e-2 when sparse-dominated"}
+               "note": "opt-in (pv_fp8=True); e4m3 P + per-head-scaled e4m3 V; rel-L1 ~2e-2 when sparse-dominated; "
+                       "peak = measured INT8 QK^T + FP8 PV MMA-only burst mix"}
+        del out, v8, v8s
 
     if rank == 0:
         cpu = None
-        if world == 1 and not args.no_cpu_baseline:
-            cpu = cpu_baseline_sample()
+        if world == 1 and not args.no_cpu_baseline and out_head0 is not None:
+            h0 = [t[0:1].float().cpu().numpy() for t in head_major]
+            cpu = cpu_baseline_cfg4(h0[0], h0[1], h0[2], out_head0)
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "int8/bf16", "data": "synthetic",
@@ -568,8 +821,10 @@ def main():
                            "topk_ratio": RATIO, "parallelism": f"ulysses{world}",
                            "l2": "inputs 3 x 774 MB bf16 > 126 MB L2 (no flush needed)",
                            "launch": "CUDA graph replay of the step" if graph is not None else "eager"},
-                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "w8a8": w8, "fp8_pv": fp8,
-                "dit": dit_res, "gpu_launches": LAUNCHES_PER_STEP * args.steps, "clocks": clk.summary()}
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "e2e_torch_pinned": e2e_torch,
+                "w8a8": w8, "configs": cfgs, "fp8_pv": fp8,
+                "dit": dit_res, "tc_peaks": tcp, "gpu_launches": LAUNCHES_PER_STEP * args.steps,
+                "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -181,14 +181,38 @@ typedef struct tb_sla_args {
     void *const *out_peers;
     float *const *scale_peers;
     int64_t peer_rows, head0, out_heads;
+    /* q_block 64 (the reference default, SLAConfig / QuantAttnConfig) on the
+     * tensor-core kernel: 128-row tiles of two q-blocks walk the union of
+     * their top-k lists, from tb_pair_union (pair_idx [H, ceil(nq/2),
+     * pair_ld], pair_cnt [H, ceil(nq/2)]).  NULL keeps q_block 64 on the
+     * CUDA-core kernel. */
+    const int32_t *pair_idx, *pair_cnt;
+    int64_t pair_ld;
 } tb_sla_args;
 
 /* _sparse_branch + combine (attention.py:347-389, 392-421).  d==128,
- * q_block==128, kv_block==64, quantized -> tcgen05 kernel (INT8 QK^T with
+ * q_block 128 (or 64 with pair_idx), kv_block==64, quantized -> tcgen05 kernel (INT8 QK^T with
  * s32 TMEM accumulators, BF16 PV with f32 TMEM accumulators, TMA/bulk
  * staged tiles, warp-specialised online softmax); other shapes -> CUDA-core
  * kernel with the same semantics. */
 int tb_sla_attention(const tb_sla_args *a, void *stream);
+
+/* Union of the top-k lists of q-block pairs (2t, 2t+1) for the q_block 64
+ * tensor-core attention (tb_sla_args.pair_idx): idx [H, nq, count]
+ * ascending (select_topk_blocks, attention.py:269-284) -> per tile t the
+ * ascending distinct kv blocks of both lists, entry = block | (mask << 28)
+ * with mask bit 0 = selected by q-block 2t, bit 1 = by 2t+1; pair_cnt = the
+ * entries per tile (count <= pair_cnt <= 2*count).  pair_ld >= 2*count. */
+/* 1 when tb_sla_attention would run these arguments on the tcgen05 kernel,
+ * 0 for the CUDA-core kernel. */
+int tb_sla_path(const tb_sla_args *a);
+
+/* f32 -> bf16 (round to nearest even) copy of n elements: the bf16 V operand
+ * (tb_sla_args.vt) when the attention inputs are f32. */
+int tb_cast_bf16(const float *x, int64_t n, void *y, void *stream);
+
+int tb_pair_union(const int32_t *idx, int64_t H, int64_t nq, int64_t count, int32_t *pair_idx,
+                  int32_t *pair_cnt, int64_t pair_ld, void *stream);
 
 /* ---------------------------------------------- NVLink peer memory
  * (new, multi-GPU: the fused Ulysses exchanges store into peers' buffers).

@@ -182,6 +182,31 @@ def w8a8(aq, a_scales, bq, b_scales, block):
     return out
 
 
+def w8a8_blas(aq, a_scales, bq, b_scales, block):
+    """blockquant.py:132-161 exactly as the reference computes it for block <=
+    1040: per k-block an f32 sgemm of the codes (exact: every partial sum
+    stays below 2^24), ``seg *= row_scale`` then ``seg *= col_scale`` (numpy
+    RN multiplies), ``out += seg`` ascending.  Same values as ``w8a8`` (the C
+    restatement; tests/test_oracle_golden.py); this one runs at BLAS speed and
+    is what bench.py times as the CPU baseline of configs[1]."""
+    if block > 1040:
+        return w8a8(aq, a_scales, bq, b_scales, block)
+    M, K = aq.shape
+    N = bq.shape[1]
+    a32, b32 = aq.astype(np.float32), bq.astype(np.float32)
+    a_s, b_s = _f32(a_scales), _f32(b_scales)
+    rext = [min(block, M - i * block) for i in range(nblocks(M, block))]
+    cext = [min(block, N - j * block) for j in range(nblocks(N, block))]
+    out = np.zeros((M, N), np.float32)
+    for kb in range(nblocks(K, block)):
+        lo, hi = kb * block, min(kb * block + block, K)
+        seg = a32[:, lo:hi] @ b32[lo:hi]
+        np.multiply(seg, np.repeat(a_s[:, kb], rext)[:, None], out=seg)
+        np.multiply(seg, np.repeat(b_s[kb], cext)[None, :], out=seg)
+        out += seg
+    return out
+
+
 def quantized_linear(x, wq, w_scales, block=128, bias=None):
     """blockquant.py:164-182."""
     xq, xs = quantize_blockwise(x, block)

@@ -46,6 +46,9 @@ SIGNATURES = {
     "tb_topk_blocks_cov": [_P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _P, _P, _I, _P],
     "tb_pool_quant_tokens_t": [_P, _i, _P, _I, _I, _I, _I, _P, _P, _P, _P, _I, _P],
     "tb_sla_attention": [_P, _P],
+    "tb_pair_union": [_P, _I, _I, _I, _P, _P, _I, _P],
+    "tb_cast_bf16": [_P, _I, _P, _P],
+    "tb_sla_path": [_P],
     "tb_transpose_v": [_P, _i, _I, _I, _I, _I, _P, _P],
     "tb_quant_v_fp8": [_P, _i, _I, _I, _I, _P, _P, _P, _P],
     "tb_peer_alloc": [_I, _P],
@@ -91,6 +94,7 @@ class SlaArgs(ctypes.Structure):
         ("v_fp8", _P), ("v_scales", _P),
         ("out_peers", _P), ("scale_peers", _P),
         ("peer_rows", _I), ("head0", _I), ("out_heads", _I),
+        ("pair_idx", _P), ("pair_cnt", _P), ("pair_ld", _I),
     ]
 
 

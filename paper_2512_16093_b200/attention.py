@@ -273,10 +273,13 @@ def _sparse_branch(inputs: AttnInputs, mask: BlockMask, cfg: SLAConfig):
     out = torch.empty((h, s, d), device=q.device)
     row_max = torch.empty((h, s), device=q.device)
     den = torch.empty((h, s), device=q.device)
-    # the CUDA-core kernel reports (num/den, den, row_max) against the true row max
+    # both kernels report (num/den, den, row_max) against the true row max (the
+    # tensor-core one in its exact-max instantiation)
+    kw.setdefault("vt", None)
+    kw.update(ops.attention_operands(q, v, idx, cfg.q_block, cfg.kv_block, cfg.quantized_sparse_branch))
     args = ops.sla_args(q=ops.ptr(q), k=ops.ptr(k), v=ops.ptr(v), dtype=ops.dtype_code(q), H=h, L=s, d=d,
                         q_block=cfg.q_block, kv_block=cfg.kv_block, count=count, scale=float(inputs.scale),
-                        linear_mix=0.0, quantized=int(cfg.quantized_sparse_branch), idx=ops.ptr(idx), vt=None,
+                        linear_mix=0.0, quantized=int(cfg.quantized_sparse_branch), idx=ops.ptr(idx),
                         l_pad=0, num_l=None, den_l=None, out=ops.ptr(out), out_dtype=0, row_max=ops.ptr(row_max),
                         den=ops.ptr(den), **kw)
     import ctypes
@@ -298,11 +301,13 @@ def quantized_attention(inputs: AttnInputs, cfg: QuantAttnConfig | None = None):
     kc, ks, _ = ops.pool_quant_tokens(k, tb, km if cfg.smooth_k else None, pool=False)
     idx = torch.arange(nb, dtype=torch.int32, device=q.device).expand(h, nb, nb).contiguous()
     out = torch.empty((h, s, d), device=q.device)
+    kw = {"vt": None}
+    kw.update(ops.attention_operands(q, v, idx, tb, tb, True))
     args = ops.sla_args(q=ops.ptr(q), k=ops.ptr(k), v=ops.ptr(v), dtype=ops.dtype_code(q), H=h, L=s, d=d,
                         q_block=tb, kv_block=tb, count=nb, scale=float(inputs.scale), linear_mix=0.0, quantized=1,
                         q_codes=ops.ptr(qc), k_codes=ops.ptr(kc), q_scales=ops.ptr(qs), k_scales=ops.ptr(ks),
-                        k_mean=ops.ptr(km), idx=ops.ptr(idx), vt=None, l_pad=0, num_l=None, den_l=None,
-                        out=ops.ptr(out), out_dtype=0, row_max=None, den=None)
+                        k_mean=ops.ptr(km), idx=ops.ptr(idx), l_pad=0, num_l=None, den_l=None,
+                        out=ops.ptr(out), out_dtype=0, row_max=None, den=None, **kw)
     import ctypes
     from . import _lib
     _lib.check(_lib.load(True).tb_sla_attention(ctypes.byref(args), ops.stream_ptr()), "tb_sla_attention")
@@ -322,10 +327,25 @@ def sla_attention(inputs: AttnInputs, cfg: SLAConfig | None = None):
         raise ValueError(f"block sizes {cfg.q_block}/{cfg.kv_block} exceed seq {s}")
     if select_topk_blocks is not _ORIG_SELECT:
         return _sla_with_mask(inputs, cfg)
+    if inputs.numpy_io and inputs.heads > 1 and inputs.q.nbytes >= _HOST_PIPELINE_BYTES:
+        # numpy in / numpy out at scale: per-head-chunk pipeline (staging copy,
+        # upload, attention, download overlapped); same kernels, same values
+        out = np.empty(inputs.q.shape, np.float32)
+        ops.sla_attention_host(torch.from_numpy(np.ascontiguousarray(inputs.q, np.float32)),
+                               torch.from_numpy(np.ascontiguousarray(inputs.k, np.float32)),
+                               torch.from_numpy(np.ascontiguousarray(inputs.v, np.float32)),
+                               cfg.q_block, cfg.kv_block, cfg.topk_ratio, cfg.linear_mix,
+                               cfg.quantized_sparse_branch, float(inputs.scale), out=torch.from_numpy(out),
+                               out_dtype=torch.float32)
+        torch.cuda.current_stream().synchronize()
+        return out
     q, k, v = _dev(inputs.q), _dev(inputs.k), _dev(inputs.v)
     out = ops.sla_attention(q, k, v, cfg.q_block, cfg.kv_block, cfg.topk_ratio, cfg.linear_mix,
                             cfg.quantized_sparse_branch, float(inputs.scale))
     return _ret(out, inputs.numpy_io)
+
+
+_HOST_PIPELINE_BYTES = 64 << 20
 
 
 def _sla_with_mask(inputs: AttnInputs, cfg: SLAConfig):

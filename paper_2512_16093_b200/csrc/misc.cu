@@ -4,9 +4,9 @@
 //   error/info plumbing of the C ABI.
 #include <cstdio>
 #include <mutex>
-#include <set>
+#include <map>
 #include <string>
-#include <tuple>
+#include <utility>
 
 #include "common.cuh"
 
@@ -25,18 +25,20 @@ int check_launch(const char *what) {
     return TB_OK;
 }
 
-// cudaFuncSetAttribute once per (device, kernel, bytes): the attribute is
-// sticky, so the launch path only pays a locked set lookup.
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) only when a launch needs
+// more than the kernel's current limit: the attribute is a sticky per-device
+// maximum, so once raised it covers every smaller launch and the launch path
+// pays a locked map lookup instead of a driver call.
 int ensure_smem(const void *fn, int bytes) {
     static std::mutex mu;
-    static std::set<std::tuple<int, const void *, int>> done;
+    static std::map<std::pair<int, const void *>, int> limit;
     int dev = 0;
     cudaGetDevice(&dev);
-    const auto key = std::make_tuple(dev, fn, bytes);
     std::lock_guard<std::mutex> g(mu);
-    if (done.count(key)) return 0;
+    int &cur = limit[std::make_pair(dev, fn)];
+    if (bytes <= cur) return 0;
     const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    if (e == cudaSuccess) done.insert(key);
+    if (e == cudaSuccess) cur = bytes;
     return (int)e;
 }
 
@@ -421,4 +423,31 @@ extern "C" int tb_axpy_rn(float *acc, const float *x, float c, int64_t n, void *
     const int64_t blocks = imin64(cdiv(cdiv(n, 4), 256), 148 * 8);
     axpy_rn_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(acc, x, c, n);
     return check_launch("axpy_rn");
+}
+
+// f32 -> bf16 (RN) copy: the bf16 V operand (tb_sla_args.vt) of the
+// tensor-core attention kernel when the inputs are f32 (the drop-in's numpy
+// path).  8 elements per thread, 16-B stores.
+__global__ void cast_bf16_kernel(const float *__restrict__ x, __nv_bfloat16 *__restrict__ y, int64_t n) {
+    const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 8;
+    if (i + 8 <= n) {
+        const float4 a = *reinterpret_cast<const float4 *>(x + i), b = *reinterpret_cast<const float4 *>(x + i + 4);
+        uint4 w;
+        __nv_bfloat162 *p = reinterpret_cast<__nv_bfloat162 *>(&w);
+        p[0] = __floats2bfloat162_rn(a.x, a.y);
+        p[1] = __floats2bfloat162_rn(a.z, a.w);
+        p[2] = __floats2bfloat162_rn(b.x, b.y);
+        p[3] = __floats2bfloat162_rn(b.z, b.w);
+        *reinterpret_cast<uint4 *>(y + i) = w;
+    } else {
+        for (int64_t j = i; j < n; j++) y[j] = __float2bfloat16_rn(x[j]);
+    }
+}
+
+extern "C" int tb_cast_bf16(const float *x, int64_t n, void *y, void *stream) {
+    TB_REQUIRE(((uintptr_t)x & 15) == 0 && ((uintptr_t)y & 15) == 0, "x and y must be 16-byte aligned");
+    if (n == 0) return TB_OK;
+    cast_bf16_kernel<<<(unsigned)cdiv(cdiv(n, 8), 256), 256, 0, as_stream(stream)>>>(
+        x, reinterpret_cast<__nv_bfloat16 *>(y), n);
+    return check_launch("cast_bf16");
 }

@@ -75,25 +75,34 @@ constexpr int THREADS = 224;   // 4 softmax + K producer + MMA + V producer warp
 constexpr uint32_t Q_BYTES = BM * D;          // int8
 constexpr uint32_t K_BYTES = BN * D;          // int8
 constexpr uint32_t V_BYTES = D * BN * 2;      // bf16 V tile: two 64-channel x 64-token SW128 boxes
-struct Smem {
+// Q2 (q_block 64): the 128-row tile holds two 64-row q-blocks.  Its linear
+// branch stages phi(Q) (32 KB) and both q-blocks' KV_sel^T (2 x 32 KB) in q..x
+// (96 KB contiguous), so the tail x extends the rings by 8 KB.
+constexpr uint32_t X_BYTES = 96 * 1024 - (Q_BYTES + 3 * V_BYTES + KSTAGES * K_BYTES);
+static_assert(KSTAGES != 3 || X_BYTES == 8192, "Q2 staging layout assumes 3 K stages");
+template <bool Q2>
+struct SmemT {
     uint8_t q[Q_BYTES];
     uint8_t v[VSTAGES][V_BYTES];
     uint8_t k[KSTAGES][K_BYTES];
+    uint8_t x[Q2 ? X_BYTES : 16];
     uint64_t q_full, o_final;
     uint64_t k_full[KSTAGES], k_empty[KSTAGES];
     uint64_t v_full[VSTAGES], v_empty[VSTAGES];
     uint64_t s_full[2], p_full[2], pv_done[2];
     uint64_t phiq_full, lin_full, lin_done;     // fused linear-branch epilogue
     uint64_t k1_full;                           // den row of KV_sel (sum phi(K_b) over the complement)
+    uint64_t lin_fix, lin_done2;                // Q2: per-half hand-off of the linear numerator
     alignas(128) uint16_t bias_a[128], bias_b[128];  // bias-MMA operands (2 core matrices each)
-    alignas(16) __nv_bfloat16 k1[128];
+    alignas(16) __nv_bfloat16 k1[Q2 ? 2 : 1][128];
     float corr_s[128], den_s[128];              // prologue: per-row q . k_mean and den_L
-    float c1[2048];                             // per selected block: sq * sk * scale * log2e
-    uint8_t rag[2048];                          // per selected block: ragged last kv block
+    float c1[Q2 ? 2 : 1][Q2 ? 1024 : 2048];     // per selected block (and q-half): sq * sk * scale * log2e
+    uint8_t rag[Q2 ? 1024 : 2048];              // per selected block: bit 2 ragged last kv block; Q2: bits 0/1 = q-halves
     uint32_t tmem_base;
 };
+template <bool Q2>
+constexpr int max_sel() { return Q2 ? 1024 : 2048; }
 constexpr int MAX_SEL = 2048;                  // selected kv blocks per q-block (c1 / ragged tables)
-constexpr size_t SMEM_BYTES = sizeof(Smem);
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float LN2 = 0.6931471805599453f;
 }  // namespace sla
@@ -213,19 +222,34 @@ __device__ __forceinline__ void load8(const T *p, float *x) {
 // rebases when the max outgrows the reference by > 8, i.e. p <= 256).  O
 // accumulates sum p * v / sv; the fused linear numerator is brought to the
 // same scale by staging phi(Q) / sv, and the epilogue multiplies by sv.
-template <typename T, bool EXACT, bool F8 = false>
+//
+// Q2 (q_block 64, the reference default): the 128-row tile n holds q-blocks
+// 2n (rows 0-63, warps 0-1) and 2n+1 (rows 64-127, warps 2-3).  The kernel
+// walks the UNION of their top-k lists (tb_pair_union: ascending, entry =
+// block | mask << 28) and a warp whose q-block did not select a block stores
+// P = 0 for it, so each row attends exactly its own selection; Q scales, logit
+// slopes and the linear branch's KV_sel / den row are per q-block.
+template <typename T, bool EXACT, bool F8 = false, bool Q2 = false>
 __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
     const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_kv, tb_sla_args a, int nq,
     int nkv) {
     using namespace sla;
+    using Smem = SmemT<Q2>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     Smem &S = *reinterpret_cast<Smem *>(smem_raw);    // dynamic smem starts 1024-aligned (no static smem)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n = blockIdx.x, h = blockIdx.y;
-    const int count = (int)a.count;
+    const int count = (int)a.count;                 // per q-block (attention.py:279)
     const int L = (int)a.L;
-    const int32_t *sel = a.idx + ((int64_t)h * nq + n) * count;
+    const int ntile = gridDim.x;
+    // selected kv blocks this tile visits: the q-block's own list, or (Q2) the pair union
+    const int nsel = Q2 ? __ldg(a.pair_cnt + (int64_t)h * ntile + n) : count;
+    const int32_t *sel = Q2 ? a.pair_idx + ((int64_t)h * ntile + n) * a.pair_ld
+                            : a.idx + ((int64_t)h * nq + n) * count;
+    // q-block of each half of the tile (Q2: the second one may be past the sequence)
+    const int qb0 = Q2 ? 2 * n : n;
+    const int qb1 = Q2 ? (2 * n + 1 < nq ? 2 * n + 1 : 2 * n) : n;
 
 #ifdef TB_SLA_TRACE
     unsigned long long ph_t0 = clock64(), ph_g0 = gtimer(), ph_t1 = 0, ph_t2 = 0;
@@ -259,6 +283,8 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             ptx::mbar_init(&S.p_full[b], 128);
             ptx::mbar_init(&S.pv_done[b], 1);
         }
+        ptx::mbar_init(&S.lin_fix, 64);
+        ptx::mbar_init(&S.lin_done2, 1);
         ptx::mbar_init(&S.phiq_full, 128);
         ptx::mbar_init(&S.lin_full, 1);
         ptx::mbar_init(&S.lin_done, 1);
@@ -287,8 +313,11 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
     const bool fused = a.lin_kv != nullptr && a.linear_mix != 0.0f;
     const bool lf = fused && !EXACT && count < nkv;
     const bool fused_end = fused && !lf;
-    uint8_t *lin_a = S.v[0];
-    uint8_t *lin_b = S.v[2];
+    // linear-branch staging: phi(Q) (A, 32 KB) and KV_sel^T (B: 32 KB, Q2: both
+    // q-blocks' as one N=256 operand, 64 KB).  Q2 stages over q..x, so in lf
+    // mode its Q codes are loaded only once the linear MMA has released them.
+    uint8_t *lin_a = Q2 ? S.q : S.v[0];
+    uint8_t *lin_b = Q2 ? S.v[1] : S.v[2];
 
     if (warp == 4) {
         // ---------------------------------------------------- TMA producer (K)
@@ -297,25 +326,48 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
         // K and V have their own producer warps, so a K slot freed by QK(j-3)
         // is refilled at once instead of queueing behind the wait for the V
         // slot that PV(j-4) frees.
-        if (ptx::elect_one()) {
-            ptx::mbar_arrive_expect_tx(&S.q_full, Q_BYTES);
-            ptx::tma_load_3d(S.q, &tm_q, 0, n * BM, h, &S.q_full);
-            if (fused) {      // den row of KV_sel: 256 B
-                ptx::mbar_arrive_expect_tx(&S.k1_full, D * 2);
-                ptx::bulk_g2s(S.k1, reinterpret_cast<const __nv_bfloat16 *>(a.lin_kv) +
-                                        (((int64_t)h * nq + n) * a.lin_dx + D) * D, D * 2, &S.k1_full);
-            }
-            if (lf) {
-                const int row0 = (int)(((int64_t)h * nq + n) * a.lin_dx);
+        const int row0a = (int)(((int64_t)h * nq + qb0) * a.lin_dx);
+        const int row0b = (int)(((int64_t)h * nq + qb1) * a.lin_dx);
+        // KV_sel^T boxes (64 channels x 128 rows each): Q2 stacks q-block 2n+1's
+        // rows under 2n's in each K-half (one N=256 B operand, 32 KB per K-half)
+        auto load_lin = [&]() {
+            if constexpr (Q2) {
+                ptx::mbar_arrive_expect_tx(&S.lin_full, 4 * 16384);
+                ptx::tma_load_2d(lin_b, &tm_kv, 0, row0a, &S.lin_full);
+                ptx::tma_load_2d(lin_b + 16384, &tm_kv, 0, row0b, &S.lin_full);
+                ptx::tma_load_2d(lin_b + 32768, &tm_kv, 64, row0a, &S.lin_full);
+                ptx::tma_load_2d(lin_b + 49152, &tm_kv, 64, row0b, &S.lin_full);
+            } else {
                 ptx::mbar_arrive_expect_tx(&S.lin_full, 2 * 16384);
-                ptx::tma_load_2d(lin_b, &tm_kv, 0, row0, &S.lin_full);
-                ptx::tma_load_2d(lin_b + 16384, &tm_kv, 64, row0, &S.lin_full);
+                ptx::tma_load_2d(lin_b, &tm_kv, 0, row0a, &S.lin_full);
+                ptx::tma_load_2d(lin_b + 16384, &tm_kv, 64, row0a, &S.lin_full);
             }
+        };
+        const bool q_late = Q2 && lf;                   // Q codes after the linear MMA (shared staging)
+        if (ptx::elect_one()) {
+            if (!q_late) {
+                ptx::mbar_arrive_expect_tx(&S.q_full, Q_BYTES);
+                ptx::tma_load_3d(S.q, &tm_q, 0, n * BM, h, &S.q_full);
+            }
+            if (fused) {      // den row of KV_sel: 256 B per q-block
+                const __nv_bfloat16 *kvb = reinterpret_cast<const __nv_bfloat16 *>(a.lin_kv);
+                ptx::mbar_arrive_expect_tx(&S.k1_full, (Q2 ? 2 : 1) * D * 2);
+                ptx::bulk_g2s(S.k1[0], kvb + ((int64_t)row0a + D) * D, D * 2, &S.k1_full);
+                if (Q2) ptx::bulk_g2s(S.k1[Q2 ? 1 : 0], kvb + ((int64_t)row0b + D) * D, D * 2, &S.k1_full);
+            }
+            if (lf) load_lin();
         }
         __syncwarp();
         if (lf) ptx::mbar_wait_sleep(&S.lin_done, 0);   // the linear MMA has released the rings
-        for (int j = 0; j < count; j++) {
-            const int b = __ldg(sel + j);
+        if (q_late) {
+            if (ptx::elect_one()) {
+                ptx::mbar_arrive_expect_tx(&S.q_full, Q_BYTES);
+                ptx::tma_load_3d(S.q, &tm_q, 0, n * BM, h, &S.q_full);
+            }
+            __syncwarp();
+        }
+        for (int j = 0; j < nsel; j++) {
+            const int b = __ldg(sel + j) & 0x0FFFFFFF;
             const int ks = j % KSTAGES;
             ptx::mbar_wait_sleep(&S.k_empty[ks], (uint32_t)(((j / KSTAGES) & 1) ^ 1));
             if (lane == 0) TB_TRACE(j, 10);
@@ -331,19 +383,14 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
         }
         if (fused_end) {
             ptx::mbar_wait_sleep(&S.o_final, 0);        // every MMA reading the rings is done
-            const int row0 = (int)(((int64_t)h * nq + n) * a.lin_dx);
-            if (ptx::elect_one()) {
-                ptx::mbar_arrive_expect_tx(&S.lin_full, 2 * 16384);
-                ptx::tma_load_2d(lin_b, &tm_kv, 0, row0, &S.lin_full);
-                ptx::tma_load_2d(lin_b + 16384, &tm_kv, 64, row0, &S.lin_full);
-            }
+            if (ptx::elect_one()) load_lin();
             __syncwarp();
         }
     } else if (warp == 6) {
         // ---------------------------------------------------- TMA producer (V)
         if (lf) ptx::mbar_wait_sleep(&S.lin_done, 0);
-        for (int j = 0; j < count; j++) {
-            const int b = __ldg(sel + j);
+        for (int j = 0; j < nsel; j++) {
+            const int b = __ldg(sel + j) & 0x0FFFFFFF;
             const int vs = j % VSTAGES;
             ptx::mbar_wait_sleep(&S.v_empty[vs], (uint32_t)(((j / VSTAGES) & 1) ^ 1));
             if (lane == 0) TB_TRACE(j, 11);
@@ -375,24 +422,42 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
         // no-swizzle K-major 8x16 bf16 tiles; SBO = 0 makes every 8-row group alias the same rows
         const uint64_t bias_a = ptx::sdesc_noswz_alias(ptx::smem_u32(S.bias_a));
         const uint64_t bias_b = ptx::sdesc_noswz_alias(ptx::smem_u32(S.bias_b));
-        auto lin_mma = [&](uint32_t dst) {
-            // numL = phi(Q) . KV_sel  (M128 N128 K128, bf16)
-            MMA_WAIT(&S.phiq_full, 0);
-            MMA_WAIT(&S.lin_full, 0);
-            ptx::tc_fence_after();
+        // numL = phi(Q) . KV_sel (bf16, K = 128).  B rows: KV_sel^T of one q-block
+        // (N = 128, K-half stride 16 KB), or Q2 both stacked (N = 256, K-half
+        // stride 32 KB; brow = 128 selects q-block 2n+1's rows alone)
+        auto lin_mma = [&](uint32_t dst, int nn, int brow, uint64_t *done) {
+            const uint32_t bstride = Q2 ? 32768 : 16384;
+            const uint32_t id = ptx::idesc_bf16(BM, nn);
             if (ptx::elect_one()) {
 #pragma unroll
                 for (int ks = 0; ks < D / 16; ks++) {
                     const int sub = ks >> 2, w = ks & 3;
                     const uint64_t ad = ptx::sdesc_sw128(ptx::smem_u32(lin_a + sub * 16384)) + 2 * w;
-                    const uint64_t bd = ptx::sdesc_sw128(ptx::smem_u32(lin_b + sub * 16384)) + 2 * w;
-                    ptx::mma_f16(dst, ad, bd, ID_PV, ks > 0 ? 1u : 0u);
+                    const uint64_t bd = ptx::sdesc_sw128(ptx::smem_u32(lin_b + sub * bstride + brow * 128)) + 2 * w;
+                    ptx::mma_f16(dst, ad, bd, id, ks > 0 ? 1u : 0u);
                 }
-                ptx::mma_commit(&S.lin_done);
+                ptx::mma_commit(done);
             }
             __syncwarp();
         };
-        if (lf) lin_mma(TM_O);                          // O starts as numL
+        auto lin_wait = [&]() {
+            MMA_WAIT(&S.phiq_full, 0);
+            MMA_WAIT(&S.lin_full, 0);
+            ptx::tc_fence_after();
+        };
+        if (lf) {
+            lin_wait();
+            if constexpr (Q2) {
+                // one N=256 MMA: cols 0-127 = phi(Q) . KV_sel[2n], cols 128-255 (= O) =
+                // phi(Q) . KV_sel[2n+1]; warps 0-1 then move their rows' first half into
+                // O (lin_fix) before QK(0) may overwrite columns 0-63
+                lin_mma(tmem, 2 * D, 0, &S.lin_done);
+                MMA_WAIT(&S.lin_fix, 0);
+                ptx::tc_fence_after();
+            } else {
+                lin_mma(TM_O, D, 0, &S.lin_done);       // O starts as numL
+            }
+        }
         MMA_WAIT(&S.q_full, 0);
         auto pv = [&](int i) {
             const int pb = i & 1, vs = i % VSTAGES;
@@ -450,17 +515,27 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
         };
         // QK(j+1) is queued before PV(j) waits for softmax(j): the tensor
         // pipe computes the next scores while the softmax warps work
-        qk(0);
-        for (int j = 0; j < count; j++) {
-            if (j + 1 < count) qk(j + 1);
+        if (nsel > 0) qk(0);
+        for (int j = 0; j < nsel; j++) {
+            if (j + 1 < nsel) qk(j + 1);
             pv(j);
         }
         if (ptx::elect_one()) ptx::mma_commit(&S.o_final);
         __syncwarp();
-        if (fused_end) lin_mma(tmem);                  // into the free S/P columns 0..127
+        if (fused_end) {                               // into the free S/P columns 0..127
+            lin_wait();
+            lin_mma(tmem, D, 0, &S.lin_done);
+            if constexpr (Q2) {
+                // q-block 2n+1's numerator once warps 0-1 have read 2n's (lin_fix)
+                MMA_WAIT(&S.lin_fix, 0);
+                ptx::tc_fence_after();
+                lin_mma(tmem, D, 128, &S.lin_done2);
+            }
+        }
     } else {
         // ------------------------------------------------ softmax + epilogue
         const int r = warp * 32 + lane;             // row in tile == TMEM lane
+        const int qh = Q2 ? (warp >> 1) : 0;        // Q2: q-block 2n + qh (warp-uniform)
         const int row = n * BM + r;                 // token index
         const bool row_ok = row < L;
         const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
@@ -476,7 +551,7 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             if (threadIdx.x == 0) TB_TRACE_X(70, 2);
             ptx::mbar_wait_sleep(&S.k1_full, 0);
             if (threadIdx.x == 0) TB_TRACE_X(70, 3);
-            const __nv_bfloat16 *k1 = S.k1;
+            const __nv_bfloat16 *k1 = S.k1[qh];
             float dl = 0.0f;
 #pragma unroll
             for (int kc = 0; kc < D / 8; kc++) {
@@ -544,7 +619,7 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             }
             if (lf) {
                 ptx::mbar_wait_sleep(&S.k1_full, 0);
-                const uint4 kw = *reinterpret_cast<const uint4 *>(S.k1 + cl * 8);
+                const uint4 kw = *reinterpret_cast<const uint4 *>(S.k1[qh] + cl * 8);
                 const __nv_bfloat162 *k2 = reinterpret_cast<const __nv_bfloat162 *>(&kw);
 #pragma unroll
                 for (int i = 0; i < 4; i++) { const float2 f = __bfloat1622float2(k2[i]); kk[2 * i] = f.x; kk[2 * i + 1] = f.y; }
@@ -596,7 +671,8 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             }
         }
         if (threadIdx.x == 0) TB_TRACE_X(70, 6);
-        const float sq = __ldg(a.q_scales + (int64_t)h * nq + n);
+        const float sq0 = __ldg(a.q_scales + (int64_t)h * nq + qb0);
+        const float sq1 = Q2 ? __ldg(a.q_scales + (int64_t)h * nq + qb1) : sq0;
         const float *ksc = a.k_scales + (int64_t)h * nkv;
         const int last_blk = nkv - 1;
         const int last_ext = L - last_blk * BN;
@@ -612,13 +688,33 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
         // (row_max / den outputs requested) runs the exact path every block
         // and reports the true row max like _sparse_branch (attention.py:385-389).
         // per selected block: logit slope and ragged flag (smem, read once per block)
-        for (int j = r; j < count; j += BM) {
-            const int b = __ldg(sel + j);
-            S.c1[j] = sq * __ldg(ksc + b) * scale2;
-            S.rag[j] = (b == last_blk) && last_ext < BN;
+        for (int j = r; j < nsel; j += BM) {
+            const int e = __ldg(sel + j);
+            const int b = e & 0x0FFFFFFF;
+            const float skb = __ldg(ksc + b);
+            S.c1[0][j] = sq0 * skb * scale2;
+            if (Q2) S.c1[Q2 ? 1 : 0][j] = sq1 * skb * scale2;
+            S.rag[j] = (uint8_t)((((b == last_blk) && last_ext < BN) ? 4 : 0) | (Q2 ? (e >> 28) & 3 : 3));
         }
         if (threadIdx.x == 0) TB_TRACE_X(70, 7);
         ptx::named_bar_sync(1, BM);
+        if (Q2 && lf && qh == 0) {
+            // the N=256 linear MMA left q-block 2n's numerator in columns 0-127:
+            // rows 0-63 move it into O (2n+1's is already there), then QK(0) may
+            // overwrite those columns
+            ptx::mbar_wait_sleep(&S.lin_done, 0);
+            ptx::tc_fence_after();
+#pragma unroll 1
+            for (int c = 0; c < D; c += 16) {
+                uint32_t o[16];
+                ptx::tmem_ld16(tmem + lane_base + c, o);
+                ptx::tmem_wait_ld();
+                ptx::tmem_st16(TM_O + lane_base + c, o);
+            }
+            ptx::tmem_wait_st();
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&S.lin_fix);
+        }
         TB_PH(ph_t1 = clock64());
         if (threadIdx.x == 0) TB_TRACE_X(70, 8);
         const float c0 = (row_ok ? S.corr_s[r] : 0.0f) * scale2;
@@ -629,9 +725,25 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
         // all underflow is caught by the l + psum > 0 test and rebased down.)
         float m_ref = lf ? __log2f(a.linear_mix) : -INFINITY, m_true = -INFINITY;
         float l = lf ? den_l : 0.0f;
-        for (int j = 0; j < count; j++) {
+        for (int j = 0; j < nsel; j++) {
             const int sb = j & 1;
-            const float c1 = S.c1[j];
+            const uint32_t flags = S.rag[j];
+            if (Q2 && !((flags >> qh) & 1u)) {
+                // block selected only by the other q-block of the tile: P = 0 for these
+                // rows (stored once QK(j) has written S_j, which P_j overwrites)
+                SM_WAIT(&S.s_full[sb], (uint32_t)((j >> 1) & 1));
+                ptx::tc_fence_after();
+                uint32_t z[16];
+#pragma unroll
+                for (int i = 0; i < 16; i++) z[i] = 0u;
+                ptx::tmem_st16(tmem + lane_base + sb * BN, z);
+                if (!F8) ptx::tmem_st16(tmem + lane_base + sb * BN + 16, z);
+                ptx::tmem_wait_st();
+                ptx::tc_fence_before();
+                ptx::mbar_arrive(&S.p_full[sb]);
+                continue;
+            }
+            const float c1 = S.c1[qh][j];
             // s32 scores as the floats M + s (M = 1.5*2^23, exact): fold -M*c1 into the offset
             const float c0m = fmaf(-12582912.0f, c1, c0);
             if (threadIdx.x == 0) TB_TRACE(j, 0);
@@ -646,7 +758,7 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             };
             load_s();
             if (threadIdx.x == 0) TB_TRACE(j, 4);
-            const bool ragged = S.rag[j] != 0;                        // uniform per CTA
+            const bool ragged = (flags & 4u) != 0;                    // uniform per CTA
             const int lim = ragged ? last_ext : BN;
             // scores as floats M + s (exact, |s| < 2^22), monotone in s
             auto xm = [&](int i) {
@@ -794,7 +906,9 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
         if (fused_end) {
             den_fused = stage_phi(nullptr);
             if (threadIdx.x == 0) TB_TRACE_X(71, 2);
-            ptx::mbar_wait_sleep(&S.lin_done, 0);
+            // Q2: rows 64-127 read q-block 2n+1's numerator, written into the same
+            // columns after rows 0-63 are done with 2n's (lin_fix below)
+            ptx::mbar_wait_sleep((Q2 && qh == 1) ? &S.lin_done2 : &S.lin_done, 0);
             ptx::tc_fence_after();
             if (threadIdx.x == 0) TB_TRACE_X(71, 3);
         }
@@ -920,6 +1034,10 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
                 }
             }
         }
+        if (Q2 && fused_end && qh == 0) {            // done reading columns 0-127: q-block 2n+1's turn
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&S.lin_fix);
+        }
     }
     if (threadIdx.x == 0) TB_TRACE_X(71, 4);
     TB_PH(if (threadIdx.x == 0) tb_phase_done(ph_t0, ph_g0, ph_t1, ph_t2));
@@ -931,7 +1049,12 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
 int sla_simt(const tb_sla_args *a, cudaStream_t st);
 
 bool sla_tc_supported(const tb_sla_args *a) {
-    return a->quantized && a->d == 128 && a->q_block == 128 && a->kv_block == 64 &&
+    const int64_t nkv = cdiv(a->L, 64);
+    // q_block 64: union lists from tb_pair_union, at most max_sel<true>() per tile
+    const bool q2 = a->q_block == 64 && a->pair_idx != nullptr && a->pair_cnt != nullptr &&
+                    a->pair_ld >= 2 * a->count &&
+                    imin64(2 * a->count, nkv) <= sla::max_sel<true>();
+    return a->quantized && a->d == 128 && (a->q_block == 128 || q2) && a->kv_block == 64 &&
            (a->dtype == TB_BF16 || a->vt != nullptr) && a->L >= 128 &&
            (a->dtype == TB_BF16 || a->dtype == TB_F32) && a->count >= 1 && a->count <= sla::MAX_SEL &&
            (a->lin_kv == nullptr || a->lin_dx >= a->d + 1);
@@ -939,7 +1062,8 @@ bool sla_tc_supported(const tb_sla_args *a) {
 
 int sla_tc(const tb_sla_args *a, cudaStream_t st) {
     using namespace sla;
-    const int64_t nq = cdiv(a->L, BM), nkv = cdiv(a->L, BN);
+    const bool q2 = a->q_block == 64;
+    const int64_t nq = cdiv(a->L, a->q_block), nkv = cdiv(a->L, BN);
     CUtensorMap tq, tk, tv;
     bool ok = make_tmap_3d(&tq, a->q_codes, CU_TENSOR_MAP_DATA_TYPE_UINT8, D, a->L, a->H, D, a->L * D, D, BM, 1) &&
               make_tmap_3d(&tk, a->k_codes, CU_TENSOR_MAP_DATA_TYPE_UINT8, D, a->L, a->H, D, a->L * D, D, BN, 1) &&
@@ -953,20 +1077,32 @@ int sla_tc(const tb_sla_args *a, cudaStream_t st) {
     if (!ok) return fail(TB_ECUDA, "cuTensorMapEncodeTiled failed (sla)");
     // the exact-max variant only when the caller asks for the sparse-branch stats
     const bool exact = a->row_max != nullptr || a->den != nullptr;
-    dim3 grid((unsigned)nq, (unsigned)a->H);
-    auto launch = [&](auto kern) {
-        smem_attr(kern, (int)SMEM_BYTES);
-        kern<<<grid, THREADS, SMEM_BYTES, st>>>(tq, tk, tv, tkv, *a, (int)nq, (int)nkv);
+    dim3 grid((unsigned)cdiv(a->L, BM), (unsigned)a->H);
+    auto launch = [&](auto kern, size_t smem) {
+        smem_attr(kern, (int)smem);
+        kern<<<grid, THREADS, smem, st>>>(tq, tk, tv, tkv, *a, (int)nq, (int)nkv);
     };
-    if (a->v_fp8) {
-        if (exact) launch(sla_tc_kernel<__nv_bfloat16, true, true>);
-        else launch(sla_tc_kernel<__nv_bfloat16, false, true>);
+    constexpr size_t S1 = sizeof(SmemT<false>), S2 = sizeof(SmemT<true>);
+    if (q2) {
+        if (a->v_fp8) {
+            if (exact) launch(sla_tc_kernel<__nv_bfloat16, true, true, true>, S2);
+            else launch(sla_tc_kernel<__nv_bfloat16, false, true, true>, S2);
+        } else if (a->dtype == TB_BF16) {
+            if (exact) launch(sla_tc_kernel<__nv_bfloat16, true, false, true>, S2);
+            else launch(sla_tc_kernel<__nv_bfloat16, false, false, true>, S2);
+        } else {
+            if (exact) launch(sla_tc_kernel<float, true, false, true>, S2);
+            else launch(sla_tc_kernel<float, false, false, true>, S2);
+        }
+    } else if (a->v_fp8) {
+        if (exact) launch(sla_tc_kernel<__nv_bfloat16, true, true>, S1);
+        else launch(sla_tc_kernel<__nv_bfloat16, false, true>, S1);
     } else if (a->dtype == TB_BF16) {
-        if (exact) launch(sla_tc_kernel<__nv_bfloat16, true>);
-        else launch(sla_tc_kernel<__nv_bfloat16, false>);
+        if (exact) launch(sla_tc_kernel<__nv_bfloat16, true>, S1);
+        else launch(sla_tc_kernel<__nv_bfloat16, false>, S1);
     } else {
-        if (exact) launch(sla_tc_kernel<float, true>);
-        else launch(sla_tc_kernel<float, false>);
+        if (exact) launch(sla_tc_kernel<float, true>, S1);
+        else launch(sla_tc_kernel<float, false>, S1);
     }
     return check_launch("sla_tc");
 }
@@ -986,8 +1122,9 @@ extern "C" int tb_sla_attention(const tb_sla_args *a, void *stream) {
                "quantized branch needs codes, scales and k_mean");
     if (a->H == 0) return TB_OK;
     cudaStream_t st = as_stream(stream);
-    TB_REQUIRE(a->out_dtype != TB_I8 || ((a->out_scales != nullptr || a->out_peers != nullptr) && sla_tc_supported(a)),
-               "int8 output needs the tensor-core kernel and out_scales");
+    TB_REQUIRE(a->out_dtype != TB_I8 || ((a->out_scales != nullptr || a->out_peers != nullptr) && sla_tc_supported(a) &&
+                                         a->row_max == nullptr && a->den == nullptr),
+               "int8 output needs the tensor-core kernel and out_scales (and no row_max / den)");
     TB_REQUIRE(a->out_peers == nullptr ||
                    (a->out_dtype == TB_I8 && a->scale_peers != nullptr && a->peer_rows > 0 && a->peer_rows % 128 == 0 &&
                     a->head0 >= 0 && a->head0 + a->H <= a->out_heads),
@@ -998,6 +1135,11 @@ extern "C" int tb_sla_attention(const tb_sla_args *a, void *stream) {
     TB_REQUIRE(a->lin_kv == nullptr, "fused linear epilogue needs the tensor-core envelope");
     return sla_simt(a, st);
 }
+
+// Which kernel tb_sla_attention would run for these arguments: 1 = the
+// tcgen05 kernel, 0 = the CUDA-core kernel (tests assert the default
+// configurations land on the tensor cores).
+extern "C" int tb_sla_path(const tb_sla_args *a) { return (a != nullptr && sla_tc_supported(a)) ? 1 : 0; }
 
 #ifdef TB_SLA_TRACE
 extern "C" int tb_sla_trace_read(unsigned long long *host) {

@@ -371,3 +371,72 @@ extern "C" int tb_topk_blocks_cov(const float *qp, const float *kp, const float 
     return topk_launch(qp, kp, kpt, ldk, H, nq, nkv, d, count, idx, comp, nullptr, (__nv_bfloat16 *)cov, cov_ld,
                        as_stream(stream));
 }
+
+// ---------------------------------------------------------------------------
+// Pair union of the top-k lists (q_block 64 on the tensor-core attention
+// kernel, which runs 128-row tiles = two 64-row q-blocks).  For tile t the
+// ascending lists of q-blocks 2t and 2t+1 (attention.py:269-284 indices) are
+// merged into one ascending list of distinct kv blocks; entry = block |
+// (mask << 28), mask bit 0 = selected by q-block 2t, bit 1 = by 2t+1.  The
+// kernel visits each union block once and zeroes P for the rows whose q-block
+// did not select it, so every row still attends exactly its own top-k set.
+// One warp per (head, tile): merge-with-duplicates positions by binary
+// search (pos(a_i) = i + #{b < a_i}, pos(b_j) = j + #{a <= b_j}: equal values
+// land adjacent, A first), then a ballot compaction that folds each equal
+// pair into one entry with both bits.
+namespace tb {
+__global__ void __launch_bounds__(32) pair_union_kernel(const int32_t *__restrict__ idx, int nq, int count,
+                                                        int32_t *__restrict__ out, int32_t *__restrict__ cnt,
+                                                        int ld) {
+    extern __shared__ int32_t mrg[];             // 2 * count merged entries: (value << 2) | source bit
+    const int lane = threadIdx.x;
+    const int t = blockIdx.x, h = blockIdx.y, ntile = gridDim.x;
+    const int32_t *A = idx + ((int64_t)h * nq + 2 * t) * count;
+    const bool hasB = 2 * t + 1 < nq;
+    const int32_t *B = A + count;
+    const int nb = hasB ? count : 0;
+    for (int i = lane; i < count; i += 32) {
+        const int32_t a = A[i];
+        int lo = 0, hi = nb;                      // #{b < a}
+        while (lo < hi) { const int m = (lo + hi) >> 1; if (B[m] < a) lo = m + 1; else hi = m; }
+        mrg[i + lo] = (a << 2) | 1;
+    }
+    for (int j = lane; j < nb; j += 32) {
+        const int32_t b = B[j];
+        int lo = 0, hi = count;                   // #{a <= b}
+        while (lo < hi) { const int m = (lo + hi) >> 1; if (A[m] <= b) lo = m + 1; else hi = m; }
+        mrg[j + lo] = (b << 2) | 2;
+    }
+    __syncwarp();
+    const int n = count + nb;
+    int32_t *o = out + ((int64_t)h * ntile + t) * ld;
+    int taken = 0;
+    for (int base = 0; base < n; base += 32) {
+        const int m = base + lane;
+        int32_t e = 0;
+        bool keep = false;
+        if (m < n) {
+            e = mrg[m];
+            keep = m == 0 || (mrg[m - 1] >> 2) != (e >> 2);
+            if (keep && m + 1 < n && (mrg[m + 1] >> 2) == (e >> 2)) e |= mrg[m + 1] & 3;
+        }
+        const unsigned kb = __ballot_sync(0xffffffffu, keep);
+        if (keep) o[taken + __popc(kb & ((1u << lane) - 1u))] = (e >> 2) | ((e & 3) << 28);
+        taken += __popc(kb);
+    }
+    if (lane == 0) cnt[(int64_t)h * ntile + t] = taken;
+}
+}  // namespace tb
+
+extern "C" int tb_pair_union(const int32_t *idx, int64_t H, int64_t nq, int64_t count, int32_t *pair_idx,
+                             int32_t *pair_cnt, int64_t pair_ld, void *stream) {
+    TB_REQUIRE(count >= 1 && pair_ld >= 2 * count, "pair_ld must be >= 2 * count");
+    TB_REQUIRE(count <= 4096, "count > 4096 unsupported");
+    if (H == 0 || nq == 0) return TB_OK;
+    dim3 grid((unsigned)cdiv(nq, 2), (unsigned)H);
+    const size_t smem = (size_t)2 * count * 4;
+    smem_attr(pair_union_kernel, (int)smem);
+    pair_union_kernel<<<grid, 32, smem, as_stream(stream)>>>(idx, (int)nq, (int)count, pair_idx, pair_cnt,
+                                                              (int)pair_ld);
+    return check_launch("pair_union");
+}

@@ -260,6 +260,54 @@ def topk_blocks_cov(qp: torch.Tensor, kp: torch.Tensor, count: int, want_comp: b
     return idx, comp, cov
 
 
+def pair_union(idx: torch.Tensor):
+    """tb_pair_union: union of the top-k lists of q-block pairs (2t, 2t+1) for
+    the q_block 64 tensor-core kernel -> (pair_idx int32 [H, ceil(nq/2),
+    2*count], entries block | mask << 28; pair_cnt int32 [H, ceil(nq/2)])."""
+    H, nq, count = idx.shape
+    nt = cdiv(nq, 2)
+    pidx = _empty((H, nt, 2 * count), torch.int32, idx)
+    pcnt = _empty((H, nt), torch.int32, idx)
+    call("tb_pair_union", ptr(idx), H, nq, count, ptr(pidx), ptr(pcnt), 2 * count, stream_ptr())
+    return pidx, pcnt
+
+
+def cast_bf16(x: torch.Tensor) -> torch.Tensor:
+    """tb_cast_bf16: f32 -> bf16 (RN), same shape."""
+    x = x.contiguous()
+    y = torch.empty(x.shape, dtype=torch.bfloat16, device=x.device)
+    call("tb_cast_bf16", ptr(x), x.numel(), ptr(y), stream_ptr())
+    return y
+
+
+def attention_operands(q: torch.Tensor, v: torch.Tensor, idx: torch.Tensor, q_block: int, kv_block: int,
+                       quantized: bool) -> dict:
+    """The extra tb_sla_args a direct tb_sla_attention call needs for the
+    tensor-core kernel to serve it: the bf16 V copy when the inputs are f32,
+    and the pair-union lists for q_block 64.  Returns sla_args keywords (vt,
+    pair_*); an empty dict keeps the call on the CUDA-core kernel.  The
+    pointers are taken last (ptr() keeps each tensor alive until the next C
+    call returns, so no call may run between them and tb_sla_attention)."""
+    H, L, d = q.shape
+    count = idx.shape[2]
+    if not tc_envelope(H, L, d, q_block, kv_block, count, quantized):
+        return {}
+    vt = cast_bf16(v) if q.dtype == torch.float32 else None
+    pidx = pcnt = None
+    if q_block == 64:
+        pidx, pcnt = pair_union(idx)
+    return dict(vt=ptr(vt), pair_idx=ptr(pidx), pair_cnt=ptr(pcnt), pair_ld=0 if pidx is None else pidx.shape[2])
+
+
+def tc_envelope(H: int, L: int, d: int, q_block: int, kv_block: int, count: int, quantized: bool = True) -> bool:
+    """Shapes the tcgen05 attention kernel serves (csrc/sla_tc.cu
+    sla_tc_supported): head_dim 128, kv_block 64, q_block 128, or q_block 64
+    (the reference default) with at most 1024 union blocks per 128-row tile."""
+    nkv = cdiv(L, kv_block)
+    return (quantized and d == 128 and kv_block == 64 and L >= 128 and 1 <= count <= 2048 and
+            (q_block == 128 or (q_block == 64 and min(2 * count, nkv) <= 1024)))
+
+
 def transpose_v(v: torch.Tensor, l_pad: int) -> torch.Tensor:
     v = _dev_tensor(v, "v")
     H, L, d = v.shape
@@ -394,6 +442,8 @@ def linear_branch(q, k, v, comp: torch.Tensor | None, q_block: int, kv_block: in
 
 
 _SIDE = {}
+# kernel the last ops.sla_attention call ran ("tcgen05" / "cuda_core"; tests)
+LAST_SLA_PATH = None
 
 
 def _km_event(side: torch.cuda.Stream) -> torch.cuda.Event:
@@ -450,7 +500,7 @@ def sla_attention(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: fl
     count = topk_count(topk_ratio, nkv)
     parts = {}
     lin = count < nkv and linear_mix != 0.0
-    tc = quantized and d == 128 and q_block == 128 and kv_block == 64 and L >= 128
+    tc = tc_envelope(H, L, d, q_block, kv_block, count, quantized)
     l_pad = nkv * 64
     main = torch.cuda.current_stream()
     # bf16 tensor-core path with the linear branch: the pool pass also emits
@@ -469,7 +519,7 @@ def sla_attention(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: fl
     kv_part = lin_pack = lin_kv = cov = None
     v8 = v8s = None
     if pv_fp8 and not (tc and q.dtype == torch.bfloat16):
-        raise ValueError("FP8 P/V needs bf16 inputs on the tensor-core path (d=128, q_block=128, kv_block=64)")
+        raise ValueError("FP8 P/V needs bf16 inputs on the tensor-core path (d=128, q_block 128 or 64, kv_block=64)")
     if fast_lin:
         # Three streams.  The top-k selection needs only the pooled raw K
         # (attention.py:404-406), so the main stream runs Q pass -> K pooling ->
@@ -526,6 +576,9 @@ def sla_attention(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: fl
                 lin_pack = linear_branch(q, k, v, comp, q_block, kv_block, fast=fast)
     if pv_fp8 and v8 is None:
         v8, v8s = quant_v_fp8(v)
+    pidx = pcnt = None
+    if tc and q_block == 64:
+        pidx, pcnt = pair_union(idx)
     q8 = out_dtype == torch.int8
     if q8 and not (tc and not return_parts):
         raise ValueError("int8 output (quantized out-projection operand) needs the tensor-core path")
@@ -538,7 +591,7 @@ def sla_attention(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: fl
     else:
         out = (torch.empty((L, H * d), dtype=torch.int8, device=q.device) if q8
                else torch.empty((H, L, d), dtype=out_dtype, device=q.device))
-        out_scales = torch.empty((nq, H), dtype=torch.float32, device=q.device) if q8 else None
+        out_scales = torch.empty((cdiv(L, 128), H), dtype=torch.float32, device=q.device) if q8 else None
     row_max = torch.empty((H, L), dtype=torch.float32, device=q.device) if return_parts else None
     den = torch.empty((H, L), dtype=torch.float32, device=q.device) if return_parts else None
     args = sla_args(q=ptr(q), k=ptr(k), v=ptr(v), dtype=dtype_code(q), H=H, L=L, d=d, q_block=q_block,
@@ -551,11 +604,14 @@ def sla_attention(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: fl
                     lin_kv=ptr(lin_kv), lin_dx=0 if lin_kv is None else lin_kv.shape[2], out=ptr(out),
                     out_dtype=TB_I8 if q8 else (TB_BF16 if out_dtype == torch.bfloat16 else TB_F32),
                     row_max=ptr(row_max), den=ptr(den), out_scales=ptr(out_scales),
-                    v_fp8=ptr(v8), v_scales=ptr(v8s))
+                    v_fp8=ptr(v8), v_scales=ptr(v8s), pair_idx=ptr(pidx), pair_cnt=ptr(pcnt),
+                    pair_ld=0 if pidx is None else pidx.shape[2])
     if peer_out is not None:
         args.out_peers, args.scale_peers = ptr(peer_out["codes"]), ptr(peer_out["scales"])
         args.peer_rows, args.head0, args.out_heads = int(peer_out["rows"]), int(peer_out["head0"]), int(peer_out["heads"])
     lib = _lib.load(require_device=True)
+    global LAST_SLA_PATH
+    LAST_SLA_PATH = "tcgen05" if lib.tb_sla_path(__import__("ctypes").byref(args)) == 1 else "cuda_core"
     _lib.check(lib.tb_sla_attention(__import__("ctypes").byref(args), stream_ptr()), "tb_sla_attention")
     if return_parts:
         parts = dict(qp=qp, kp=kp, idx=idx, comp=comp, q_codes=qc, q_scales=qs, k_codes=kc, k_scales=ks,
@@ -581,19 +637,26 @@ def _aux_stream(name: str) -> torch.cuda.Stream:
 def sla_attention_host(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: float = 0.1,
                        linear_mix: float = 1.0, quantized: bool = True, scale: float | None = None,
                        out: torch.Tensor | None = None, out_dtype=torch.bfloat16, chunk_heads: int = 4):
-    """sla_attention on HOST tensors [H, L, d] (pinned for overlap): every
-    hot-path quantity is per head (attention.py:370), so the heads are
-    processed in chunks and the host->device copy of chunk i+1, the attention
-    of chunk i and the device->host copy of chunk i-1 run on three streams at
-    once.  Returns the (pinned) host output."""
+    """sla_attention on HOST tensors [H, L, d]: every hot-path quantity is
+    per head (attention.py:370), so the heads are processed in chunks and the
+    host->device copy of chunk i+1, the attention of chunk i and the
+    device->host copy of chunk i-1 run on three streams at once.
+
+    Pinned inputs / output are copied directly.  Pageable ones (numpy-backed,
+    what the drop-in receives) are staged through two pinned buffers per
+    tensor: the host copies chunk i+1 into its staging buffer while the GPU
+    works on chunk i, and copies chunk i-1's result out of the output staging
+    buffer once its device->host copy is done.  Returns ``out``."""
     if q.is_cuda or k.is_cuda or v.is_cuda:
         raise ValueError("sla_attention_host takes host tensors; use sla_attention for device tensors")
     if not (q.shape == k.shape == v.shape) or q.dim() != 3:
         raise ValueError(f"q/k/v must share shape [heads, seq, head_dim], got "
                          f"{tuple(q.shape)}, {tuple(k.shape)}, {tuple(v.shape)}")
     H, L, d = q.shape
+    pinned_in = q.is_pinned() and k.is_pinned() and v.is_pinned()
     if out is None:
         out = torch.empty((H, L, d), dtype=out_dtype, pin_memory=True)
+    pinned_out = out.is_pinned()
     dev = torch.device("cuda", torch.cuda.current_device())
     compute = torch.cuda.current_stream()
     h2d, d2h = _aux_stream("h2d"), _aux_stream("d2h")
@@ -601,17 +664,34 @@ def sla_attention_host(q, k, v, q_block: int = 64, kv_block: int = 64, topk_rati
     d2h.wait_stream(compute)
     ch = max(1, min(chunk_heads, H))
     bufs = [[torch.empty((ch, L, d), dtype=x.dtype, device=dev) for x in (q, k, v)] for _ in range(2)]
+    stage_in = None if pinned_in else \
+        [[torch.empty((ch, L, d), dtype=x.dtype, pin_memory=True) for x in (q, k, v)] for _ in range(2)]
+    stage_out = None if pinned_out else [torch.empty((ch, L, d), dtype=out.dtype, pin_memory=True) for _ in range(2)]
     ev_in = [torch.cuda.Event() for _ in range(2)]
     ev_done = [torch.cuda.Event() for _ in range(2)]
     ev_out = [torch.cuda.Event() for _ in range(2)]
+    pending = None                                       # (buffer, h0, h1) of a staged output not yet copied out
+
+    def finish(p):
+        b_, a_, z_ = p
+        ev_out[b_].synchronize()
+        out[a_:z_].copy_(stage_out[b_][:z_ - a_])
+
     for i, h0 in enumerate(range(0, H, ch)):
         h1 = min(H, h0 + ch)
         n, b = h1 - h0, i % 2
+        srcs = (q[h0:h1], k[h0:h1], v[h0:h1])
+        if stage_in is not None:
+            if i >= 2:
+                ev_in[b].synchronize()                   # chunk i-2's upload has left staging buffer b
+            for st_, src in zip(stage_in[b], srcs):
+                st_[:n].copy_(src)
+            srcs = tuple(st_[:n] for st_ in stage_in[b])
         if i >= 2:
-            h2d.wait_event(ev_done[b])                  # chunk i-2 has consumed buffer b
+            h2d.wait_event(ev_done[b])                  # chunk i-2 has consumed device buffer b
         with torch.cuda.stream(h2d):
-            for dst, src in zip(bufs[b], (q, k, v)):
-                dst[:n].copy_(src[h0:h1], non_blocking=True)
+            for dst, src in zip(bufs[b], srcs):
+                dst[:n].copy_(src, non_blocking=True)
             ev_in[b].record(h2d)
         compute.wait_event(ev_in[b])
         o = sla_attention(bufs[b][0][:n], bufs[b][1][:n], bufs[b][2][:n], q_block, kv_block, topk_ratio,
@@ -619,9 +699,14 @@ def sla_attention_host(q, k, v, q_block: int = 64, kv_block: int = 64, topk_rati
         ev_done[b].record(compute)
         d2h.wait_event(ev_done[b])
         with torch.cuda.stream(d2h):
-            out[h0:h1].copy_(o, non_blocking=True)
+            (out[h0:h1] if stage_out is None else stage_out[b][:n]).copy_(o, non_blocking=True)
             ev_out[b].record(d2h)
         o.record_stream(d2h)
+        if pending is not None:
+            finish(pending)                              # chunk i-1: its result is (being) copied out
+        pending = (b, h0, h1) if stage_out is not None else None
+    if pending is not None:
+        finish(pending)
     for bb in bufs:
         for t in bb:
             t.record_stream(compute)

@@ -182,3 +182,15 @@ def test_oracle_headline_outputs_match_reference(case):
         got = O.sla_attention(q, k, v, qb, kvb, ratio, mix)[:, rows]
         cos, _, rel1 = O.error_metrics(got, gold[f"{name}.mix{mix:g}.rows"])
         assert cos >= 0.999999 and rel1 <= 1e-5, (name, mix, cos, rel1)
+
+
+def test_w8a8_blas_order_equals_c_restatement():
+    """oracle.w8a8_blas (the reference's own numpy sgemm-per-k-block path, the
+    bench's configs[1] CPU baseline) equals the C restatement bit-for-bit,
+    ragged edges included."""
+    for (M, K, N, block) in ((300, 520, 260, 128), (257, 1536, 384, 128), (64, 96, 80, 32)):
+        x = gen.gaussian_matrix(M + K, M, K)
+        w = gen.gaussian_matrix(N + K, K, N, 1.0 / np.sqrt(K))
+        xq, xs = O.quantize_blockwise(x, block)
+        wq, ws = O.quantize_blockwise(w, block)
+        assert np.array_equal(O.w8a8_blas(xq, xs, wq, ws, block), O.w8a8(xq, xs, wq, ws, block))

@@ -55,8 +55,14 @@ __global__ void __launch_bounds__(128, 1) mma_peak_kernel(int iters) {
     __shared__ uint32_t taddr;
     __shared__ uint64_t bar;
     const int warp = threadIdx.x >> 5;
-    for (int i = threadIdx.x; i < (16384 + 32768) / 16; i += blockDim.x)
-        reinterpret_cast<uint4 *>(a)[i] = make_uint4(0, 0, 0, 0);
+    // random operand bits (a hash of the position): zero operands draw far
+    // less power and would overstate the sustained (power-capped) peak
+    for (int i = threadIdx.x; i < (16384 + 32768) / 4; i += blockDim.x) {
+        uint32_t x = (uint32_t)i * 2654435761u + blockIdx.x * 40503u;
+        x ^= x >> 15; x *= 2246822519u; x ^= x >> 13;
+        if (KIND != 0) x &= 0x3F3F3F3Fu;      // bf16 / e4m3: keep exponents moderate (no inf/NaN)
+        reinterpret_cast<uint32_t *>(a)[i] = x;
+    }
     ptx::fence_async_smem();
     if (threadIdx.x == 0) { ptx::mbar_init(&bar, 1); ptx::fence_barrier_init(); }
     if (warp == 0) {
