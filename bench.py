@@ -382,7 +382,8 @@ def time_graph(fn, reps=10):
 
 def bench_configs(tcp, cpu: bool):
     """configs[0] (cfg1) and configs[2] (cfg3) at the reference default block
-    sizes (64/64) and at q_block 128: device step time, executed-work TOPS,
+    sizes (64/64) and at q_block 128, and configs[3] (cfg4) at 64/64 (its
+    q_block 128 form is the headline): device step time, executed-work TOPS,
     and (rank 0) the oracle on one head of the same inputs with parity."""
     import numpy as np
     import torch
@@ -390,10 +391,11 @@ def bench_configs(tcp, cpu: bool):
     from oracle import oracle as O
     res = {}
     peak = mixed_peak(tcp["int8"][0], tcp["bf16"][0]) if tcp else None
-    for (name, H, L, seed) in (("cfg1", 2, 4096, 11), ("cfg3", 12, 32760, 12)):
+    for (name, H, L, seed, qbs) in (("cfg1", 2, 4096, 11, (64, 128)), ("cfg3", 12, 32760, 12, (64, 128)),
+                                    ("cfg4", 40, 75600, 13, (64,))):
         g = torch.Generator(device="cuda").manual_seed(seed)
         qkv = [torch.randn((H, L, D_), generator=g, device="cuda").to(torch.bfloat16) for _ in range(3)]
-        for qb in (64, 128):
+        for qb in qbs:
             ms, out, gr = time_graph(lambda: ops.sla_attention(qkv[0], qkv[1], qkv[2], qb, 64, RATIO, 1.0,
                                                                out_dtype=torch.bfloat16))
             ops_ = sparse_ops(H=H, L=L, qb=qb)
