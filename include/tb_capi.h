@@ -203,6 +203,18 @@ int tb_sla_attention(const tb_sla_args *a, void *stream);
  * ascending distinct kv blocks of both lists, entry = block | (mask << 28)
  * with mask bit 0 = selected by q-block 2t, bit 1 = by 2t+1; pair_cnt = the
  * entries per tile (count <= pair_cnt <= 2*count).  pair_ld >= 2*count. */
+/* linear_attention (attention.py:287-335) on CUDA cores, f32, for shapes
+ * outside the tensor-core envelope: kv_part_ws [H, nkv, d, d+1] = per kv
+ * block phi(K_b)^T [V_b | 1]; kv_sel_ws [H, nq, d, d+1] = its sum over the
+ * complement blocks of each q-block (comp uint8 [H, nq, nkv], 1 = block in
+ * the complement; NULL = every block, the unmasked form with nq = nkv = 1,
+ * q_block = kv_block = L); out [H, nq*q_block, dx_out] f32 = phi(q_row) .
+ * kv_sel (columns 0..d-1 numerator, column d denominator, the rest 0). */
+int tb_linear_branch_simt(const void *q, const void *k, const void *v, int dtype, int64_t H, int64_t L,
+                          int64_t d, const uint8_t *comp, int64_t nq, int64_t nkv, int64_t q_block,
+                          int64_t kv_block, float *kv_part_ws, float *kv_sel_ws, float *out, int64_t dx_out,
+                          void *stream);
+
 /* 1 when tb_sla_attention would run these arguments on the tcgen05 kernel,
  * 0 for the CUDA-core kernel. */
 int tb_sla_path(const tb_sla_args *a);

@@ -49,6 +49,7 @@ SIGNATURES = {
     "tb_pair_union": [_P, _I, _I, _I, _P, _P, _I, _P],
     "tb_cast_bf16": [_P, _I, _P, _P],
     "tb_sla_path": [_P],
+    "tb_linear_branch_simt": [_P, _P, _P, _i, _I, _I, _I, _P, _I, _I, _I, _I, _P, _P, _P, _I, _P],
     "tb_transpose_v": [_P, _i, _I, _I, _I, _I, _P, _P],
     "tb_quant_v_fp8": [_P, _i, _I, _I, _I, _P, _P, _P, _P],
     "tb_peer_alloc": [_I, _P],

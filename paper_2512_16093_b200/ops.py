@@ -388,57 +388,37 @@ def gemm_bf16_batched(a: torch.Tensor, b: torch.Tensor, K: int | None = None, ou
     return c
 
 
-def _phi_t(x, rows):
-    """phi on device for head dims outside the vectorised kernel (d % 8 != 0)."""
-    H, L, d = x.shape
-    out = torch.zeros((H, rows, d), dtype=torch.float32, device=x.device)
-    xf = x.float()
-    out[:, :L] = torch.where(xf >= 0, xf + 1.0, torch.exp(torch.clamp(xf, max=0.0)))
-    return out
-
-
 def linear_branch(q, k, v, comp: torch.Tensor | None, q_block: int, kv_block: int, fast: bool = False,
                   lvt: int = 0):
-    """linear_attention over the complement mask (attention.py:293-335).
+    """linear_attention over the complement mask (attention.py:293-335) on CUDA
+    cores (tb_linear_branch_simt), for shapes outside the tensor-core envelope
+    (which runs kv_part + the coverage GEMM + the attention kernel's fused
+    MMA instead).
 
     comp: uint8 [H, nq, nkv] (1 = block in the complement) or None for the
-    unmasked form.  One operand pass (tb_linear_operands: phi(Q), phi(K) and
-    V extended with a ones column, so the denominator rides along as column
-    d), then three batched GEMMs on cuBLAS: kv_part = phi(K_b)^T [V_b|1] per
-    kv block, kv_sel = cov . kv_part per q block, num = phi(Q_rows) . kv_sel
-    (f32 output).  bf16 operands with f32 accumulation when ``fast``, f32
-    otherwise.  Returns the packed f32 tensor [H, lq, dx] (columns 0..d-1 =
-    numerator, column d = denominator) with lq = nq*q_block (or L when comp is
-    None).
-    """
+    unmasked form.  Returns the packed f32 tensor [H, lq, dx] (columns
+    0..d-1 = numerator, column d = denominator) with lq = nq*q_block (or L
+    when comp is None).  ``fast`` / ``lvt`` are accepted for API stability
+    (the CUDA-core path is f32 only and needs no V^T)."""
+    q, k, v = _dev_tensor(q, "q"), _dev_tensor(k, "k"), _dev_tensor(v, "v")
+    if k.dtype != q.dtype or v.dtype != q.dtype:
+        k, v = k.to(q.dtype), v.to(q.dtype)
     H, L, d = q.shape
-    dt = torch.bfloat16 if fast else torch.float32
     dx = -(-(d + 1) // 16) * 16
     if comp is None:
         q_block = kv_block = L
         nq = nkv = 1
     else:
         nq, nkv = comp.shape[1], comp.shape[2]
-    lk, lq = nkv * kv_block, nq * q_block
-    vt = None
-    if d % 8 == 0:
-        phiq, phik, vext, vt = linear_operands(q, k, v, lq, lk, dx, dt, lvt=lvt)
-    else:
-        phiq, phik = _phi_t(q, lq).to(dt), _phi_t(k, lk).to(dt)
-        vext = torch.zeros((H, lk, dx), dtype=dt, device=q.device)
-        vext[:, :L, :d] = v.to(dt)
-        vext[:, :L, d] = 1.0
-    kv_part = torch.bmm(phik.view(H * nkv, kv_block, d).transpose(1, 2), vext.view(H * nkv, kv_block, dx))
-    if comp is None:
-        kv_sel = kv_part.view(H, d, dx)
-    else:
-        kv_sel = torch.bmm(comp.to(dt), kv_part.view(H, nkv, d * dx))           # [H, nq, d*dx]
-    out_dtype = torch.float32 if dt == torch.bfloat16 else None
-    num = torch.bmm(phiq.view(H * nq, q_block, d), kv_sel.reshape(H * nq, d, dx), out_dtype=out_dtype) \
-        if out_dtype else torch.bmm(phiq.view(H * nq, q_block, d), kv_sel.reshape(H * nq, d, dx))
+        comp = comp.to(torch.uint8).contiguous()
+    part = torch.empty((H, nkv, d, d + 1), dtype=torch.float32, device=q.device)
+    sel = torch.empty((H, nq, d, d + 1), dtype=torch.float32, device=q.device)
+    out = torch.empty((H, nq * q_block, dx), dtype=torch.float32, device=q.device)
+    call("tb_linear_branch_simt", ptr(q), ptr(k), ptr(v), dtype_code(q), H, L, d, ptr(comp), nq, nkv, q_block,
+         kv_block, ptr(part), ptr(sel), ptr(out), dx, stream_ptr())
     if lvt:
-        return num.view(H, lq, dx), vt
-    return num.view(H, lq, dx)
+        return out, None
+    return out
 
 
 _SIDE = {}
