@@ -86,3 +86,56 @@ def test_dit_block_two_ranks_equals_one_rank(tmp_path, p2p):
         p.join(timeout=60)
     for rank, same, err in res:
         assert same, (rank, err)
+
+
+STEPS = 3
+
+
+def _sample(world, rank):
+    """Full rCM sample (sampler.py:281-302) of a 2-layer toy DiT: the initial
+    state and every step's noise are the reference's (seed, step) streams
+    (sampler.py:116-123, drawn for the WHOLE sequence) and each rank keeps its
+    token shard, so the sharded sample must equal the one-rank sample."""
+    import numpy as np
+    from paper_2512_16093_b200 import dit, sampler, ulysses
+    layers = dit.random_layers(DIM, FFN, 2, seed=4)
+    lo, hi = ulysses.token_bounds(L, world, rank, dit.TOKEN_ALIGN)
+    sig = sampler.make_schedule(STEPS).sigmas.tolist()
+    eps = [torch.from_numpy(sampler.step_noise(11, i, (L, DIM))[lo:hi].copy()).cuda() for i in range(STEPS)]
+    out = dit.rcm_sample(layers, HEADS, SLA, eps[0], eps[1:], sig, L_global=L)
+    return out.cpu(), lo, hi
+
+
+def _sample_worker(rank, world, port, ref_path, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    try:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        dist.all_to_all_single = _staged_all_to_all
+        torch.cuda.set_device(0)
+        out, lo, hi = _sample(world, rank)
+        ref = torch.load(ref_path)
+        out_q.put((rank, torch.equal(out, ref[lo:hi]), (out - ref[lo:hi]).abs().max().item()))
+        dist.destroy_process_group()
+    except Exception as e:
+        out_q.put((rank, False, repr(e)))
+
+
+@pytest.mark.gpu
+def test_rcm_sample_two_ranks_equals_one_rank(tmp_path):
+    """the sampler is replicated, each rank's noise is its token
+    slice of the global (seed, step) stream -> bit-identical to one GPU."""
+    ref, _, _ = _sample(1, 0)
+    assert torch.isfinite(ref).all()
+    ref_path = str(tmp_path / "ref_sample.pt")
+    torch.save(ref, ref_path)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sample_worker, args=(r, 2, port, ref_path, q), daemon=True) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, same, err in res:
+        assert same, (rank, err)
