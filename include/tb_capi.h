@@ -215,6 +215,36 @@ int tb_linear_branch_simt(const void *q, const void *k, const void *v, int dtype
                           int64_t kv_block, float *kv_part_ws, float *kv_sel_ws, float *out, int64_t dx_out,
                           void *stream);
 
+/* ---------------------------------------------- Ulysses exchange (NCCL)
+ * (no reference function -- the reference is
+ * single-process).  Token shard x [L_p, H, d] (rank r owns
+ * tokens [r*per, min((r+1)*per, L)), per = tb_ulysses_shard(L, P, align))
+ * -> head shard out [H/P, L, d] (heads [r*H/P, (r+1)*H/P)), and back.
+ * Elements are esize bytes (bf16 2, int8 1, f32 4; d*esize % 16 == 0).
+ * send_ws / recv_ws: caller-allocated, tb_ulysses_workspace_bytes each,
+ * layout [P, per, H/P, d].  comm: the caller's ncclComm_t (one grouped
+ * ncclSend/ncclRecv per peer; NULL allowed when P == 1).  stages: TB_UL_PACK
+ * | TB_UL_EXCHANGE | TB_UL_UNPACK (TB_UL_ALL for the whole op; the pieces let a
+ * host run the exchange itself).  Stream-ordered. */
+#define TB_UL_PACK 1
+#define TB_UL_EXCHANGE 2
+#define TB_UL_UNPACK 4
+#define TB_UL_ALL 7
+int64_t tb_ulysses_shard(int64_t L, int64_t P, int64_t align);
+int64_t tb_ulysses_workspace_bytes(int64_t L, int64_t H, int64_t d, int64_t esize, int64_t P, int64_t align);
+int tb_ulysses_seq_to_heads(const void *x, int64_t L, int64_t H, int64_t d, int64_t esize, int64_t P,
+                            int64_t rank, int64_t align, void *send_ws, void *recv_ws, void *out,
+                            void *comm, int stages, void *stream);
+int tb_ulysses_heads_to_seq(const void *o, int64_t L, int64_t H, int64_t d, int64_t esize, int64_t P,
+                            int64_t rank, int64_t align, void *send_ws, void *recv_ws, void *out,
+                            void *comm, int stages, void *stream);
+/* NCCL communicator helpers for C-ABI hosts (libnccl.so.2 resolved at run
+ * time): a 128-byte ncclUniqueId made on one rank and shared by the host's
+ * own means, then one communicator per rank. */
+int tb_nccl_unique_id(void *id128);
+int tb_nccl_comm_init(void **comm, const void *id128, int64_t nranks, int64_t rank);
+int tb_nccl_comm_destroy(void *comm);
+
 /* 1 when tb_sla_attention would run these arguments on the tcgen05 kernel,
  * 0 for the CUDA-core kernel. */
 int tb_sla_path(const tb_sla_args *a);

@@ -49,6 +49,13 @@ SIGNATURES = {
     "tb_pair_union": [_P, _I, _I, _I, _P, _P, _I, _P],
     "tb_cast_bf16": [_P, _I, _P, _P],
     "tb_sla_path": [_P],
+    "tb_ulysses_shard": [_I, _I, _I],
+    "tb_ulysses_workspace_bytes": [_I, _I, _I, _I, _I, _I],
+    "tb_ulysses_seq_to_heads": [_P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _i, _P],
+    "tb_ulysses_heads_to_seq": [_P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _i, _P],
+    "tb_nccl_unique_id": [_P],
+    "tb_nccl_comm_init": [_P, _P, _I, _I],
+    "tb_nccl_comm_destroy": [_P],
     "tb_linear_branch_simt": [_P, _P, _P, _i, _I, _I, _I, _P, _I, _I, _I, _I, _P, _P, _P, _I, _P],
     "tb_transpose_v": [_P, _i, _I, _I, _I, _I, _P, _P],
     "tb_quant_v_fp8": [_P, _i, _I, _I, _I, _P, _P, _P, _P],
@@ -68,7 +75,8 @@ SIGNATURES = {
     "tb_layernorm": [_P, _P, _P, _I, _I, _f, _P, _P],
     "tb_gelu": [_P, _I, _P, _P],
 }
-_RESTYPES = {"tb_last_error": ctypes.c_char_p, "tb_build_info": ctypes.c_char_p}
+_RESTYPES = {"tb_last_error": ctypes.c_char_p, "tb_build_info": ctypes.c_char_p,
+             "tb_ulysses_shard": ctypes.c_int64, "tb_ulysses_workspace_bytes": ctypes.c_int64}
 
 
 class SlaArgs(ctypes.Structure):

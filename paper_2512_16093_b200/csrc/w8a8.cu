@@ -268,6 +268,11 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) w8a8_tc_kernel(
 #ifndef TB_W8_STG2
 #define TB_W8_STG2 1
 #endif
+// fast mode: 16-column chunks (bit c of the mask) seeded with the f32 bits of
+// 1.5*2^23 and converted on the FMA pipe; the rest converted by I2FP (ALU)
+#ifndef TB_W8_SEED
+#define TB_W8_SEED 0xAA
+#endif
 namespace gemm2 {
 constexpr int BM = 128, BN = 256, BK = 128, STAGES = 5;
 constexpr int EPI_WARPS = 8;
@@ -428,7 +433,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
 #pragma unroll
             for (int i = 0; i < 16; i++) { mbits[i] = 0x4B400000u; zero[i] = 0u; }
 #pragma unroll
-            for (int c = 0; c < CW / 16; c++) ptx::tmem_st16(taddr + c * 16, (c & 1) ? mbits : zero);
+            for (int c = 0; c < CW / 16; c++) ptx::tmem_st16(taddr + c * 16, ((TB_W8_SEED >> c) & 1) ? mbits : zero);
             ptx::tmem_wait_st();
         };
 #pragma unroll
@@ -484,7 +489,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
 #pragma unroll
                     for (int i = 0; i < G; i += 2) {
                         float2 x;
-                        if (!EXACT && (((g * G + i) >> 4) & 1)) {        // seeded chunk: M + seg
+                        if (!EXACT && ((TB_W8_SEED >> ((g * G + i) >> 4)) & 1)) {   // seeded chunk: M + seg
                             x = ptx::fadd2(make_float2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])),
                                            make_float2(-12582912.0f, -12582912.0f));
                         } else {

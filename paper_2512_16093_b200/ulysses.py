@@ -384,3 +384,90 @@ def ulysses_sla_attention_q8_p2p(q_shard, k_shard, v_shard, L: int, attn_peer_fn
         raise ValueError(f"heads {q_shard.shape[1]} not divisible by world size {P}")
     qh, kh, vh = seq_to_heads_qkv(q_shard, k_shard, v_shard, L, group, block)
     return attn_return_p2p(qh, kh, vh, L, attn_peer_fn, group, block)
+
+
+# ------------------------------------------------ C-ABI exchange (native)
+# The same two exchanges as entry points of libtb200.so (csrc/ulysses.cu:
+# tb_ulysses_seq_to_heads / tb_ulysses_heads_to_seq): pack,
+# grouped ncclSend/ncclRecv over a caller-provided communicator, unpack -- the
+# path a host that binds the C ABI (not torch.distributed) uses.  Identical
+# layout to _pack_seq / _unpack_heads above.
+
+TB_UL_PACK, TB_UL_EXCHANGE, TB_UL_UNPACK, TB_UL_ALL = 1, 2, 4, 7
+_ESIZE = {torch.bfloat16: 2, torch.float16: 2, torch.float32: 4, torch.int8: 1, torch.uint8: 1}
+
+
+def native_seq_to_heads(x: torch.Tensor, L: int, P: int, rank: int, align: int = 1, comm=None,
+                        stages: int = TB_UL_ALL, send=None, recv=None, out=None):
+    """tb_ulysses_seq_to_heads: token shard [L_p, H, d] -> head shard [H/P, L, d].
+    Returns (out, send, recv) (the workspaces are returned so a caller running
+    the exchange itself -- stages without TB_UL_EXCHANGE -- can fill recv)."""
+    from . import _lib
+    from .ops import ptr, stream_ptr
+    import ctypes
+    Lp, H, d = x.shape
+    lib = _lib.load(require_device=True)
+    per = lib.tb_ulysses_shard(L, P, align)
+    if send is None:
+        send = torch.empty((P, per, H // P, d), dtype=x.dtype, device=x.device)
+    if recv is None:
+        recv = torch.empty_like(send)
+    if out is None:
+        out = torch.empty((H // P, L, d), dtype=x.dtype, device=x.device)
+    _check(lib.tb_ulysses_seq_to_heads(ptr(x.contiguous()), L, H, d, _ESIZE[x.dtype], P, rank, align, ptr(send),
+                                       ptr(recv), ptr(out), ctypes.c_void_p(comm), stages, stream_ptr()),
+           "tb_ulysses_seq_to_heads")
+    return out, send, recv
+
+
+def native_heads_to_seq(o: torch.Tensor, L: int, P: int, rank: int, align: int = 1, comm=None,
+                        stages: int = TB_UL_ALL, send=None, recv=None, out=None):
+    """tb_ulysses_heads_to_seq: head shard [H/P, L, d] -> token shard [L_p, H, d]."""
+    from . import _lib
+    from .ops import ptr, stream_ptr
+    import ctypes
+    hp, _, d = o.shape
+    H = hp * P
+    lib = _lib.load(require_device=True)
+    per = lib.tb_ulysses_shard(L, P, align)
+    lo, hi = token_bounds(L, P, rank, align)
+    if send is None:
+        send = torch.empty((P, per, hp, d), dtype=o.dtype, device=o.device)
+    if recv is None:
+        recv = torch.empty_like(send)
+    if out is None:
+        out = torch.empty((hi - lo, H, d), dtype=o.dtype, device=o.device)
+    _check(lib.tb_ulysses_heads_to_seq(ptr(o.contiguous()), L, H, d, _ESIZE[o.dtype], P, rank, align, ptr(send),
+                                       ptr(recv), ptr(out), ctypes.c_void_p(comm), stages, stream_ptr()),
+           "tb_ulysses_heads_to_seq")
+    return out, send, recv
+
+
+class NcclComm:
+    """An NCCL communicator made through the C ABI (tb_nccl_unique_id /
+    tb_nccl_comm_init) for a torch.distributed group: rank 0's unique id is
+    broadcast with broadcast_object_list, every rank joins.  ``handle`` is
+    the raw ncclComm_t for native_seq_to_heads / native_heads_to_seq."""
+
+    def __init__(self, group=None):
+        import ctypes
+        from . import _lib
+        self.lib = _lib.load(require_device=True)
+        self.P, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        uid = ctypes.create_string_buffer(128)
+        if self.rank == 0:
+            _check(self.lib.tb_nccl_unique_id(uid), "tb_nccl_unique_id")
+        obj = [bytes(uid.raw)]
+        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        self._h = ctypes.c_void_p()
+        _check(self.lib.tb_nccl_comm_init(ctypes.byref(self._h), ctypes.create_string_buffer(obj[0], 128),
+                                          self.P, self.rank), "tb_nccl_comm_init")
+
+    @property
+    def handle(self) -> int:
+        return self._h.value
+
+    def close(self):
+        if self._h is not None and self._h.value:
+            _check(self.lib.tb_nccl_comm_destroy(self._h), "tb_nccl_comm_destroy")
+        self._h = None
