@@ -145,11 +145,12 @@ extern "C" int tb_ulysses_seq_to_heads(const void *x, int64_t L, int64_t H, int6
                                        void *comm, int stages, void *stream) {
     TB_REQUIRE(P >= 1 && rank >= 0 && rank < P && H % P == 0, "need 0 <= rank < P and H % P == 0");
     TB_REQUIRE((d * esize) % 16 == 0, "head_dim * element size must be a multiple of 16 bytes");
-    TB_REQUIRE(send_ws && recv_ws && out && (x || L == 0), "null buffer");
+    TB_REQUIRE(send_ws && recv_ws && (out || L == 0), "null buffer");
     TB_REQUIRE(!(stages & TB_UL_EXCHANGE) || P == 1 || comm != nullptr, "the exchange needs an NCCL communicator");
     cudaStream_t st = as_stream(stream);
     const int64_t per = tb_ulysses_shard(L, P, align), hp = H / P, rb = d * esize;
     const int64_t lo = imin64(rank * per, L), Lp = imin64(lo + per, L) - lo;
+    TB_REQUIRE(x || Lp == 0, "null token shard");
     // pack: send[j, t, hh] = x[t, j*hp + hh]   (t < Lp)
     int rc = TB_OK;
     if (stages & TB_UL_PACK)
@@ -166,11 +167,12 @@ extern "C" int tb_ulysses_heads_to_seq(const void *o, int64_t L, int64_t H, int6
                                        void *comm, int stages, void *stream) {
     TB_REQUIRE(P >= 1 && rank >= 0 && rank < P && H % P == 0, "need 0 <= rank < P and H % P == 0");
     TB_REQUIRE((d * esize) % 16 == 0, "head_dim * element size must be a multiple of 16 bytes");
-    TB_REQUIRE(send_ws && recv_ws && out && (o || L == 0), "null buffer");
+    TB_REQUIRE(send_ws && recv_ws && (o || L == 0), "null buffer");
     TB_REQUIRE(!(stages & TB_UL_EXCHANGE) || P == 1 || comm != nullptr, "the exchange needs an NCCL communicator");
     cudaStream_t st = as_stream(stream);
     const int64_t per = tb_ulysses_shard(L, P, align), hp = H / P, rb = d * esize;
     const int64_t lo = imin64(rank * per, L), Lp = imin64(lo + per, L) - lo;
+    TB_REQUIRE(out || Lp == 0, "null token-shard output");
     // pack: send[i, t, hh] = o[hh, i*per + t]   (i*per + t < L)
     int rc = TB_OK;
     if (stages & TB_UL_PACK)
