@@ -690,7 +690,8 @@ def main():
         hn = [t.float().cpu().numpy() for t in head_major]             # f32 numpy, as the reference takes
         cfg = SLAConfig(q_block=QB, kv_block=KVB, topk_ratio=RATIO, linear_mix=1.0)
         inp = AttnInputs(hn[0], hn[1], hn[2])
-        dropin_sla(inp, cfg)
+        for _ in range(2):              # the caching host allocator pins the result blocks once
+            dropin_sla(inp, cfg)
         torch.cuda.synchronize()
         times = []
         for _ in range(3):
@@ -699,9 +700,12 @@ def main():
             times.append(time.perf_counter() - t0)
         ems = statistics.median(times) * 1e3
         e2e = {"value": total_ops / (ems * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": ems,
-               "h2d_bytes_per_step": sum(x.nbytes for x in hn), "d2h_bytes_per_step": o_np.nbytes,
+               "h2d_bytes_per_step": hn[0].nbytes + hn[1].nbytes + hn[2].nbytes // 2, "d2h_bytes_per_step": o_np.nbytes,
                "api": "paper_2512_16093_b200.attention.sla_attention(AttnInputs(numpy f32), SLAConfig) -> numpy f32 "
-                      "(drop-in for turbobench.attention.sla_attention); host wall clock, median of 3"}
+                      "(drop-in for turbobench.attention.sla_attention); host wall clock, median of 3; per 4-head "
+                      "chunk: numpy->pinned staging (V rounded to bf16 on the host), H2D, attention, D2H straight "
+                      "into the page-locked result array",
+               "h2d_bytes_note": "q, k f32 + v bf16 cross PCIe (the kernels read V only as bf16)"}
         if out_head0 is not None:
             e2e["parity_vs_device_step_head0"] = parity(o_np[0:1], out_head0)
         del hn, inp, o_np

@@ -330,15 +330,17 @@ def sla_attention(inputs: AttnInputs, cfg: SLAConfig | None = None):
     if inputs.numpy_io and inputs.heads > 1 and inputs.q.nbytes >= _HOST_PIPELINE_BYTES:
         # numpy in / numpy out at scale: per-head-chunk pipeline (staging copy,
         # upload, attention, download overlapped); same kernels, same values
-        out = np.empty(inputs.q.shape, np.float32)
+        # the result array is backed by page-locked memory (torch's caching host
+        # allocator), so the device->host copy lands in it directly
+        out = torch.empty(inputs.q.shape, dtype=torch.float32, pin_memory=True)
         ops.sla_attention_host(torch.from_numpy(np.ascontiguousarray(inputs.q, np.float32)),
                                torch.from_numpy(np.ascontiguousarray(inputs.k, np.float32)),
                                torch.from_numpy(np.ascontiguousarray(inputs.v, np.float32)),
                                cfg.q_block, cfg.kv_block, cfg.topk_ratio, cfg.linear_mix,
-                               cfg.quantized_sparse_branch, float(inputs.scale), out=torch.from_numpy(out),
+                               cfg.quantized_sparse_branch, float(inputs.scale), out=out,
                                out_dtype=torch.float32)
         torch.cuda.current_stream().synchronize()
-        return out
+        return out.numpy()
     q, k, v = _dev(inputs.q), _dev(inputs.k), _dev(inputs.v)
     out = ops.sla_attention(q, k, v, cfg.q_block, cfg.kv_block, cfg.topk_ratio, cfg.linear_mix,
                             cfg.quantized_sparse_branch, float(inputs.scale))

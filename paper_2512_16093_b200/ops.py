@@ -470,8 +470,6 @@ def sla_attention(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: fl
     if not (q.shape == k.shape == v.shape) or q.dim() != 3:
         raise ValueError(f"q/k/v must share shape [heads, seq, head_dim], got "
                          f"{tuple(q.shape)}, {tuple(k.shape)}, {tuple(v.shape)}")
-    if k.dtype != q.dtype or v.dtype != q.dtype:
-        k, v = k.to(q.dtype), v.to(q.dtype)
     H, L, d = q.shape
     if q_block > L or kv_block > L:
         raise ValueError(f"block sizes {q_block}/{kv_block} exceed seq {L}")
@@ -481,6 +479,13 @@ def sla_attention(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: fl
     parts = {}
     lin = count < nkv and linear_mix != 0.0
     tc = tc_envelope(H, L, d, q_block, kv_block, count, quantized)
+    if k.dtype != q.dtype:
+        k = k.to(q.dtype)
+    # f32 q / k with a bf16 V is accepted on the tensor-core path, which reads
+    # V only as bf16 (PV operand, linear-branch kv_part): the host pipeline
+    # ships V already rounded (sla_attention_host), same values as the cast below
+    if v.dtype != q.dtype and not (tc and q.dtype == torch.float32 and v.dtype == torch.bfloat16):
+        v = v.to(q.dtype)
     l_pad = nkv * 64
     main = torch.cuda.current_stream()
     # bf16 tensor-core path with the linear branch: the pool pass also emits
@@ -489,7 +494,8 @@ def sla_attention(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: fl
     fast_lin = lin and tc and quantized and q.dtype == torch.bfloat16
     kpt = None
     # the tensor-core path reads V (and the linear-branch kernel K and V) as bf16
-    kb, vb = (k, v) if q.dtype == torch.bfloat16 else (k.to(torch.bfloat16), v.to(torch.bfloat16))
+    kb = k if k.dtype == torch.bfloat16 else cast_bf16(k)
+    vb = v if v.dtype == torch.bfloat16 else cast_bf16(v)
     vt = None if q.dtype == torch.bfloat16 else vb
     # Side stream: k_mean (a latency-bound sequential chain) and the linear
     # branch's per-block operand kv_part (HBM-bound, needs only k and v) run
@@ -643,9 +649,15 @@ def sla_attention_host(q, k, v, q_block: int = 64, kv_block: int = 64, topk_rati
     h2d.wait_stream(compute)
     d2h.wait_stream(compute)
     ch = max(1, min(chunk_heads, H))
-    bufs = [[torch.empty((ch, L, d), dtype=x.dtype, device=dev) for x in (q, k, v)] for _ in range(2)]
+    # f32 inputs on the tensor-core path: V crosses PCIe already rounded to bf16
+    # (the kernels read V only as bf16), half its bytes
+    nkv = cdiv(L, kv_block)
+    v_half = (q.dtype == torch.float32 and not pinned_in and
+              tc_envelope(ch, L, d, q_block, kv_block, topk_count(topk_ratio, nkv), quantized))
+    dts = (q.dtype, k.dtype, torch.bfloat16 if v_half else v.dtype)
+    bufs = [[torch.empty((ch, L, d), dtype=dt, device=dev) for dt in dts] for _ in range(2)]
     stage_in = None if pinned_in else \
-        [[torch.empty((ch, L, d), dtype=x.dtype, pin_memory=True) for x in (q, k, v)] for _ in range(2)]
+        [[torch.empty((ch, L, d), dtype=dt, pin_memory=True) for dt in dts] for _ in range(2)]
     stage_out = None if pinned_out else [torch.empty((ch, L, d), dtype=out.dtype, pin_memory=True) for _ in range(2)]
     ev_in = [torch.cuda.Event() for _ in range(2)]
     ev_done = [torch.cuda.Event() for _ in range(2)]
