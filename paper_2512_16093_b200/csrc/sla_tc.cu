@@ -96,12 +96,12 @@ struct SmemT {
     alignas(128) uint16_t bias_a[128], bias_b[128];  // bias-MMA operands (2 core matrices each)
     alignas(16) __nv_bfloat16 k1[Q2 ? 2 : 1][128];
     float corr_s[128], den_s[128];              // prologue: per-row q . k_mean and den_L
-    float c1[Q2 ? 2 : 1][Q2 ? 1024 : 2048];     // per selected block (and q-half): sq * sk * scale * log2e
-    uint8_t rag[Q2 ? 1024 : 2048];              // per selected block: bit 2 ragged last kv block; Q2: bits 0/1 = q-halves
+    float c1[2048];                             // per selected block: sq * sk * scale * log2e (Q2: sk * scale * log2e)
+    uint8_t rag[2048];                          // per selected block: bit 2 ragged last kv block; Q2: bits 0/1 = q-halves
     uint32_t tmem_base;
 };
 template <bool Q2>
-constexpr int max_sel() { return Q2 ? 1024 : 2048; }
+constexpr int max_sel() { return 2048; }
 constexpr int MAX_SEL = 2048;                  // selected kv blocks per q-block (c1 / ragged tables)
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float LN2 = 0.6931471805599453f;
@@ -692,8 +692,7 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             const int e = __ldg(sel + j);
             const int b = e & 0x0FFFFFFF;
             const float skb = __ldg(ksc + b);
-            S.c1[0][j] = sq0 * skb * scale2;
-            if (Q2) S.c1[Q2 ? 1 : 0][j] = sq1 * skb * scale2;
+            S.c1[j] = Q2 ? skb * scale2 : sq0 * skb * scale2;   // Q2: the q-half's sq is applied per warp
             S.rag[j] = (uint8_t)((((b == last_blk) && last_ext < BN) ? 4 : 0) | (Q2 ? (e >> 28) & 3 : 3));
         }
         if (threadIdx.x == 0) TB_TRACE_X(70, 7);
@@ -743,7 +742,7 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
                 ptx::mbar_arrive(&S.p_full[sb]);
                 continue;
             }
-            const float c1 = S.c1[qh][j];
+            const float c1 = Q2 ? (qh ? sq1 : sq0) * S.c1[j] : S.c1[j];
             // s32 scores as the floats M + s (M = 1.5*2^23, exact): fold -M*c1 into the offset
             const float c0m = fmaf(-12582912.0f, c1, c0);
             if (threadIdx.x == 0) TB_TRACE(j, 0);

@@ -302,10 +302,10 @@ def attention_operands(q: torch.Tensor, v: torch.Tensor, idx: torch.Tensor, q_bl
 def tc_envelope(H: int, L: int, d: int, q_block: int, kv_block: int, count: int, quantized: bool = True) -> bool:
     """Shapes the tcgen05 attention kernel serves (csrc/sla_tc.cu
     sla_tc_supported): head_dim 128, kv_block 64, q_block 128, or q_block 64
-    (the reference default) with at most 1024 union blocks per 128-row tile."""
+    (the reference default) with at most 2048 union blocks per 128-row tile."""
     nkv = cdiv(L, kv_block)
     return (quantized and d == 128 and kv_block == 64 and L >= 128 and 1 <= count <= 2048 and
-            (q_block == 128 or (q_block == 64 and min(2 * count, nkv) <= 1024)))
+            (q_block == 128 or (q_block == 64 and min(2 * count, nkv) <= 2048)))
 
 
 def transpose_v(v: torch.Tensor, l_pad: int) -> torch.Tensor:

@@ -151,3 +151,13 @@ def test_dropin_defaults_numpy(tb):
     got = sla_attention(AttnInputs(q, k, v), SLAConfig())
     want = O.sla_attention(q, k, v, 64, 64, 0.1, 1.0)
     check(got, want, "drop-in defaults")
+
+
+def test_q64_union_beyond_1024_blocks(tb):
+    """topk_ratio 1.0 at L = 66000 (nkv 1032): every tile walks all 1032 blocks
+    (the union table holds up to 2048 entries per tile)."""
+    q, k, v = gen.gaussian_qkv(37, 1, 66000, 128, bf16=True)
+    got = tb.sla_attention(dev(q, True), dev(k, True), dev(v, True), 64, 64, 1.0, 1.0)
+    assert tb.LAST_SLA_PATH == "tcgen05"
+    want = O.sla_attention(q, k, v, 64, 64, 1.0, 1.0)
+    check(got.cpu().numpy(), want, "q64 all blocks, L 66000")
