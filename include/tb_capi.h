@@ -253,6 +253,16 @@ int tb_sla_path(const tb_sla_args *a);
  * (tb_sla_args.vt) when the attention inputs are f32. */
 int tb_cast_bf16(const float *x, int64_t n, void *y, void *stream);
 
+/* HOST staging for host-array callers (replaces the implicit numpy -> f32
+ * conversion of AttnInputs, attention.py:38-60, on the upload side): copies n
+ * elements of src into dst (normally page-locked), src_dtype -> dst_dtype in
+ * {F32->F32, BF16->BF16, I8->I8, F32->BF16 (round to nearest even)}, on a
+ * persistent pool of nthreads host threads (<= 0: TB_HOST_THREADS or every
+ * hardware thread; fixed at the first call) with non-temporal stores.
+ * Synchronous; no device work. */
+int tb_host_stage(void *dst, const void *src, int64_t n, int src_dtype, int dst_dtype, int64_t nthreads);
+int64_t tb_host_threads(void);
+
 int tb_pair_union(const int32_t *idx, int64_t H, int64_t nq, int64_t count, int32_t *pair_idx,
                   int32_t *pair_cnt, int64_t pair_ld, void *stream);
 

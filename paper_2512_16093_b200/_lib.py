@@ -48,6 +48,8 @@ SIGNATURES = {
     "tb_sla_attention": [_P, _P],
     "tb_pair_union": [_P, _I, _I, _I, _P, _P, _I, _P],
     "tb_cast_bf16": [_P, _I, _P, _P],
+    "tb_host_stage": [_P, _P, _I, _i, _i, _I],
+    "tb_host_threads": [],
     "tb_sla_path": [_P],
     "tb_ulysses_shard": [_I, _I, _I],
     "tb_ulysses_workspace_bytes": [_I, _I, _I, _I, _I, _I],
@@ -76,7 +78,7 @@ SIGNATURES = {
     "tb_gelu": [_P, _I, _P, _P],
 }
 _RESTYPES = {"tb_last_error": ctypes.c_char_p, "tb_build_info": ctypes.c_char_p,
-             "tb_ulysses_shard": ctypes.c_int64, "tb_ulysses_workspace_bytes": ctypes.c_int64}
+             "tb_ulysses_shard": ctypes.c_int64, "tb_host_threads": ctypes.c_int64, "tb_ulysses_workspace_bytes": ctypes.c_int64}
 
 
 class SlaArgs(ctypes.Structure):

@@ -338,7 +338,7 @@ def sla_attention(inputs: AttnInputs, cfg: SLAConfig | None = None):
                                torch.from_numpy(np.ascontiguousarray(inputs.v, np.float32)),
                                cfg.q_block, cfg.kv_block, cfg.topk_ratio, cfg.linear_mix,
                                cfg.quantized_sparse_branch, float(inputs.scale), out=out,
-                               out_dtype=torch.float32)
+                               out_dtype=torch.float32, chunk_heads=_HOST_CHUNK_HEADS)
         torch.cuda.current_stream().synchronize()
         return out.numpy()
     q, k, v = _dev(inputs.q), _dev(inputs.k), _dev(inputs.v)
@@ -348,6 +348,7 @@ def sla_attention(inputs: AttnInputs, cfg: SLAConfig | None = None):
 
 
 _HOST_PIPELINE_BYTES = 64 << 20
+_HOST_CHUNK_HEADS = 2          # heads per upload / attention / download chunk
 
 
 def _sla_with_mask(inputs: AttnInputs, cfg: SLAConfig):

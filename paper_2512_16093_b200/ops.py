@@ -620,6 +620,21 @@ def _aux_stream(name: str) -> torch.cuda.Stream:
     return s
 
 
+_HOST_CODES = {torch.float32: TB_F32, torch.bfloat16: TB_BF16, torch.int8: TB_I8}
+
+
+def host_stage(dst: torch.Tensor, src: torch.Tensor) -> torch.Tensor:
+    """dst.copy_(src) for contiguous HOST tensors on the library's pool of
+    host threads with non-temporal stores (tb_host_stage); f32 -> bf16 rounds
+    to nearest even like torch's cast.  Other layouts / dtypes: torch's copy."""
+    sc, dc = _HOST_CODES.get(src.dtype), _HOST_CODES.get(dst.dtype)
+    if (src.is_cuda or dst.is_cuda or sc is None or dc is None or dst.shape != src.shape
+            or not (src.is_contiguous() and dst.is_contiguous()) or not (sc == dc or (sc, dc) == (TB_F32, TB_BF16))):
+        return dst.copy_(src)
+    call("tb_host_stage", dst.data_ptr(), src.data_ptr(), src.numel(), sc, dc, 0)
+    return dst
+
+
 def sla_attention_host(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: float = 0.1,
                        linear_mix: float = 1.0, quantized: bool = True, scale: float | None = None,
                        out: torch.Tensor | None = None, out_dtype=torch.bfloat16, chunk_heads: int = 4):
@@ -677,7 +692,7 @@ def sla_attention_host(q, k, v, q_block: int = 64, kv_block: int = 64, topk_rati
             if i >= 2:
                 ev_in[b].synchronize()                   # chunk i-2's upload has left staging buffer b
             for st_, src in zip(stage_in[b], srcs):
-                st_[:n].copy_(src)
+                host_stage(st_[:n], src)
             srcs = tuple(st_[:n] for st_ in stage_in[b])
         if i >= 2:
             h2d.wait_event(ev_done[b])                  # chunk i-2 has consumed device buffer b

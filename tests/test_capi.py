@@ -63,3 +63,34 @@ def test_sla_args_layout_matches_header():
     body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
     fields = re.findall(r"\*?\s*(\w+)\s*[,;]", body.split("{", 1)[1])
     assert [f[0] for f in _lib.SlaArgs._fields_] == fields
+
+
+def test_host_stage_copy_and_bf16_rounding():
+    """tb_host_stage (host staging of numpy inputs): bit copies, and f32 -> bf16
+    identical to torch's round-to-nearest-even cast incl. ties, inf, subnormals;
+    NaN stays NaN.  Host-only entry point (no device needed)."""
+    import numpy as np
+    import torch
+    from paper_2512_16093_b200 import _lib
+    lib = _lib.load()
+    rng = np.random.default_rng(0)
+    for n in (0, 1, 17, 1000003, (1 << 18) * 3 + 5):
+        x = (rng.standard_normal(n) * 3).astype(np.float32)
+        if n > 20:
+            x[:8] = [np.nan, np.inf, -np.inf, 0.0, -0.0, 1e-40, -1e-45, 3.4e38]
+            x[9] = np.float32(1.00390625)                      # exact bf16 tie
+            x[10] = np.float32(1.01171875)                     # tie, odd
+        y = np.empty(n, dtype=np.uint16)
+        assert lib.tb_host_stage(y.ctypes.data, x.ctypes.data, n, _lib.TB_F32, _lib.TB_BF16, 0) == 0
+        ref = torch.from_numpy(x).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+        nan = np.isnan(x)
+        assert np.array_equal(y[~nan], ref[~nan])
+        assert np.all((y[nan] & 0x7F80) == 0x7F80) and np.all((y[nan] & 0x7F) != 0)
+        z = np.empty_like(x)
+        assert lib.tb_host_stage(z.ctypes.data, x.ctypes.data, n, _lib.TB_F32, _lib.TB_F32, 0) == 0
+        assert np.array_equal(z.view(np.uint32), x.view(np.uint32))
+    i8 = rng.integers(-128, 128, 12345, dtype=np.int8)
+    o8 = np.empty_like(i8)
+    assert lib.tb_host_stage(o8.ctypes.data, i8.ctypes.data, i8.size, _lib.TB_I8, _lib.TB_I8, 0) == 0
+    assert np.array_equal(o8, i8)
+    assert lib.tb_host_stage(o8.ctypes.data, i8.ctypes.data, i8.size, _lib.TB_I8, _lib.TB_F32, 0) == _lib.TB_EINVAL
