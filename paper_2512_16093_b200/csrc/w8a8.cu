@@ -269,9 +269,13 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) w8a8_tc_kernel(
 #define TB_W8_STG2 1
 #endif
 // fast mode: 16-column chunks (bit c of the mask) seeded with the f32 bits of
-// 1.5*2^23 and converted on the FMA pipe; the rest converted by I2FP (ALU)
+// 1.5*2^23 (tcgen05.st before the MMA accumulates) and converted on the FMA
+// pipe; the rest converted by I2FP (ALU).  Default 0 = no seeding: in
+// same-box A/B runs (tools/ab_w8.sh) every seed mask was 1.5-5% slower than
+// converting every column with I2FP -- the re-seeding stores cost more than
+// the ALU relief buys.
 #ifndef TB_W8_SEED
-#define TB_W8_SEED 0xAA
+#define TB_W8_SEED 0
 #endif
 namespace gemm2 {
 constexpr int BM = 128, BN = 256, BK = 128, STAGES = 5;
@@ -289,6 +293,7 @@ struct Smem {
     uint64_t seg_full[2], seg_empty[2];
     uint32_t tmem_base;
     float qred[2][4];                          // OUTM 2: per (column half, row quarter) absmax
+    alignas(16) uint32_t magic[2][16];         // f32 bits of 1.5*2^23: the fast-mode segment seed
     alignas(1024) uint8_t stage_out[EPI_WARPS][32 * 128];
 #if TB_W8_STG2
     // second staging buffer per warp: the TMA store of chunk c drains while
@@ -340,6 +345,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
     int M, int N, int K, int plane, int act, float *__restrict__ qscales, const __grid_constant__ PeerMaps pm) {
     using namespace gemm2;
     constexpr bool OUT_BF16 = OUTM == 1;
+    // fast mode with a non-empty seed mask: the MMA accumulates onto seeded buffers
+    constexpr bool SEEDED = !EXACT && TB_W8_SEED != 0;
     constexpr int CW = BN / 2;
     constexpr uint32_t TMEM_COLS = 2 * BN;
     extern __shared__ uint8_t smem_raw[];
@@ -354,6 +361,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < STAGES; s++) { ptx::mbar_init(&S.full[s], 1); ptx::mbar_init(&S.empty[s], 1); }
         for (int b = 0; b < 2; b++) { ptx::mbar_init(&S.seg_full[b], 1); ptx::mbar_init(&S.seg_empty[b], 2 * EPI_WARPS); }
+        for (int i = 0; i < 32; i++) S.magic[i >> 4][i & 15] = 0x4B400000u;
         ptx::fence_barrier_init();
         ptx::prefetch_tmap(&tma_a);
         ptx::prefetch_tmap(&tma_b);
@@ -401,7 +409,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
                     if (ptx::elect_one()) {
 #pragma unroll
                         for (int k = 0; k < BK / 32; k++)
-                            ptx::mma_i8_pair(tmem + buf * BN, ad + 2 * k, bd + 2 * k, idesc, (!EXACT || k > 0) ? 1u : 0u);
+                            ptx::mma_i8_pair(tmem + buf * BN, ad + 2 * k, bd + 2 * k, idesc, (SEEDED || k > 0) ? 1u : 0u);
                         ptx::mma_commit_pair(&S.empty[stage], 0x3);
                         ptx::mma_commit_pair(&S.seg_full[buf], 0x3);
                     }
@@ -415,9 +423,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
     }
     } else {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" :: "n"(EPI_REGS));
-        const int ew = warp - 4;
-        const int quarter = warp & 3;
+        // warp index through a shuffle: provably warp-uniform, so the TMEM
+        // addresses below live in uniform registers (no R2UR per tcgen05 op)
+        const int wu = __shfl_sync(0xffffffffu, warp, 0);
+        const int ew = wu - 4;
+        const int quarter = wu & 3;
         const int half = ew >> 2;
+        // fast mode: the seed values stay in 16 registers for the whole kernel
+        // (loaded once; rematerialising them per k-block cost ~50 issue slots).
+        // The lane-dependent source row keeps them out of the uniform register
+        // file (tcgen05.st reads vector registers: no UR -> R moves per store)
+        uint32_t mg[16];
+        if (!EXACT) {
+            const uint32_t ms = ptx::smem_u32(S.magic[lane & 1]);
+#pragma unroll
+            for (int i = 0; i < 16; i += 4)
+                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(mg[i]), "=r"(mg[i + 1]), "=r"(mg[i + 2]), "=r"(mg[i + 3]) : "r"(ms + 4 * i));
+        }
         const uint32_t seg_empty0 = ptx::mapa(ptx::smem_u32(&S.seg_empty[0]), 0);
         const uint32_t seg_empty1 = ptx::mapa(ptx::smem_u32(&S.seg_empty[1]), 0);
         int buf = 0;
@@ -428,17 +451,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
         // the FMA pipe converts a pair), even chunks with 0 (I2FP on the ALU
         // pipe) -- the conversion load split between the two pipes.
         // |seg| <= 128*127^2 < 2^22 keeps M + seg exact.
+        const uint32_t zero16[16] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+        auto st_seed = [&](uint32_t taddr, bool m) {
+            if (m) ptx::tmem_st16(taddr, mg);
+            else ptx::tmem_st16(taddr, zero16);
+        };
         auto seed = [&](uint32_t taddr) {
-            uint32_t mbits[16], zero[16];
 #pragma unroll
-            for (int i = 0; i < 16; i++) { mbits[i] = 0x4B400000u; zero[i] = 0u; }
-#pragma unroll
-            for (int c = 0; c < CW / 16; c++) ptx::tmem_st16(taddr + c * 16, ((TB_W8_SEED >> c) & 1) ? mbits : zero);
+            for (int c = 0; c < CW / 16; c++) st_seed(taddr + c * 16, (TB_W8_SEED >> c) & 1);
             ptx::tmem_wait_st();
         };
 #pragma unroll
         for (int b = 0; b < 2; b++) {
-            if (!EXACT) seed(tmem + ((uint32_t)(quarter * 32) << 16) + b * BN + half * CW);
+            if (SEEDED) seed(tmem + ((uint32_t)(quarter * 32) << 16) + b * BN + half * CW);
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive_cluster(b ? seg_empty1 : seg_empty0);
@@ -453,13 +478,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
             float2 acc2[CW / 2];
 #pragma unroll
             for (int i = 0; i < CW / 2; i++) acc2[i] = make_float2(0.0f, 0.0f);
-            float s_a = __ldg(sa + (size_t)mbs * nkb), s_b = __ldg(sb + nb);
+            // per-k-block scales by pointer walk (next k-block's pair prefetched)
+            const float *pa = sa + (size_t)mbs * nkb, *pb = sb + nb;
+            float s_a = __ldg(pa), s_b = __ldg(pb);
             for (int kb = 0; kb < nkb; kb++) {
                 const float2 sa2 = make_float2(s_a, s_a), sb2 = make_float2(s_b, s_b);
                 const float2 sab2 = make_float2(s_a * s_b, s_a * s_b);
                 if (kb + 1 < nkb) {
-                    s_a = __ldg(sa + (size_t)mbs * nkb + kb + 1);
-                    s_b = __ldg(sb + (size_t)(kb + 1) * nnb + nb);
+                    pa += 1;
+                    pb += nnb;
+                    s_a = __ldg(pa);
+                    s_b = __ldg(pb);
                 }
                 ptx::mbar_wait_sleep(&S.seg_full[buf], bphase);
                 ptx::tc_fence_after();
@@ -471,7 +500,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
                 continue;
 #endif
                 const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + buf * BN + half * CW;
-                // 32-column groups, double-buffered: tcgen05.wait::ld covers every
+                if constexpr (!EXACT) {
+                    // 32-column groups: wait for group g, re-seed its columns at once
+                    // (the stores drain under the math; the MMA of k-block kb+2 finds
+                    // M or 0 there), load group g+1, then promote group g
+                    constexpr int G = 32, NG = CW / G;
+                    uint32_t rb[2][G];
+                    ptx::tmem_ld16(taddr, *reinterpret_cast<uint32_t (*)[16]>(&rb[0][0]));
+                    ptx::tmem_ld16(taddr + 16, *reinterpret_cast<uint32_t (*)[16]>(&rb[0][16]));
+#pragma unroll
+                    for (int g = 0; g < NG; g++) {
+                        ptx::tmem_wait_ld();
+                        if (SEEDED) {
+                            st_seed(taddr + g * G, (TB_W8_SEED >> (2 * g)) & 1);
+                            st_seed(taddr + g * G + 16, (TB_W8_SEED >> (2 * g + 1)) & 1);
+                        }
+                        if (g + 1 < NG) {
+                            ptx::tmem_ld16(taddr + (g + 1) * G, *reinterpret_cast<uint32_t (*)[16]>(&rb[(g + 1) & 1][0]));
+                            ptx::tmem_ld16(taddr + (g + 1) * G + 16,
+                                           *reinterpret_cast<uint32_t (*)[16]>(&rb[(g + 1) & 1][16]));
+                        }
+                        const uint32_t (&r)[G] = rb[g & 1];
+#pragma unroll
+                        for (int i = 0; i < G; i += 2) {
+                            float2 x;
+                            if ((TB_W8_SEED >> ((g * G + i) >> 4)) & 1) {   // seeded chunk: M + seg
+                                x = ptx::fadd2(make_float2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])),
+                                               make_float2(-12582912.0f, -12582912.0f));
+                            } else {
+                                x = make_float2(__int2float_rn((int)r[i]), __int2float_rn((int)r[i + 1]));
+                            }
+                            float2 &o = acc2[(g * G + i) >> 1];
+                            o = ptx::ffma2(x, sab2, o);
+                        }
+                    }
+                    if (SEEDED) ptx::tmem_wait_st();
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive_cluster(buf ? seg_empty1 : seg_empty0);   // the leader's barrier
+                    buf ^= 1;
+                    if (buf == 0) bphase ^= 1;
+                    continue;
+                }
+                // exact: 32-column groups, double-buffered: tcgen05.wait::ld covers every
                 // outstanding load, so the next group's two loads are issued before
                 // this group's math
                 constexpr int G = 32, NG = CW / G;
@@ -509,7 +580,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
                     }
                     if (g + 1 < NG) ptx::tmem_wait_ld();
                 }
-                if (!EXACT) seed(taddr);
+                if (SEEDED) seed(taddr);
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive_cluster(buf ? seg_empty1 : seg_empty0);   // the leader's barrier
