@@ -334,6 +334,15 @@ int tb_linear_kv_part(const void *k, const void *v, int64_t H, int64_t L, int64_
  * (sampler.py:34-53 semantics, eps added inside the root). */
 int tb_add_norm(const float *x, const float *y, const float *emb, float alpha, const float *gain, const float *offset,
                 int64_t rows, int64_t cols, float eps, int layer_norm, float *sum_out, void *norm_out, void *stream);
+/* tb_add_norm fused with tb_quantize_blockwise (block 128) of its bf16 norm
+ * output -- the norm-fed activation quantizations of the DiT block (the
+ * RMSNorm -> qkv and LayerNorm -> mlp_in operands, sampler.py:161,180 with
+ * quantized_linear_forward's blockquant.py:174) in one HBM pass: q int8
+ * [rows, cols], scales f32 [ceil(rows/128), cols/128], bit-identical to the
+ * two calls.  cols % 128 == 0, cols <= 6144; sum_out optional. */
+int tb_add_norm_quant(const float *x, const float *y, const float *emb, float alpha, const float *gain,
+                      const float *offset, int64_t rows, int64_t cols, float eps, int layer_norm, float *sum_out,
+                      int8_t *q, float *scales, void *stream);
 
 /* Delta merge step (replaces the loop body of merge.apply_deltas,
  * merge.py:63-70): acc[i] = acc[i] + fl(c * x[i]) with two RN roundings, the

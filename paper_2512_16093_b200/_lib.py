@@ -74,6 +74,7 @@ SIGNATURES = {
     "tb_rmsnorm": [_P, _P, _I, _I, _f, _P, _P],
     "tb_axpy_rn": [_P, _P, _f, _I, _P],
     "tb_add_norm": [_P, _P, _P, _f, _P, _P, _I, _I, _f, _i, _P, _P, _P],
+    "tb_add_norm_quant": [_P, _P, _P, _f, _P, _P, _I, _I, _f, _i, _P, _P, _P, _P],
     "tb_layernorm": [_P, _P, _P, _I, _I, _f, _P, _P],
     "tb_gelu": [_P, _I, _P, _P],
 }

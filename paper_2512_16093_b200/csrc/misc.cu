@@ -285,6 +285,179 @@ __global__ void __launch_bounds__(256) add_norm_kernel(
     }
 }
 
+
+// add_norm + quantize_blockwise(., 128) of its bf16 output in ONE pass over
+// HBM (the norm-fed activation quantizations of the DiT block,
+// RMSNorm -> qkv and LayerNorm -> mlp_in, sampler.py:161,180).  A 128-row
+// quantization band is one cluster of 8 CTAs, 16 rows each (one warp per
+// row): pass A forms s = x (+ y) (+ alpha*emb) (stored when sum_out) and the
+// row statistics, pass B normalises (s re-read from L2) into a bf16 copy of
+// the CTA's rows in shared memory and the per-128-column absmax of those 16
+// rows, the band's block maxima are combined across the cluster through
+// distributed shared memory, and pass C writes the int8 codes from shared
+// memory.  HBM: x, y read once, s and the codes written once (13 B per
+// element instead of the two-kernel 17 B: no bf16 round trip).
+// The row reduction reproduces add_norm_kernel exactly (virtual thread t =
+// lane + 32k holds chunks t + 256 i; per-virtual-warp xor shuffles; the 8
+// partials summed in order), so the bf16 values -- and therefore the codes
+// and scales -- are bit-identical to tb_add_norm followed by
+// tb_quantize_blockwise.
+constexpr int ANQ_ROWS = 16, ANQ_CLUSTER = 8;
+template <int MODE>
+__global__ void __cluster_dims__(ANQ_CLUSTER, 1, 1) __launch_bounds__(ANQ_ROWS * 32, 1) add_norm_quant_kernel(
+    const float *__restrict__ x, const float *__restrict__ y, const float *__restrict__ emb, float alpha,
+    const float *__restrict__ g, const float *__restrict__ b, int64_t rows, int cols, float eps,
+    float *__restrict__ sum_out, int8_t *__restrict__ q, float *__restrict__ scales) {
+    extern __shared__ __align__(16) uint8_t anq_smem[];
+    const int nc4 = cols >> 2, nb = cols >> 7;
+    __nv_bfloat16 *a_s = reinterpret_cast<__nv_bfloat16 *>(anq_smem);                       // [16][cols]
+    float *amax = reinterpret_cast<float *>(anq_smem + (size_t)ANQ_ROWS * cols * 2);         // [16][nb]
+    float *bmax = amax + ANQ_ROWS * nb;                                                       // [nb] CTA maxima
+    float *bsc = bmax + nb;                                                                   // [nb] band scales
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t rank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    const int64_t band = blockIdx.x / ANQ_CLUSTER;
+    const int64_t row = band * 128 + (int64_t)rank * ANQ_ROWS + warp;
+    const bool ok = row < rows;
+    auto load_s = [&](int c4) {
+        float4 a = reinterpret_cast<const float4 *>(x + row * cols)[c4];
+        if (y) {
+            const float4 t = reinterpret_cast<const float4 *>(y + row * cols)[c4];
+            a.x += t.x; a.y += t.y; a.z += t.z; a.w += t.w;
+        }
+        if (emb) {
+            const float4 e = reinterpret_cast<const float4 *>(emb)[c4];
+            a.x = fmaf(alpha, e.x, a.x); a.y = fmaf(alpha, e.y, a.y);
+            a.z = fmaf(alpha, e.z, a.z); a.w = fmaf(alpha, e.w, a.w);
+        }
+        return a;
+    };
+    // s again in pass B: from the stored sum (an L2 hit) or recomputed (same ops)
+    auto reload_s = [&](int c4) {
+        return sum_out ? reinterpret_cast<const float4 *>(sum_out + row * cols)[c4] : load_s(c4);
+    };
+    auto xor_sum = [&](float v) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        return v;
+    };
+    if (ok) {
+        // pass A: s, sum_out, row statistics in add_norm_kernel's order
+        float s1 = 0.0f, s2 = 0.0f;
+#pragma unroll 1
+        for (int k = 0; k < 8; k++) {                      // virtual warp k: threads 32k + lane
+            float p1 = 0.0f, p2 = 0.0f;
+#pragma unroll
+            for (int i = 0; i < ADD_NORM_CHUNKS; i++) {
+                const int c4 = lane + 32 * k + 256 * i;
+                if (c4 < nc4) {
+                    const float4 a = load_s(c4);
+                    if (sum_out) reinterpret_cast<float4 *>(sum_out + row * cols)[c4] = a;
+                    p1 += (a.x + a.y) + (a.z + a.w);
+                    p2 = fmaf(a.x, a.x, fmaf(a.y, a.y, fmaf(a.z, a.z, fmaf(a.w, a.w, p2))));
+                }
+            }
+            s1 += xor_sum(p1);                             // 0 + red[0] + red[1] + ... in order
+            s2 += xor_sum(p2);
+        }
+        const float n = (float)cols;
+        float mu = 0.0f, inv;
+        if (MODE == 0) {
+            inv = rsqrtf(s2 / n + eps);
+        } else {
+            mu = s1 / n;
+            float s3 = 0.0f;
+#pragma unroll 1
+            for (int k = 0; k < 8; k++) {
+                float p3 = 0.0f;
+#pragma unroll
+                for (int i = 0; i < ADD_NORM_CHUNKS; i++) {
+                    const int c4 = lane + 32 * k + 256 * i;
+                    if (c4 < nc4) {
+                        const float4 a = reload_s(c4);
+                        const float dx = a.x - mu, dy = a.y - mu, dz = a.z - mu, dw = a.w - mu;
+                        p3 = fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, fmaf(dw, dw, p3))));
+                    }
+                }
+                s3 += xor_sum(p3);
+            }
+            inv = rsqrtf(s3 / n + eps);
+        }
+        // pass B: bf16 normalised row into shared memory; iteration it covers
+        // columns [128 it, 128 it + 128) = quantization block it
+#pragma unroll 1
+        for (int it = 0; it < nb; it++) {
+            const int c4 = it * 32 + lane;
+            const float4 a = reload_s(c4);
+            const float4 gg = reinterpret_cast<const float4 *>(g)[c4];
+            float4 o;
+            o.x = (a.x - mu) * inv * gg.x; o.y = (a.y - mu) * inv * gg.y;
+            o.z = (a.z - mu) * inv * gg.z; o.w = (a.w - mu) * inv * gg.w;
+            if (MODE == 1) {
+                const float4 bb = reinterpret_cast<const float4 *>(b)[c4];
+                o.x += bb.x; o.y += bb.y; o.z += bb.z; o.w += bb.w;
+            }
+            const __nv_bfloat162 p0 = __floats2bfloat162_rn(o.x, o.y), p1 = __floats2bfloat162_rn(o.z, o.w);
+            uint2 wv;
+            wv.x = *reinterpret_cast<const uint32_t *>(&p0);
+            wv.y = *reinterpret_cast<const uint32_t *>(&p1);
+            reinterpret_cast<uint2 *>(a_s + (size_t)warp * cols)[c4] = wv;
+            const float2 f0 = __bfloat1622float2(p0), f1 = __bfloat1622float2(p1);
+            float m = fmaxf(fmaxf(fabsf(f0.x), fabsf(f0.y)), fmaxf(fabsf(f1.x), fabsf(f1.y)));
+            m = warp_max<32>(m);
+            if (lane == 0) amax[warp * nb + it] = m;
+        }
+    } else {
+        for (int it = lane; it < nb; it += 32) amax[warp * nb + it] = 0.0f;   // padding rows of the last band
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < nb; t += blockDim.x) {
+        float m = 0.0f;
+#pragma unroll
+        for (int r = 0; r < ANQ_ROWS; r++) m = fmaxf(m, amax[r * nb + t]);
+        bmax[t] = m;
+    }
+    // the band's block maxima over the 8 CTAs of the cluster (DSMEM)
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    for (int t = threadIdx.x; t < nb; t += blockDim.x) {
+        float m = 0.0f;
+        const uint32_t local = (uint32_t)__cvta_generic_to_shared(bmax + t);
+#pragma unroll
+        for (int r = 0; r < ANQ_CLUSTER; r++) {
+            uint32_t remote;
+            float v;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(r));
+            asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(remote) : "memory");
+            m = fmaxf(m, v);
+        }
+        const float sc = quant_scale(m);
+        bsc[t] = sc;
+        if (rank == 0) scales[band * nb + t] = sc;
+    }
+    __syncthreads();
+    if (ok) {
+        // pass C: codes from shared memory (quantize_blockwise rule, blockquant.py:106-109)
+#pragma unroll 1
+        for (int it = 0; it < nb; it++) {
+            const float sc = bsc[it];
+            const float safe = (sc == 0.0f) ? 1.0f : sc;
+            const float rq = __frcp_rn(safe);
+            const bool exq = !(safe >= 1.17549435e-38f && rq <= 3.0e38f);   // subnormal scale: exact division
+            const int c4 = it * 32 + lane;
+            const uint2 wv = reinterpret_cast<const uint2 *>(a_s + (size_t)warp * cols)[c4];
+            const float2 f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&wv.x));
+            const float2 f1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&wv.y));
+            const float v4[4] = {f0.x, f0.y, f1.x, f1.y};
+            uint32_t w[1];
+            quant_fast_n<4>(v4, safe, rq, exq, w);
+            reinterpret_cast<uint32_t *>(q + row * cols)[c4] = w[0];
+        }
+    }
+    // no CTA leaves while a peer may still read its block maxima
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 __global__ void gelu_kernel(const float *__restrict__ x, int64_t n, float *__restrict__ out) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -396,6 +569,36 @@ extern "C" int tb_add_norm(const float *x, const float *y, const float *emb, flo
         add_norm_kernel<0><<<(unsigned)rows, 256, 0, st>>>(x, y, emb, alpha, gain, offset, cols, eps, sum_out,
                                                           (__nv_bfloat16 *)norm_out);
     return check_launch("add_norm");
+}
+
+// add_norm + block-128 quantization of the normalised (bf16-rounded) rows in
+// one kernel: codes [rows, cols] int8 + scales [ceil(rows/128), cols/128] f32,
+// bit-identical to tb_add_norm (norm_out) followed by tb_quantize_blockwise
+// (block 128).  cols % 128 == 0, cols <= 6144.
+extern "C" int tb_add_norm_quant(const float *x, const float *y, const float *emb, float alpha, const float *gain,
+                                 const float *offset, int64_t rows, int64_t cols, float eps, int layer_norm,
+                                 float *sum_out, int8_t *q, float *scales, void *stream) {
+    TB_REQUIRE(eps > 0.0f, "eps must be > 0");
+    TB_REQUIRE(cols % 128 == 0 && cols >= 128 && cols <= 6144, "cols must be a multiple of 128, <= 6144");
+    TB_REQUIRE(!layer_norm || offset != nullptr, "layer norm needs an offset");
+    TB_REQUIRE(((uintptr_t)x % 16) == 0 && ((uintptr_t)q % 4) == 0 && (y == nullptr || (uintptr_t)y % 16 == 0) &&
+                   (sum_out == nullptr || (uintptr_t)sum_out % 16 == 0),
+               "x, y, sum_out must be 16-byte aligned, q 4-byte aligned");
+    if (rows == 0) return TB_OK;
+    const int nb = (int)(cols / 128);
+    const size_t smem = (size_t)ANQ_ROWS * cols * 2 + (size_t)(ANQ_ROWS + 2) * nb * 4;
+    const unsigned grid = (unsigned)(cdiv(rows, 128) * ANQ_CLUSTER);
+    cudaStream_t st = as_stream(stream);
+    if (layer_norm) {
+        smem_attr(add_norm_quant_kernel<1>, (int)smem);
+        add_norm_quant_kernel<1><<<grid, ANQ_ROWS * 32, smem, st>>>(x, y, emb, alpha, gain, offset, rows, (int)cols,
+                                                                     eps, sum_out, q, scales);
+    } else {
+        smem_attr(add_norm_quant_kernel<0>, (int)smem);
+        add_norm_quant_kernel<0><<<grid, ANQ_ROWS * 32, smem, st>>>(x, y, emb, alpha, gain, offset, rows, (int)cols,
+                                                                     eps, sum_out, q, scales);
+    }
+    return check_launch("add_norm_quant");
 }
 
 // ------------------------------------------------------------ delta merging

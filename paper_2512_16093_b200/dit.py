@@ -106,14 +106,20 @@ def block_forward(x: torch.Tensor, sigma: float, w: DeviceLayer, heads: int, sla
     left to the next block's fused add+norm (or to ``model_forward``)."""
     Lp, dim = x.shape
     hd = dim // heads
-    # x1 = x (+ pending residual) + sigma*emb and a = RMSNorm(x1), one pass (bf16 a)
-    x1, a = ops.add_norm(x, pending, w.sigma_emb, float(sigma), w.rms_gain)
+    # x1 = x (+ pending residual) + sigma*emb and the block-quantized RMSNorm(x1)
+    # (the qkv projection's A operand), one pass (SURVEY §8 f1)
+    fused_nq = ops.add_norm_quant_ok(dim)
+    if fused_nq:
+        x1, aq, asc = ops.add_norm_quant(x, pending, w.sigma_emb, float(sigma), w.rms_gain)
+    else:
+        x1, a = ops.add_norm(x, pending, w.sigma_emb, float(sigma), w.rms_gain)
 
     def attn(qh, kh, vh):
         return ops.sla_attention(qh, kh, vh, sla["q_block"], sla["kv_block"], sla["topk_ratio"],
                                  sla.get("linear_mix", 1.0), True, out_dtype=torch.bfloat16)
 
-    aq, asc = ops.quantize_blockwise(a, 128, check_finite=False)
+    if not fused_nq:
+        aq, asc = ops.quantize_blockwise(a, 128, check_finite=False)
     multi = dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1
     if multi and hd == 128 and os.environ.get("TB_ULYSSES_P2P") == "1":
         # both exchanges fused into their producers over peer memory: the qkv
@@ -155,9 +161,13 @@ def block_forward(x: torch.Tensor, sigma: float, w: DeviceLayer, heads: int, sla
             o = attn(qkv[:heads], qkv[heads:2 * heads], qkv[2 * heads:])           # [H, L, hd]
             oq, osc = ops.quantize_blockwise_planar(o)
     po = ops.w8a8_gemm(oq, osc, w.out_proj.bt, w.out_proj.scales, 128, None, torch.float32, exact=False)
-    # x2 = x1 + po and b = LayerNorm(x2), one pass (x2 overwrites x1)
-    x2, b = ops.add_norm(x1, po, None, 0.0, w.ln_gain, w.ln_offset, layer_norm=True, sum_out=x1)
-    bq, bsc = ops.quantize_blockwise(b, 128, check_finite=False)
+    # x2 = x1 + po and the block-quantized LayerNorm(x2) (mlp_in's A operand),
+    # one pass (x2 overwrites x1)
+    if fused_nq:
+        x2, bq, bsc = ops.add_norm_quant(x1, po, None, 0.0, w.ln_gain, w.ln_offset, layer_norm=True, sum_out=x1)
+    else:
+        x2, b = ops.add_norm(x1, po, None, 0.0, w.ln_gain, w.ln_offset, layer_norm=True, sum_out=x1)
+        bq, bsc = ops.quantize_blockwise(b, 128, check_finite=False)
     # mlp_in -> GELU -> block quantization for mlp_out, all in the GEMM epilogue
     hq, hsc = ops.w8a8_gemm_quant(bq, bsc, w.mlp_in.bt, w.mlp_in.scales, 128, None, act=1)
     p2 = ops.w8a8_gemm(hq, hsc, w.mlp_out.bt, w.mlp_out.scales, 128, None, torch.float32, exact=False)

@@ -753,6 +753,26 @@ def add_norm(x, y=None, emb=None, alpha: float = 0.0, gain=None, offset=None, la
     return (sum_out if write_sum else None), norm
 
 
+def add_norm_quant(x, y=None, emb=None, alpha: float = 0.0, gain=None, offset=None, layer_norm: bool = False,
+                   eps: float = 1e-6, sum_out=None, write_sum: bool = True):
+    """add_norm fused with quantize_blockwise(., 128) of the bf16 norm output
+    (tb_add_norm_quant): -> (s f32 | None, codes int8 [rows, cols], scales
+    [ceil(rows/128), cols/128]), bit-identical to add_norm + quantize_blockwise
+    with one HBM pass.  cols % 128 == 0 and cols <= 6144."""
+    rows, cols = x.shape
+    if write_sum and sum_out is None:
+        sum_out = torch.empty_like(x)
+    q = torch.empty((rows, cols), dtype=torch.int8, device=x.device)
+    sc = torch.empty((cdiv(rows, 128), cols // 128), dtype=torch.float32, device=x.device)
+    call("tb_add_norm_quant", ptr(x), ptr(y), ptr(emb), float(alpha), ptr(gain), ptr(offset), rows, cols,
+         float(eps), int(layer_norm), ptr(sum_out if write_sum else None), ptr(q), ptr(sc), stream_ptr())
+    return (sum_out if write_sum else None), q, sc
+
+
+def add_norm_quant_ok(cols: int) -> bool:
+    return cols % 128 == 0 and 128 <= cols <= 6144
+
+
 def axpy_rn(acc: torch.Tensor, x: torch.Tensor, c: float) -> torch.Tensor:
     """acc += fl(c * x) in place (f32, two RN roundings; merge.py:68)."""
     assert acc.dtype == torch.float32 and x.dtype == torch.float32 and acc.is_contiguous()

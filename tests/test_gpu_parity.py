@@ -370,6 +370,33 @@ def test_add_norm_matches_reference_norms(tb, layer_norm):
     assert torch.allclose(n.float(), ref, rtol=1e-2, atol=1e-2)
 
 
+@pytest.mark.parametrize("layer_norm", [False, True])
+@pytest.mark.parametrize("rows,cols,with_y,with_emb,write_sum",
+                         [(300, 5120, True, True, True), (256, 1536, False, True, False), (77, 5120, True, False, True),
+                          (1029, 6144, True, True, True)])
+def test_add_norm_quant_equals_two_pass(tb, layer_norm, rows, cols, with_y, with_emb, write_sum):
+    """tb_add_norm_quant (norm + block-128 quantization in one pass, SURVEY §8
+    f1) is bit-identical to tb_add_norm followed by tb_quantize_blockwise:
+    codes, scales and the stored sum; ragged last bands (77, 300, 1029 rows)."""
+    g = torch.Generator(device="cuda").manual_seed(rows + cols)
+    x = torch.randn((rows, cols), device="cuda", generator=g) * 3 + 1
+    y = torch.randn((rows, cols), device="cuda", generator=g) if with_y else None
+    emb = torch.randn(cols, device="cuda", generator=g) if with_emb else None
+    gain = torch.rand(cols, device="cuda", generator=g) + 0.5
+    off = torch.randn(cols, device="cuda", generator=g) if layer_norm else None
+    if rows > 1000:
+        x[5, :] = 0.0                                   # an all-zero row (scale of its blocks from the others)
+        x[1000:, :] *= 1e-30                            # tiny rows in the last band
+    s_ref, n_ref = tb.add_norm(x, y, emb, 0.7, gain, off, layer_norm=layer_norm, write_sum=write_sum)
+    q_ref, sc_ref = tb.quantize_blockwise(n_ref, 128, check_finite=False)
+    s, q, sc = tb.add_norm_quant(x, y, emb, 0.7, gain, off, layer_norm=layer_norm, write_sum=write_sum)
+    torch.cuda.synchronize()
+    assert torch.equal(q, q_ref)
+    assert torch.equal(sc, sc_ref)
+    if write_sum:
+        assert torch.equal(s, s_ref)
+
+
 # ------------------------------------------------ FP8 P/V (SURVEY §8 a17)
 
 @pytest.mark.parametrize("L", [1000, 4096])
