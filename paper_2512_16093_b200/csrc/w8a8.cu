@@ -265,46 +265,66 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) w8a8_tc_kernel(
 // the operand-full and segment-free barriers and issues the MMAs; commits are
 // multicast to both CTAs; both CTAs' epilogues drain their own TMEM rows with
 // the same promotion as the single-SM kernel and TMA-store their rows.
-#ifndef TB_W8_STG2
-#define TB_W8_STG2 1
-#endif
-// fast mode: 16-column chunks (bit c of the mask) seeded with the f32 bits of
-// 1.5*2^23 (tcgen05.st before the MMA accumulates) and converted on the FMA
-// pipe; the rest converted by I2FP (ALU).  Default 0 = no seeding: in
-// same-box A/B runs (tools/ab_w8.sh) every seed mask was 1.5-5% slower than
-// converting every column with I2FP -- the re-seeding stores cost more than
-// the ALU relief buys.
-#ifndef TB_W8_SEED
-#define TB_W8_SEED 0
-#endif
+// Epilogue width: EPW = 8 (two warps per SM sub-partition, 128 columns each)
+// or 16 (four per sub-partition, 64 columns each).  The promotion is
+// latency-bound at ~200 instructions per warp per k-block (ncu source view:
+// fixed-latency and TMEM-load dependencies, profiles/r02_source_level_stalls.md),
+// so 16 warps hide twice the latency; the register file then allows 112 per
+// epilogue thread (64 accumulators + a 16-column TMEM group).  The quantizing
+// epilogue (OUTM 2) keeps EPW = 8 (its 128x128 block absmax spans one warp
+// quarter-set).  Fast mode converts every s32 segment with I2FP: re-seeding
+// TMEM with 1.5*2^23 for FADD2 conversions (or IMAD-based ones) measured
+// 1.5-7% slower in same-box A/B runs.
 namespace gemm2 {
-constexpr int BM = 128, BN = 256, BK = 128, STAGES = 5;
-constexpr int EPI_WARPS = 8;
-// warpgroup 0: TMA warp, MMA warp, two idle warps; warpgroups 1-2: the 8
-// epilogue warps.  setmaxnreg moves the control warpgroup's registers to the
-// epilogue (each role's code sits inside the branch that resized it, so ptxas
-// allocates the epilogue against the larger budget)
-constexpr int THREADS = 128 + EPI_WARPS * 32;
-constexpr int CTRL_REGS = 56, EPI_REGS = 224;     // 128*56 + 256*224 <= 64K
+constexpr int BM = 128, BN = 256, BK = 128;
+template <int EPW>
+struct Cfg {
+    static constexpr int THREADS = 128 + EPW * 32;
+    // warpgroup 0: TMA warp, MMA warp, two idle warps; the rest: epilogue.
+    // setmaxnreg moves the control warpgroup's registers to the epilogue
+    // (each role's code sits inside the branch that resized it)
+    // setmaxnreg only moves registers inside the CTA's launch allocation
+    // (THREADS x LAUNCH_REGS): what the control warpgroup releases must cover
+    // what the epilogue warps acquire, or the increase waits forever
+    static constexpr int LAUNCH_REGS = (65536 / THREADS) / 8 * 8;
+    static constexpr int CTRL_REGS = EPW == 8 ? 56 : 32;
+    static constexpr int EPI_REGS = EPW == 8 ? 224 : 112;
+    static constexpr int STAGES = EPW == 8 ? 5 : 4;
+    static constexpr bool STG2 = EPW == 8;                      // second staging buffer per warp
+    static constexpr int CW = BN / (EPW / 4);                    // columns per epilogue warp
+};
+static_assert(128 * (Cfg<8>::LAUNCH_REGS - Cfg<8>::CTRL_REGS) >= 32 * 8 * (Cfg<8>::EPI_REGS - Cfg<8>::LAUNCH_REGS) &&
+                  128 * (Cfg<16>::LAUNCH_REGS - Cfg<16>::CTRL_REGS) >=
+                      32 * 16 * (Cfg<16>::EPI_REGS - Cfg<16>::LAUNCH_REGS),
+              "setmaxnreg budget: the control warps must release what the epilogue warps take");
+template <int EPW>
 struct Smem {
-    uint8_t a[STAGES][BM * BK];
-    uint8_t b[STAGES][(BN / 2) * BK];
-    uint64_t full[STAGES], empty[STAGES];
+    uint8_t a[Cfg<EPW>::STAGES][BM * BK];
+    uint8_t b[Cfg<EPW>::STAGES][(BN / 2) * BK];
+    uint64_t full[Cfg<EPW>::STAGES], empty[Cfg<EPW>::STAGES];
     uint64_t seg_full[2], seg_empty[2];
     uint32_t tmem_base;
     float qred[2][4];                          // OUTM 2: per (column half, row quarter) absmax
-    alignas(16) uint32_t magic[2][16];         // f32 bits of 1.5*2^23: the fast-mode segment seed
-    alignas(1024) uint8_t stage_out[EPI_WARPS][32 * 128];
-#if TB_W8_STG2
-    // second staging buffer per warp: the TMA store of chunk c drains while
-    // chunk c+1 is staged (the tile-end store no longer serialises on each
-    // store's shared-memory read)
-    alignas(1024) uint8_t stage_out2[EPI_WARPS][32 * 128];
-#endif
+    alignas(1024) uint8_t stage_out[EPW][32 * 128];
+    // EPW 8: second staging buffer per warp -- the TMA store of chunk c drains
+    // while chunk c+1 is staged
+    alignas(1024) uint8_t stage_out2[Cfg<EPW>::STG2 ? EPW : 1][32 * 128];
 };
-constexpr size_t SMEM_BYTES = sizeof(Smem) + 1024;
-static_assert(SMEM_BYTES <= 232448, "2-SM W8A8 shared memory over the 227 KB opt-in limit");
+template <int EPW>
+constexpr size_t smem_bytes() { return sizeof(Smem<EPW>) + 1024; }
+static_assert(smem_bytes<8>() <= 232448 && smem_bytes<16>() <= 232448, "2-SM W8A8 shared memory over 227 KB");
 }  // namespace gemm2
+
+// Epilogue warps per mode: the exact promotion (three rounded ops per element,
+// FMA-pipe heavy) gains 3-8% from 16 warps; the fast one (one FFMA2 per pair)
+// loses 5-9% to the smaller ring and single-buffered staging 16 warps leave
+// room for (same-box A/B, tools/ab_w8.sh)
+#ifndef TB_W8_EPW_EXACT
+#define TB_W8_EPW_EXACT 16
+#endif
+#ifndef TB_W8_EPW_FAST
+#define TB_W8_EPW_FAST 8
+#endif
 
 // Tile raster of the 2-SM kernel: groups of W8_GROUP_M row-pair bands, row
 // band fastest inside a group, so the ~74 co-running clusters share a few A
@@ -337,20 +357,21 @@ struct alignas(64) PeerMaps {
 // OUTM: 0 f32, 1 bf16, 2 block-quantized INT8 (the next projection's A
 // operand: the bf16-rounded result quantized per 128x128 block exactly like
 // quantize_blockwise, codes TMA-stored, one f32 scale per block to qscales).
-template <bool EXACT, int OUTM>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w8a8_2sm_kernel(
+template <bool EXACT, int OUTM, int EPW>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::Cfg<EPW>::THREADS, 1) w8a8_2sm_kernel(
     const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
     const __grid_constant__ CUtensorMap tma_out,
     const float *__restrict__ sa, const float *__restrict__ sb, const float *__restrict__ bias,
     int M, int N, int K, int plane, int act, float *__restrict__ qscales, const __grid_constant__ PeerMaps pm) {
     using namespace gemm2;
+    using C = Cfg<EPW>;
+    constexpr int STAGES = C::STAGES;
     constexpr bool OUT_BF16 = OUTM == 1;
-    // fast mode with a non-empty seed mask: the MMA accumulates onto seeded buffers
-    constexpr bool SEEDED = !EXACT && TB_W8_SEED != 0;
-    constexpr int CW = BN / 2;
+    constexpr int CW = C::CW;
+    static_assert(OUTM != 2 || EPW == 8, "the quantizing epilogue needs 8 epilogue warps (128-column halves)");
     constexpr uint32_t TMEM_COLS = 2 * BN;
     extern __shared__ uint8_t smem_raw[];
-    Smem &S = *reinterpret_cast<Smem *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    Smem<EPW> &S = *reinterpret_cast<Smem<EPW> *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = ptx::cluster_ctarank();
     const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
@@ -360,8 +381,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < STAGES; s++) { ptx::mbar_init(&S.full[s], 1); ptx::mbar_init(&S.empty[s], 1); }
-        for (int b = 0; b < 2; b++) { ptx::mbar_init(&S.seg_full[b], 1); ptx::mbar_init(&S.seg_empty[b], 2 * EPI_WARPS); }
-        for (int i = 0; i < 32; i++) S.magic[i >> 4][i & 15] = 0x4B400000u;
+        for (int b = 0; b < 2; b++) { ptx::mbar_init(&S.seg_full[b], 1); ptx::mbar_init(&S.seg_empty[b], 2 * EPW); }
         ptx::fence_barrier_init();
         ptx::prefetch_tmap(&tma_a);
         ptx::prefetch_tmap(&tma_b);
@@ -373,7 +393,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
     const uint32_t tmem = S.tmem_base;
 
     if (warp < 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" :: "n"(CTRL_REGS));
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" :: "n"(C::CTRL_REGS));
     if (warp == 0) {
         if (ptx::elect_one()) {
             int stage = 0;
@@ -399,8 +419,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
             constexpr uint32_t idesc = ptx::idesc_i8(2 * BM, BN);
             for (int tile = cluster; tile < ntiles; tile += nclusters) {
                 for (int kb = 0; kb < nkb; kb++) {
-                    // segment buffer drained (and, fast mode, re-seeded) by both CTAs'
-                    // epilogues; their initial arrive completes phase 0 before first use
+                    // segment buffer drained by both CTAs' epilogues; their initial
+                    // arrive completes phase 0 before first use
                     ptx::mbar_wait_sleep(&S.seg_empty[buf], bphase);
                     ptx::mbar_wait_sleep(&S.full[stage], phase);
                     ptx::tc_fence_after();
@@ -409,7 +429,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
                     if (ptx::elect_one()) {
 #pragma unroll
                         for (int k = 0; k < BK / 32; k++)
-                            ptx::mma_i8_pair(tmem + buf * BN, ad + 2 * k, bd + 2 * k, idesc, (SEEDED || k > 0) ? 1u : 0u);
+                            ptx::mma_i8_pair(tmem + buf * BN, ad + 2 * k, bd + 2 * k, idesc, k > 0 ? 1u : 0u);
                         ptx::mma_commit_pair(&S.empty[stage], 0x3);
                         ptx::mma_commit_pair(&S.seg_full[buf], 0x3);
                     }
@@ -422,56 +442,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
         }
     }
     } else {
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" :: "n"(EPI_REGS));
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" :: "n"(C::EPI_REGS));
         // warp index through a shuffle: provably warp-uniform, so the TMEM
         // addresses below live in uniform registers (no R2UR per tcgen05 op)
         const int wu = __shfl_sync(0xffffffffu, warp, 0);
         const int ew = wu - 4;
-        const int quarter = wu & 3;
-        const int half = ew >> 2;
-        // fast mode: the seed values stay in 16 registers for the whole kernel
-        // (loaded once; rematerialising them per k-block cost ~50 issue slots).
-        // The lane-dependent source row keeps them out of the uniform register
-        // file (tcgen05.st reads vector registers: no UR -> R moves per store)
-        uint32_t mg[16];
-        if (!EXACT) {
-            const uint32_t ms = ptx::smem_u32(S.magic[lane & 1]);
-#pragma unroll
-            for (int i = 0; i < 16; i += 4)
-                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                             : "=r"(mg[i]), "=r"(mg[i + 1]), "=r"(mg[i + 2]), "=r"(mg[i + 3]) : "r"(ms + 4 * i));
-        }
+        const int quarter = wu & 3;                // TMEM lanes this warp may touch
+        const int cg = ew >> 2;                    // column group of CW columns
         const uint32_t seg_empty0 = ptx::mapa(ptx::smem_u32(&S.seg_empty[0]), 0);
         const uint32_t seg_empty1 = ptx::mapa(ptx::smem_u32(&S.seg_empty[1]), 0);
         int buf = 0;
         uint32_t bphase = 0;
-        // fast mode seeds each segment buffer before the MMA accumulates into it:
-        // odd 16-column chunks with the f32 bits of M = 1.5*2^23 (the integer MMA
-        // adds on top, the chunk reads back as the float M + seg and one FADD2 on
-        // the FMA pipe converts a pair), even chunks with 0 (I2FP on the ALU
-        // pipe) -- the conversion load split between the two pipes.
-        // |seg| <= 128*127^2 < 2^22 keeps M + seg exact.
-        const uint32_t zero16[16] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-        auto st_seed = [&](uint32_t taddr, bool m) {
-            if (m) ptx::tmem_st16(taddr, mg);
-            else ptx::tmem_st16(taddr, zero16);
-        };
-        auto seed = [&](uint32_t taddr) {
-#pragma unroll
-            for (int c = 0; c < CW / 16; c++) st_seed(taddr + c * 16, (TB_W8_SEED >> c) & 1);
-            ptx::tmem_wait_st();
-        };
 #pragma unroll
         for (int b = 0; b < 2; b++) {
-            if (SEEDED) seed(tmem + ((uint32_t)(quarter * 32) << 16) + b * BN + half * CW);
-            ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive_cluster(b ? seg_empty1 : seg_empty0);
         }
         for (int tile = cluster; tile < ntiles; tile += nclusters) {
             int mp, nt;
             tile_coords(tile, nmp, nnt, mp, nt);
-            const int col0 = nt * BN + half * CW;
+            const int col0 = nt * BN + cg * CW;
             const int nb = col0 / 128;
             const int mb = 2 * mp + (int)rank;                    // this CTA's 128-row scale block
             const int mbs = mb < nmb ? mb : nmb - 1;              // (rows past M are clipped anyway)
@@ -492,81 +482,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
                 }
                 ptx::mbar_wait_sleep(&S.seg_full[buf], bphase);
                 ptx::tc_fence_after();
-#ifdef TB_W8_NOEPI
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive_cluster(buf ? seg_empty1 : seg_empty0);
-                buf ^= 1;
-                if (buf == 0) bphase ^= 1;
-                continue;
-#endif
-                const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + buf * BN + half * CW;
-                if constexpr (!EXACT) {
-                    // 32-column groups: wait for group g, re-seed its columns at once
-                    // (the stores drain under the math; the MMA of k-block kb+2 finds
-                    // M or 0 there), load group g+1, then promote group g
-                    constexpr int G = 32, NG = CW / G;
-                    uint32_t rb[2][G];
-                    ptx::tmem_ld16(taddr, *reinterpret_cast<uint32_t (*)[16]>(&rb[0][0]));
-                    ptx::tmem_ld16(taddr + 16, *reinterpret_cast<uint32_t (*)[16]>(&rb[0][16]));
+                const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + buf * BN + cg * CW;
+                auto promote = [&](const uint32_t *r, int c0, int n) {
 #pragma unroll
-                    for (int g = 0; g < NG; g++) {
-                        ptx::tmem_wait_ld();
-                        if (SEEDED) {
-                            st_seed(taddr + g * G, (TB_W8_SEED >> (2 * g)) & 1);
-                            st_seed(taddr + g * G + 16, (TB_W8_SEED >> (2 * g + 1)) & 1);
-                        }
-                        if (g + 1 < NG) {
-                            ptx::tmem_ld16(taddr + (g + 1) * G, *reinterpret_cast<uint32_t (*)[16]>(&rb[(g + 1) & 1][0]));
-                            ptx::tmem_ld16(taddr + (g + 1) * G + 16,
-                                           *reinterpret_cast<uint32_t (*)[16]>(&rb[(g + 1) & 1][16]));
-                        }
-                        const uint32_t (&r)[G] = rb[g & 1];
-#pragma unroll
-                        for (int i = 0; i < G; i += 2) {
-                            float2 x;
-                            if ((TB_W8_SEED >> ((g * G + i) >> 4)) & 1) {   // seeded chunk: M + seg
-                                x = ptx::fadd2(make_float2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])),
-                                               make_float2(-12582912.0f, -12582912.0f));
-                            } else {
-                                x = make_float2(__int2float_rn((int)r[i]), __int2float_rn((int)r[i + 1]));
-                            }
-                            float2 &o = acc2[(g * G + i) >> 1];
-                            o = ptx::ffma2(x, sab2, o);
-                        }
-                    }
-                    if (SEEDED) ptx::tmem_wait_st();
-                    ptx::tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive_cluster(buf ? seg_empty1 : seg_empty0);   // the leader's barrier
-                    buf ^= 1;
-                    if (buf == 0) bphase ^= 1;
-                    continue;
-                }
-                // exact: 32-column groups, double-buffered: tcgen05.wait::ld covers every
-                // outstanding load, so the next group's two loads are issued before
-                // this group's math
-                constexpr int G = 32, NG = CW / G;
-                uint32_t rb[2][G];
-                ptx::tmem_ld16(taddr, *reinterpret_cast<uint32_t (*)[16]>(&rb[0][0]));
-                ptx::tmem_ld16(taddr + 16, *reinterpret_cast<uint32_t (*)[16]>(&rb[0][16]));
-                ptx::tmem_wait_ld();
-#pragma unroll
-                for (int g = 0; g < NG; g++) {
-                    if (g + 1 < NG) {
-                        ptx::tmem_ld16(taddr + (g + 1) * G, *reinterpret_cast<uint32_t (*)[16]>(&rb[(g + 1) & 1][0]));
-                        ptx::tmem_ld16(taddr + (g + 1) * G + 16, *reinterpret_cast<uint32_t (*)[16]>(&rb[(g + 1) & 1][16]));
-                    }
-                    const uint32_t (&r)[G] = rb[g & 1];
-#pragma unroll
-                    for (int i = 0; i < G; i += 2) {
-                        float2 x;
-                        if (!EXACT && ((TB_W8_SEED >> ((g * G + i) >> 4)) & 1)) {   // seeded chunk: M + seg
-                            x = ptx::fadd2(make_float2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])),
-                                           make_float2(-12582912.0f, -12582912.0f));
-                        } else {
-                            x = make_float2(__int2float_rn((int)r[i]), __int2float_rn((int)r[i + 1]));
-                        }
-                        float2 &o = acc2[(g * G + i) >> 1];
+                    for (int i = 0; i < n; i += 2) {
+                        const float2 x = make_float2(__int2float_rn((int)r[i]), __int2float_rn((int)r[i + 1]));
+                        float2 &o = acc2[(c0 + i) >> 1];
                         if constexpr (EXACT) {
                             // the reference sequence bit-for-bit: packed RN ops round each
                             // lane like the scalar op, but ptxas contracts a packed multiply
@@ -578,9 +499,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
                             o = ptx::ffma2(x, sab2, o);
                         }
                     }
-                    if (g + 1 < NG) ptx::tmem_wait_ld();
+                };
+                if constexpr (EPW == 8) {
+                    // 32-column groups, double-buffered: tcgen05.wait::ld covers every
+                    // outstanding load, so group g+1's loads are issued before group g's math
+                    constexpr int G = 32, NG = CW / G;
+                    uint32_t rb[2][G];
+                    ptx::tmem_ld16(taddr, *reinterpret_cast<uint32_t (*)[16]>(&rb[0][0]));
+                    ptx::tmem_ld16(taddr + 16, *reinterpret_cast<uint32_t (*)[16]>(&rb[0][16]));
+#pragma unroll
+                    for (int g = 0; g < NG; g++) {
+                        ptx::tmem_wait_ld();
+                        if (g + 1 < NG) {
+                            ptx::tmem_ld16(taddr + (g + 1) * G, *reinterpret_cast<uint32_t (*)[16]>(&rb[(g + 1) & 1][0]));
+                            ptx::tmem_ld16(taddr + (g + 1) * G + 16,
+                                           *reinterpret_cast<uint32_t (*)[16]>(&rb[(g + 1) & 1][16]));
+                        }
+                        promote(rb[g & 1], g * G, G);
+                    }
+                } else {
+                    // 16-column groups, one in flight: the four warps of each SM
+                    // sub-partition interleave their load / promote phases
+                    constexpr int G = 16, NG = CW / G;
+#pragma unroll
+                    for (int g = 0; g < NG; g++) {
+                        uint32_t r[G];
+                        ptx::tmem_ld16(taddr + g * G, r);
+                        ptx::tmem_wait_ld();
+                        promote(r, g * G, G);
+                    }
                 }
-                if (SEEDED) seed(taddr);
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive_cluster(buf ? seg_empty1 : seg_empty0);   // the leader's barrier
@@ -603,6 +551,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
             if constexpr (OUTM == 2) {
                 // block absmax of the bf16-rounded values (rows >= M excluded) over
                 // the 4 row-quarter warps of this column half (named barrier per half)
+                const int half = cg;
                 const bool rok = row0 + lane < M;
                 float am = 0.0f;
 #pragma unroll
@@ -642,18 +591,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
                 }
                 continue;
             }
-            constexpr int CPC = OUT_BF16 ? 64 : 32;
-            static_assert(!TB_W8_STG2 || (CW / CPC) % 2 == 0, "chunk count per tile must be even");
+            constexpr int CPC = OUT_BF16 ? 64 : 32;             // columns per 128-B staged row
+            static_assert(!C::STG2 || (CW / CPC) % 2 == 0, "chunk count per tile must be even");
 #pragma unroll
             for (int ch = 0; ch < CW / CPC; ch++) {
-#if TB_W8_STG2
-                uint8_t *stg = (ch & 1) ? S.stage_out2[ew] : S.stage_out[ew];
-                const uint32_t stg_s = ptx::smem_u32(stg);
-                if (lane == 0) ptx::bulk_wait_read1();         // the store that last used this buffer has read it
-#else
-                uint8_t *stg = S.stage_out[ew];
-                if (lane == 0) ptx::bulk_wait_read0();
-#endif
+                uint8_t *stg = (C::STG2 && (ch & 1)) ? S.stage_out2[C::STG2 ? ew : 0] : S.stage_out[ew];
+                const uint32_t stg_c = ptx::smem_u32(stg);
+                if (lane == 0) {
+                    if (C::STG2) ptx::bulk_wait_read1();        // the store that last used this buffer has read it
+                    else ptx::bulk_wait_read0();
+                }
                 __syncwarp();
 #pragma unroll
                 for (int u = 0; u < 8; u++) {
@@ -671,7 +618,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
                         w0 = __float_as_uint(acc2[p].x); w1 = __float_as_uint(acc2[p].y);
                         w2 = __float_as_uint(acc2[p + 1].x); w3 = __float_as_uint(acc2[p + 1].y);
                     }
-                    const uint32_t dst = stg_s + lane * 128 + ((u ^ (lane & 7)) * 16);
+                    const uint32_t dst = stg_c + lane * 128 + ((u ^ (lane & 7)) * 16);
                     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" :: "r"(dst), "r"(w0), "r"(w1), "r"(w2),
                                  "r"(w3) : "memory");
                 }
@@ -694,6 +641,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1) w
                     ptx::bulk_commit();
                 }
             }
+            (void)stg_s;
         }
         if (lane == 0) ptx::bulk_wait_read0();
     }
@@ -826,9 +774,11 @@ int w8a8_dispatch(const int8_t *a, const float *sa, const int8_t *bt, const floa
         memset(&no_peers, 0, sizeof(no_peers));
 #define TB_GEMM2(E, B)                                                                                     \
     {                                                                                                      \
-        auto kern = w8a8_2sm_kernel<E, (B) ? 1 : 0>;                                                       \
-        smem_attr(kern, (int)gemm2::SMEM_BYTES);   \
-        kern<<<grid, gemm2::THREADS, gemm2::SMEM_BYTES, st>>>(ta, tbm, tout, sa, sb, bias, (int)M, (int)N, (int)K, \
+        constexpr int EPW = (E) ? TB_W8_EPW_EXACT : TB_W8_EPW_FAST;                                       \
+        auto kern = w8a8_2sm_kernel<E, (B) ? 1 : 0, EPW>;                                                  \
+        smem_attr(kern, (int)gemm2::smem_bytes<EPW>());                                                    \
+        kern<<<grid, gemm2::Cfg<EPW>::THREADS, gemm2::smem_bytes<EPW>(), st>>>(                            \
+            ta, tbm, tout, sa, sb, bias, (int)M, (int)N, (int)K,                                           \
                                                               (int)plane, act, nullptr, no_peers);               \
     }
         if (exact && !obf) TB_GEMM2(true, false)
@@ -927,11 +877,11 @@ extern "C" int tb_w8a8_gemm_quant(const int8_t *a, const float *sa, const int8_t
     const int ntiles = (int)(cdiv(M, 256) * (N / 256));
     int clusters = num_sms() / 2;
     if (ntiles < clusters) clusters = ntiles;
-    auto kern = w8a8_2sm_kernel<false, 2>;
-    smem_attr(kern, (int)gemm2::SMEM_BYTES);
+    auto kern = w8a8_2sm_kernel<false, 2, 8>;
+    smem_attr(kern, (int)gemm2::smem_bytes<8>());
     PeerMaps no_peers;
     memset(&no_peers, 0, sizeof(no_peers));
-    kern<<<2 * clusters, gemm2::THREADS, gemm2::SMEM_BYTES, as_stream(stream)>>>(
+    kern<<<2 * clusters, gemm2::Cfg<8>::THREADS, gemm2::smem_bytes<8>(), as_stream(stream)>>>(
         ta, tbm, tout, sa, sb, bias, (int)M, (int)N, (int)K, 0, act, scales_out, no_peers);
     return check_launch("w8a8_gemm_quant");
 }
@@ -968,9 +918,10 @@ extern "C" int tb_w8a8_gemm_qkv_peers(const int8_t *a, const float *sa, const in
     const int ntiles = (int)(cdiv(M, 256) * (N / 256));
     int clusters = num_sms() / 2;
     if (ntiles < clusters) clusters = ntiles;
-    auto kern = w8a8_2sm_kernel<false, 1>;
-    smem_attr(kern, (int)gemm2::SMEM_BYTES);
-    kern<<<2 * clusters, gemm2::THREADS, gemm2::SMEM_BYTES, as_stream(stream)>>>(
+    auto kern = w8a8_2sm_kernel<false, 1, TB_W8_EPW_FAST>;
+    smem_attr(kern, (int)gemm2::smem_bytes<TB_W8_EPW_FAST>());
+    kern<<<2 * clusters, gemm2::Cfg<TB_W8_EPW_FAST>::THREADS, gemm2::smem_bytes<TB_W8_EPW_FAST>(),
+           as_stream(stream)>>>(
         ta, tbm, ta, sa, sb, bias, (int)M, (int)N, (int)K, 128, 0, nullptr, pm);
     return check_launch("w8a8_gemm_qkv_peers");
 }

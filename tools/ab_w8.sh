@@ -7,7 +7,7 @@ for v in "$@"; do
   if [ $v = base ]; then unset TB200_LIB; else export TB200_LIB=$PWD/paper_2512_16093_b200/libtb200_$v.so; fi
   echo "== $v"
   for sh in 32760x1536x1536 32760x1536x4608 32760x1536x8960 32760x8960x1536 75600x5120x15360 75600x13824x5120; do
-    python tools/bench_gemm.py $sh 2>&1 | python -c "
+    timeout 120 python tools/bench_gemm.py $sh 2>&1 | python -c "
 import sys, json
 for l in sys.stdin:
     if not l.startswith('{'):
