@@ -263,6 +263,10 @@ int tb_cast_bf16(const float *x, int64_t n, void *y, void *stream);
 int tb_host_stage(void *dst, const void *src, int64_t n, int src_dtype, int dst_dtype, int64_t nthreads);
 int64_t tb_host_threads(void);
 
+/* Instrumentation: writes the device %globaltimer (ns) to *dst when the
+ * one-thread kernel runs on `stream` (graph-capturable stream timeline). */
+int tb_timestamp(unsigned long long *dst, void *stream);
+
 int tb_pair_union(const int32_t *idx, int64_t H, int64_t nq, int64_t count, int32_t *pair_idx,
                   int32_t *pair_cnt, int64_t pair_ld, void *stream);
 

@@ -50,6 +50,7 @@ SIGNATURES = {
     "tb_cast_bf16": [_P, _I, _P, _P],
     "tb_host_stage": [_P, _P, _I, _i, _i, _I],
     "tb_host_threads": [],
+    "tb_timestamp": [_P, _P],
     "tb_sla_path": [_P],
     "tb_ulysses_shard": [_I, _I, _I],
     "tb_ulysses_workspace_bytes": [_I, _I, _I, _I, _I, _I],

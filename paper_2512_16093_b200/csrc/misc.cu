@@ -458,6 +458,15 @@ __global__ void __cluster_dims__(ANQ_CLUSTER, 1, 1) __launch_bounds__(ANQ_ROWS *
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// Instrumentation (tools/step_ablate.py): the %globaltimer value when this
+// one-thread kernel runs on its stream -- usable inside CUDA graphs, where
+// event timing is not.
+__global__ void timestamp_kernel(unsigned long long *dst) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    *dst = t;
+}
+
 __global__ void gelu_kernel(const float *__restrict__ x, int64_t n, float *__restrict__ out) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -552,6 +561,11 @@ extern "C" int tb_gelu(const float *x, int64_t n, float *out, void *stream) {
     if (n == 0) return TB_OK;
     gelu_kernel<<<(unsigned)cdiv(n, 256), 256, 0, as_stream(stream)>>>(x, n, out);
     return check_launch("gelu");
+}
+
+extern "C" int tb_timestamp(unsigned long long *dst, void *stream) {
+    timestamp_kernel<<<1, 1, 0, as_stream(stream)>>>(dst);
+    return check_launch("timestamp");
 }
 
 extern "C" int tb_add_norm(const float *x, const float *y, const float *emb, float alpha, const float *gain,
