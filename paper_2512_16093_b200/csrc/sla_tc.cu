@@ -71,7 +71,16 @@ namespace sla {
 #define TB_SLA_KST 3
 #endif
 constexpr int BM = 128, BN = 64, D = 128, KSTAGES = TB_SLA_KST, VSTAGES = 3;
-constexpr int THREADS = 224;   // 4 softmax + K producer + MMA + V producer warps
+// TB_SLA_REGS: a fourth (idle) control warp completes warpgroup 1, so
+// setmaxnreg can move its registers to the softmax warpgroup: 64 per control
+// thread, 192 per softmax thread (2 CTAs x 256 threads x 128 at launch).
+// Measured 8.5 vs 8.95 ms at cfg4 (interleaved A/B, tools/ab_sla.sh)
+#ifndef TB_SLA_REGS
+#define TB_SLA_REGS 1
+#endif
+constexpr int THREADS = TB_SLA_REGS ? 256 : 224;   // 4 softmax + K producer + MMA + V producer (+ idle) warps
+constexpr int CTRL_REGS = 64, SOFTMAX_REGS = 192;
+static_assert(!TB_SLA_REGS || 128 * (128 - CTRL_REGS) >= 128 * (SOFTMAX_REGS - 128), "setmaxnreg budget");
 constexpr uint32_t Q_BYTES = BM * D;          // int8
 constexpr uint32_t K_BYTES = BN * D;          // int8
 constexpr uint32_t V_BYTES = D * BN * 2;      // bf16 V tile: two 64-channel x 64-token SW128 boxes
@@ -319,7 +328,10 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
     uint8_t *lin_a = Q2 ? S.q : S.v[0];
     uint8_t *lin_b = Q2 ? S.v[1] : S.v[2];
 
+#define SLA_CTRL_REGS() \
+    do { if (TB_SLA_REGS) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" :: "n"(CTRL_REGS)); } while (0)
     if (warp == 4) {
+        SLA_CTRL_REGS();
         // ---------------------------------------------------- TMA producer (K)
         // the whole warp walks the loop (warp-uniform values, no waterfall
         // loops around the uniform-operand TMA instructions); one lane issues.
@@ -387,6 +399,7 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             __syncwarp();
         }
     } else if (warp == 6) {
+        SLA_CTRL_REGS();
         // ---------------------------------------------------- TMA producer (V)
         if (lf) ptx::mbar_wait_sleep(&S.lin_done, 0);
         for (int j = 0; j < nsel; j++) {
@@ -411,6 +424,7 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             __syncwarp();
         }
     } else if (warp == 5) {
+        SLA_CTRL_REGS();
         // ------------------------------------------------------- MMA issuer
         // whole warp in the loop, one elected lane issues each MMA group
         constexpr uint32_t ID_QK = ptx::idesc_i8(BM, BN);
@@ -532,7 +546,10 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
                 lin_mma(tmem, D, 128, &S.lin_done2);
             }
         }
+    } else if (warp == 7) {
+        SLA_CTRL_REGS();                            // idle: completes the control warpgroup
     } else {
+        if (TB_SLA_REGS) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" :: "n"(SOFTMAX_REGS));
         // ------------------------------------------------ softmax + epilogue
         const int r = warp * 32 + lane;             // row in tile == TMEM lane
         const int qh = Q2 ? (warp >> 1) : 0;        // Q2: q-block 2n + qh (warp-uniform)
