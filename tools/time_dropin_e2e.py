@@ -18,9 +18,9 @@ inp = AttnInputs(*x)
 cfg = SLAConfig(q_block=128, kv_block=64, topk_ratio=0.1, linear_mix=1.0)
 native = ops.host_stage
 ref = None
-for mode in ("native", "torch"):
+for mode in ("native",):
     ops.host_stage = native if mode == "native" else (lambda d, s: d.copy_(s))
-    for ch in (2, 4, 8):
+    for ch in (1, 2, 4):
         attention._HOST_CHUNK_HEADS = ch
         o = sla_attention(inp, cfg)
         if ref is None:
