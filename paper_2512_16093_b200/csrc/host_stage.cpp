@@ -26,6 +26,8 @@
 #include <thread>
 #include <vector>
 
+#include <unistd.h>
+
 #include "../../include/tb_capi.h"
 
 namespace {
@@ -102,9 +104,14 @@ class Pool {
 
 Pool &pool(int want) {
     static Pool *p = nullptr;
+    static pid_t owner = 0;
     static std::mutex m;
     std::lock_guard<std::mutex> g(m);
+    // a forked child inherits the pointer but not the worker threads: start a
+    // fresh pool there (the parent's object is left alone)
+    if (p != nullptr && owner != getpid()) p = nullptr;
     if (p == nullptr) {
+        owner = getpid();
         int n = want;
         if (n <= 0) {
             const char *e = getenv("TB_HOST_THREADS");
