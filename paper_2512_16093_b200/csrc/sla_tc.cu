@@ -79,7 +79,13 @@ constexpr int BM = 128, BN = 64, D = 128, KSTAGES = TB_SLA_KST, VSTAGES = 3;
 #define TB_SLA_REGS 1
 #endif
 constexpr int THREADS = TB_SLA_REGS ? 256 : 224;   // 4 softmax + K producer + MMA + V producer (+ idle) warps
-constexpr int CTRL_REGS = 64, SOFTMAX_REGS = 192;
+#ifndef TB_SLA_CTRL_REGS
+#define TB_SLA_CTRL_REGS 64
+#endif
+#ifndef TB_SLA_SETMAXNREG
+#define TB_SLA_SETMAXNREG 1
+#endif
+constexpr int CTRL_REGS = TB_SLA_CTRL_REGS, SOFTMAX_REGS = 128 + (128 - TB_SLA_CTRL_REGS);
 static_assert(!TB_SLA_REGS || 128 * (128 - CTRL_REGS) >= 128 * (SOFTMAX_REGS - 128), "setmaxnreg budget");
 constexpr uint32_t Q_BYTES = BM * D;          // int8
 constexpr uint32_t K_BYTES = BN * D;          // int8
@@ -329,7 +335,7 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
     uint8_t *lin_b = Q2 ? S.v[1] : S.v[2];
 
 #define SLA_CTRL_REGS() \
-    do { if (TB_SLA_REGS) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" :: "n"(CTRL_REGS)); } while (0)
+    do { if (TB_SLA_REGS && TB_SLA_SETMAXNREG) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" :: "n"(CTRL_REGS)); } while (0)
     if (warp == 4) {
         SLA_CTRL_REGS();
         // ---------------------------------------------------- TMA producer (K)
@@ -549,7 +555,7 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
     } else if (warp == 7) {
         SLA_CTRL_REGS();                            // idle: completes the control warpgroup
     } else {
-        if (TB_SLA_REGS) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" :: "n"(SOFTMAX_REGS));
+        if (TB_SLA_REGS && TB_SLA_SETMAXNREG) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" :: "n"(SOFTMAX_REGS));
         // ------------------------------------------------ softmax + epilogue
         const int r = warp * 32 + lane;             // row in tile == TMEM lane
         const int qh = Q2 ? (warp >> 1) : 0;        // Q2: q-block 2n + qh (warp-uniform)
