@@ -1,5 +1,5 @@
 """cfg4 coverage GEMM (cov . kv_part, 40 heads) alone and the full step, CUDA
-graph replay; TB_GEMM_2SM selects the CTA-pair kernel (tools only)."""
+graph replay (tools only)."""
 import os
 import sys
 
@@ -40,5 +40,5 @@ def graph_ms(fn, reps=10):
 
 gemm = graph_ms(lambda: ops.linear_kv_sel(kv_part, cov, nkv))
 step = graph_ms(lambda: ops.sla_attention(q, k, v, 128, 64, 0.1, 1.0, out_dtype=torch.bfloat16))
-print(f"TB_GEMM_2SM={os.environ.get('TB_GEMM_2SM', '1')}: coverage GEMM {gemm:.3f} ms ({0.9296e3 / gemm:.0f} TFLOP/s), "
+print(f"coverage GEMM {gemm:.3f} ms ({0.9296e3 / gemm:.0f} TFLOP/s), "
       f"step {step:.3f} ms")
