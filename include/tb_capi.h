@@ -245,6 +245,24 @@ int tb_nccl_unique_id(void *id128);
 int tb_nccl_comm_init(void **comm, const void *id128, int64_t nranks, int64_t rank);
 int tb_nccl_comm_destroy(void *comm);
 
+/* The whole sla_attention (attention.py:392-421) in one stream-ordered call
+ * (SURVEY.md §8 b4 tb_sla_sage_fwd): k_mean and the smoothed K codes, the Q
+ * pool + codes, the K pool, the top-k selection and coverage matrix, the
+ * linear branch's kv_part and coverage GEMM, the q_block-64 pair unions, and
+ * the fused tcgen05 kernel -- the sequence ops.sla_attention issues, with two
+ * internal helper streams forked from and joined back into `stream` by events
+ * (graph-capturable).  count = ceil(topk_ratio * num_kv) in double precision
+ * (attention.py:279).  Every intermediate lives in `workspace` (256-byte
+ * aligned, at least tb_sla_workspace_bytes(...) bytes, SURVEY b4
+ * tb_workspace_bytes); nothing is allocated.  Tensor-core envelope only (d 128,
+ * kv_block 64, q_block 128 or 64, quantized branch): TB_EUNSUPPORTED otherwise.
+ * q, k, v [H, L, d] f32 or bf16; out [H, L, d] f32 or bf16. */
+int64_t tb_sla_workspace_bytes(int64_t H, int64_t L, int64_t d, int64_t q_block, int64_t kv_block, double topk_ratio,
+                               float linear_mix, int dtype);
+int tb_sla_forward(const void *q, const void *k, const void *v, int dtype, int64_t H, int64_t L, int64_t d,
+                   int64_t q_block, int64_t kv_block, double topk_ratio, float linear_mix, float scale,
+                   void *workspace, int64_t workspace_bytes, void *out, int out_dtype, void *stream);
+
 /* 1 when tb_sla_attention would run these arguments on the tcgen05 kernel,
  * 0 for the CUDA-core kernel. */
 int tb_sla_path(const tb_sla_args *a);

@@ -51,6 +51,8 @@ SIGNATURES = {
     "tb_host_stage": [_P, _P, _I, _i, _i, _I],
     "tb_host_threads": [],
     "tb_timestamp": [_P, _P],
+    "tb_sla_workspace_bytes": [_I, _I, _I, _I, _I, ctypes.c_double, _f, _i],
+    "tb_sla_forward": [_P, _P, _P, _i, _I, _I, _I, _I, _I, ctypes.c_double, _f, _f, _P, _I, _P, _i, _P],
     "tb_sla_path": [_P],
     "tb_ulysses_shard": [_I, _I, _I],
     "tb_ulysses_workspace_bytes": [_I, _I, _I, _I, _I, _I],
@@ -80,7 +82,7 @@ SIGNATURES = {
     "tb_gelu": [_P, _I, _P, _P],
 }
 _RESTYPES = {"tb_last_error": ctypes.c_char_p, "tb_build_info": ctypes.c_char_p,
-             "tb_ulysses_shard": ctypes.c_int64, "tb_host_threads": ctypes.c_int64, "tb_ulysses_workspace_bytes": ctypes.c_int64}
+             "tb_ulysses_shard": ctypes.c_int64, "tb_host_threads": ctypes.c_int64, "tb_sla_workspace_bytes": ctypes.c_int64, "tb_ulysses_workspace_bytes": ctypes.c_int64}
 
 
 class SlaArgs(ctypes.Structure):

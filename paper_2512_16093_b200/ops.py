@@ -609,6 +609,34 @@ def sla_attention(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: fl
     return (out, out_scales) if q8 else out
 
 
+def sla_forward(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: float = 0.1, linear_mix: float = 1.0,
+                scale: float | None = None, out_dtype=torch.float32):
+    """The single-call C-ABI pipeline (tb_sla_forward: every prep pass and the
+    fused kernel, intermediates in one workspace from tb_sla_workspace_bytes)
+    on device tensors [H, L, d] -- what a non-Python host binds.  Same kernels
+    and values as sla_attention on the tensor-core envelope."""
+    q, k, v = _dev_tensor(q, "q"), _dev_tensor(k, "k"), _dev_tensor(v, "v")
+    if not (q.shape == k.shape == v.shape) or q.dim() != 3:
+        raise ValueError("q/k/v must share shape [heads, seq, head_dim]")
+    if k.dtype != q.dtype:
+        k = k.to(q.dtype)
+    if v.dtype != q.dtype:
+        v = v.to(q.dtype)
+    H, L, d = q.shape
+    scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+    lib = _lib.load(require_device=True)
+    nbytes = lib.tb_sla_workspace_bytes(H, L, d, q_block, kv_block, float(topk_ratio), float(linear_mix),
+                                        dtype_code(q))
+    if nbytes < 0:
+        _lib.check(int(nbytes), "tb_sla_workspace_bytes")
+    ws = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=q.device)
+    out = torch.empty((H, L, d), dtype=out_dtype, device=q.device)
+    call("tb_sla_forward", ptr(q), ptr(k), ptr(v), dtype_code(q), H, L, d, q_block, kv_block, float(topk_ratio),
+         float(linear_mix), scale, ptr(ws), int(nbytes), ptr(out), TB_BF16 if out_dtype == torch.bfloat16 else TB_F32,
+         stream_ptr())
+    return out
+
+
 _AUX = {}
 
 

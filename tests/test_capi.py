@@ -94,3 +94,25 @@ def test_host_stage_copy_and_bf16_rounding():
     assert lib.tb_host_stage(o8.ctypes.data, i8.ctypes.data, i8.size, _lib.TB_I8, _lib.TB_I8, 0) == 0
     assert np.array_equal(o8, i8)
     assert lib.tb_host_stage(o8.ctypes.data, i8.ctypes.data, i8.size, _lib.TB_I8, _lib.TB_F32, 0) == _lib.TB_EINVAL
+
+
+def test_sla_workspace_bytes_host_only():
+    """tb_sla_workspace_bytes (SURVEY §8 b4 tb_workspace_bytes): sizes of every
+    intermediate tb_sla_forward carves out of the caller's workspace, computed
+    on the host (no device); bad ratios map to TB_EINVAL."""
+    from paper_2512_16093_b200 import _lib
+    lib = _lib.load()
+    H, L, d = 40, 75600, 128
+    nkv, nq = -(-L // 64), -(-L // 128)
+    count = -(-int(0.1 * nkv * 10) // 10)
+    n = lib.tb_sla_workspace_bytes(H, L, d, 128, 64, 0.1, 1.0, _lib.TB_BF16)
+    # at least the codes, kv_part and KV_sel (the big ones)
+    assert n >= 2 * H * L * d + H * nkv * 130 * d * 2 + H * nq * 130 * d * 2
+    assert n < 4 * H * L * d + 2 * (H * nkv * 130 * d * 2) + (1 << 30)
+    assert n % 256 == 0
+    assert lib.tb_sla_workspace_bytes(H, L, d, 128, 64, 0.1, 1.0, _lib.TB_F32) > n     # + bf16 copies of k, v
+    assert lib.tb_sla_workspace_bytes(H, L, d, 128, 64, 0.1, 0.0, _lib.TB_BF16) < n    # no linear branch
+    assert lib.tb_sla_workspace_bytes(H, L, d, 64, 64, 0.1, 1.0, _lib.TB_BF16) > 0
+    assert lib.tb_sla_workspace_bytes(H, L, d, 128, 64, 0.0, 1.0, _lib.TB_BF16) == _lib.TB_EINVAL
+    assert lib.tb_sla_workspace_bytes(H, L, d, 128, 64, 1.5, 1.0, _lib.TB_BF16) == _lib.TB_EINVAL
+    assert count == 119
