@@ -281,6 +281,14 @@ int tb_cast_bf16(const float *x, int64_t n, void *y, void *stream);
 int tb_host_stage(void *dst, const void *src, int64_t n, int src_dtype, int dst_dtype, int64_t nthreads);
 int64_t tb_host_threads(void);
 
+/* Lossless narrow upload encoding for the same staging step: when every one of
+ * the n f32 values in src is exactly representable in bf16 (low 16 bits zero --
+ * activations of a bf16 model handed over as f32 arrays), writes their bf16
+ * bit patterns to dst and returns 1; otherwise returns 0 and dst is
+ * unspecified (the caller stages f32).  The device widens bf16 -> f32
+ * exactly, so the kernels see the caller's f32 values either way. */
+int tb_host_stage_bf16_exact(void *dst, const float *src, int64_t n, int64_t nthreads);
+
 /* Instrumentation: writes the device %globaltimer (ns) to *dst when the
  * one-thread kernel runs on `stream` (graph-capturable stream timeline). */
 int tb_timestamp(unsigned long long *dst, void *stream);

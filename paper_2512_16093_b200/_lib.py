@@ -50,6 +50,7 @@ SIGNATURES = {
     "tb_cast_bf16": [_P, _I, _P, _P],
     "tb_host_stage": [_P, _P, _I, _i, _i, _I],
     "tb_host_threads": [],
+    "tb_host_stage_bf16_exact": [_P, _P, _I, _I],
     "tb_timestamp": [_P, _P],
     "tb_sla_workspace_bytes": [_I, _I, _I, _I, _I, ctypes.c_double, _f, _i],
     "tb_sla_forward": [_P, _P, _P, _i, _I, _I, _I, _I, _I, ctypes.c_double, _f, _f, _P, _I, _P, _i, _P],

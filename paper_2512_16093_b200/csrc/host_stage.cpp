@@ -6,10 +6,15 @@
 // page-locked staging buffers and uploaded from there at PCIe rate.  That copy
 // (and, for V, the f32 -> bf16 rounding the kernels consume) is host-memory
 // bound: a persistent pool of worker threads splits it into
-// spans (1 Mi elements each) and writes the staging buffer with non-temporal stores (no
+// spans (64 Ki elements each) and writes the staging buffer with non-temporal stores (no
 // read-for-ownership of the destination lines, which would otherwise add a
 // third of the traffic and contend with the DMA engine reading the previous
 // chunk out of the same memory).
+//
+// bf16-valued f32 arrays (low 16 bits zero -- a bf16 model's activations handed
+// over as f32) can be staged as their bf16 bit patterns instead
+// (tb_host_stage_bf16_exact): lossless, half the PCIe bytes; the check rides
+// along with the copy and gives up at the first inexact value.
 //
 // Not a compute path: the values are moved (or rounded to bf16 exactly like
 // __float2bfloat16_rn / torch's cast), never computed on.
@@ -174,6 +179,47 @@ __attribute__((target("avx2"))) void to_bf16_avx2(uint16_t *dst, const float *sr
     _mm_sfence();
 }
 
+// f32 -> bf16 when every value is exactly representable (low 16 bits zero):
+// the upper halves, streamed; false as soon as a 1 K-element run holds a value
+// that is not (the destination is then unspecified)
+__attribute__((target("avx2"))) bool to_bf16_exact_avx2(uint16_t *dst, const float *src, int64_t n) {
+    const uint32_t *u = reinterpret_cast<const uint32_t *>(src);
+    int64_t i = 0;
+    for (; i < n && ((uintptr_t)(dst + i) & 31); i++) {
+        if (u[i] & 0xFFFFu) return false;
+        dst[i] = (uint16_t)(u[i] >> 16);
+    }
+    const __m256i low = _mm256_set1_epi32(0xFFFF);
+    while (i + 16 <= n) {
+        const int64_t run = std::min<int64_t>(n - (n - i) % 16, i + 1024);
+        __m256i seen = _mm256_setzero_si256();
+        for (; i < run; i += 16) {
+            const __m256i a = _mm256_loadu_si256((const __m256i *)(u + i));
+            const __m256i b = _mm256_loadu_si256((const __m256i *)(u + i + 8));
+            seen = _mm256_or_si256(seen, _mm256_or_si256(a, b));
+            const __m256i pk = _mm256_permute4x64_epi64(
+                _mm256_packus_epi32(_mm256_srli_epi32(a, 16), _mm256_srli_epi32(b, 16)), 0xD8);
+            _mm256_stream_si256((__m256i *)(dst + i), pk);
+        }
+        if (!_mm256_testz_si256(seen, low)) { _mm_sfence(); return false; }
+    }
+    for (; i < n; i++) {
+        if (u[i] & 0xFFFFu) { _mm_sfence(); return false; }
+        dst[i] = (uint16_t)(u[i] >> 16);
+    }
+    _mm_sfence();
+    return true;
+}
+
+bool to_bf16_exact_scalar(uint16_t *dst, const float *src, int64_t n) {
+    const uint32_t *u = reinterpret_cast<const uint32_t *>(src);
+    for (int64_t i = 0; i < n; i++) {
+        if (u[i] & 0xFFFFu) return false;
+        dst[i] = (uint16_t)(u[i] >> 16);
+    }
+    return true;
+}
+
 void copy_scalar(uint8_t *dst, const uint8_t *src, int64_t bytes) { std::memcpy(dst, src, (size_t)bytes); }
 void to_bf16_scalar(uint16_t *dst, const float *src, int64_t n) {
     for (int64_t i = 0; i < n; i++) dst[i] = bf16_rn(src[i]);
@@ -184,7 +230,10 @@ bool have_avx2() {
     return ok;
 }
 
-constexpr int64_t SPAN = 1 << 18;                         // elements per work item (1 MB of f32)
+// elements per work item (256 KB of f32): ~18 spans per thread for a 2-head
+// cfg4 chunk keeps the 16 threads evenly loaded (2^18: 74 spans, 5 rounds with
+// the last one 10/16 full -- 73 vs 75 ms drop-in e2e; 2^20: 86 ms)
+constexpr int64_t SPAN = 1 << 16;
 
 }  // namespace
 
@@ -220,3 +269,25 @@ extern "C" int tb_host_stage(void *dst, const void *src, int64_t n, int src_dtyp
 }
 
 extern "C" int64_t tb_host_threads(void) { return pool(0).size(); }
+
+extern "C" int tb_host_stage_bf16_exact(void *dst, const float *src, int64_t n, int64_t nthreads) {
+    if (n < 0 || (n > 0 && (dst == nullptr || src == nullptr))) return TB_EINVAL;
+    if (n == 0) return 1;
+    const int64_t parts = (n + SPAN - 1) / SPAN;
+    Pool &p = pool((int)nthreads);
+    const bool v = have_avx2();
+    std::atomic<bool> inexact{false};
+    auto body = [&](int i) {
+        if (inexact.load(std::memory_order_relaxed)) return;     // another span already failed
+        const int64_t a = (int64_t)i * SPAN, z = std::min(n, a + SPAN);
+        uint16_t *d = (uint16_t *)dst + a;
+        const bool ok = v ? to_bf16_exact_avx2(d, src + a, z - a) : to_bf16_exact_scalar(d, src + a, z - a);
+        if (!ok) inexact.store(true, std::memory_order_relaxed);
+    };
+    if (parts == 1 || p.size() == 1) {
+        for (int i = 0; i < (int)parts && !inexact.load(); i++) body(i);
+    } else {
+        p.run((int)parts, body);
+    }
+    return inexact.load() ? 0 : 1;
+}

@@ -10,6 +10,8 @@ a CUDA device and the library must be built (no fallback).
 from __future__ import annotations
 
 import math
+import os
+import time
 
 import torch
 
@@ -663,6 +665,15 @@ def host_stage(dst: torch.Tensor, src: torch.Tensor) -> torch.Tensor:
     return dst
 
 
+# tools: set to a dict to accumulate sla_attention_host's host wall time per
+# phase (stage / wait_upload / enqueue / wait_d2h), seconds
+HOST_PROFILE: dict | None = None
+
+# bytes the last sla_attention_host call moved across PCIe (and how many head
+# chunks took the lossless bf16 upload), for the e2e report
+LAST_HOST_TRANSFER: dict = {}
+
+
 def sla_attention_host(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: float = 0.1,
                        linear_mix: float = 1.0, quantized: bool = True, scale: float | None = None,
                        out: torch.Tensor | None = None, out_dtype=torch.bfloat16, chunk_heads: int = 4):
@@ -698,6 +709,11 @@ def sla_attention_host(q, k, v, q_block: int = 64, kv_block: int = 64, topk_rati
     v_half = (q.dtype == torch.float32 and not pinned_in and
               tc_envelope(ch, L, d, q_block, kv_block, topk_count(topk_ratio, nkv), quantized))
     dts = (q.dtype, k.dtype, torch.bfloat16 if v_half else v.dtype)
+    # bf16-valued f32 q / k (a bf16 model's activations handed over as f32
+    # arrays) cross PCIe as their exact bf16 bit patterns, checked per chunk
+    # while staging (tb_host_stage_bf16_exact); the bf16 kernels widen them
+    # back exactly, so the result is the f32 path's.  Anything else ships f32.
+    narrow = v_half and k.dtype == torch.float32 and q.is_contiguous() and k.is_contiguous()
     bufs = [[torch.empty((ch, L, d), dtype=dt, device=dev) for dt in dts] for _ in range(2)]
     stage_in = None if pinned_in else \
         [[torch.empty((ch, L, d), dtype=dt, pin_memory=True) for dt in dts] for _ in range(2)]
@@ -706,30 +722,71 @@ def sla_attention_host(q, k, v, q_block: int = 64, kv_block: int = 64, topk_rati
     ev_done = [torch.cuda.Event() for _ in range(2)]
     ev_out = [torch.cuda.Event() for _ in range(2)]
     pending = None                                       # (buffer, h0, h1) of a staged output not yet copied out
+    moved = LAST_HOST_TRANSFER
+    moved.update(h2d_bytes=0, d2h_bytes=0, narrow_chunks=0, chunks=cdiv(H, ch))
+
+    prof = HOST_PROFILE                                  # optional per-phase host wall times (tools)
+    tick = time.perf_counter if prof is not None else None
+
+    def mark(key, t0):
+        if prof is not None:
+            prof[key] = prof.get(key, 0.0) + tick() - t0
 
     def finish(p):
         b_, a_, z_ = p
+        t0 = tick() if tick else 0.0
         ev_out[b_].synchronize()
+        mark("wait_d2h", t0)
         out[a_:z_].copy_(stage_out[b_][:z_ - a_])
 
-    for i, h0 in enumerate(range(0, H, ch)):
-        h1 = min(H, h0 + ch)
+    def stage(i):
+        """chunk i's (sources, device destinations); pageable inputs are first
+        staged into page-locked buffer i % 2 (bf16 bit patterns when exact)"""
+        h0, h1 = i * ch, min(H, (i + 1) * ch)
         n, b = h1 - h0, i % 2
         srcs = (q[h0:h1], k[h0:h1], v[h0:h1])
-        if stage_in is not None:
-            if i >= 2:
-                ev_in[b].synchronize()                   # chunk i-2's upload has left staging buffer b
+        dsts = tuple(t[:n] for t in bufs[b])
+        if stage_in is None:
+            return srcs, dsts
+        torch.cuda.set_device(dev)                       # the worker thread's device
+        t0 = tick() if tick else 0.0
+        if i >= 2:
+            ev_in[b].synchronize()                       # chunk i-2's upload has left staging buffer b
+        mark("wait_upload", t0)
+        t0 = tick() if tick else 0.0
+        sq, sk = _bf16_view(stage_in[b][0], n), _bf16_view(stage_in[b][1], n)
+        if narrow and host_stage_bf16_exact(sq, srcs[0]) and host_stage_bf16_exact(sk, srcs[1]):
+            host_stage(stage_in[b][2][:n], srcs[2])
+            srcs = (sq, sk, stage_in[b][2][:n])
+            dsts = (_bf16_view(bufs[b][0], n), _bf16_view(bufs[b][1], n), bufs[b][2][:n])
+        else:
             for st_, src in zip(stage_in[b], srcs):
                 host_stage(st_[:n], src)
             srcs = tuple(st_[:n] for st_ in stage_in[b])
+        mark("stage", t0)
+        return srcs, dsts
+
+    nch = cdiv(H, ch)
+    # staging of chunk i+1 (host threads, GIL released in the native call) runs
+    # on a worker while this thread enqueues chunk i's upload / attention / download
+    worker = _stage_worker() if stage_in is not None and nch > 1 else None
+    staged = stage(0)
+    for i in range(nch):
+        h0, h1 = i * ch, min(H, (i + 1) * ch)
+        n, b = h1 - h0, i % 2
+        nxt = worker.submit(stage, i + 1) if worker is not None and i + 1 < nch else None
+        srcs, dsts = staged
+        t0 = tick() if tick else 0.0
         if i >= 2:
             h2d.wait_event(ev_done[b])                  # chunk i-2 has consumed device buffer b
+        moved["h2d_bytes"] += sum(t.numel() * t.element_size() for t in srcs)
+        moved["narrow_chunks"] += int(dsts[0].dtype == torch.bfloat16 and q.dtype == torch.float32)
         with torch.cuda.stream(h2d):
-            for dst, src in zip(bufs[b], srcs):
-                dst[:n].copy_(src, non_blocking=True)
+            for dst, src in zip(dsts, srcs):
+                dst.copy_(src, non_blocking=True)
             ev_in[b].record(h2d)
         compute.wait_event(ev_in[b])
-        o = sla_attention(bufs[b][0][:n], bufs[b][1][:n], bufs[b][2][:n], q_block, kv_block, topk_ratio,
+        o = sla_attention(dsts[0], dsts[1], dsts[2], q_block, kv_block, topk_ratio,
                           linear_mix, quantized, scale, out_dtype=out.dtype)
         ev_done[b].record(compute)
         d2h.wait_event(ev_done[b])
@@ -737,9 +794,15 @@ def sla_attention_host(q, k, v, q_block: int = 64, kv_block: int = 64, topk_rati
             (out[h0:h1] if stage_out is None else stage_out[b][:n]).copy_(o, non_blocking=True)
             ev_out[b].record(d2h)
         o.record_stream(d2h)
+        moved["d2h_bytes"] += o.numel() * o.element_size()
+        mark("enqueue", t0)
         if pending is not None:
             finish(pending)                              # chunk i-1: its result is (being) copied out
         pending = (b, h0, h1) if stage_out is not None else None
+        if i + 1 < nch:
+            t0 = tick() if tick else 0.0
+            staged = nxt.result() if nxt is not None else stage(i + 1)
+            mark("join_stage", t0)
     if pending is not None:
         finish(pending)
     for bb in bufs:
@@ -748,6 +811,38 @@ def sla_attention_host(q, k, v, q_block: int = 64, kv_block: int = 64, topk_rati
             t.record_stream(h2d)
     compute.wait_stream(d2h)                            # the caller's stream covers the output copy
     return out
+
+
+_WORKER = {}
+
+
+def _stage_worker():
+    """One background thread per process for sla_attention_host's staging."""
+    import concurrent.futures
+    pid = os.getpid()
+    w = _WORKER.get(pid)
+    if w is None:
+        w = _WORKER[pid] = concurrent.futures.ThreadPoolExecutor(max_workers=1, thread_name_prefix="tb-stage")
+    return w
+
+
+def _bf16_view(t: torch.Tensor, n: int) -> torch.Tensor:
+    """The first n heads' worth of a [ch, L, d] f32 buffer's bytes as a bf16 [n, L, d] tensor."""
+    return t.view(-1).view(torch.bfloat16)[: n * t.shape[1] * t.shape[2]].view(n, t.shape[1], t.shape[2])
+
+
+def host_stage_bf16_exact(dst: torch.Tensor, src: torch.Tensor) -> bool:
+    """Stage contiguous host f32 ``src`` into host bf16 ``dst`` when every value
+    is exactly representable in bf16 (tb_host_stage_bf16_exact): True and dst
+    holds the same values, or False (dst unspecified) -- the lossless narrow
+    upload encoding of bf16-valued f32 inputs."""
+    if (src.is_cuda or dst.is_cuda or src.dtype != torch.float32 or dst.dtype != torch.bfloat16
+            or dst.shape != src.shape or not (src.is_contiguous() and dst.is_contiguous())):
+        raise ValueError("host_stage_bf16_exact takes contiguous host f32 -> bf16 tensors of one shape")
+    rc = _lib.load().tb_host_stage_bf16_exact(dst.data_ptr(), src.data_ptr(), src.numel(), 0)
+    if rc < 0:
+        _lib.check(int(rc), "tb_host_stage_bf16_exact")
+    return rc == 1
 
 
 # ------------------------------------------------------------------ DiT rows

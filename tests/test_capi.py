@@ -96,6 +96,30 @@ def test_host_stage_copy_and_bf16_rounding():
     assert lib.tb_host_stage(o8.ctypes.data, i8.ctypes.data, i8.size, _lib.TB_I8, _lib.TB_F32, 0) == _lib.TB_EINVAL
 
 
+def test_host_stage_bf16_exact_detects_and_narrows():
+    """tb_host_stage_bf16_exact: bf16-valued f32 arrays (NaN / inf / -0.0 /
+    subnormal bf16 values included) come back as their bf16 bit patterns with
+    rc 1; one value with a nonzero low half anywhere (any span, any thread,
+    head / tail / aligned body) gives rc 0."""
+    import numpy as np
+    import torch
+    from paper_2512_16093_b200 import _lib
+    lib = _lib.load()
+    rng = np.random.default_rng(1)
+    for n in (0, 1, 31, 1000003, (1 << 18) * 5 + 7):
+        x = torch.from_numpy(rng.standard_normal(n).astype(np.float32)).to(torch.bfloat16).float().numpy()
+        if n > 20:
+            x[:6] = [np.nan, np.inf, -np.inf, -0.0, 9.18355e-41, 1.0]
+            x[:6] = torch.from_numpy(x[:6]).to(torch.bfloat16).float().numpy()
+        y = np.empty(n, dtype=np.uint16)
+        assert lib.tb_host_stage_bf16_exact(y.ctypes.data, x.ctypes.data, n, 0) == 1
+        assert np.array_equal(y, (x.view(np.uint32) >> 16).astype(np.uint16))
+        for pos in sorted({0, n // 3, n - 1}) if n else []:
+            z = x.copy()
+            z.view(np.uint32)[pos] |= 1
+            assert lib.tb_host_stage_bf16_exact(y.ctypes.data, z.ctypes.data, n, 0) == 0, (n, pos)
+
+
 def test_sla_workspace_bytes_host_only():
     """tb_sla_workspace_bytes (SURVEY §8 b4 tb_workspace_bytes): sizes of every
     intermediate tb_sla_forward carves out of the caller's workspace, computed

@@ -286,6 +286,23 @@ def test_sla_attention_host_pipeline_matches_device(tb):
     assert torch.equal(got, want)
 
 
+@pytest.mark.parametrize("bf16_valued_k", [True, False])
+def test_sla_attention_host_narrow_upload_is_lossless(tb, bf16_valued_k):
+    """Pageable f32 inputs (the drop-in's numpy arrays): bf16-valued q and k
+    cross PCIe as bf16 bit patterns (tb_host_stage_bf16_exact), anything else
+    as f32 -- both give exactly the device path's f32 result on the same values
+    (V rounded to bf16 either way, as the kernels read it)."""
+    q, k, v = gen.gaussian_qkv(43, 5, 1024, 128, bf16=True)
+    if not bf16_valued_k:
+        k = k + np.float32(1e-6) * np.sign(k)          # no longer bf16-exact: the f32 upload
+    hq, hk, hv = (torch.from_numpy(np.ascontiguousarray(x, np.float32)) for x in (q, k, v))
+    want = tb.sla_attention(hq.cuda(), hk.cuda(), hv.cuda().to(torch.bfloat16), 128, 64, 0.1, 1.0,
+                            out_dtype=torch.float32).cpu()
+    got = tb.sla_attention_host(hq, hk, hv, 128, 64, 0.1, 1.0, out_dtype=torch.float32, chunk_heads=2)
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)
+
+
 def test_w8a8_planar_output_and_gelu_epilogue(tb):
     """tb_w8a8_gemm_fast_ex: the planar (head-major) store equals the row-major
     result split into 128-column planes, and the fused GELU equals GELU-tanh of

@@ -28,8 +28,10 @@ def rate(fn, nbytes, reps=6):
     return nbytes * reps / (time.perf_counter() - t0) / 1e9
 
 
+xb = torch.from_numpy(x).to(torch.bfloat16).float().numpy()      # bf16-valued f32
 cases = {
     "native copy f32": (lambda: lib.tb_host_stage(pin.data_ptr(), x.ctypes.data, n, 0, 0, 0), n * 4),
+    "native f32->bf16 exact (bf16-valued)": (lambda: lib.tb_host_stage_bf16_exact(pb.data_ptr(), xb.ctypes.data, n, 0), n * 4),
     "native f32->bf16": (lambda: lib.tb_host_stage(pb.data_ptr(), x.ctypes.data, n, 0, 1, 0), n * 4),
     "torch copy_ f32": (lambda: pin.copy_(torch.from_numpy(x)), n * 4),
     "torch f32->bf16": (lambda: pb.copy_(torch.from_numpy(x)), n * 4),
@@ -49,7 +51,7 @@ with torch.cuda.stream(s):
 s.synchronize()
 h2d_alone = 3 * 4 * n * 4 / (time.perf_counter() - t0) / 1e9
 print(f"H2D pinned alone: {h2d_alone:.1f} GB/s", flush=True)
-for k in ("native copy f32", "torch copy_ f32"):
+for k in ("native copy f32", "native f32->bf16", "native f32->bf16 exact (bf16-valued)", "torch copy_ f32"):
     fn, nb = cases[k]
     with torch.cuda.stream(s):
         ev0 = torch.cuda.Event(enable_timing=True)
