@@ -295,10 +295,10 @@ __global__ void __launch_bounds__(128) pool_quant_tokens_d128_kernel(
 // one CTA per 128-token tile of one head (one Q block of 128 or two K blocks
 // of 64), 256 threads.  The 32 KB tile arrives in shared memory with one bulk
 // copy and is read twice from there:
-//   pass 1 (64 threads per block, one channel pair each): numpy's reduceat
-//          order for the pooled sum (seed + 8-accumulator pairwise body +
-//          sequential tail, both channels in f32x2 lanes) and the absmax of
-//          the (centered) values
+//   pass 1 (all threads: channel pair x a share of the 8 pairwise
+//          accumulators): numpy's reduceat order for the pooled sum (seed +
+//          8-accumulator pairwise body + sequential tail, both channels in
+//          f32x2 lanes) and the absmax of the (centered) values
 //   pass 2 (all threads, 16 channels x one token each): codes via
 //          quant_code_fast (bit-exact with the IEEE division), 16-B stores.
 template <int BLOCK>
@@ -309,7 +309,8 @@ __global__ void __launch_bounds__(256) pool_quant_tile_kernel(
     constexpr int TT = 128, NBLK = TT / BLOCK;
     __shared__ __align__(128) __nv_bfloat16 tile[TT * 128];
     __shared__ __align__(8) uint64_t full;
-    __shared__ float red[NBLK][4];
+    __shared__ float red[NBLK][2 * (256 / (64 * NBLK))];   // per warp: absmax of its values
+    __shared__ float2 part[NBLK][256 / (64 * NBLK)][64];    // per sub: its pairwise subtree
     __shared__ float bsafe[NBLK], binv[NBLK];
     __shared__ int bexact[NBLK];
     const int64_t h = blockIdx.y;
@@ -324,63 +325,97 @@ __global__ void __launch_bounds__(256) pool_quant_tile_kernel(
     __syncthreads();
     ptx::mbar_wait(&full, 0);
     const int tid = threadIdx.x;
-    // ---- pass 1: pooled sums (raw x) + absmax (centered), one channel pair per thread
-    if (tid < 64 * NBLK) {
-        const int blk = tid >> 6, cp = tid & 63;
-        const int t0 = blk * BLOCK;
-        const int e = min(BLOCK, et - t0);
-        if (e > 0) {
-            const float2 ctr = center ? *reinterpret_cast<const float2 *>(center + h * 128 + 2 * cp)
-                                      : make_float2(0.0f, 0.0f);
-            const uint32_t *col = reinterpret_cast<const uint32_t *>(tile) + cp;   // row stride 64 words
-            auto ld = [&](int t) {
-                const uint32_t w = col[(t0 + t) * 64];
-                return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
-            };
-            float am0 = 0.0f, am1 = 0.0f;
-            auto amax = [&](float2 v) {
-                am0 = fmaxf(am0, fabsf(__fsub_rn(v.x, ctr.x)));
-                am1 = fmaxf(am1, fabsf(__fsub_rn(v.y, ctr.y)));
-            };
-            const float2 seed = ld(0);
-            amax(seed);
-            const int n = e - 1;
-            float2 res = make_float2(-0.0f, -0.0f);
-            if (n >= 8) {
-                float2 r[8];
-#pragma unroll
-                for (int j = 0; j < 8; j++) { r[j] = ld(1 + j); amax(r[j]); }
-                const int full8 = n - (n % 8);
-                for (int i = 8; i < full8; i += 8) {
-#pragma unroll
-                    for (int j = 0; j < 8; j++) { const float2 w = ld(1 + i + j); r[j] = ptx::fadd2(r[j], w); amax(w); }
-                }
-                res = ptx::fadd2(ptx::fadd2(ptx::fadd2(r[0], r[1]), ptx::fadd2(r[2], r[3])),
-                                 ptx::fadd2(ptx::fadd2(r[4], r[5]), ptx::fadd2(r[6], r[7])));
-                for (int i = full8; i < n; i++) { const float2 w = ld(1 + i); res = ptx::fadd2(res, w); amax(w); }
-            } else {
-                for (int i = 0; i < n; i++) { const float2 w = ld(1 + i); res = ptx::fadd2(res, w); amax(w); }
-            }
-            if (pooled) {
-                const float2 acc = (n > 0) ? ptx::fadd2(seed, res) : seed;
-                const int64_t b = lo / BLOCK + blk;
-                const float2 pm = make_float2(__fdiv_rn(acc.x, (float)e), __fdiv_rn(acc.y, (float)e));
-                *reinterpret_cast<float2 *>(pooled + (h * nb + b) * 128 + 2 * cp) = pm;
-                if (pooled_t) {                 // [H][d][ldt] copy: the top-k kernel's coalesced operand
-                    pooled_t[(h * 128 + 2 * cp) * ldt + b] = pm.x;
-                    pooled_t[(h * 128 + 2 * cp + 1) * ldt + b] = pm.y;
-                }
-            }
-            float am = fmaxf(am0, am1);
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
-            if ((tid & 31) == 0) red[blk][(tid >> 5) & 1] = am;
+    // ---- pass 1: pooled sums (raw x) + absmax (centered).  Thread = (block,
+    // channel pair, sub): a full block's 8 pairwise accumulators are split over
+    // SUBS threads (independent chains, combined below in numpy's tree order);
+    // a ragged last block runs the whole order on its sub-0 thread.  A warp is
+    // 32 channel pairs of one (block, sub): conflict-free shared-memory reads.
+    constexpr int SUBS = 256 / (64 * NBLK), JPS = 8 / SUBS;
+    const int cp = tid & 63, grp = tid >> 6, blk = grp % NBLK, sub = grp / NBLK;
+    const int t0 = blk * BLOCK;
+    const int e = min(BLOCK, et - t0);
+    const bool whole = e == BLOCK;                           // uniform per warp
+    const float2 ctr = center ? *reinterpret_cast<const float2 *>(center + h * 128 + 2 * cp) : make_float2(0.0f, 0.0f);
+    const uint32_t *col = reinterpret_cast<const uint32_t *>(tile) + cp;   // row stride 64 words
+    auto ld = [&](int t) {
+        const uint32_t w = col[(t0 + t) * 64];
+        return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+    };
+    float am0 = 0.0f, am1 = 0.0f;
+    auto amax = [&](float2 v) {
+        am0 = fmaxf(am0, fabsf(__fsub_rn(v.x, ctr.x)));
+        am1 = fmaxf(am1, fabsf(__fsub_rn(v.y, ctr.y)));
+    };
+    auto store_pool = [&](float2 acc, int cnt) {
+        const int64_t b = lo / BLOCK + blk;
+        const float2 pm = make_float2(__fdiv_rn(acc.x, (float)cnt), __fdiv_rn(acc.y, (float)cnt));
+        *reinterpret_cast<float2 *>(pooled + (h * nb + b) * 128 + 2 * cp) = pm;
+        if (pooled_t) {                                      // [H][d][ldt] copy: the top-k kernel's coalesced operand
+            pooled_t[(h * 128 + 2 * cp) * ldt + b] = pm.x;
+            pooled_t[(h * 128 + 2 * cp + 1) * ldt + b] = pm.y;
         }
+    };
+    // full block: n = BLOCK - 1 elements after the seed, body i < FULL8 in 8 chains, tail FULL8..n-1
+    constexpr int N1 = BLOCK - 1, FULL8 = N1 - N1 % 8;
+    if (whole) {
+        float2 r[JPS];
+#pragma unroll
+        for (int u = 0; u < JPS; u++) { r[u] = ld(1 + sub * JPS + u); amax(r[u]); }
+#pragma unroll 4
+        for (int i = 8; i < FULL8; i += 8) {
+#pragma unroll
+            for (int u = 0; u < JPS; u++) { const float2 w = ld(1 + i + sub * JPS + u); r[u] = ptx::fadd2(r[u], w); amax(w); }
+        }
+        // this thread's subtree of ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7))
+        float2 p = ptx::fadd2(r[0], r[1]);
+        if constexpr (JPS == 4) p = ptx::fadd2(p, ptx::fadd2(r[2], r[3]));
+        part[blk][sub][cp] = p;
+        if (sub == 0) {
+            amax(ld(0));
+#pragma unroll
+            for (int i = FULL8; i < N1; i++) amax(ld(1 + i));
+        }
+    } else if (sub == 0 && e > 0) {
+        const float2 seed = ld(0);
+        amax(seed);
+        const int n = e - 1;
+        float2 res = make_float2(-0.0f, -0.0f);
+        if (n >= 8) {
+            float2 r[8];
+#pragma unroll
+            for (int j = 0; j < 8; j++) { r[j] = ld(1 + j); amax(r[j]); }
+            const int full8 = n - (n % 8);
+            for (int i = 8; i < full8; i += 8) {
+#pragma unroll
+                for (int j = 0; j < 8; j++) { const float2 w = ld(1 + i + j); r[j] = ptx::fadd2(r[j], w); amax(w); }
+            }
+            res = ptx::fadd2(ptx::fadd2(ptx::fadd2(r[0], r[1]), ptx::fadd2(r[2], r[3])),
+                             ptx::fadd2(ptx::fadd2(r[4], r[5]), ptx::fadd2(r[6], r[7])));
+            for (int i = full8; i < n; i++) { const float2 w = ld(1 + i); res = ptx::fadd2(res, w); amax(w); }
+        } else {
+            for (int i = 0; i < n; i++) { const float2 w = ld(1 + i); res = ptx::fadd2(res, w); amax(w); }
+        }
+        if (pooled) store_pool((n > 0) ? ptx::fadd2(seed, res) : seed, e);
+    }
+    {
+        float am = fmaxf(am0, am1);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
+        if ((tid & 31) == 0) red[blk][sub * 2 + ((tid >> 5) & 1)] = am;
+    }
+    __syncthreads();
+    if (whole && sub == 0 && pooled) {
+        float2 res = ptx::fadd2(part[blk][0][cp], part[blk][1][cp]);
+        if constexpr (SUBS == 4) res = ptx::fadd2(res, ptx::fadd2(part[blk][2][cp], part[blk][3][cp]));
+#pragma unroll
+        for (int i = FULL8; i < N1; i++) res = ptx::fadd2(res, ld(1 + i));
+        store_pool(ptx::fadd2(ld(0), res), BLOCK);
     }
     if (codes == nullptr) return;                            // pooling only (uniform)
-    __syncthreads();
     if (tid < NBLK && tid * BLOCK < et) {
-        const float am = fmaxf(red[tid][0], red[tid][1]);
+        float am = red[tid][0];
+#pragma unroll
+        for (int i = 1; i < 2 * SUBS; i++) am = fmaxf(am, red[tid][i]);
         const float s = quant_scale(am);
         scales[h * nb + lo / BLOCK + tid] = s;
         const float safe = (s == 0.0f) ? 1.0f : s;

@@ -235,9 +235,13 @@ def test_sla_topk_one_equals_dense_unquantized(tb):
 
 
 def test_gemm_bf16_batched_mn_major(tb):
-    """tcgen05 bf16 GEMM with an MN-major B operand (linear-branch coverage GEMM)."""
+    """tcgen05 bf16 GEMM with an MN-major B operand (linear-branch coverage GEMM).
+    f32 output: the 1-SM kernel; bf16 output with N % 256 == 0: the transposed
+    CTA-pair kernel (column tiles of 208 / 176 / 16 ..., ragged K blocks), which
+    must agree with the f32 result rounded to bf16 to within one bf16 ulp."""
     g = torch.Generator(device="cuda").manual_seed(3)
-    for (H, M, K, N) in ((2, 200, 300, 512), (3, 591, 1182, 256), (1, 128, 64, 256)):
+    for (H, M, K, N) in ((2, 200, 300, 512), (3, 591, 1182, 256), (1, 128, 64, 256), (2, 5, 70, 768),
+                         (1, 17, 1, 256), (2, 257, 129, 16640)):
         lda = -(-K // 8) * 8
         a = torch.zeros((H, M, lda), dtype=torch.bfloat16, device="cuda")
         a[:, :, :K] = torch.randn((H, M, K), generator=g, device="cuda").to(torch.bfloat16)
@@ -249,6 +253,9 @@ def test_gemm_bf16_batched_mn_major(tb):
         got16 = tb.gemm_bf16_batched(a, b, K=K)
         cos, _, rel1 = metrics(got16.float().cpu().numpy(), want.cpu().numpy())
         assert cos > 0.99999 and rel1 < 5e-3
+        ref16 = got.to(torch.bfloat16)
+        ulp = (ref16.float().abs() * 2.0 ** -7).clamp_min(1e-30)
+        assert ((got16.float() - ref16.float()).abs() <= ulp).all(), (H, M, K, N)
 
 
 def test_linear_kv_part_blocks(tb):

@@ -40,5 +40,5 @@ def graph_ms(fn, reps=10):
 
 gemm = graph_ms(lambda: ops.linear_kv_sel(kv_part, cov, nkv))
 step = graph_ms(lambda: ops.sla_attention(q, k, v, 128, 64, 0.1, 1.0, out_dtype=torch.bfloat16))
-print(f"coverage GEMM {gemm:.3f} ms ({0.9296e3 / gemm:.0f} TFLOP/s), "
+print(f"T2={os.environ.get('TB_GEMM_T2', '1')} coverage GEMM {gemm:.3f} ms ({0.9296e3 / gemm:.0f} TFLOP/s), "
       f"step {step:.3f} ms")
