@@ -43,6 +43,9 @@ namespace tb {
 // TB_SLA_BIAS: seed each S tile with the float bits of 1.5*2^23 through one
 // kind::f16 MMA, so the s32 scores come out of TMEM already as the floats
 // M + s (no per-element integer add in the softmax)
+#ifndef TB_SLA_UNI
+#define TB_SLA_UNI 1
+#endif
 #ifndef TB_SLA_BIAS
 #define TB_SLA_BIAS 1
 #endif
@@ -561,7 +564,18 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
         const int qh = Q2 ? (warp >> 1) : 0;        // Q2: q-block 2n + qh (warp-uniform)
         const int row = n * BM + r;                 // token index
         const bool row_ok = row < L;
+        // this warp's TMEM lane quarter, through a shuffle so it is provably
+        // warp-uniform: the tcgen05.ld/st addresses below stay in uniform registers
+        // (no R2UR per tcgen05 op in the block loop)
+#if TB_SLA_UNI
+        const uint32_t tw = __shfl_sync(0xffffffffu, tmem + ((uint32_t)(warp * 32) << 16), 0);
+        const uint32_t lane_base = 0;
+#define TMW tw
+#else
         const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+#define TMW tmem
+#endif
+        const uint32_t tw_o = TMW + (TM_O - tmem);
         const float scale2 = a.scale * LOG2E;
         // F8: V codes carry the per-head scale sv (O accumulates p * v / sv)
         const float vsc = F8 ? __ldg(a.v_scales + h) : 1.0f;
@@ -729,9 +743,9 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
 #pragma unroll 1
             for (int c = 0; c < D; c += 16) {
                 uint32_t o[16];
-                ptx::tmem_ld16(tmem + lane_base + c, o);
+                ptx::tmem_ld16(TMW + lane_base + c, o);
                 ptx::tmem_wait_ld();
-                ptx::tmem_st16(TM_O + lane_base + c, o);
+                ptx::tmem_st16(tw_o + lane_base + c, o);
             }
             ptx::tmem_wait_st();
             ptx::tc_fence_before();
@@ -758,8 +772,8 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
                 uint32_t z[16];
 #pragma unroll
                 for (int i = 0; i < 16; i++) z[i] = 0u;
-                ptx::tmem_st16(tmem + lane_base + sb * BN, z);
-                if (!F8) ptx::tmem_st16(tmem + lane_base + sb * BN + 16, z);
+                ptx::tmem_st16(TMW + lane_base + sb * BN, z);
+                if (!F8) ptx::tmem_st16(TMW + lane_base + sb * BN + 16, z);
                 ptx::tmem_wait_st();
                 ptx::tc_fence_before();
                 ptx::mbar_arrive(&S.p_full[sb]);
@@ -775,7 +789,7 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             uint32_t s[4][16];
             auto load_s = [&]() {
 #pragma unroll
-                for (int q4 = 0; q4 < 4; q4++) ptx::tmem_ld16(tmem + lane_base + sb * BN + q4 * 16, s[q4]);
+                for (int q4 = 0; q4 < 4; q4++) ptx::tmem_ld16(TMW + lane_base + sb * BN + q4 * 16, s[q4]);
                 ptx::tmem_wait_ld();
             };
             load_s();
@@ -893,11 +907,11 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
 #pragma unroll 1
                         for (int c = 0; c < D; c += 16) {
                             uint32_t o[16];
-                            ptx::tmem_ld16(TM_O + lane_base + c, o);
+                            ptx::tmem_ld16(tw_o + lane_base + c, o);
                             ptx::tmem_wait_ld();
 #pragma unroll
                             for (int i = 0; i < 16; i++) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-                            ptx::tmem_st16(TM_O + lane_base + c, o);
+                            ptx::tmem_st16(tw_o + lane_base + c, o);
                         }
                         l *= alpha;
                         if (need) m_ref = mx;
@@ -908,8 +922,8 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             if (threadIdx.x == 0) TB_TRACE(j, 5);
             l += psum;
             // P_j overwrites S_j's first 32 columns (A operand of PV, bf16x2 per column)
-            ptx::tmem_st16(tmem + lane_base + sb * BN, pk[0]);
-            if (!F8) ptx::tmem_st16(tmem + lane_base + sb * BN + 16, pk[1]);
+            ptx::tmem_st16(TMW + lane_base + sb * BN, pk[0]);
+            if (!F8) ptx::tmem_st16(TMW + lane_base + sb * BN + 16, pk[1]);
             ptx::tmem_wait_st();
             if (threadIdx.x == 0) TB_TRACE(j, 6);
             ptx::tc_fence_before();
@@ -962,8 +976,8 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
         // linear numerator when fused_end) and the combine factors above
         auto out16 = [&](int c, float (&v)[16]) {
             uint32_t o[16], nlt[16];
-            ptx::tmem_ld16(TM_O + lane_base + c, o);
-            if (fused_end) ptx::tmem_ld16(tmem + lane_base + c, nlt);
+            ptx::tmem_ld16(tw_o + lane_base + c, o);
+            if (fused_end) ptx::tmem_ld16(TMW + lane_base + c, nlt);
             ptx::tmem_wait_ld();
             if (fused_end) {
 #pragma unroll
@@ -1067,6 +1081,7 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
     __syncthreads();
     if (warp == 5) ptx::tmem_dealloc<256>(tmem);
 }
+#undef TMW
 
 int sla_simt(const tb_sla_args *a, cudaStream_t st);
 
