@@ -358,6 +358,14 @@ int tb_gemm_bf16_batched(const void *A, const void *B, void *C, int64_t H, int64
 int tb_linear_kv_part(const void *k, const void *v, int64_t H, int64_t L, int64_t d, int64_t kv_block,
                       int64_t dx, void *kv_part, void *stream);
 
+/* tb_linear_kv_part that also writes the raw K block means kp [H, nkv, d] f32
+ * (pool_block_means of k, attention.py:256-266, numpy's reduceat order,
+ * bit-exact) and, when kpt != NULL, their transposed copy kpt [H, d, ldt]
+ * (ldt >= nkv) -- the operands of tb_topk_blocks_cov -- from the K tiles the
+ * kernel already holds: no separate K pooling pass. */
+int tb_linear_kv_part_pool(const void *k, const void *v, int64_t H, int64_t L, int64_t d, int64_t kv_block,
+                           int64_t dx, void *kv_part, float *kp, float *kpt, int64_t ldt, void *stream);
+
 /* DiT glue in one pass: s = x (+ y) (+ alpha * emb[cols]) -> sum_out (f32,
  * optional, may alias x or y) and RMSNorm(s) * gain (layer_norm = 0) or
  * LayerNorm(s) * gain + offset (layer_norm = 1) as bf16 norm_out

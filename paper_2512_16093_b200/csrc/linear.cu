@@ -17,6 +17,9 @@
 //   * the f32 accumulator goes TMEM -> registers -> bf16 swizzled smem tile
 //     -> TMA store (two 64-column boxes)
 // The kernel is HBM-bound: 32 KB read + (dx*d*2) B written per block.
+// Optionally (tb_linear_kv_part_pool) it also emits the raw K block means
+// (pool_block_means) and their transposed copy from the tile it already holds,
+// which saves the separate K pooling pass over HBM on the top-k's path.
 #include "common.cuh"
 #include "ptx.cuh"
 #include "tmap.cuh"
@@ -41,7 +44,9 @@ __global__ void __launch_bounds__(lkv::THREADS) kv_part_kernel(const __grid_cons
                                                                 const __grid_constant__ CUtensorMap tm_v,
                                                                 const __grid_constant__ CUtensorMap tm_out,
                                                                 int L, int nkv, int dx,
-                                                                __nv_bfloat16 *__restrict__ kv_part) {
+                                                                __nv_bfloat16 *__restrict__ kv_part,
+                                                                float *__restrict__ kp, float *__restrict__ kpt,
+                                                                int64_t ldt) {
     using namespace lkv;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     Smem &S = *reinterpret_cast<Smem *>(smem_raw);
@@ -71,6 +76,39 @@ __global__ void __launch_bounds__(lkv::THREADS) kv_part_kernel(const __grid_cons
         *reinterpret_cast<uint4 *>(kv_part + (row0 + r) * D + c) = make_uint4(0u, 0u, 0u, 0u);
     }
     ptx::mbar_wait(&S.full, 0);
+    if (kp != nullptr) {
+        // the raw K block's mean per channel (pool_block_means, attention.py:256-266) from
+        // the tile already in shared memory, in numpy's reduceat order: seed + 8-accumulator
+        // pairwise body + sequential tail (as pool_quant_tile_kernel); thread = channel
+        const int c = threadIdx.x, e = min(BN, L - b * BN);
+        const uint8_t *colp = S.k + (c >> 6) * (TILE / 2) + (c & 7) * 2;
+        const int g = (c & 63) >> 3;
+        auto ld = [&](int t) {
+            return __bfloat162float(*reinterpret_cast<const __nv_bfloat16 *>(colp + t * 128 + ((g ^ (t & 7)) * 16)));
+        };
+        const float seed = ld(0);
+        const int n = e - 1;
+        float res = -0.0f;
+        if (n >= 8) {
+            float r[8];
+#pragma unroll
+            for (int j = 0; j < 8; j++) r[j] = ld(1 + j);
+            const int full8 = n - (n % 8);
+            for (int i = 8; i < full8; i += 8) {
+#pragma unroll
+                for (int j = 0; j < 8; j++) r[j] = __fadd_rn(r[j], ld(1 + i + j));
+            }
+            res = __fadd_rn(__fadd_rn(__fadd_rn(r[0], r[1]), __fadd_rn(r[2], r[3])),
+                            __fadd_rn(__fadd_rn(r[4], r[5]), __fadd_rn(r[6], r[7])));
+            for (int i = full8; i < n; i++) res = __fadd_rn(res, ld(1 + i));
+        } else {
+            for (int i = 0; i < n; i++) res = __fadd_rn(res, ld(1 + i));
+        }
+        const float pm = __fdiv_rn(n > 0 ? __fadd_rn(seed, res) : seed, (float)e);
+        kp[((int64_t)h * nkv + b) * D + c] = pm;
+        if (kpt) kpt[((int64_t)h * D + c) * ldt + b] = pm;   // [H][d][ldt]: the top-k kernel's coalesced operand
+        __syncthreads();                                   // every read of the raw tile before phi overwrites it
+    }
     {
         // phi in place: thread = (channel half, 8-channel group g, 8-token slice tq)
         const int half = threadIdx.x >> 6, g = (threadIdx.x >> 3) & 7, tq = threadIdx.x & 7;
@@ -170,9 +208,11 @@ __global__ void __launch_bounds__(lkv::THREADS) kv_part_kernel(const __grid_cons
 
 using namespace tb;
 
-extern "C" int tb_linear_kv_part(const void *k, const void *v, int64_t H, int64_t L, int64_t d, int64_t kv_block,
-                                 int64_t dx, void *kv_part, void *stream) {
+extern "C" int tb_linear_kv_part_pool(const void *k, const void *v, int64_t H, int64_t L, int64_t d,
+                                      int64_t kv_block, int64_t dx, void *kv_part, float *kp, float *kpt,
+                                      int64_t ldt, void *stream) {
     using namespace lkv;
+    TB_REQUIRE(kpt == nullptr || (kp != nullptr && ldt >= cdiv(L, kv_block)), "kpt needs kp and ldt >= blocks");
     TB_REQUIRE(d == D && kv_block == BN, "tb_linear_kv_part: d == 128 and kv_block == 64 only");
     TB_REQUIRE(dx > d && dx * d % 256 == 0, "dx must exceed d with dx*d a multiple of 256");
     TB_REQUIRE(((uintptr_t)k % 16) == 0 && ((uintptr_t)v % 16) == 0 && ((uintptr_t)kv_part % 16) == 0, "unaligned");
@@ -186,7 +226,12 @@ extern "C" int tb_linear_kv_part(const void *k, const void *v, int64_t H, int64_
         return fail(TB_ECUDA, "cuTensorMapEncodeTiled failed (kv_part)");
     cudaStream_t st = as_stream(stream);
     smem_attr(kv_part_kernel, (int)SMEM_BYTES);
-    kv_part_kernel<<<dim3((unsigned)nkv, (unsigned)H), THREADS, SMEM_BYTES, st>>>(tk, tv, to, (int)L, (int)nkv,
-                                                                                  (int)dx, (__nv_bfloat16 *)kv_part);
+    kv_part_kernel<<<dim3((unsigned)nkv, (unsigned)H), THREADS, SMEM_BYTES, st>>>(
+        tk, tv, to, (int)L, (int)nkv, (int)dx, (__nv_bfloat16 *)kv_part, kp, kpt, ldt);
     return check_launch("kv_part");
+}
+
+extern "C" int tb_linear_kv_part(const void *k, const void *v, int64_t H, int64_t L, int64_t d, int64_t kv_block,
+                                 int64_t dx, void *kv_part, void *stream) {
+    return tb_linear_kv_part_pool(k, v, H, L, d, kv_block, dx, kv_part, nullptr, nullptr, 0, stream);
 }

@@ -5,8 +5,9 @@
 //
 //   side stream    k_mean (sequential chain) -> K codes (smoothed K; f32
 //                  inputs: with the K pool, which top-k then waits for)
-//   third stream   kv_part (per-block phi(K_b)^T [V_b | 1], linear branch)
-//   caller stream  Q pool + codes -> K pool (+ transposed copy) -> top-k and
+//   third stream   kv_part (per-block phi(K_b)^T [V_b | 1], linear branch;
+//                  bf16 inputs: with the raw K pool + transposed copy)
+//   caller stream  Q pool + codes -> [K pool (+ transposed copy)] -> top-k and
 //                  the coverage matrix -> coverage GEMM (KV_sel) -> [q_block
 //                  64: pair unions] -> fused tcgen05 attention
 //
@@ -149,14 +150,22 @@ extern "C" int tb_sla_forward(const void *q, const void *k, const void *v, int d
     TB_CALL(tb_pool_quant_tokens(k, dtype, km, H, L, d, kv_block, (int8_t *)at(o.kc), (float *)at(o.ks),
                                  o.f32 ? (float *)at(o.kp) : nullptr, side));
     cudaEventRecord(e_side, side);
-    // third: the linear branch's per-block operand
-    if (o.lin) TB_CALL(tb_linear_kv_part(kb, vb, H, L, d, kv_block, o.dx, at(o.kvp), third));
+    // third: the linear branch's per-block operand; bf16 inputs: with the raw K pool
+    // and its transposed copy (the top-k operands) from the same tiles
+    const bool kv_pool = o.lin && !o.f32;
+    if (kv_pool)
+        TB_CALL(tb_linear_kv_part_pool(kb, vb, H, L, d, kv_block, o.dx, at(o.kvp), (float *)at(o.kp),
+                                       (float *)at(o.kpt), o.ldt, third));
+    else if (o.lin)
+        TB_CALL(tb_linear_kv_part(kb, vb, H, L, d, kv_block, o.dx, at(o.kvp), third));
     cudaEventRecord(e_third, third);
     // caller stream: pools, Q codes, top-k + coverage, coverage GEMM, fused kernel
     TB_CALL(tb_pool_quant_tokens(q, dtype, nullptr, H, L, d, q_block, (int8_t *)at(o.qc), (float *)at(o.qs),
                                  (float *)at(o.qp), stream));
-    if (!o.f32) {
-        // bf16: the raw K pool with its transposed copy (the coalesced top-k operand), no k_mean wait
+    if (kv_pool) {
+        cudaStreamWaitEvent(main, e_third, 0);   // the K pool came with kv_part
+    } else if (!o.f32) {
+        // bf16 without the linear branch: the raw K pool with its transposed copy, no k_mean wait
         TB_CALL(tb_pool_quant_tokens_t(k, dtype, nullptr, H, L, d, kv_block, nullptr, nullptr, (float *)at(o.kp),
                                        (float *)at(o.kpt), o.ldt, stream));
     } else {

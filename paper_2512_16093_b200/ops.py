@@ -352,15 +352,24 @@ def linear_kv_dx(d: int) -> int:
     return dx
 
 
-def linear_kv_part(k, v, kv_block: int):
+def linear_kv_part(k, v, kv_block: int, pool: bool = False):
     """tb_linear_kv_part: per kv block [V_b | 1]^T phi(K_b) (attention.py:320-325)
-    straight from bf16 k, v -> [H, nkv, dx, d] bf16 (one tcgen05 kernel)."""
+    straight from bf16 k, v -> [H, nkv, dx, d] bf16 (one tcgen05 kernel).
+    pool=True (tb_linear_kv_part_pool): also the raw K block means and their
+    transposed copy from the same tiles -> (kv_part, kp, kpt), as pool_tokens_t."""
     H, L, d = k.shape
     nkv = cdiv(L, kv_block)
     dx = linear_kv_dx(d)
     kv_part = torch.empty((H, nkv, dx, d), dtype=torch.bfloat16, device=k.device)
-    call("tb_linear_kv_part", ptr(k), ptr(v), H, L, d, kv_block, dx, ptr(kv_part), stream_ptr())
-    return kv_part
+    if not pool:
+        call("tb_linear_kv_part", ptr(k), ptr(v), H, L, d, kv_block, dx, ptr(kv_part), stream_ptr())
+        return kv_part
+    ldt = -(-nkv // 4) * 4
+    kp = torch.empty((H, nkv, d), dtype=torch.float32, device=k.device)
+    kpt = torch.empty((H, d, ldt), dtype=torch.float32, device=k.device)
+    call("tb_linear_kv_part_pool", ptr(k), ptr(v), H, L, d, kv_block, dx, ptr(kv_part), ptr(kp), ptr(kpt), ldt,
+         stream_ptr())
+    return kv_part, kp, kpt
 
 
 def linear_kv_sel(kv_part: torch.Tensor, cov: torch.Tensor, nkv: int):
@@ -514,17 +523,29 @@ def sla_attention(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: fl
         # top-k -> coverage GEMM without waiting for k_mean; k_mean (a
         # sequential chain) and the K codes that need it run on the side
         # stream, kv_part (HBM-bound, needs only k and v) on a third from t=0.
+        # _KV_POOL: kv_part also pools the raw K blocks from the tiles it holds
+        # (no separate K pooling pass) and top-k waits for it after the Q pass
         third = _aux_stream("kvpart")
         third.wait_stream(main)
         with torch.cuda.stream(third):
-            kv_part = linear_kv_part(kb, vb, kv_block)
+            if _KV_POOL:
+                kv_part, kp, kpt = linear_kv_part(kb, vb, kv_block, pool=True)
+            else:
+                kv_part = linear_kv_part(kb, vb, kv_block)
+            ev_kv = torch.cuda.Event()
+            ev_kv.record(third)
             if pv_fp8:                                  # V codes only need v
                 v8, v8s = quant_v_fp8(v)
         with torch.cuda.stream(side):
             km = kmean(k)
             kc, ks, _ = pool_quant_tokens(k, kv_block, km, pool=False)
         qc, qs, qp = pool_quant_tokens(q, q_block, None, pool=True)
-        kp, kpt = pool_tokens_t(k, kv_block)
+        if _KV_POOL:
+            main.wait_event(ev_kv)
+            for t in (kp, kpt):
+                t.record_stream(main)
+        else:
+            kp, kpt = pool_tokens_t(k, kv_block)
         idx, comp, cov = topk_blocks_cov(qp, kp, count, want_comp=return_parts, kpt=kpt)
         main.wait_stream(third)
         kv_part.record_stream(main)
@@ -640,6 +661,10 @@ def sla_forward(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: floa
 
 
 _AUX = {}
+
+# bf16 tensor-core path: the raw K pool comes from kv_part's tiles (True) or
+# from a separate pooling pass on the caller's stream (False; tools A/B)
+_KV_POOL = True
 
 
 def _aux_stream(name: str) -> torch.cuda.Stream:

@@ -258,6 +258,24 @@ def test_gemm_bf16_batched_mn_major(tb):
         assert ((got16.float() - ref16.float()).abs() <= ulp).all(), (H, M, K, N)
 
 
+@pytest.mark.parametrize("L", [1000, 4096, 75600 // 8 + 3])
+def test_linear_kv_part_pool_equals_pool_pass(tb, L):
+    """tb_linear_kv_part_pool: the raw K block means (and the transposed copy)
+    it computes from its own tiles are bit-identical to the pooling pass
+    (tb_pool_quant_tokens_t, pinned to the reference's reduceat order), ragged
+    last block included; kv_part itself is unchanged."""
+    H, d = 3, 128
+    _, k, v = gen.gaussian_qkv(37, H, L, d, bf16=True)
+    kd, vd = dev(k, True), dev(v, True)
+    kvp, kp, kpt = tb.linear_kv_part(kd, vd, 64, pool=True)
+    want_kp, want_kpt = tb.pool_tokens_t(kd, 64)
+    torch.cuda.synchronize()
+    assert torch.equal(kp, want_kp)
+    nkv = want_kp.shape[1]
+    assert torch.equal(kpt[:, :, :nkv], want_kpt[:, :, :nkv])
+    assert torch.equal(kvp, tb.linear_kv_part(kd, vd, 64))
+
+
 def test_linear_kv_part_blocks(tb):
     """tb_linear_kv_part vs the per-block einsums of linear_attention
     (attention.py:320-325): V_b^T phi(K_b) and sum phi(K_b), padded tokens

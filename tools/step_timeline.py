@@ -2,7 +2,8 @@
 passes re-issued with tb_timestamp kernels (%globaltimer) after each pass on
 its stream, captured in a CUDA graph like bench.py's step, replayed; prints
 the median end time of every pass relative to the step start.
-Usage: python tools/step_timeline.py [order ...]  (ops._PREP_ORDER values)."""
+Usage: python tools/step_timeline.py [order ...]: 3 = the shipped order (kv_part pools K),
+0-2 = the earlier orders with a separate K pooling pass."""
 import math
 import os
 import sys
@@ -42,19 +43,30 @@ def step(order):
         if order == 0:
             kc, ks, _ = ops.pool_quant_tokens(k, 64, km, pool=False)
             stamp("K codes", side)
-    if order == 0:
+    if order in (0, 3, 4):
         third.wait_stream(main)
+    if order == 3:                     # kv_part pools the raw K blocks itself
+        with torch.cuda.stream(third):
+            kv_part, kp, kpt = ops.linear_kv_part(k, v, 64, pool=True)
+            stamp("kv_part + K pool", third)
     qc, qs, qp = ops.pool_quant_tokens(q, 128, None, pool=True)
     stamp("Q pass", main)
-    if order == 1:
-        third.wait_stream(main)
-    kp, kpt = ops.pool_tokens_t(k, 64)
-    stamp("K pool", main)
-    if order == 2:
-        third.wait_stream(main)
-    with torch.cuda.stream(third):
-        kv_part = ops.linear_kv_part(k, v, 64)
-        stamp("kv_part", third)
+    if order == 4:                     # the same, kv_part enqueued after the Q pass
+        with torch.cuda.stream(third):
+            kv_part, kp, kpt = ops.linear_kv_part(k, v, 64, pool=True)
+            stamp("kv_part + K pool", third)
+    if order in (3, 4):
+        main.wait_stream(third)
+    else:
+        if order == 1:
+            third.wait_stream(main)
+        kp, kpt = ops.pool_tokens_t(k, 64)
+        stamp("K pool", main)
+        if order == 2:
+            third.wait_stream(main)
+        with torch.cuda.stream(third):
+            kv_part = ops.linear_kv_part(k, v, 64)
+            stamp("kv_part", third)
     idx, comp, cov = ops.topk_blocks_cov(qp, kp, count, want_comp=False, kpt=kpt)
     stamp("top-k", main)
     if order != 0:
@@ -81,7 +93,7 @@ def step(order):
     return out
 
 
-for order in [int(x) for x in sys.argv[1:]] or [0, 1]:
+for order in [int(x) for x in sys.argv[1:]] or [3, 4, 0]:
     for _ in range(2):
         step(order)
     torch.cuda.synchronize()
