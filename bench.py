@@ -191,6 +191,11 @@ class ClockSampler:
 
 # --------------------------------------------------------------- reference arm
 
+def _dropin_chunk():
+    from paper_2512_16093_b200 import attention
+    return attention._HOST_CHUNK_HEADS
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -704,8 +709,9 @@ def main():
         e2e = {"value": total_ops / (ems * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": ems,
                "h2d_bytes_per_step": moved["h2d_bytes"], "d2h_bytes_per_step": o_np.nbytes,
                "api": "paper_2512_16093_b200.attention.sla_attention(AttnInputs(numpy f32), SLAConfig) -> numpy f32 "
-                      "(drop-in for turbobench.attention.sla_attention); host wall clock, median of 3; per 2-head "
-                      "chunk: numpy->pinned staging, H2D, attention, D2H straight into the page-locked result array",
+                      "(drop-in for turbobench.attention.sla_attention); host wall clock, median of 3; per "
+                      f"{_dropin_chunk()}-head chunk: numpy->pinned staging (next chunk on a worker thread), H2D, "
+                      "attention, D2H straight into the page-locked result array",
                "h2d_bytes_note": (f"{moved['narrow_chunks']}/{moved['chunks']} head chunks had bf16-valued q and k "
                                   "(generator G: bf16-rounded Gaussians), detected on the fly while staging and "
                                   "uploaded as their exact bf16 bit patterns (lossless); V always crosses as bf16 "

@@ -348,7 +348,7 @@ def sla_attention(inputs: AttnInputs, cfg: SLAConfig | None = None):
 
 
 _HOST_PIPELINE_BYTES = 64 << 20
-_HOST_CHUNK_HEADS = 2          # heads per upload / attention / download chunk
+_HOST_CHUNK_HEADS = 4          # heads per upload / attention / download chunk (4: 73-78 ms vs 74-80 for 2 at cfg4, profiles/r02_dropin_e2e_staging.log)
 
 
 def _sla_with_mask(inputs: AttnInputs, cfg: SLAConfig):
