@@ -46,6 +46,13 @@ namespace tb {
 #ifndef TB_SLA_UNI
 #define TB_SLA_UNI 1
 #endif
+// TB_SLA_EARLY: linear-first (non-Q2) tiles keep phi(Q) in TMEM (the second S
+// buffer's columns) and KV_sel^T in v[0] + k[0..1] only, so the K / V
+// producers start at once (rings offset past the staging slots) and QK(0)
+// runs under the softmax warps' prologue
+#ifndef TB_SLA_EARLY
+#define TB_SLA_EARLY 1
+#endif
 #ifndef TB_SLA_BIAS
 #define TB_SLA_BIAS 1
 #endif
@@ -336,6 +343,15 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
     // mode its Q codes are loaded only once the linear MMA has released them.
     uint8_t *lin_a = Q2 ? S.q : S.v[0];
     uint8_t *lin_b = Q2 ? S.v[1] : S.v[2];
+    // early (TB_SLA_EARLY, linear-first, not Q2): phi(Q) in TMEM columns 64..127
+    // (S buffer 1, free until QK(1)), KV_sel^T's K-halves in v[0] and k[0..1];
+    // block j's K slot is (j + KOFF) % KSTAGES and V slot (j + VOFF) % 3, the
+    // staging counting as the first use of k[0], k[1], v[0] (released by the
+    // linear MMA's commit), so K(0), V(0), V(1) load at once
+    const bool early = TB_SLA_EARLY && !Q2 && lf && KSTAGES >= 3;
+    const int KOFF = early ? 2 : 0, VOFF = early ? 1 : 0;
+    uint8_t *lin_b1 = early ? S.k[0] : lin_b + 16384;       // second K-half of KV_sel^T (non-Q2)
+    if (early) lin_b = S.v[0];
 
 #define SLA_CTRL_REGS() \
     do { if (TB_SLA_REGS && TB_SLA_SETMAXNREG) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" :: "n"(CTRL_REGS)); } while (0)
@@ -361,7 +377,7 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             } else {
                 ptx::mbar_arrive_expect_tx(&S.lin_full, 2 * 16384);
                 ptx::tma_load_2d(lin_b, &tm_kv, 0, row0a, &S.lin_full);
-                ptx::tma_load_2d(lin_b + 16384, &tm_kv, 64, row0a, &S.lin_full);
+                ptx::tma_load_2d(lin_b1, &tm_kv, 64, row0a, &S.lin_full);
             }
         };
         const bool q_late = Q2 && lf;                   // Q codes after the linear MMA (shared staging)
@@ -379,7 +395,7 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             if (lf) load_lin();
         }
         __syncwarp();
-        if (lf) ptx::mbar_wait_sleep(&S.lin_done, 0);   // the linear MMA has released the rings
+        if (lf && !early) ptx::mbar_wait_sleep(&S.lin_done, 0);   // the linear MMA has released the rings
         if (q_late) {
             if (ptx::elect_one()) {
                 ptx::mbar_arrive_expect_tx(&S.q_full, Q_BYTES);
@@ -389,8 +405,8 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
         }
         for (int j = 0; j < nsel; j++) {
             const int b = __ldg(sel + j) & 0x0FFFFFFF;
-            const int ks = j % KSTAGES;
-            ptx::mbar_wait_sleep(&S.k_empty[ks], (uint32_t)(((j / KSTAGES) & 1) ^ 1));
+            const int jv = j + KOFF, ks = jv % KSTAGES;
+            ptx::mbar_wait_sleep(&S.k_empty[ks], (uint32_t)(((jv / KSTAGES) & 1) ^ 1));
             if (lane == 0) TB_TRACE(j, 10);
             if (ptx::elect_one()) {
 #ifdef TB_X_NOLOAD
@@ -410,11 +426,11 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
     } else if (warp == 6) {
         SLA_CTRL_REGS();
         // ---------------------------------------------------- TMA producer (V)
-        if (lf) ptx::mbar_wait_sleep(&S.lin_done, 0);
+        if (lf && !early) ptx::mbar_wait_sleep(&S.lin_done, 0);
         for (int j = 0; j < nsel; j++) {
             const int b = __ldg(sel + j) & 0x0FFFFFFF;
-            const int vs = j % VSTAGES;
-            ptx::mbar_wait_sleep(&S.v_empty[vs], (uint32_t)(((j / VSTAGES) & 1) ^ 1));
+            const int jv = j + VOFF, vs = jv % VSTAGES;
+            ptx::mbar_wait_sleep(&S.v_empty[vs], (uint32_t)(((jv / VSTAGES) & 1) ^ 1));
             if (lane == 0) TB_TRACE(j, 11);
             if (ptx::elect_one()) {
 #ifdef TB_X_NOLOAD
@@ -449,17 +465,26 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
         // (N = 128, K-half stride 16 KB), or Q2 both stacked (N = 256, K-half
         // stride 32 KB; brow = 128 selects q-block 2n+1's rows alone)
         auto lin_mma = [&](uint32_t dst, int nn, int brow, uint64_t *done) {
-            const uint32_t bstride = Q2 ? 32768 : 16384;
             const uint32_t id = ptx::idesc_bf16(BM, nn);
             if (ptx::elect_one()) {
 #pragma unroll
                 for (int ks = 0; ks < D / 16; ks++) {
                     const int sub = ks >> 2, w = ks & 3;
-                    const uint64_t ad = ptx::sdesc_sw128(ptx::smem_u32(lin_a + sub * 16384)) + 2 * w;
-                    const uint64_t bd = ptx::sdesc_sw128(ptx::smem_u32(lin_b + sub * bstride + brow * 128)) + 2 * w;
-                    ptx::mma_f16(dst, ad, bd, id, ks > 0 ? 1u : 0u);
+                    uint8_t *bh = Q2 ? lin_b + sub * 32768 : (sub ? lin_b1 : lin_b);
+                    const uint64_t bd = ptx::sdesc_sw128(ptx::smem_u32(bh + brow * 128)) + 2 * w;
+                    if (early) {          // A = phi(Q) in TMEM columns 64.. (8 per K16 step)
+                        ptx::mma_f16_ts(dst, tmem + 64 + 8 * ks, bd, id, ks > 0 ? 1u : 0u);
+                    } else {
+                        const uint64_t ad = ptx::sdesc_sw128(ptx::smem_u32(lin_a + sub * 16384)) + 2 * w;
+                        ptx::mma_f16(dst, ad, bd, id, ks > 0 ? 1u : 0u);
+                    }
                 }
                 ptx::mma_commit(done);
+                if (early) {              // the staging slots of the rings are free again
+                    ptx::mma_commit(&S.k_empty[0]);
+                    ptx::mma_commit(&S.k_empty[1]);
+                    ptx::mma_commit(&S.v_empty[0]);
+                }
             }
             __syncwarp();
         };
@@ -468,7 +493,7 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             MMA_WAIT(&S.lin_full, 0);
             ptx::tc_fence_after();
         };
-        if (lf) {
+        if (lf && !early) {
             lin_wait();
             if constexpr (Q2) {
                 // one N=256 MMA: cols 0-127 = phi(Q) . KV_sel[2n], cols 128-255 (= O) =
@@ -483,9 +508,10 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
         }
         MMA_WAIT(&S.q_full, 0);
         auto pv = [&](int i) {
-            const int pb = i & 1, vs = i % VSTAGES;
+            const int pb = i & 1, iv = i + VOFF, vs = iv % VSTAGES;
             if (lane == 0) TB_TRACE(i, 13);
-            MMA_WAIT(&S.v_full[vs], (uint32_t)((i / VSTAGES) & 1));
+            // v_full completes once per real load: the staging use of slots < VOFF has none
+            MMA_WAIT(&S.v_full[vs], (uint32_t)((iv / VSTAGES - (vs < VOFF ? 1 : 0)) & 1));
             if (lane == 0) TB_TRACE(i, 14);
             MMA_WAIT(&S.p_full[pb], (uint32_t)((i >> 1) & 1));
             ptx::tc_fence_after();
@@ -515,9 +541,9 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             __syncwarp();
         };
         auto qk = [&](int j) {
-            const int ks = j % KSTAGES, sb = j & 1;
+            const int jv = j + KOFF, ks = jv % KSTAGES, sb = j & 1;
             if (lane == 0) TB_TRACE(j, 15);
-            MMA_WAIT(&S.k_full[ks], (uint32_t)((j / KSTAGES) & 1));
+            MMA_WAIT(&S.k_full[ks], (uint32_t)((jv / KSTAGES - (ks < KOFF ? 1 : 0)) & 1));
             ptx::tc_fence_after();
             if (lane == 0) TB_TRACE(j, 8);
             const uint64_t kd = ptx::sdesc_sw128(ptx::smem_u32(S.k[ks]));
@@ -539,6 +565,10 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
         // QK(j+1) is queued before PV(j) waits for softmax(j): the tensor
         // pipe computes the next scores while the softmax warps work
         if (nsel > 0) qk(0);
+        if (early) {                                    // under QK(0); before QK(1) reuses columns 64..
+            lin_wait();
+            lin_mma(TM_O, D, 0, &S.lin_done);           // O starts as numL
+        }
         for (int j = 0; j < nsel; j++) {
             if (j + 1 < nsel) qk(j + 1);
             pv(j);
@@ -626,6 +656,61 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
             if (threadIdx.x == 0) TB_TRACE_X(70, 5);
             return dl;
         };
+        float corr_e = 0.0f, den_e = 0.0f;             // early: this row's q . k_mean and den_L
+        if (early) {
+            // Prologue per row (thread = row = TMEM lane): corr = q . k_mean,
+            // phi(q) -> bf16 pairs -> TMEM columns 64..127 (the linear MMA's A
+            // operand), den_L = phi(q) . sum phi(K_b) over the complement.
+            const float *kmh = a.k_mean + (int64_t)h * D;
+            // bf16: the whole row (16 x 16 B) in flight before the den-row wait
+            uint4 qv[sizeof(T) == 2 ? 16 : 1];
+            if constexpr (sizeof(T) == 2) {
+#pragma unroll
+                for (int i = 0; i < 16; i++)
+                    qv[i] = row_ok ? __ldg(reinterpret_cast<const uint4 *>(qrow) + i) : make_uint4(0, 0, 0, 0);
+            }
+            ptx::mbar_wait_sleep(&S.k1_full, 0);
+            const __nv_bfloat16 *k1 = S.k1[0];
+#pragma unroll
+            for (int c32 = 0; c32 < D; c32 += 32) {
+                uint32_t pk[16];
+#pragma unroll
+                for (int c8 = 0; c8 < 32; c8 += 8) {
+                    float x[8];
+                    if constexpr (sizeof(T) == 2) {
+                        const __nv_bfloat162 *b2 = reinterpret_cast<const __nv_bfloat162 *>(&qv[(c32 + c8) >> 3]);
+#pragma unroll
+                        for (int i = 0; i < 4; i++) { const float2 f = __bfloat1622float2(b2[i]); x[2 * i] = f.x; x[2 * i + 1] = f.y; }
+                    } else if (row_ok) {
+                        load8(qrow + c32 + c8, x);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 8; i++) x[i] = 0.0f;
+                    }
+                    const float4 ka = __ldg(reinterpret_cast<const float4 *>(kmh + c32 + c8));
+                    const float4 kb = __ldg(reinterpret_cast<const float4 *>(kmh + c32 + c8 + 4));
+                    const float km8[8] = {ka.x, ka.y, ka.z, ka.w, kb.x, kb.y, kb.z, kb.w};
+                    const uint4 kw = *reinterpret_cast<const uint4 *>(k1 + c32 + c8);
+                    const __nv_bfloat162 *k2 = reinterpret_cast<const __nv_bfloat162 *>(&kw);
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const float x0 = x[2 * u], x1 = x[2 * u + 1];
+                        corr_e = fmaf(x0, km8[2 * u], corr_e);
+                        corr_e = fmaf(x1, km8[2 * u + 1], corr_e);
+                        const float f0 = x0 >= 0.0f ? x0 + 1.0f : ex2(x0 * LOG2E);
+                        const float f1 = x1 >= 0.0f ? x1 + 1.0f : ex2(x1 * LOG2E);
+                        const float2 kk = __bfloat1622float2(k2[u]);
+                        den_e = fmaf(f0, kk.x, fmaf(f1, kk.y, den_e));
+                        __nv_bfloat162 pp = F8 ? __floats2bfloat162_rn(f0 * ivsc, f1 * ivsc) : __floats2bfloat162_rn(f0, f1);
+                        pk[(c8 >> 1) + u] = *reinterpret_cast<uint32_t *>(&pp);
+                    }
+                }
+                ptx::tmem_st16(TMW + lane_base + 64 + (c32 >> 1), pk);
+            }
+            ptx::tmem_wait_st();
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&S.phiq_full);
+        } else
         // Prologue, warp-cooperative and coalesced: each warp walks its 32 rows
         // two at a time (lanes 0-15 row 2i, 16-31 row 2i+1, 16 B of the row per
         // lane), so every load instruction reads 512 contiguous bytes.  Per row:
@@ -753,8 +838,8 @@ __global__ void __launch_bounds__(sla::THREADS, 2) sla_tc_kernel(
         }
         TB_PH(ph_t1 = clock64());
         if (threadIdx.x == 0) TB_TRACE_X(70, 8);
-        const float c0 = (row_ok ? S.corr_s[r] : 0.0f) * scale2;
-        const float den_l = S.den_s[r];
+        const float c0 = (row_ok ? (early ? corr_e : S.corr_s[r]) : 0.0f) * scale2;
+        const float den_l = early ? den_e : S.den_s[r];
         // lf: O already holds numL at the reference log2(linear_mix), l = den_L.
         // (Warp-uniform start: the rebase below is warp-collective.  A row with
         // l == 0 -- phi(q) underflowed, or a padding row -- whose exponentials

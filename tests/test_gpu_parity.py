@@ -226,6 +226,21 @@ def test_sla_tensor_core_path_peaky_logits(tb):
         assert cos >= COS_MIN and rel1 <= REL_L1_MAX, (mix, cos, rel1)
 
 
+@pytest.mark.parametrize("ratio", [0.01, 0.02, 0.04, 0.5])
+def test_sla_tensor_core_few_selected_blocks(tb, ratio):
+    """1-3 (and 32) selected kv blocks per q-block on the tcgen05 kernel, with
+    and without the linear-first path: the staging slots of the K / V rings
+    are shared with the linear branch (early start), so the shortest block
+    lists exercise the ring offsets' first uses."""
+    q, k, v = gen.gaussian_qkv(14, 3, 4096, 128, bf16=True)
+    for qb in (128, 64):
+        for mix in (1.0, 0.0):
+            want = O.sla_attention(q, k, v, qb, 64, ratio, mix)
+            got = tb.sla_attention(dev(q, True), dev(k, True), dev(v, True), qb, 64, ratio, mix).cpu().numpy()
+            cos, _, rel1 = metrics(got, want)
+            assert cos >= COS_MIN and rel1 <= REL_L1_MAX, (ratio, qb, mix, cos, rel1)
+
+
 def test_sla_topk_one_equals_dense_unquantized(tb):
     q, k, v = gen.gaussian_qkv(21, 2, 128, 16, bf16=False)
     out = tb.sla_attention(dev(q), dev(k), dev(v), 32, 32, 1.0, 1.0, quantized=False).cpu().numpy()
