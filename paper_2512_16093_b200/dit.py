@@ -107,8 +107,12 @@ def block_forward(x: torch.Tensor, sigma: float, w: DeviceLayer, heads: int, sla
     Lp, dim = x.shape
     hd = dim // heads
     # x1 = x (+ pending residual) + sigma*emb and the block-quantized RMSNorm(x1)
-    # (the qkv projection's A operand), one pass
-    fused_nq = ops.add_norm_quant_ok(dim)
+    # (the qkv projection's A operand).  Default: tb_add_norm + the blockwise
+    # quantizer, two streaming passes (1.23 / 1.39 ms at cfg5); the one-pass
+    # clustered tb_add_norm_quant (bit-identical) moves fewer
+    # bytes but serialises its band phases at one CTA per SM (2.37 / 2.86 ms,
+    # tools/time_add_norm.py), so it is opt-in: TB_DIT_FUSED_NORM_QUANT=1
+    fused_nq = os.environ.get("TB_DIT_FUSED_NORM_QUANT") == "1" and ops.add_norm_quant_ok(dim)
     if fused_nq:
         x1, aq, asc = ops.add_norm_quant(x, pending, w.sigma_emb, float(sigma), w.rms_gain)
     else:
@@ -161,8 +165,8 @@ def block_forward(x: torch.Tensor, sigma: float, w: DeviceLayer, heads: int, sla
             o = attn(qkv[:heads], qkv[heads:2 * heads], qkv[2 * heads:])           # [H, L, hd]
             oq, osc = ops.quantize_blockwise_planar(o)
     po = ops.w8a8_gemm(oq, osc, w.out_proj.bt, w.out_proj.scales, 128, None, torch.float32, exact=False)
-    # x2 = x1 + po and the block-quantized LayerNorm(x2) (mlp_in's A operand),
-    # one pass (x2 overwrites x1)
+    # x2 = x1 + po and the block-quantized LayerNorm(x2) (mlp_in's A operand);
+    # x2 overwrites x1
     if fused_nq:
         x2, bq, bsc = ops.add_norm_quant(x1, po, None, 0.0, w.ln_gain, w.ln_offset, layer_norm=True, sum_out=x1)
     else:
