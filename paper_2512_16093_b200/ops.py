@@ -748,7 +748,11 @@ def sla_attention_host(q, k, v, q_block: int = 64, kv_block: int = 64, topk_rati
     ev_out = [torch.cuda.Event() for _ in range(2)]
     pending = None                                       # (buffer, h0, h1) of a staged output not yet copied out
     moved = LAST_HOST_TRANSFER
-    moved.update(h2d_bytes=0, d2h_bytes=0, narrow_chunks=0, chunks=cdiv(H, ch))
+    # chunk boundaries: a one-head chunk first and last (the pipeline's fill --
+    # staging + upload of chunk 0 -- and drain -- attention + download of the
+    # last chunk -- are not overlapped with anything), ch heads in between
+    bounds = _chunk_bounds(H, ch)
+    moved.update(h2d_bytes=0, d2h_bytes=0, narrow_chunks=0, chunks=len(bounds))
 
     prof = HOST_PROFILE                                  # optional per-phase host wall times (tools)
     tick = time.perf_counter if prof is not None else None
@@ -767,7 +771,7 @@ def sla_attention_host(q, k, v, q_block: int = 64, kv_block: int = 64, topk_rati
     def stage(i):
         """chunk i's (sources, device destinations); pageable inputs are first
         staged into page-locked buffer i % 2 (bf16 bit patterns when exact)"""
-        h0, h1 = i * ch, min(H, (i + 1) * ch)
+        h0, h1 = bounds[i]
         n, b = h1 - h0, i % 2
         srcs = (q[h0:h1], k[h0:h1], v[h0:h1])
         dsts = tuple(t[:n] for t in bufs[b])
@@ -791,13 +795,13 @@ def sla_attention_host(q, k, v, q_block: int = 64, kv_block: int = 64, topk_rati
         mark("stage", t0)
         return srcs, dsts
 
-    nch = cdiv(H, ch)
+    nch = len(bounds)
     # staging of chunk i+1 (host threads, GIL released in the native call) runs
     # on a worker while this thread enqueues chunk i's upload / attention / download
     worker = _stage_worker() if stage_in is not None and nch > 1 else None
     staged = stage(0)
     for i in range(nch):
-        h0, h1 = i * ch, min(H, (i + 1) * ch)
+        h0, h1 = bounds[i]
         n, b = h1 - h0, i % 2
         nxt = worker.submit(stage, i + 1) if worker is not None and i + 1 < nch else None
         srcs, dsts = staged
@@ -835,6 +839,22 @@ def sla_attention_host(q, k, v, q_block: int = 64, kv_block: int = 64, topk_rati
             t.record_stream(compute)
             t.record_stream(h2d)
     compute.wait_stream(d2h)                            # the caller's stream covers the output copy
+    return out
+
+
+_HOST_EDGE_CHUNKS = True        # single-head first / last chunks (tools A/B)
+
+
+def _chunk_bounds(H: int, ch: int) -> list[tuple[int, int]]:
+    """Head ranges of sla_attention_host's chunks: [0, 1), then ch heads at a
+    time, the last chunk again a single head (H > ch + 1)."""
+    if H <= ch + 1 or ch <= 1 or not _HOST_EDGE_CHUNKS:
+        return [(h, min(H, h + ch)) for h in range(0, H, ch)]
+    out, h = [(0, 1)], 1
+    while h < H - 1:
+        out.append((h, min(H - 1, h + ch)))
+        h = out[-1][1]
+    out.append((H - 1, H))
     return out
 
 

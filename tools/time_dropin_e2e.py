@@ -26,6 +26,8 @@ refs = {}
 import os
 MODES = os.environ.get("E2E_MODES", "f32-valued, no narrow attempt;f32-valued;bf16-valued").split(";")
 for rep in range(2):
+  for edge in [x == "1" for x in os.environ.get("E2E_EDGE", "1").split(",")]:
+    ops._HOST_EDGE_CHUNKS = edge
     for mode in MODES:
         x[0][...], x[1][...] = (xb if mode == "bf16-valued" else xf)
         ops.host_stage_bf16_exact = (lambda d, s: False) if "no narrow" in mode else exact_fn
@@ -45,7 +47,7 @@ for rep in range(2):
                 ts.append(time.perf_counter() - t0)
                 del o
             m = ops.LAST_HOST_TRANSFER
-            print(f"drop-in e2e {mode} chunk {ch}: ms {[round(t * 1e3, 1) for t in ts]} median "
+            print(f"drop-in e2e {mode} edge={int(edge)} chunk {ch}: ms {[round(t * 1e3, 1) for t in ts]} median "
                   f"{np.median(ts) * 1e3:.1f}  h2d {m['h2d_bytes'] / 1e9:.2f} GB, narrow chunks "
                   f"{m['narrow_chunks']}/{m['chunks']}  host ms/call "
                   f"{ {k_: round(v_ * 250, 1) for k_, v_ in ops.HOST_PROFILE.items()} }", flush=True)
