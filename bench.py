@@ -42,9 +42,10 @@ H_, L_, D_ = 40, 75600, 128
 QB, KVB, RATIO = 128, 64, 0.1
 METRIC = "SLA-Sage attn TOPS & W8A8 GEMM TOPS at Wan2.1-14B-720P shapes, 1/2/4/8 B200"
 # kernels one sla_attention step launches (bf16 tensor-core path with the linear branch):
-# kv_part (third stream), k_mean + K codes (side stream), Q pool/quant, K pooling
-# (+ transposed kp), top-k (+ coverage matrix), coverage GEMM, fused attention
-LAUNCHES_PER_STEP = 8
+# kv_part + raw K pooling (third stream), k_mean + K codes (side stream), Q pool/quant,
+# top-k (+ coverage matrix), coverage GEMM, fused attention
+# (profiles/r02_launches_sla_step.csv lists them per step)
+LAUNCHES_PER_STEP = 7
 UNIT = "TOPS"
 
 
