@@ -22,6 +22,12 @@
 #include "ptx.cuh"
 #include "tmap.cuh"
 
+// exact promotion: (seg * sa) * sb with the second product as a packed FMA with
+// a +0 addend (A/B knob; 0 = two scalar multiplies)
+#ifndef TB_W8_EXACT_FMA0
+#define TB_W8_EXACT_FMA0 1
+#endif
+
 namespace tb {
 
 // ------------------------------------------------------------ tcgen05 path
@@ -185,7 +191,15 @@ __global__ void __launch_bounds__(gemm::THREADS, 1) w8a8_tc_kernel(
                             // feeding a packed add into FFMA2 (tools/ubench_f32x2.cu), so the
                             // product that feeds the add is formed with scalar RN multiplies
                             const float2 p = ptx::fmul2(x, sa2);
+#if TB_W8_EXACT_FMA0
+                            // p * sb as a packed FMA with a +0 addend: the RN product except
+                            // that -0 becomes +0, which cannot change o (it starts at +0, and
+                            // x + (+0) == x + (-0) for every x != -0); ptxas neither folds it
+                            // into a multiply nor contracts it into the add
+                            o = ptx::fadd2(o, ptx::ffma2(p, sb2, make_float2(0.0f, 0.0f)));
+#else
                             o = ptx::fadd2(o, make_float2(__fmul_rn(p.x, sb2.x), __fmul_rn(p.y, sb2.y)));
+#endif
                         } else {
                             o = ptx::ffma2(x, sab2, o);
                         }
@@ -494,7 +508,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::Cfg<EPW>::THR
                             // feeding a packed add into FFMA2 (tools/ubench_f32x2.cu), so the
                             // product that feeds the add is formed with scalar RN multiplies
                             const float2 p = ptx::fmul2(x, sa2);
+#if TB_W8_EXACT_FMA0
+                            // p * sb as a packed FMA with a +0 addend: the RN product except
+                            // that -0 becomes +0, which cannot change o (it starts at +0, and
+                            // x + (+0) == x + (-0) for every x != -0); ptxas neither folds it
+                            // into a multiply nor contracts it into the add
+                            o = ptx::fadd2(o, ptx::ffma2(p, sb2, make_float2(0.0f, 0.0f)));
+#else
                             o = ptx::fadd2(o, make_float2(__fmul_rn(p.x, sb2.x), __fmul_rn(p.y, sb2.y)));
+#endif
                         } else {
                             o = ptx::ffma2(x, sab2, o);
                         }
