@@ -1201,6 +1201,11 @@ int sla_tc(const tb_sla_args *a, cudaStream_t st) {
     const bool exact = a->row_max != nullptr || a->den != nullptr;
     dim3 grid((unsigned)cdiv(a->L, BM), (unsigned)a->H);
     auto launch = [&](auto kern, size_t smem) {
+#ifdef TB_SLA_TRACE
+        // trace build only: TB_SLA_SMEM_PAD extra bytes (e.g. one CTA per SM, for
+        // per-block phase timings without a co-resident CTA)
+        if (const char *e = getenv("TB_SLA_SMEM_PAD")) smem += (size_t)atol(e);
+#endif
         smem_attr(kern, (int)smem);
         kern<<<grid, THREADS, smem, st>>>(tq, tk, tv, tkv, *a, (int)nq, (int)nkv);
     };
