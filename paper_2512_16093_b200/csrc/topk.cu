@@ -16,6 +16,16 @@
 #ifndef TB_TOPK_ROWS
 #define TB_TOPK_ROWS 8
 #endif
+// kp loads in flight per thread (dims per batch) and CTAs per SM of the 8-row
+// kernel: 4 x 16 B and three CTAs (64 registers) -- 0.334 vs 0.367 ms at cfg4
+// for 8 and two CTAs (96 registers); 2 / 3 0.375, 4 / 4 and 2 / 4 spill
+// (0.46-0.53) (tools/time_topk.py, interleaved A/B)
+#ifndef TB_TOPK_KB
+#define TB_TOPK_KB 4
+#endif
+#ifndef TB_TOPK_MINB
+#define TB_TOPK_MINB 3
+#endif
 
 namespace tb {
 
@@ -199,7 +209,7 @@ __global__ void __launch_bounds__(320, MINB) topk16_kernel(
         for (int r = 0; r < R / 2; r++)
 #pragma unroll
             for (int u = 0; u < JT; u++) acc[r][u] = make_float2(0.0f, 0.0f);
-        // 8 dims per batch: the 8 coalesced float4 loads are all in flight before the FFMA2s
+        // TB_TOPK_KB dims per batch: the batch's coalesced float4 loads are all in flight before the FFMA2s
         auto step = [&](int t, const float4 kv) {
             const float4 *qrow = reinterpret_cast<const float4 *>(qt + t * R);
             float2 qpair[R / 2];
@@ -218,12 +228,12 @@ __global__ void __launch_bounds__(320, MINB) topk16_kernel(
             }
         };
         int t = 0;
-        for (; t + 8 <= d; t += 8) {
-            float4 kv[8];
+        for (; t + TB_TOPK_KB <= d; t += TB_TOPK_KB) {
+            float4 kv[TB_TOPK_KB];
 #pragma unroll
-            for (int i = 0; i < 8; i++) kv[i] = __ldg(reinterpret_cast<const float4 *>(kth + (int64_t)(t + i) * ldk + j0));
+            for (int i = 0; i < TB_TOPK_KB; i++) kv[i] = __ldg(reinterpret_cast<const float4 *>(kth + (int64_t)(t + i) * ldk + j0));
 #pragma unroll
-            for (int i = 0; i < 8; i++) step(t + i, kv[i]);
+            for (int i = 0; i < TB_TOPK_KB; i++) step(t + i, kv[i]);
         }
         for (; t < d; t++) step(t, __ldg(reinterpret_cast<const float4 *>(kth + (int64_t)t * ldk + j0)));
 #pragma unroll
@@ -338,11 +348,11 @@ static int topk_launch(const float *qp, const float *kp, const float *kpt, int64
                         (((uintptr_t)kpt) % 16) == 0 && nkv <= 2560;
     if (fast16) {
         constexpr int JT = 4;                        // 320 threads x 4 columns >= 1182 kv blocks (cfg4) in one pass
-        constexpr int R = TB_TOPK_ROWS;              // q rows per CTA (8: two CTAs per SM)
+        constexpr int R = TB_TOPK_ROWS;              // q rows per CTA (8: TB_TOPK_MINB CTAs per SM)
         const size_t smem = (((size_t)R * nkv * 4 + 15) & ~(size_t)15) + (size_t)d * R * 4 + 10 * 256 * 4;
         dim3 grid((unsigned)cdiv(nq, R), (unsigned)H);
-        smem_attr(topk16_kernel<JT, R, R == 16 ? 1 : (R == 8 ? 2 : 3)>, (int)smem);
-        topk16_kernel<JT, R, R == 16 ? 1 : (R == 8 ? 2 : 3)><<<grid, 320, smem, st>>>(qp, kpt, ldk, (int)nq, (int)nkv, (int)d, (int)count, idx, comp,
+        smem_attr(topk16_kernel<JT, R, R == 16 ? 1 : (R == 8 ? TB_TOPK_MINB : 3)>, (int)smem);
+        topk16_kernel<JT, R, R == 16 ? 1 : (R == 8 ? TB_TOPK_MINB : 3)><<<grid, 320, smem, st>>>(qp, kpt, ldk, (int)nq, (int)nkv, (int)d, (int)count, idx, comp,
                                                   scores_out, cov, cov_ld);
         return check_launch("topk16");
     }
