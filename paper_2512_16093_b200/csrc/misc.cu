@@ -198,8 +198,14 @@ __global__ void layernorm_kernel(const float *__restrict__ x, const float *__res
 // per row, 256 threads, each thread 4-float chunks kept in registers
 // (cols <= 256 * 4 * ADD_NORM_CHUNKS).
 constexpr int ADD_NORM_CHUNKS = 8;
+// five CTAs per SM (48 registers): RMSNorm 1.34 -> 1.17 ms and LayerNorm
+// 1.67 -> 1.21 ms for add_norm + the blockwise quantizer at cfg5 (four: 1.22 /
+// 1.25; tools/time_add_norm.py, interleaved A/B)
+#ifndef TB_ADDNORM_MINB
+#define TB_ADDNORM_MINB 5
+#endif
 template <int MODE>
-__global__ void __launch_bounds__(256) add_norm_kernel(
+__global__ void __launch_bounds__(256, TB_ADDNORM_MINB) add_norm_kernel(
     const float *__restrict__ x, const float *__restrict__ y, const float *__restrict__ emb, float alpha,
     const float *__restrict__ g, const float *__restrict__ b, int64_t cols, float eps, float *__restrict__ sum_out,
     __nv_bfloat16 *__restrict__ norm_out) {
