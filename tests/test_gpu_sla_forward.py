@@ -25,11 +25,13 @@ def tb():
     return ops
 
 
+@pytest.mark.parametrize("L", [5000, 200])
 @pytest.mark.parametrize("qb", [128, 64])
 @pytest.mark.parametrize("bf16", [True, False])
 @pytest.mark.parametrize("mix", [1.0, 0.0])
-def test_sla_forward_equals_device_op(tb, qb, bf16, mix):
-    q, k, v = gen.gaussian_qkv(21, 3, 5000, 128, bf16=True)          # ragged last kv block (5000 % 64 = 8)
+def test_sla_forward_equals_device_op(tb, qb, bf16, mix, L):
+    # 5000: ragged last kv block (5000 % 64 = 8); 200: two q-blocks, four kv blocks, one selected
+    q, k, v = gen.gaussian_qkv(21, 3, L, 128, bf16=True)
     dt = torch.bfloat16 if bf16 else torch.float32
     dq, dk, dv = (torch.from_numpy(t).cuda().to(dt) for t in (q, k, v))
     want = tb.sla_attention(dq, dk, dv, qb, 64, 0.1, mix, out_dtype=torch.float32)
