@@ -1,4 +1,4 @@
-"""cfg4 step (CUDA graph replay) and k_mean alone for library variants given as
+"""cfg4 step (CUDA graph replay), k_mean and kv_part (with the K pool) alone for library variants given as
 TB200_LIB paths on the command line (interleaved, 3 rounds); tools only."""
 import os
 import subprocess
@@ -32,7 +32,8 @@ if len(sys.argv) > 1 and sys.argv[1] == "--child":
 
     step = graph_ms(lambda: ops.sla_attention(q, k, v, 128, 64, 0.1, 1.0, out_dtype=torch.bfloat16))
     km = graph_ms(lambda: ops.kmean(k))
-    print(f"{step:.3f} {km:.3f}")
+    kvp = graph_ms(lambda: ops.linear_kv_part(k, v, 64, pool=True))
+    print(f"{step:.3f} {km:.3f} {kvp:.3f}")
     sys.exit(0)
 
 libs = sys.argv[1:]
@@ -46,4 +47,4 @@ for _ in range(3):
         line = [x for x in out.stdout.splitlines() if x.strip()]
         res[lib].append(line[-1] if line else out.stderr[-300:])
 for lib, r in res.items():
-    print(os.path.basename(lib), "step ms / k_mean ms:", r)
+    print(os.path.basename(lib), "step ms / k_mean ms / kv_part ms:", r)
