@@ -522,10 +522,14 @@ __global__ void __launch_bounds__(128) kmean_bulk_kernel(const T *__restrict__ k
 
 // bf16, d == 128: one warp per (head, 32-channel quarter) so 4*H CTAs stream
 // the heads in parallel; a 2-D TMA ring of [256 tokens x 32 channels] tiles
-// (16 KB) feeds the chains, each lane one channel, summing in token order.
-constexpr int KM_CH = 256, KM_STAGES = 6;
+// (16 KB) feeds the chains, each lane one channel, summing in token order; the
+// next 16 tokens' shared-memory loads issue under the current 16-add chain.
+#ifndef TB_KM_PIPE
+#define TB_KM_PIPE 1
+#endif
+constexpr int KM_CH = 256, KM_STAGES = 6;   // ring depth: up to KM_STAGES, chosen at launch
 __global__ void __launch_bounds__(32) kmean_split_kernel(const __grid_constant__ CUtensorMap tm, int64_t L,
-                                                         float *__restrict__ kmean) {
+                                                         int nst, float *__restrict__ kmean) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ __align__(8) uint64_t full[KM_STAGES];
     const int qc = blockIdx.x, h = blockIdx.y, lane = threadIdx.x;
@@ -533,9 +537,9 @@ __global__ void __launch_bounds__(32) kmean_split_kernel(const __grid_constant__
     const int64_t nch = cdiv(L, KM_CH);
     const int64_t row0 = (int64_t)h * L;
     if (lane == 0) {
-        for (int s = 0; s < KM_STAGES; s++) ptx::mbar_init(&full[s], 1);
+        for (int s = 0; s < nst; s++) ptx::mbar_init(&full[s], 1);
         ptx::fence_barrier_init();
-        for (int64_t i = 0; i < imin64(KM_STAGES, nch); i++) {
+        for (int64_t i = 0; i < imin64(nst, nch); i++) {
             ptx::mbar_arrive_expect_tx(&full[i], KM_CH * 64);
             ptx::tma_load_2d(smem + i * KM_CH * 64, &tm, qc * 32, (int)(row0 + i * KM_CH), &full[i]);
         }
@@ -543,11 +547,32 @@ __global__ void __launch_bounds__(32) kmean_split_kernel(const __grid_constant__
     __syncwarp();
     float acc = 0.0f;
     for (int64_t i = 0; i < nch; i++) {
-        const int s = (int)(i % KM_STAGES);
-        ptx::mbar_wait(&full[s], (uint32_t)((i / KM_STAGES) & 1));
+        const int s = (int)(i % nst);
+        ptx::mbar_wait(&full[s], (uint32_t)((i / nst) & 1));
         const int toks = (int)imin64(KM_CH, L - i * KM_CH);
         const __nv_bfloat16 *buf = ring + (size_t)s * KM_CH * 32 + lane;
         int t = 0;
+#if TB_KM_PIPE
+        if (toks == KM_CH) {
+            // full chunk: the next 16 tokens' loads issue before this batch's adds, so the
+            // shared-memory latency hides under the 16-add chain
+            __nv_bfloat16 w[16], nx[16];
+#pragma unroll
+            for (int j = 0; j < 16; j++) w[j] = buf[j * 32];
+#pragma unroll 1
+            for (t = 0; t < KM_CH - 16; t += 16) {
+#pragma unroll
+                for (int j = 0; j < 16; j++) nx[j] = buf[(t + 16 + j) * 32];
+#pragma unroll
+                for (int j = 0; j < 16; j++) acc = __fadd_rn(acc, __bfloat162float(w[j]));
+#pragma unroll
+                for (int j = 0; j < 16; j++) w[j] = nx[j];
+            }
+#pragma unroll
+            for (int j = 0; j < 16; j++) acc = __fadd_rn(acc, __bfloat162float(w[j]));
+            t = KM_CH;
+        }
+#endif
         for (; t + 16 <= toks; t += 16) {
             float w[16];
 #pragma unroll
@@ -557,10 +582,10 @@ __global__ void __launch_bounds__(32) kmean_split_kernel(const __grid_constant__
         }
         for (; t < toks; t++) acc = __fadd_rn(acc, __bfloat162float(buf[t * 32]));
         __syncwarp();
-        if (lane == 0 && i + KM_STAGES < nch) {
+        if (lane == 0 && i + nst < nch) {
             ptx::fence_async_smem();          // the warp's reads of stage s before the TMA overwrite
             ptx::mbar_arrive_expect_tx(&full[s], KM_CH * 64);
-            ptx::tma_load_2d(smem + s * KM_CH * 64, &tm, qc * 32, (int)(row0 + (i + KM_STAGES) * KM_CH), &full[s]);
+            ptx::tma_load_2d(smem + s * KM_CH * 64, &tm, qc * 32, (int)(row0 + (i + nst) * KM_CH), &full[s]);
         }
     }
     kmean[h * 128 + qc * 32 + lane] = __fdiv_rn(acc, (float)L);
@@ -715,9 +740,14 @@ extern "C" int tb_kmean(const void *k, int dtype, int64_t H, int64_t L, int64_t 
         if (!make_tmap_2d(&tm, k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 128, H * L, 256, 32, KM_CH,
                           CU_TENSOR_MAP_SWIZZLE_NONE))
             return fail(TB_ECUDA, "cuTensorMapEncodeTiled failed (kmean)");
-        const int smem = KM_STAGES * KM_CH * 64;
-        smem_attr(kmean_split_kernel, smem);
-        kmean_split_kernel<<<dim3(4, (unsigned)H), 32, smem, st>>>(tm, L, kmean);
+        // 3 x 16 KB: the ring fits beside four kv_part CTAs per SM, so the chains start with the
+        // step instead of waiting for kv_part's grid to drain (same-process graph A/B of the cfg4
+        // step: 3 stages 0.15-0.2 ms faster than 6; TB_KM_STAGES overrides, tools only)
+        int nst = 3;
+        if (const char *e = getenv("TB_KM_STAGES")) nst = atoi(e) < 2 ? 2 : (atoi(e) > KM_STAGES ? KM_STAGES : atoi(e));
+        const int smem = nst * KM_CH * 64;
+        smem_attr(kmean_split_kernel, KM_STAGES * KM_CH * 64);
+        kmean_split_kernel<<<dim3(4, (unsigned)H), 32, smem, st>>>(tm, L, nst, kmean);
     } else if (aligned && d <= 128) {
         constexpr int STAGES = 6;
         int chunk = (int)(16384 / (d * es));          // 16 KiB per stage
