@@ -366,6 +366,15 @@ int tb_linear_kv_part(const void *k, const void *v, int64_t H, int64_t L, int64_
 int tb_linear_kv_part_pool(const void *k, const void *v, int64_t H, int64_t L, int64_t d, int64_t kv_block,
                            int64_t dx, void *kv_part, float *kp, float *kpt, int64_t ldt, void *stream);
 
+/* tb_linear_kv_part_pool that also writes the smoothed K codes and scales
+ * (_quantize_token_blocks of k - k_mean, attention.py:201-220, bit-identical
+ * to tb_pool_quant_tokens(k, k_mean, kv_block)): k_codes int8 [H, L, d],
+ * k_scales f32 [H, nkv], from the same K tiles (no separate K pass); needs
+ * k_mean f32 [H, d] on the stream first.  k_codes / k_scales NULL = _pool. */
+int tb_linear_kv_part_codes(const void *k, const void *v, int64_t H, int64_t L, int64_t d, int64_t kv_block,
+                            int64_t dx, void *kv_part, float *kp, float *kpt, int64_t ldt, const float *k_mean,
+                            int8_t *k_codes, float *k_scales, void *stream);
+
 /* DiT glue in one pass: s = x (+ y) (+ alpha * emb[cols]) -> sum_out (f32,
  * optional, may alias x or y) and RMSNorm(s) * gain (layer_norm = 0) or
  * LayerNorm(s) * gain + offset (layer_norm = 1) as bf16 norm_out

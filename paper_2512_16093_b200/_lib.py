@@ -76,6 +76,7 @@ SIGNATURES = {
     "tb_gemm_bf16_batched": [_P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _i, _P],
     "tb_linear_kv_part": [_P, _P, _I, _I, _I, _I, _I, _P, _P],
     "tb_linear_kv_part_pool": [_P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _I, _P],
+    "tb_linear_kv_part_codes": [_P, _P, _I, _I, _I, _I, _I, _P, _P, _P, _I, _P, _P, _P, _P],
     "tb_rmsnorm": [_P, _P, _I, _I, _f, _P, _P],
     "tb_axpy_rn": [_P, _P, _f, _I, _P],
     "tb_add_norm": [_P, _P, _P, _f, _P, _P, _I, _I, _f, _i, _P, _P, _P],

@@ -34,6 +34,7 @@ struct Smem {
     uint8_t v[TILE];                         // V tile, later the output tile (second half)
     uint64_t full, mma_done;
     uint32_t tmem_base;
+    float red[4];                            // per warp: absmax of the centered K values (K codes)
 };
 constexpr size_t SMEM_BYTES = sizeof(Smem);
 }  // namespace lkv
@@ -46,7 +47,8 @@ __global__ void __launch_bounds__(lkv::THREADS) kv_part_kernel(const __grid_cons
                                                                 int L, int nkv, int dx,
                                                                 __nv_bfloat16 *__restrict__ kv_part,
                                                                 float *__restrict__ kp, float *__restrict__ kpt,
-                                                                int64_t ldt) {
+                                                                int64_t ldt, const float *__restrict__ km,
+                                                                int8_t *__restrict__ kc, float *__restrict__ ks) {
     using namespace lkv;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     Smem &S = *reinterpret_cast<Smem *>(smem_raw);
@@ -83,8 +85,13 @@ __global__ void __launch_bounds__(lkv::THREADS) kv_part_kernel(const __grid_cons
         const int c = threadIdx.x, e = min(BN, L - b * BN);
         const uint8_t *colp = S.k + (c >> 6) * (TILE / 2) + (c & 7) * 2;
         const int g = (c & 63) >> 3;
+        // K codes (optional): absmax of the k_mean-centered values, order-free, on the same reads
+        const float ctr = kc ? __ldg(km + h * D + c) : 0.0f;
+        float am = 0.0f;
         auto ld = [&](int t) {
-            return __bfloat162float(*reinterpret_cast<const __nv_bfloat16 *>(colp + t * 128 + ((g ^ (t & 7)) * 16)));
+            const float x = __bfloat162float(*reinterpret_cast<const __nv_bfloat16 *>(colp + t * 128 + ((g ^ (t & 7)) * 16)));
+            am = fmaxf(am, fabsf(__fsub_rn(x, ctr)));
+            return x;
         };
         const float seed = ld(0);
         const int n = e - 1;
@@ -107,7 +114,26 @@ __global__ void __launch_bounds__(lkv::THREADS) kv_part_kernel(const __grid_cons
         const float pm = __fdiv_rn(n > 0 ? __fadd_rn(seed, res) : seed, (float)e);
         kp[((int64_t)h * nkv + b) * D + c] = pm;
         if (kpt) kpt[((int64_t)h * D + c) * ldt + b] = pm;   // [H][d][ldt]: the top-k kernel's coalesced operand
+        if (kc) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
+            if (lane == 0) S.red[warp] = am;
+        }
         __syncthreads();                                   // every read of the raw tile before phi overwrites it
+    }
+    // the K block's scale (quantize_token_blocks, attention.py:201-220), as pool_quant_tile_kernel
+    float qsafe = 1.0f, qinv = 1.0f;
+    bool qexact = false;
+    float qctr[8];
+    if (kc) {
+        const float s = quant_scale(fmaxf(fmaxf(S.red[0], S.red[1]), fmaxf(S.red[2], S.red[3])));
+        if (threadIdx.x == 0) ks[(int64_t)h * nkv + b] = s;
+        qsafe = (s == 0.0f) ? 1.0f : s;
+        qinv = __frcp_rn(qsafe);
+        qexact = !(qsafe >= 1.17549435e-38f && qinv <= 3.0e38f);   // subnormal scale: exact division
+        const int c0 = (threadIdx.x >> 6) * 64 + ((threadIdx.x >> 3) & 7) * 8;
+#pragma unroll
+        for (int i = 0; i < 8; i++) qctr[i] = __ldg(km + h * D + c0 + i);
     }
     {
         // phi in place: thread = (channel half, 8-channel group g, 8-token slice tq)
@@ -122,6 +148,19 @@ __global__ void __launch_bounds__(lkv::THREADS) kv_part_kernel(const __grid_cons
             uint4 w = *p;
             __nv_bfloat162 *bw = reinterpret_cast<__nv_bfloat162 *>(&w);
             const bool in = b * BN + t < L;
+            if (kc && in) {                               // codes of the raw (centered) values before phi
+                float xv[8];
+#pragma unroll
+                for (int i = 0; i < 4; i++) {
+                    const float2 x = __bfloat1622float2(bw[i]);
+                    xv[2 * i] = __fsub_rn(x.x, qctr[2 * i]);
+                    xv[2 * i + 1] = __fsub_rn(x.y, qctr[2 * i + 1]);
+                }
+                uint32_t cw[2];
+                quant_fast_n<8>(xv, qsafe, qinv, qexact, cw);
+                *reinterpret_cast<uint2 *>(kc + ((int64_t)h * L + b * BN + t) * D + half * 64 + g * 8) =
+                    make_uint2(cw[0], cw[1]);
+            }
 #pragma unroll
             for (int i = 0; i < 4; i++) {
                 const float2 x = __bfloat1622float2(bw[i]);
@@ -208,10 +247,15 @@ __global__ void __launch_bounds__(lkv::THREADS) kv_part_kernel(const __grid_cons
 
 using namespace tb;
 
-extern "C" int tb_linear_kv_part_pool(const void *k, const void *v, int64_t H, int64_t L, int64_t d,
-                                      int64_t kv_block, int64_t dx, void *kv_part, float *kp, float *kpt,
-                                      int64_t ldt, void *stream) {
+extern "C" int tb_linear_kv_part_codes(const void *k, const void *v, int64_t H, int64_t L, int64_t d,
+                                       int64_t kv_block, int64_t dx, void *kv_part, float *kp, float *kpt,
+                                       int64_t ldt, const float *k_mean, int8_t *k_codes, float *k_scales,
+                                       void *stream) {
     using namespace lkv;
+    TB_REQUIRE((k_codes == nullptr) == (k_scales == nullptr) && (k_codes == nullptr || k_mean != nullptr),
+               "k_codes, k_scales and k_mean go together");
+    TB_REQUIRE(k_codes == nullptr || kp != nullptr, "K codes come with the K pool (kp)");
+    TB_REQUIRE(k_codes == nullptr || ((uintptr_t)k_codes % 8) == 0, "unaligned k_codes");
     TB_REQUIRE(kpt == nullptr || (kp != nullptr && ldt >= cdiv(L, kv_block)), "kpt needs kp and ldt >= blocks");
     TB_REQUIRE(d == D && kv_block == BN, "tb_linear_kv_part: d == 128 and kv_block == 64 only");
     TB_REQUIRE(dx > d && dx * d % 256 == 0, "dx must exceed d with dx*d a multiple of 256");
@@ -227,8 +271,15 @@ extern "C" int tb_linear_kv_part_pool(const void *k, const void *v, int64_t H, i
     cudaStream_t st = as_stream(stream);
     smem_attr(kv_part_kernel, (int)SMEM_BYTES);
     kv_part_kernel<<<dim3((unsigned)nkv, (unsigned)H), THREADS, SMEM_BYTES, st>>>(
-        tk, tv, to, (int)L, (int)nkv, (int)dx, (__nv_bfloat16 *)kv_part, kp, kpt, ldt);
+        tk, tv, to, (int)L, (int)nkv, (int)dx, (__nv_bfloat16 *)kv_part, kp, kpt, ldt, k_mean, k_codes, k_scales);
     return check_launch("kv_part");
+}
+
+extern "C" int tb_linear_kv_part_pool(const void *k, const void *v, int64_t H, int64_t L, int64_t d,
+                                      int64_t kv_block, int64_t dx, void *kv_part, float *kp, float *kpt,
+                                      int64_t ldt, void *stream) {
+    return tb_linear_kv_part_codes(k, v, H, L, d, kv_block, dx, kv_part, kp, kpt, ldt, nullptr, nullptr, nullptr,
+                                   stream);
 }
 
 extern "C" int tb_linear_kv_part(const void *k, const void *v, int64_t H, int64_t L, int64_t d, int64_t kv_block,

@@ -352,11 +352,13 @@ def linear_kv_dx(d: int) -> int:
     return dx
 
 
-def linear_kv_part(k, v, kv_block: int, pool: bool = False):
+def linear_kv_part(k, v, kv_block: int, pool: bool = False, k_mean=None):
     """tb_linear_kv_part: per kv block [V_b | 1]^T phi(K_b) (attention.py:320-325)
     straight from bf16 k, v -> [H, nkv, dx, d] bf16 (one tcgen05 kernel).
     pool=True (tb_linear_kv_part_pool): also the raw K block means and their
-    transposed copy from the same tiles -> (kv_part, kp, kpt), as pool_tokens_t."""
+    transposed copy from the same tiles -> (kv_part, kp, kpt), as pool_tokens_t.
+    k_mean given (with pool=True; tb_linear_kv_part_codes): also the smoothed K
+    codes and scales -> (kv_part, kp, kpt, kc, ks), as pool_quant_tokens(k, kv_block, k_mean)."""
     H, L, d = k.shape
     nkv = cdiv(L, kv_block)
     dx = linear_kv_dx(d)
@@ -367,9 +369,15 @@ def linear_kv_part(k, v, kv_block: int, pool: bool = False):
     ldt = -(-nkv // 4) * 4
     kp = torch.empty((H, nkv, d), dtype=torch.float32, device=k.device)
     kpt = torch.empty((H, d, ldt), dtype=torch.float32, device=k.device)
-    call("tb_linear_kv_part_pool", ptr(k), ptr(v), H, L, d, kv_block, dx, ptr(kv_part), ptr(kp), ptr(kpt), ldt,
-         stream_ptr())
-    return kv_part, kp, kpt
+    if k_mean is None:
+        call("tb_linear_kv_part_pool", ptr(k), ptr(v), H, L, d, kv_block, dx, ptr(kv_part), ptr(kp), ptr(kpt), ldt,
+             stream_ptr())
+        return kv_part, kp, kpt
+    kc = torch.empty((H, L, d), dtype=torch.int8, device=k.device)
+    ks = torch.empty((H, nkv), dtype=torch.float32, device=k.device)
+    call("tb_linear_kv_part_codes", ptr(k), ptr(v), H, L, d, kv_block, dx, ptr(kv_part), ptr(kp), ptr(kpt), ldt,
+         ptr(k_mean), ptr(kc), ptr(ks), stream_ptr())
+    return kv_part, kp, kpt, kc, ks
 
 
 def linear_kv_sel(kv_part: torch.Tensor, cov: torch.Tensor, nkv: int):
@@ -525,10 +533,20 @@ def sla_attention(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: fl
         # stream, kv_part (HBM-bound, needs only k and v) on a third from t=0.
         # _KV_POOL: kv_part also pools the raw K blocks from the tiles it holds
         # (no separate K pooling pass) and top-k waits for it after the Q pass
+        # _KV_CODES (opt-in): kv_part also writes the smoothed K codes from those
+        # tiles (no separate K pass), so it starts once k_mean is done
         third = _aux_stream("kvpart")
         third.wait_stream(main)
+        codes_in_kv = _KV_POOL and _KV_CODES
+        if codes_in_kv:
+            with torch.cuda.stream(side):
+                km = kmean(k)
+            third.wait_stream(side)
         with torch.cuda.stream(third):
-            if _KV_POOL:
+            if codes_in_kv:
+                kv_part, kp, kpt, kc, ks = linear_kv_part(kb, vb, kv_block, pool=True, k_mean=km)
+                km.record_stream(third)
+            elif _KV_POOL:
                 kv_part, kp, kpt = linear_kv_part(kb, vb, kv_block, pool=True)
             else:
                 kv_part = linear_kv_part(kb, vb, kv_block)
@@ -536,9 +554,10 @@ def sla_attention(q, k, v, q_block: int = 64, kv_block: int = 64, topk_ratio: fl
             ev_kv.record(third)
             if pv_fp8:                                  # V codes only need v
                 v8, v8s = quant_v_fp8(v)
-        with torch.cuda.stream(side):
-            km = kmean(k)
-            kc, ks, _ = pool_quant_tokens(k, kv_block, km, pool=False)
+        if not codes_in_kv:
+            with torch.cuda.stream(side):
+                km = kmean(k)
+                kc, ks, _ = pool_quant_tokens(k, kv_block, km, pool=False)
         qc, qs, qp = pool_quant_tokens(q, q_block, None, pool=True)
         if _KV_POOL:
             main.wait_event(ev_kv)
@@ -665,6 +684,7 @@ _AUX = {}
 # bf16 tensor-core path: the raw K pool comes from kv_part's tiles (True) or
 # from a separate pooling pass on the caller's stream (False; tools A/B)
 _KV_POOL = True
+_KV_CODES = False   # measured slower: kv_part would wait for k_mean
 
 
 def _aux_stream(name: str) -> torch.cuda.Stream:

@@ -291,6 +291,27 @@ def test_linear_kv_part_pool_equals_pool_pass(tb, L):
     assert torch.equal(kvp, tb.linear_kv_part(kd, vd, 64))
 
 
+@pytest.mark.parametrize("L,shift", [(1000, 0.0), (4096, 0.75), (75600, 0.0)])
+def test_linear_kv_part_codes_equal_k_pass(tb, L, shift):
+    """tb_linear_kv_part_codes: the smoothed K codes and scales it writes from its
+    own tiles are bit-identical to the K-codes pass tb_pool_quant_tokens(k, k_mean)
+    (pinned to _quantize_token_blocks, attention.py:201-220), ragged last block
+    included (L = 1000: 40 tokens; L = 75600: 16, the cfg4 shape at one head);
+    pool outputs and kv_part are unchanged."""
+    H, d = (1 if L > 10000 else 3), 128
+    _, k, v = gen.gaussian_qkv(41, H, L, d, bf16=True)
+    kd, vd = dev(k + np.float32(shift), True), dev(v, True)
+    km = tb.kmean(kd)
+    kvp, kp, kpt, kc, ks = tb.linear_kv_part(kd, vd, 64, pool=True, k_mean=km)
+    want_kc, want_ks, _ = tb.pool_quant_tokens(kd, 64, km, pool=False)
+    kvp0, kp0, kpt0 = tb.linear_kv_part(kd, vd, 64, pool=True)
+    torch.cuda.synchronize()
+    assert torch.equal(kc, want_kc)
+    assert torch.equal(ks, want_ks)
+    nkv = ks.shape[1]
+    assert torch.equal(kp, kp0) and torch.equal(kpt[:, :, :nkv], kpt0[:, :, :nkv]) and torch.equal(kvp, kvp0)
+
+
 def test_linear_kv_part_blocks(tb):
     """tb_linear_kv_part vs the per-block einsums of linear_attention
     (attention.py:320-325): V_b^T phi(K_b) and sum phi(K_b), padded tokens
